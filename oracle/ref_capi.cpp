@@ -1,0 +1,416 @@
+// ORACLE TEST INFRASTRUCTURE ONLY.
+//
+// extern "C" façade over the UNMODIFIED reference library (compiled in place
+// from /root/reference/proj/core/src by oracle/Makefile into
+// oracle/_ref/libcdg_ref.so). It lets pytest (ctypes) drive the reference's
+// own mesh generators, DgLevel construction, compute_rhs, rk_step and the
+// viscosity model on the same inputs the GPU path sees. Only tests/,
+// __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg
+// load this library, and only as the checker / CPU baseline.
+//
+// Reference entry points wrapped (all under /root/reference/proj/core):
+//   make_cube_mesh / make_single_tet / make_two_tets / make_sphere_shell_mesh
+//                                           src/meshgen.cpp:41-225
+//   DgLevel::DgLevel                         src/solver.cpp:97-179
+//   make_workspace / compute_rhs / rk_step   src/solver.cpp:72-85, 325-492
+//   compute_timestep                         src/solver.cpp:494-526
+//   current_viscosity / aux_gradient         src/solver.cpp:87-91
+//   random_admissible_store recipe           src/bench.cpp:22-40 (restated: it
+//                                            is file-static in the reference)
+#include <omp.h>
+
+#include <cstring>
+#include <memory>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "cdg/curved_mesh.hpp"
+#include "cdg/meshgen.hpp"
+#include "cdg/refelem.hpp"
+#include "cdg/solver.hpp"
+
+using namespace cdg;
+
+namespace {
+
+struct RefMesh {
+  Mesh mesh;
+};
+
+struct RefLevel {
+  const RefMesh* mesh = nullptr;
+  std::unique_ptr<CurvedMesh> cmesh;
+  std::unique_ptr<DgLevel> level;
+  std::shared_ptr<RhsWorkspace> ws;
+};
+
+void copy_err(const std::exception& e, char* err, size_t n) {
+  if (err && n) {
+    std::strncpy(err, e.what(), n - 1);
+    err[n - 1] = 0;
+  }
+}
+
+int status_of(const std::exception& e) {
+  if (dynamic_cast<const NumericsError*>(&e)) return 3;
+  if (dynamic_cast<const ConfigError*>(&e)) return 2;
+  return 1;
+}
+
+}  // namespace
+
+extern "C" {
+
+// Mirrors cdg_gpu_run_config in include/cdg_gpu.h (same field order).
+struct ref_run_cfg {
+  int riemann;  // 0 llf, 1 hllc
+  double gamma;
+  int visc_enabled;
+  double eps0, kappa, s0_offset;
+  int indicator_component;
+  int jacobian_weighted;
+  double cfl;
+};
+
+static RunConfig to_cfg(const ref_run_cfg* c) {
+  RunConfig cfg;
+  cfg.riemann = c->riemann == 1 ? "hllc" : "llf";
+  cfg.gas.gamma = c->gamma;
+  cfg.viscosity.enabled = c->visc_enabled != 0;
+  cfg.viscosity.eps0 = c->eps0;
+  cfg.viscosity.kappa = c->kappa;
+  cfg.viscosity.s0_offset = c->s0_offset;
+  cfg.viscosity.indicator_component = c->indicator_component;
+  cfg.viscosity.jacobian_weighted = c->jacobian_weighted != 0;
+  cfg.cfl = c->cfl;
+  return cfg;
+}
+
+static ConservedState to_state(const double* f) {
+  ConservedState s;
+  s.rho = f[0];
+  s.mom = {f[1], f[2], f[3]};
+  s.rhoE = f[4];
+  return s;
+}
+
+int ref_num_threads(int n) {
+  if (n > 0) omp_set_num_threads(n);
+  return omp_get_max_threads();
+}
+
+// ---- reference element tables (refelem.cpp:301-358) -----------------------
+// sizes[0..3] = n_basis, n_cub, n_face_quad, degree
+int ref_refelem_sizes(int p, int cub_override, int face_override, int* sizes) {
+  try {
+    auto re = get_reference_element(p, cub_override, face_override);
+    sizes[0] = re->n_basis();
+    sizes[1] = re->n_cub();
+    sizes[2] = re->n_face_quad();
+    sizes[3] = re->degree();
+    return 0;
+  } catch (const std::exception&) {
+    return 2;
+  }
+}
+
+static void put(const Eigen::MatrixXd& m, double* out) {
+  // row-major export
+  for (Eigen::Index i = 0; i < m.rows(); ++i)
+    for (Eigen::Index j = 0; j < m.cols(); ++j) out[i * m.cols() + j] = m(i, j);
+}
+
+// Row-major dumps. colloc/cub/face nodes are [n][3].
+int ref_refelem_tables(int p, int cub_override, int face_override, double* colloc,
+                       double* cub_nodes, double* cub_w, double* face_nodes, double* face_w,
+                       double* vand, double* vand_inv, double* interp_cub,
+                       double* interp_face, double* dr, double* ds, double* dt) {
+  auto re = get_reference_element(p, cub_override, face_override);
+  for (size_t i = 0; i < re->colloc_nodes().size(); ++i)
+    for (int d = 0; d < 3; ++d) colloc[3 * i + d] = re->colloc_nodes()[i][d];
+  for (size_t i = 0; i < re->cub_nodes().size(); ++i)
+    for (int d = 0; d < 3; ++d) cub_nodes[3 * i + d] = re->cub_nodes()[i][d];
+  for (size_t i = 0; i < re->face_nodes().size(); ++i)
+    for (int d = 0; d < 3; ++d) face_nodes[3 * i + d] = re->face_nodes()[i][d];
+  std::memcpy(cub_w, re->cub_weights().data(), sizeof(double) * re->cub_weights().size());
+  std::memcpy(face_w, re->face_weights().data(), sizeof(double) * re->face_weights().size());
+  put(re->vandermonde(), vand);
+  put(re->vandermonde_inv(), vand_inv);
+  put(re->interp_cub(), interp_cub);
+  put(re->interp_face(), interp_face);
+  put(re->deriv_r(), dr);
+  put(re->deriv_s(), ds);
+  put(re->deriv_t(), dt);
+  return 0;
+}
+
+// ---- meshes (meshgen.cpp) ---------------------------------------------------
+void* ref_mesh_cube(int n, double scale) {
+  auto* m = new RefMesh;
+  m->mesh = make_cube_mesh(n, "wall");
+  if (scale != 1.0)
+    for (auto& v : m->mesh.vertices) v = v * scale;
+  return m;
+}
+void* ref_mesh_single_tet() {
+  auto* m = new RefMesh;
+  m->mesh = make_single_tet("wall");
+  return m;
+}
+void* ref_mesh_two_tets() {
+  auto* m = new RefMesh;
+  m->mesh = make_two_tets("wall");
+  return m;
+}
+// All boundary faces of the sphere shell get tag "wall" or "farfield" via the
+// reference tags "sphere"/"farfield".
+void* ref_mesh_sphere_shell(double r_in, double r_out, int subdiv, int layers) {
+  auto* m = new RefMesh;
+  m->mesh = make_sphere_shell_mesh(r_in, r_out, subdiv, layers, "sphere", "farfield");
+  return m;
+}
+void ref_mesh_free(void* h) { delete static_cast<RefMesh*>(h); }
+
+// sizes: [0]=n_vertices [1]=n_elements [2]=n_boundary_faces
+void ref_mesh_sizes(void* h, int* sizes) {
+  const Mesh& m = static_cast<RefMesh*>(h)->mesh;
+  sizes[0] = static_cast<int>(m.vertices.size());
+  sizes[1] = m.n_elements();
+  sizes[2] = static_cast<int>(m.boundary_faces.size());
+}
+
+// verts [nv][3]; tets [ne][4]; neighbor/neighbor_face/perm [ne][4](perm packed
+// p0+3p1+9p2); bnd_tag [ne][4]: -1 interior, else index into a tag list where
+// "wall"/"sphere"=0, "farfield"=1, other=2.
+void ref_mesh_export(void* h, double* verts, int* tets, int* neighbor, int* neighbor_face,
+                     int* perm, int* bnd_tag) {
+  const Mesh& m = static_cast<RefMesh*>(h)->mesh;
+  for (size_t i = 0; i < m.vertices.size(); ++i)
+    for (int d = 0; d < 3; ++d) verts[3 * i + d] = m.vertices[i][d];
+  for (int e = 0; e < m.n_elements(); ++e) {
+    for (int k = 0; k < 4; ++k) tets[4 * e + k] = m.tets[e][k];
+    for (int f = 0; f < 4; ++f) {
+      const int idx = 4 * e + f;
+      if (m.links[e][f]) {
+        neighbor[idx] = m.links[e][f]->other.element;
+        neighbor_face[idx] = m.links[e][f]->other.local_face;
+        const auto& p = m.links[e][f]->perm;
+        perm[idx] = p[0] + 3 * p[1] + 9 * p[2];
+        bnd_tag[idx] = -1;
+      } else {
+        neighbor[idx] = -1;
+        neighbor_face[idx] = -1;
+        perm[idx] = -1;
+        const std::string& tag = m.boundary_faces[m.boundary_index[e][f]].tag;
+        bnd_tag[idx] = (tag == "wall" || tag == "sphere") ? 0 : (tag == "farfield" ? 1 : 2);
+      }
+    }
+  }
+}
+
+// ---- levels (solver.cpp:97-179) ----------------------------------------------
+// bc_wall / bc_far: BcKind (0 SlipWall, 1 Farfield, 2 Symmetry) for the
+// "wall"/"sphere" and "farfield" tags.
+void* ref_level_create(void* mesh_h, int p, int bc_wall, int bc_far, int padded,
+                       int curved_quadrature, char* err, size_t errn) {
+  try {
+    auto* lv = new RefLevel;
+    lv->mesh = static_cast<RefMesh*>(mesh_h);
+    lv->cmesh = std::make_unique<CurvedMesh>(lv->mesh->mesh, p);
+    RunConfig cfg;
+    cfg.curved_quadrature = curved_quadrature != 0;
+    auto re = level_reference_element(*lv->cmesh, p, cfg);
+    const BcMap bcs = {{"wall", static_cast<BcKind>(bc_wall)},
+                       {"sphere", static_cast<BcKind>(bc_wall)},
+                       {"farfield", static_cast<BcKind>(bc_far)}};
+    lv->level = std::make_unique<DgLevel>(*lv->cmesh, re, bcs, padded != 0);
+    lv->ws = make_workspace(*lv->level);
+    return lv;
+  } catch (const std::exception& e) {
+    copy_err(e, err, errn);
+    return nullptr;
+  }
+}
+void ref_level_free(void* h) { delete static_cast<RefLevel*>(h); }
+
+// sizes: [0]=K [1]=n_basis [2]=n_cub [3]=n_face_quad [4]=block [5]=trace_block [6]=degree
+void ref_level_sizes(void* h, int* sizes) {
+  const DgLevel& lv = *static_cast<RefLevel*>(h)->level;
+  sizes[0] = lv.n_elements();
+  sizes[1] = lv.refelem().n_basis();
+  sizes[2] = lv.refelem().n_cub();
+  sizes[3] = lv.refelem().n_face_quad();
+  const SolutionStore s = lv.make_store();
+  const SolutionStore t = lv.make_trace_store();
+  sizes[4] = s.block_length();
+  sizes[5] = t.block_length();
+  sizes[6] = lv.refelem().degree();
+}
+
+// Per-element geometry + coupling as the reference built it.
+//  cub_dr [K][ncub][9], cub_jac [K][ncub], face_normal [K][nf][3],
+//  face_sjac [K][nf], face_phys [K][nf][3], h [K], neighbor/nface/bc [K][4],
+//  node_map [K][4][ng] (-1 on boundary faces). Any pointer may be null.
+void ref_level_geometry(void* h, double* cub_dr, double* cub_jac, double* face_normal,
+                        double* face_sjac, double* face_phys, double* hk, int* neighbor,
+                        int* neighbor_face, int* bc, int* node_map) {
+  const DgLevel& lv = *static_cast<RefLevel*>(h)->level;
+  const int ne = lv.n_elements(), ncub = lv.refelem().n_cub(),
+            ng = lv.refelem().n_face_quad(), nf = 4 * ng;
+  for (int e = 0; e < ne; ++e) {
+    const auto& g = lv.geom(e);
+    for (int q = 0; q < ncub; ++q) {
+      if (cub_dr)
+        for (int k = 0; k < 9; ++k) cub_dr[(static_cast<size_t>(e) * ncub + q) * 9 + k] = g.cub_dr[q][k];
+      if (cub_jac) cub_jac[static_cast<size_t>(e) * ncub + q] = g.cub_jac[q];
+    }
+    for (int q = 0; q < nf; ++q) {
+      for (int d = 0; d < 3; ++d) {
+        if (face_normal) face_normal[(static_cast<size_t>(e) * nf + q) * 3 + d] = g.face_normal[q][d];
+        if (face_phys) face_phys[(static_cast<size_t>(e) * nf + q) * 3 + d] = g.face_phys[q][d];
+      }
+      if (face_sjac) face_sjac[static_cast<size_t>(e) * nf + q] = g.face_sjac[q];
+    }
+    if (hk) hk[e] = g.h();
+    for (int f = 0; f < 4; ++f) {
+      const auto& fc = lv.coupling(e, f);
+      if (neighbor) neighbor[4 * e + f] = fc.neighbor;
+      if (neighbor_face) neighbor_face[4 * e + f] = fc.neighbor_face;
+      if (bc) bc[4 * e + f] = fc.neighbor >= 0 ? -1 : static_cast<int>(fc.bc);
+      if (node_map)
+        for (int gg = 0; gg < ng; ++gg)
+          node_map[(static_cast<size_t>(e) * 4 + f) * ng + gg] =
+              fc.neighbor >= 0 ? fc.node_map[gg] : -1;
+    }
+  }
+}
+
+// Per-element operators (operators.cpp:123-167), row-major:
+//  S [3][np][ncub], face_mass [np][nf], mass [np][np], mass_chol (column-major
+//  as stored by the reference), for one element e.
+void ref_level_operators(void* h, int e, double* s, double* face_mass, double* mass,
+                         double* mass_chol) {
+  const DgLevel& lv = *static_cast<RefLevel*>(h)->level;
+  const auto& ops = lv.ops(e);
+  const int np = ops.n_basis, ncub = ops.n_cub, nf = ops.n_face;
+  for (int m = 0; m < 3; ++m)
+    for (int i = 0; i < np; ++i)
+      for (int q = 0; q < ncub; ++q) s[(static_cast<size_t>(m) * np + i) * ncub + q] = ops.s[m](i, q);
+  for (int i = 0; i < np; ++i)
+    for (int q = 0; q < nf; ++q) face_mass[static_cast<size_t>(i) * nf + q] = ops.face_mass(i, q);
+  std::memcpy(mass, ops.mass.data(), sizeof(double) * ops.mass.size());
+  std::memcpy(mass_chol, ops.mass_chol.data(), sizeof(double) * ops.mass_chol.size());
+}
+
+// Raw store access: data arrays are the SolutionStore raw() layout
+// (e*5+c)*block + i, length K*5*block.
+static void load_store(SolutionStore& s, const double* in) {
+  std::memcpy(s.raw().data(), in, sizeof(double) * s.raw().size());
+}
+static void save_store(const SolutionStore& s, double* out) {
+  std::memcpy(out, s.raw().data(), sizeof(double) * s.raw().size());
+}
+
+// bench.cpp:22-40 recipe (mt19937(seed), +/-0.05 jitter), restated here
+// because the reference keeps it file-static.
+void ref_random_admissible_store(void* h, unsigned seed, double* out) {
+  const DgLevel& lv = *static_cast<RefLevel*>(h)->level;
+  std::mt19937 gen(seed);
+  std::uniform_real_distribution<double> jitter(-0.05, 0.05);
+  SolutionStore store = lv.make_store();
+  const int np = lv.refelem().n_basis();
+  for (int e = 0; e < lv.n_elements(); ++e)
+    for (int i = 0; i < np; ++i) {
+      const double rho = 1.0 + jitter(gen);
+      const Vec3 v{0.3 + jitter(gen), jitter(gen), jitter(gen)};
+      const double p = 1.0 + jitter(gen);
+      store.field(e, 0)[i] = rho;
+      store.field(e, 1)[i] = rho * v.x;
+      store.field(e, 2)[i] = rho * v.y;
+      store.field(e, 3)[i] = rho * v.z;
+      store.field(e, 4)[i] = p / 0.4 + 0.5 * rho * dot(v, v);
+    }
+  save_store(store, out);
+}
+
+int ref_compute_rhs(void* h, const ref_run_cfg* c, const double* freestream, const double* u_in,
+                    double* rhs_out, char* err, size_t errn) {
+  auto* lv = static_cast<RefLevel*>(h);
+  try {
+    SolutionStore u = lv->level->make_store();
+    load_store(u, u_in);
+    SolutionStore rhs = lv->level->make_store();
+    compute_rhs(*lv->level, u, to_cfg(c), to_state(freestream), rhs, *lv->ws);
+    save_store(rhs, rhs_out);
+    return 0;
+  } catch (const std::exception& e) {
+    copy_err(e, err, errn);
+    return status_of(e);
+  }
+}
+
+int ref_interpolate_to_faces(void* h, const double* u_in, double* traces_out) {
+  auto* lv = static_cast<RefLevel*>(h);
+  SolutionStore u = lv->level->make_store();
+  load_store(u, u_in);
+  SolutionStore t = lv->level->make_trace_store();
+  interpolate_to_faces(*lv->level, u, t);
+  save_store(t, traces_out);
+  return 0;
+}
+
+// nsteps x rk_step with the Carpenter-Kennedy scheme (rk.hpp:13-30).
+int ref_rk_steps(void* h, const ref_run_cfg* c, const double* freestream, double dt, int nsteps,
+                 double* u_io, double* res_io, char* err, size_t errn) {
+  auto* lv = static_cast<RefLevel*>(h);
+  try {
+    SolutionStore u = lv->level->make_store();
+    SolutionStore res = lv->level->make_store();
+    load_store(u, u_io);
+    load_store(res, res_io);
+    const RunConfig cfg = to_cfg(c);
+    const ConservedState fs = to_state(freestream);
+    const RKScheme scheme = RKScheme::low_storage_rk4();
+    for (int s = 0; s < nsteps; ++s) rk_step(*lv->level, u, res, cfg, fs, dt, scheme, *lv->ws);
+    save_store(u, u_io);
+    save_store(res, res_io);
+    return 0;
+  } catch (const std::exception& e) {
+    copy_err(e, err, errn);
+    return status_of(e);
+  }
+}
+
+// Viscosity + aux gradient of the last compute_rhs (solver.cpp:87-91).
+// q_out [3][K*5*block] (only filled when the last RHS was viscous).
+int ref_last_viscosity(void* h, double* eps_out, double* q_out) {
+  auto* lv = static_cast<RefLevel*>(h);
+  const auto& eps = current_viscosity(*lv->ws);
+  std::memcpy(eps_out, eps.data(), sizeof(double) * eps.size());
+  if (q_out) {
+    const SolutionStore& q0 = aux_gradient(*lv->ws, 0);
+    if (q0.n_elements() == 0) return 1;
+    const size_t n = q0.raw().size();
+    for (int m = 0; m < 3; ++m) save_store(aux_gradient(*lv->ws, m), q_out + m * n);
+  }
+  return 0;
+}
+
+int ref_compute_timestep(void* h, const ref_run_cfg* c, const double* u_in, const double* eps,
+                         double* dt_out, char* err, size_t errn) {
+  auto* lv = static_cast<RefLevel*>(h);
+  try {
+    SolutionStore u = lv->level->make_store();
+    load_store(u, u_in);
+    std::vector<double> ev;
+    if (eps) ev.assign(eps, eps + lv->level->n_elements());
+    *dt_out = compute_timestep(*lv->level, u, to_cfg(c), eps ? &ev : nullptr);
+    return 0;
+  } catch (const std::exception& e) {
+    copy_err(e, err, errn);
+    return status_of(e);
+  }
+}
+
+}  // extern "C"
