@@ -1,0 +1,193 @@
+/* cdg_gpu.h -- C ABI of the B200 (sm_100a) RKDG hot path.
+ *
+ * Drop-in boundary for the reference's solver kernels
+ * (/root/reference/proj/core/include/cdg/solver.hpp:83-109). Every entry point
+ * below replaces one reference interface; the C++ adapter a maintainer adds on
+ * the reference side is shown in INTEGRATION.md.
+ *
+ *   cdg_gpu_level_create / _destroy  <- cdg::DgLevel (solver.hpp:52-79) +
+ *                                       cdg::make_workspace (solver.hpp:84)
+ *   cdg_gpu_set_state / _get_state   <- SolutionStore raw() layout
+ *                                       (solution_store.hpp:16-77), flat copy
+ *   cdg_gpu_interpolate_to_faces     <- cdg::interpolate_to_faces (solver.hpp:87-88)
+ *   cdg_gpu_compute_rhs              <- cdg::compute_rhs (solver.hpp:94-96)
+ *   cdg_gpu_rk_steps                 <- cdg::rk_step (solver.hpp:107-109), N steps
+ *                                       device-resident
+ *   cdg_gpu_viscosity                <- cdg::current_viscosity (solver.hpp:100)
+ *   cdg_gpu_aux_gradient             <- cdg::aux_gradient (solver.hpp:103)
+ *   cdg_gpu_timestep                 <- cdg::compute_timestep (solver.hpp:114-116)
+ *   cdg_gpu_residual                 <- residual_norm (solver.cpp:572-590)
+ *
+ * Conventions
+ *  - Plain pointers and sizes only. All arrays are row-major, float64 / int32.
+ *  - Status codes mirror the reference exception types and the CLI exit codes
+ *    (curveddg_main.cpp:10-31): 0 ok, 2 ConfigError, 3 NumericsError; 4 is a
+ *    CUDA/runtime failure, 1 any other error. `err` (nullable) receives the
+ *    reference's message text, e.g. "inadmissible state in element E at
+ *    cubature node Q (rho=...)" (solver.cpp:377-379,425-426).
+ *  - A level owns all device buffers; u and res stay device-resident between
+ *    calls. Calls on one level are not re-entrant (the reference workspace is
+ *    likewise single-caller, solver.cpp:80).
+ *  - There is no CPU fallback: without a CUDA device every call fails with 4.
+ */
+#ifndef CDG_GPU_H
+#define CDG_GPU_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CDG_GPU_OK 0
+#define CDG_GPU_ERR_OTHER 1
+#define CDG_GPU_ERR_CONFIG 2
+#define CDG_GPU_ERR_NUMERICS 3
+#define CDG_GPU_ERR_CUDA 4
+
+/* Boundary kinds: cdg::BcKind (euler.hpp:65) in declaration order. */
+#define CDG_GPU_BC_SLIP_WALL 0
+#define CDG_GPU_BC_FARFIELD 1
+#define CDG_GPU_BC_SYMMETRY 2
+
+/* Riemann solvers: RunConfig::riemann "llf" / "hllc" (solver.cpp:17-21). */
+#define CDG_GPU_RIEMANN_LLF 0
+#define CDG_GPU_RIEMANN_HLLC 1
+
+/* The RunConfig fields the hot path reads (solver.hpp:18-36; viscosity.hpp:11-20). */
+typedef struct cdg_gpu_run_config {
+  int riemann;              /* CDG_GPU_RIEMANN_* */
+  double gamma;             /* GasModel::gamma */
+  int visc_enabled;         /* ViscosityModel::enabled */
+  double eps0, kappa, s0_offset;
+  int indicator_component;  /* conserved-variable index of the sensor */
+  int jacobian_weighted;    /* 1: physical-space (J-weighted) indicator */
+  double cfl;               /* RunConfig::cfl (timestep only) */
+} cdg_gpu_run_config;
+
+/* Everything the kernels need for one polynomial level (DgLevel). The caller
+ * keeps ownership of every pointer; level_create copies what it needs. */
+typedef struct cdg_gpu_level_desc {
+  int degree;        /* p (1..8) */
+  int n_basis;       /* N_p  = ReferenceElement::n_basis() */
+  int n_cub;         /* N_cub = n_cub() */
+  int n_face_quad;   /* N_g  = n_face_quad() (per face) */
+  int n_elements;    /* K owned elements; rows 0..K-1 of every [K] array */
+  int n_halo;        /* ghost elements K..K+n_halo-1 whose traces arrive by
+                        halo exchange (multi-GPU); 0 on one GPU */
+  int padded;        /* caller's SolutionStore layout: 1 = block pad16(N_p) */
+
+  /* Reference-element tables, row-major (refelem.hpp:56-75). */
+  const double *interp_cub;      /* [N_cub][N_p]  I_cub */
+  const double *interp_face;     /* [4N_g][N_p]   I_g (face-major) */
+  const double *deriv_r, *deriv_s, *deriv_t; /* [N_cub][N_p] D_m at cub nodes */
+  const double *cub_weights;     /* [N_cub] */
+  const double *face_weights;    /* [N_g]   2D rule, sums to 2 */
+  const double *vandermonde_inv; /* [N_p][N_p] (sensor, viscosity.cpp:18) */
+
+  /* Affine element geometry (ElementGeometry, operators.hpp:14-37, which is
+   * constant per element/face on straight tets). */
+  const double *metric;          /* [K][9]  cub_dr[q][m*3+i] = dr_m/dx_i */
+  const double *jac;             /* [K]     cub_jac (det dx/dr) */
+  const double *face_normal;     /* [K][4][3] outward unit normal per face */
+  const double *face_sjac;       /* [K][4]  face_sjac per face */
+  const double *h;               /* [K]     ElementGeometry::h() = 6V/A */
+
+  /* Face coupling (FaceCoupling, solver.hpp:44-49). neighbor indexes
+   * 0..K+n_halo-1, -1 on boundary faces. */
+  const int *neighbor;           /* [K][4] */
+  const int *neighbor_face;      /* [K][4] */
+  const int *bc;                 /* [K][4] CDG_GPU_BC_* on boundary faces */
+  const int *node_map;           /* [K][4][N_g] my g -> neighbour face node;
+                                    may be NULL when face_code is given */
+  const int *face_code;          /* [K][4] index into code_node_map, or NULL */
+  const int *code_node_map;      /* [n_codes][N_g] */
+  int n_codes;
+
+  double freestream[5];          /* farfield ghost state (euler.cpp:157-158) */
+} cdg_gpu_level_desc;
+
+typedef struct cdg_gpu_level cdg_gpu_level;
+
+/* Build device tables + workspace on `device`. Returns status. */
+int cdg_gpu_level_create(const cdg_gpu_level_desc *desc, int device, cdg_gpu_level **out,
+                         char *err, size_t errlen);
+void cdg_gpu_level_destroy(cdg_gpu_level *lv);
+
+/* Sizes: [0]=K [1]=N_p [2]=N_cub [3]=N_g [4]=caller block [5]=caller trace
+ * block [6]=device block [7]=n_halo. */
+void cdg_gpu_level_sizes(const cdg_gpu_level *lv, int *sizes);
+
+/* State transfer in the caller's SolutionStore raw() layout
+ * ((e*5+c)*block + i over the K owned elements). res may be NULL (zeroed on
+ * set, skipped on get). Host pointers may be pageable or pinned. */
+int cdg_gpu_set_state(cdg_gpu_level *lv, const double *u, const double *res);
+int cdg_gpu_get_state(cdg_gpu_level *lv, double *u, double *res);
+/* Same as set_state with DEVICE source pointers (caller layout). */
+int cdg_gpu_set_state_device(cdg_gpu_level *lv, const double *u, const double *res);
+/* Device pointers of the resident u / res / traces buffers (device layout,
+ * block = sizes[6]); lets a caller that already holds device memory skip the
+ * host round trip. */
+int cdg_gpu_device_buffers(cdg_gpu_level *lv, double **u, double **res, double **traces);
+
+/* traces = I_g u for the resident state; out: [K][5][pad16(4N_g) or 4N_g]. */
+int cdg_gpu_interpolate_to_faces(cdg_gpu_level *lv, double *traces_out);
+
+/* rhs = RHS(u) for the resident state (no update). rhs_out (host, caller
+ * layout) may be NULL to leave it on device. */
+int cdg_gpu_compute_rhs(cdg_gpu_level *lv, const cdg_gpu_run_config *cfg, double *rhs_out,
+                        char *err, size_t errlen);
+
+/* nsteps low-storage RK steps on the resident (u, res):
+ *   for stage i: res = a[i] res + dt RHS(u); u += b[i] res   (solver.cpp:469-492) */
+int cdg_gpu_rk_steps(cdg_gpu_level *lv, const cdg_gpu_run_config *cfg, int nsteps, double dt,
+                     const double a[5], const double b[5], char *err, size_t errlen);
+
+/* Per-element eps of the last viscous RHS (current_viscosity). eps_out [K]. */
+int cdg_gpu_viscosity(cdg_gpu_level *lv, double *eps_out);
+/* q_m of the last viscous RHS (aux_gradient), caller layout; m in 0..2. */
+int cdg_gpu_aux_gradient(cdg_gpu_level *lv, int m, double *q_out);
+
+/* CFL time step for the resident u (compute_timestep, solver.cpp:494-526);
+ * use_viscosity=1 applies the h^2/(eps (p+1)^4) limit with the last eps. */
+int cdg_gpu_timestep(cdg_gpu_level *lv, const cdg_gpu_run_config *cfg, int use_viscosity,
+                     double *dt_out, char *err, size_t errlen);
+
+/* Snapshot u into the level's `before` buffer; then residual_norm(u, before,
+ * dt, kind) with kind 0 = "inf", 1 = "l2" (solver.cpp:572-590). */
+int cdg_gpu_snapshot(cdg_gpu_level *lv);
+int cdg_gpu_residual(cdg_gpu_level *lv, int kind, double dt, double *out);
+
+/* ---- multi-GPU halo plumbing (one process per GPU) --------------------------
+ * send_idx: [n_send] trace rows (element*4+face) whose 5*N_g trace values are
+ * packed into a contiguous device send buffer; recv rows land in ghost
+ * elements K.. (element index, face). The transport (NCCL send/recv over
+ * NVLink) is driven by the caller on `stream`. */
+int cdg_gpu_halo_setup(cdg_gpu_level *lv, int n_send, const int *send_elem_face, int n_recv,
+                       const int *recv_elem_face, double **send_buf, double **recv_buf);
+int cdg_gpu_halo_pack(cdg_gpu_level *lv);
+int cdg_gpu_halo_unpack(cdg_gpu_level *lv);
+/* Runs one RK stage in split form for overlap: trace kernel, then (caller
+ * exchanges halos) then RHS+update. phase 0 = traces + pack, phase 1 =
+ * unpack + RHS + update for stage `stage`. */
+int cdg_gpu_rk_stage_phase(cdg_gpu_level *lv, const cdg_gpu_run_config *cfg, int stage, int phase,
+                           double dt, const double a[5], const double b[5], char *err,
+                           size_t errlen);
+
+/* CUDA stream (cudaStream_t) the level launches on. */
+void *cdg_gpu_stream(cdg_gpu_level *lv);
+/* Kernel launches issued by this level since creation (evidence counter). */
+long long cdg_gpu_launch_count(const cdg_gpu_level *lv);
+/* Device-time of the last rk_steps call split by kernel: [0]=trace kernel ms
+ * [1]=rhs kernel ms [2]=launches, measured with cudaEvents on the level's
+ * stream when profiling is enabled. */
+int cdg_gpu_set_profiling(cdg_gpu_level *lv, int enabled);
+int cdg_gpu_last_profile(cdg_gpu_level *lv, double *out3);
+
+const char *cdg_gpu_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CDG_GPU_H */

@@ -1,0 +1,67 @@
+"""In-tree build of the sm_100a extension (nvcc) and the oracle checkers.
+
+    python -m paper_1208_4772_b200.build          # libcdg_gpu.so (+ oracle when present)
+
+The product library is ``paper_1208_4772_b200/libcdg_gpu.so`` (C ABI,
+include/cdg_gpu.h). Compiled for sm_100a only; -lineinfo for ncu source maps.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+LIB = PKG / "libcdg_gpu.so"
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+              "-Xcompiler", "-fPIC", "-shared", "-ccbin", "/usr/bin/g++"]
+
+
+def _nvcc() -> str:
+    for c in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", shutil.which("nvcc")):
+        if c and Path(c).exists():
+            return c
+    raise FileNotFoundError("nvcc not found")
+
+
+def _stale(target: Path, sources) -> bool:
+    if not target.exists():
+        return True
+    t = target.stat().st_mtime
+    return any(s.stat().st_mtime > t for s in sources)
+
+
+def build_gpu(force: bool = False, verbose: bool = False) -> Path:
+    sources = sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "cdg_gpu.h"]
+    if force or _stale(LIB, sources):
+        cmd = [_nvcc(), *NVCC_FLAGS, "-I", str(ROOT / "include"), "-o", str(LIB), str(CSRC / "cdg_gpu.cu")]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+    return LIB
+
+
+def build_oracle(verbose: bool = False) -> None:
+    """oracle/: the C restatement always; oracle/_ref when /root/reference exists."""
+    env = dict(os.environ)
+    env.pop("CXX", None)
+    env.pop("CC", None)
+    subprocess.run(["make", "-s", "-C", str(ROOT / "oracle"), "-j8", "port"], check=True, env=env)
+    if Path("/root/reference/proj/core/src/solver.cpp").exists():
+        subprocess.run(["make", "-s", "-C", str(ROOT / "oracle"), "-j8", "ref"], check=True, env=env)
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    build_gpu(force="--force" in argv, verbose=True)
+    if "--no-oracle" not in argv:
+        build_oracle()
+    print(f"built {LIB}")
+
+
+if __name__ == "__main__":
+    main()

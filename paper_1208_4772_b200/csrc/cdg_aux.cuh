@@ -1,0 +1,307 @@
+// cdg_aux.cuh -- artificial-viscosity sensor, auxiliary gradient, time step,
+// residual and halo kernels (sm_100a).
+#pragma once
+
+#include "cdg_kernels.cuh"
+
+namespace cdg_gpu {
+
+// ---------------------------------------------------------------------------
+// Persson-Peraire modal-decay sensor + viscosity ramp, one warp per element
+// (compute_element_viscosities, solver.cpp:239-260; smoothness_indicator,
+// viscosity.cpp:11-34; viscosity_amount, viscosity.cpp:48-56).
+// ---------------------------------------------------------------------------
+struct SensorParams {
+  const double* u;
+  const double* vinv;  // [np][np]
+  double* eps;
+  double* sqrt_eps;
+  unsigned long long* maxeps;  // bit pattern of max eps (non-negative doubles)
+  int K, np, np_prev, bp, comp;
+  double eps0, kappa, s0;
+};
+
+__global__ void __launch_bounds__(256) k_sensor(SensorParams p) {
+  const int lane = threadIdx.x & 31;
+  const int e = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (e >= p.K) return;
+  const double* f = p.u + ((size_t)e * 5 + p.comp) * p.bp;
+  double total = 0.0, top = 0.0;
+  for (int j = lane; j < p.np; j += 32) {
+    double m = 0.0;
+    const double* row = p.vinv + (size_t)j * p.np;
+    for (int i = 0; i < p.np; ++i) m += __ldg(row + i) * f[i];
+    const double en = m * m;
+    total += en;
+    if (j >= p.np_prev) top += en;
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    total += __shfl_xor_sync(0xffffffffu, total, off);
+    top += __shfl_xor_sync(0xffffffffu, top, off);
+  }
+  if (lane == 0) {
+    const double sk_val = total <= 0.0 ? 0.0 : top / total;
+    double eps = 0.0;
+    if (sk_val > 0.0) {
+      const double sk = log10(sk_val);
+      if (sk < p.s0 - p.kappa)
+        eps = 0.0;
+      else if (sk > p.s0 + p.kappa)
+        eps = p.eps0;
+      else
+        eps = 0.5 * p.eps0 * (1.0 + sin(M_PI * (sk - p.s0) / (2.0 * p.kappa)));
+    }
+    p.eps[e] = eps;
+    p.sqrt_eps[e] = sqrt(eps);
+    atomicMax(p.maxeps, (unsigned long long)__double_as_longlong(eps));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Auxiliary gradient (compute_aux_gradient, solver.cpp:264-312), affine form:
+//   q_m = -se sum_k A_k (r_{k,m} U_cub) + LIFT (scale * 1/2 (se U- + snb U+) n_m)
+// Same chunked DMMA structure as k_rhs, one pass per direction m.
+// ---------------------------------------------------------------------------
+struct AuxParams {
+  const double* u;
+  double* q;  // [3][K*5][BP]
+  const double* traces;
+  const double* metric;
+  const double4* face;
+  const int2* conn;
+  const int* code_map;
+  const double* frag_icub;
+  const double* frag_aux;
+  const double* sqrt_eps;
+  int K, n_tiles;
+  GasParams gas;
+};
+
+template <class C>
+__global__ void __launch_bounds__(kThreads, 1) k_aux_q(AuxParams p) {
+  extern __shared__ __align__(16) double smem[];
+  double* sU = smem;
+  double* sC = sU + C::SMEM_U;
+  double* sG = sC + C::SMEM_C;
+  double* sMet = sG + C::SMEM_G;
+  double4* sFace = reinterpret_cast<double4*>(sMet + C::E * 9);
+  double* sSe = reinterpret_cast<double*>(sFace + C::E * 4);
+  int2* sConn = reinterpret_cast<int2*>(sSe + C::E);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const int n_rows = p.K * 5;
+  const size_t qstride = (size_t)p.K * 5 * C::BP;
+  const int t_begin = (warp * C::T2) / kWarps, t_end = ((warp + 1) * C::T2) / kWarps;
+
+  for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+    const int e0 = tile * C::E, row0 = e0 * 5;
+    constexpr int V = C::KP / 2;
+    for (int idx = tid; idx < C::R * V; idx += kThreads) {
+      const int r = idx / V, v = idx % V;
+      double2 x = make_double2(0.0, 0.0);
+      if (row0 + r < n_rows) x = *(reinterpret_cast<const double2*>(p.u + (size_t)(row0 + r) * C::BP) + v);
+      *reinterpret_cast<double2*>(sU + r * C::LDU + 2 * v) = x;
+    }
+    for (int idx = tid; idx < C::E * 9; idx += kThreads)
+      sMet[idx] = e0 + idx / 9 < p.K ? p.metric[(size_t)e0 * 9 + idx] : 0.0;
+    for (int idx = tid; idx < C::E * 4; idx += kThreads) {
+      const bool ok = e0 + idx / 4 < p.K;
+      sFace[idx] = ok ? p.face[(size_t)e0 * 4 + idx] : make_double4(0, 0, 1, 0);
+      sConn[idx] = ok ? p.conn[(size_t)e0 * 4 + idx] : make_int2(-1, pack_face(0, 0, 1, 0));
+    }
+    for (int idx = tid; idx < C::E; idx += kThreads) sSe[idx] = e0 + idx < p.K ? p.sqrt_eps[e0 + idx] : 0.0;
+    __syncthreads();
+
+    for (int m = 0; m < 3; ++m) {
+      double acc[C::MAXT2][4];
+#pragma unroll
+      for (int i = 0; i < C::MAXT2; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.0;
+      for (int ch = 0; ch < C::NCH; ++ch) {
+        const int q0 = ch * C::CH;
+        const int w = (C::NCUB8 - q0) < C::CH ? (C::NCUB8 - q0) : C::CH;
+        const int nt1 = w / 8, T1 = C::MT * nt1;
+        for (int t = warp; t < T1; t += kWarps) {
+          const int mt = t / nt1, nt = t % nt1;
+          double c1[4] = {0.0, 0.0, 0.0, 0.0};
+          const double* a_ptr = sU + (mt * 16 + g) * C::LDU + tq;
+          const double* b_ptr = p.frag_icub + ((size_t)(q0 / 8 + nt) * C::KS1) * 32 + lane;
+          for (int ks = 0; ks < C::KS1; ++ks)
+            dmma_k4(c1, a_ptr[ks * 4], a_ptr[8 * C::LDU + ks * 4], __ldg(b_ptr + ks * 32));
+          double* o = sC + (mt * 16 + g) * C::LDC + nt * 8 + 2 * tq;
+          *reinterpret_cast<double2*>(o) = make_double2(c1[0], c1[1]);
+          *reinterpret_cast<double2*>(o + 8 * C::LDC) = make_double2(c1[2], c1[3]);
+        }
+        __syncthreads();
+        // G_k = -se * r_{k,m} * U_cub  for every field
+        for (int idx = tid; idx < C::R * w; idx += kThreads) {
+          const int r = idx / w, ql = idx % w, e = r / 5;
+          const double uc = (q0 + ql < C::NCUB) ? sC[r * C::LDC + ql] : 0.0;
+          const double se = sSe[e];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) sG[r * C::LDG + k * w + ql] = -se * (sMet[e * 9 + k * 3 + m] * uc);
+        }
+        __syncthreads();
+        const int ks0 = (3 * q0) / 4, nks = (3 * w) / 4;
+#pragma unroll
+        for (int i = 0; i < C::MAXT2; ++i) {
+          const int t = t_begin + i;
+          if (t < t_end) {
+            const int mt = t / C::NT2, nt = t % C::NT2;
+            const double* a_ptr = sG + (mt * 16 + g) * C::LDG + tq;
+            const double* b_ptr = p.frag_aux + ((size_t)nt * C::KS2 + ks0) * 32 + lane;
+            for (int ks = 0; ks < nks; ++ks)
+              dmma_k4(acc[i], a_ptr[ks * 4], a_ptr[8 * C::LDG + ks * 4], __ldg(b_ptr + ks * 32));
+          }
+        }
+        __syncthreads();
+      }
+      for (int fc = 0; fc < C::NFCH; ++fc) {
+        const int f0 = fc * C::FCH;
+        const int w = (C::NF - f0) < C::FCH ? (C::NF - f0) : C::FCH;
+        for (int idx = tid; idx < C::E * w; idx += kThreads) {
+          const int e = idx / w, fl = idx % w, fq = f0 + fl;
+          const int f = fq / C::NG, gq = fq - f * C::NG;
+          const int eg = e0 + e;
+          double* gout = sG + (e * 5) * C::LDG + fl;
+          if (eg >= p.K) {
+            for (int c = 0; c < 5; ++c) gout[c * C::LDG] = 0.0;
+            continue;
+          }
+          const double* tm = p.traces + (size_t)eg * 5 * C::TB + fq;
+          const State5 um{tm[0], tm[C::TB], tm[2 * C::TB], tm[3 * C::TB], tm[4 * C::TB]};
+          const double4 fn = sFace[e * 4 + f];
+          const int2 cw = sConn[e * 4 + f];
+          const double se = sSe[e];
+          State5 up;
+          double snb;
+          if (cw.x >= 0) {
+            const int h = __ldg(p.code_map + (cw.y >> 8) * C::NG + gq);
+            const double* tp = p.traces + (size_t)cw.x * 5 * C::TB + (cw.y & 3) * C::NG + h;
+            up = State5{tp[0], tp[C::TB], tp[2 * C::TB], tp[3 * C::TB], tp[4 * C::TB]};
+            snb = p.sqrt_eps[cw.x];
+          } else {
+            up = boundary_state(um, fn.x, fn.y, fn.z, (cw.y >> 2) & 3, p.gas);
+            snb = se;
+          }
+          const double nm = m == 0 ? fn.x : (m == 1 ? fn.y : fn.z);
+          const double umv[5] = {um.r, um.mx, um.my, um.mz, um.E};
+          const double upv[5] = {up.r, up.mx, up.my, up.mz, up.E};
+          for (int c = 0; c < 5; ++c) gout[c * C::LDG] = fn.w * (0.5 * (se * umv[c] + snb * upv[c]) * nm);
+        }
+        __syncthreads();
+        const int ks0 = (C::K2CUB + f0) / 4, nks = w / 4;
+#pragma unroll
+        for (int i = 0; i < C::MAXT2; ++i) {
+          const int t = t_begin + i;
+          if (t < t_end) {
+            const int mt = t / C::NT2, nt = t % C::NT2;
+            const double* a_ptr = sG + (mt * 16 + g) * C::LDG + tq;
+            const double* b_ptr = p.frag_aux + ((size_t)nt * C::KS2 + ks0) * 32 + lane;
+            for (int ks = 0; ks < nks; ++ks)
+              dmma_k4(acc[i], a_ptr[ks * 4], a_ptr[8 * C::LDG + ks * 4], __ldg(b_ptr + ks * 32));
+          }
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int i = 0; i < C::MAXT2; ++i) {
+        const int t = t_begin + i;
+        if (t < t_end) {
+          const int mt = t / C::NT2, nt = t % C::NT2;
+          for (int hh = 0; hh < 2; ++hh) {
+            const int grow = row0 + mt * 16 + g + 8 * hh;
+            if (grow >= n_rows) continue;
+            for (int v = 0; v < 2; ++v) {
+              const int col = nt * 8 + 2 * tq + v;
+              if (col < C::NP) p.q[m * qstride + (size_t)grow * C::BP + col] = acc[i][2 * hh + v];
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CFL time step (compute_timestep, solver.cpp:494-526): min over elements.
+// ---------------------------------------------------------------------------
+struct TimestepParams {
+  const double* u;
+  const double* h;
+  const double* eps;
+  int K, np, bp;
+  double gamma, pfac;
+  unsigned long long* out;
+  DevError* err;
+};
+
+__global__ void k_timestep(TimestepParams p) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= p.K) return;
+  const double* f = p.u + (size_t)e * 5 * p.bp;
+  double lambda = 0.0;
+  for (int i = 0; i < p.np; ++i) {
+    const State5 s{f[i], f[p.bp + i], f[2 * p.bp + i], f[3 * p.bp + i], f[4 * p.bp + i]};
+    if (!admissible(s, p.gamma)) {
+      record_error(p.err, 3, e, i, 0, s.r);
+      return;
+    }
+    const double pres = pressure(s, p.gamma);
+    const double c = sqrt(p.gamma * pres / s.r);
+    lambda = fmax(lambda, sqrt(s.mx * s.mx + s.my * s.my + s.mz * s.mz) / s.r + c);
+  }
+  const double h = p.h[e];
+  if (h <= 0.0 || lambda <= 0.0) {
+    record_error(p.err, 4, e, 0, 0, 0.0);
+    return;
+  }
+  double dte = h / (lambda * p.pfac);
+  if (p.eps && p.eps[e] > 0.0) dte = fmin(dte, h * h / (p.eps[e] * p.pfac * p.pfac));
+  atomicMin(p.out, (unsigned long long)__double_as_longlong(dte));
+}
+
+// ---------------------------------------------------------------------------
+// Residual partials (residual_norm, solver.cpp:572-590): per-block max|d| or
+// sum d^2 in a fixed order (deterministic run to run).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_residual(const double* __restrict__ a, const double* __restrict__ b,
+                                                  size_t n, int kind, double* partial) {
+  __shared__ double red[256];
+  double acc = 0.0;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const double d = a[i] - b[i];
+    acc = kind == 1 ? acc + d * d : fmax(acc, fabs(d));
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = 128; s; s >>= 1) {
+    if (threadIdx.x < s)
+      red[threadIdx.x] = kind == 1 ? red[threadIdx.x] + red[threadIdx.x + s]
+                                   : fmax(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
+// ---------------------------------------------------------------------------
+// Halo face traces: dir 0 packs traces[(elem, face)] -> buf, dir 1 unpacks.
+// idx[i] = elem*4 + face; buf[i][5][ng].
+// ---------------------------------------------------------------------------
+__global__ void k_halo_copy(double* traces, double* buf, const int* idx, int n, int ng, int tb, int dir) {
+  const int item = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (item >= n) return;
+  const int ef = idx[item], elem = ef >> 2, face = ef & 3;
+  for (int k = threadIdx.x & 31; k < 5 * ng; k += 32) {
+    const int c = k / ng, gq = k % ng;
+    double* t = traces + ((size_t)elem * 5 + c) * tb + face * ng + gq;
+    double* s = buf + ((size_t)item * 5 + c) * ng + gq;
+    if (dir == 0)
+      *s = *t;
+    else
+      *t = *s;
+  }
+}
+
+}  // namespace cdg_gpu

@@ -1,0 +1,924 @@
+// cdg_gpu.cu -- host side of the C ABI (include/cdg_gpu.h) and the level's
+// device resources. Kernels live in cdg_kernels.cuh / cdg_aux.cuh.
+//
+// Reference interfaces replaced: see include/cdg_gpu.h. Host-side operator
+// preparation restates operators.cpp:123-167 (mass matrix, stiffness and face
+// mass) in the factored, element-independent form the GPU kernels consume.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "cdg_aux.cuh"
+#include "cdg_gpu.h"
+#include "cdg_kernels.cuh"
+
+using namespace cdg_gpu;
+
+namespace {
+
+struct Status : std::runtime_error {
+  int code;
+  Status(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CUDA_OK(x)                                                                       \
+  do {                                                                                   \
+    cudaError_t e_ = (x);                                                                \
+    if (e_ != cudaSuccess)                                                               \
+      throw Status(CDG_GPU_ERR_CUDA, std::string("CUDA error: ") + cudaGetErrorString(e_) + \
+                                         " at " #x);                                     \
+  } while (0)
+
+void set_err(char* err, size_t n, const std::string& msg) {
+  if (err && n) {
+    std::strncpy(err, msg.c_str(), n - 1);
+    err[n - 1] = 0;
+  }
+}
+
+int pad16(int n) { return 16 * ((n + 15) / 16); }
+
+// ---- kernel dispatch per (N_p, N_cub, N_g) ---------------------------------
+struct KernelSet {
+  int np, ncub, ng, E;
+  size_t smem_traces, smem_rhs;
+  void (*traces)(const double*, double*, const double*, int, int);
+  void (*rhs_update)(RhsParams);
+  void (*rhs_only)(RhsParams);
+  void (*aux_q)(AuxParams);
+  void (*visc_rhs_update)(RhsParams);
+  void (*visc_rhs_only)(RhsParams);
+};
+
+template <int NP, int NCUB, int NG, int E>
+KernelSet make_set() {
+  using C = Cfg<NP, NCUB, NG, E>;
+  KernelSet k;
+  k.np = NP;
+  k.ncub = NCUB;
+  k.ng = NG;
+  k.E = E;
+  k.smem_traces = sizeof(double) * C::R * C::LDU;
+  k.smem_rhs = C::SMEM_BYTES;
+  k.traces = &k_traces<C>;
+  k.rhs_update = &k_rhs<C, true, false>;
+  k.rhs_only = &k_rhs<C, false, false>;
+  k.aux_q = &k_aux_q<C>;
+  k.visc_rhs_update = &k_rhs<C, true, true>;
+  k.visc_rhs_only = &k_rhs<C, false, true>;
+  return k;
+}
+
+const std::vector<KernelSet>& kernel_sets() {
+  static const std::vector<KernelSet> sets = {
+      // straight-sided strengths (2p+1 / 2p): refelem.cpp:311-317
+      make_set<4, 5, 3, 32>(), make_set<10, 15, 6, 32>(), make_set<20, 35, 12, 32>(),
+      make_set<35, 70, 16, 32>(), make_set<56, 126, 56, 32>(), make_set<84, 210, 84, 16>(),
+      make_set<120, 330, 120, 16>(), make_set<165, 495, 165, 16>(),
+      // curved-mesh strengths (3p-3 / 3p-2): refelem.hpp:118-119
+      make_set<20, 35, 16, 32>(), make_set<35, 70, 56, 32>(), make_set<56, 210, 84, 32>(),
+      make_set<84, 330, 165, 16>(), make_set<120, 715, 220, 16>(),
+      make_set<165, 1001, 364, 16>()};
+  return sets;
+}
+
+const KernelSet* find_set(int np, int ncub, int ng) {
+  for (const auto& k : kernel_sets())
+    if (k.np == np && k.ncub == ncub && k.ng == ng) return &k;
+  return nullptr;
+}
+
+// ---- small dense host linear algebra (setup only) --------------------------
+// Inverse of an SPD matrix via Cholesky (the reference factors M per element,
+// operators.cpp:151-158; here the reference mass matrix is inverted once).
+std::vector<double> spd_inverse(const std::vector<double>& m, int n) {
+  std::vector<double> l(n * n, 0.0);
+  for (int j = 0; j < n; ++j) {
+    double d = m[j * n + j];
+    for (int k = 0; k < j; ++k) d -= l[j * n + k] * l[j * n + k];
+    if (!(d > 0.0)) throw Status(CDG_GPU_ERR_NUMERICS, "build_operators: mass matrix factorization failed");
+    const double ljj = std::sqrt(d);
+    l[j * n + j] = ljj;
+    for (int i = j + 1; i < n; ++i) {
+      double s = m[i * n + j];
+      for (int k = 0; k < j; ++k) s -= l[i * n + k] * l[j * n + k];
+      l[i * n + j] = s / ljj;
+    }
+  }
+  std::vector<double> inv(n * n, 0.0), y(n), x(n);
+  for (int col = 0; col < n; ++col) {
+    for (int i = 0; i < n; ++i) {
+      double s = (i == col) ? 1.0 : 0.0;
+      for (int k = 0; k < i; ++k) s -= l[i * n + k] * y[k];
+      y[i] = s / l[i * n + i];
+    }
+    for (int i = n - 1; i >= 0; --i) {
+      double s = y[i];
+      for (int k = i + 1; k < n; ++k) s -= l[k * n + i] * x[k];
+      x[i] = s / l[i * n + i];
+    }
+    for (int i = 0; i < n; ++i) inv[i * n + col] = x[i];
+  }
+  return inv;
+}
+
+// B-operand fragments for mma.m16n8k4 (.col): frag[nt][ks][lane] =
+// op[nt*8 + lane/4][ks*4 + lane%4], zero outside [rows x cols].
+std::vector<double> make_frag(const std::vector<double>& op, int rows, int cols, int rows8,
+                              int cols4) {
+  std::vector<double> f((size_t)rows8 / 8 * (cols4 / 4) * 32, 0.0);
+  for (int nt = 0; nt < rows8 / 8; ++nt)
+    for (int ks = 0; ks < cols4 / 4; ++ks)
+      for (int lane = 0; lane < 32; ++lane) {
+        const int r = nt * 8 + lane / 4, c = ks * 4 + lane % 4;
+        if (r < rows && c < cols)
+          f[((size_t)nt * (cols4 / 4) + ks) * 32 + lane] = op[(size_t)r * cols + c];
+      }
+  return f;
+}
+
+template <typename T>
+T* dev_upload(const std::vector<T>& h) {
+  T* d = nullptr;
+  if (h.empty()) return nullptr;
+  CUDA_OK(cudaMalloc(&d, h.size() * sizeof(T)));
+  CUDA_OK(cudaMemcpy(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return d;
+}
+
+}  // namespace
+
+struct cdg_gpu_level {
+  int device = 0;
+  int K = 0, n_halo = 0, np = 0, ncub = 0, ng = 0, nf = 0, degree = 0;
+  int caller_block = 0, caller_tblock = 0, bp = 0, tb = 0;
+  bool caller_padded = true;
+  const KernelSet* ks = nullptr;
+  cudaStream_t stream = nullptr;
+  int n_sms = 148;
+  long long launches = 0;
+  // state
+  double *u = nullptr, *res = nullptr, *rhs = nullptr, *traces = nullptr, *before = nullptr;
+  // viscous workspace
+  double *q = nullptr, *qtr = nullptr, *eps = nullptr, *sqrt_eps = nullptr;
+  double* d_vinv = nullptr;
+  double* d_icub = nullptr;  // row-major I_cub (viscous volume term)
+  unsigned long long* d_maxeps = nullptr;
+  bool last_viscous = false;
+  // geometry / coupling
+  double* metric = nullptr;
+  double4* face = nullptr;
+  int2* conn = nullptr;
+  int* code_map = nullptr;
+  double* h = nullptr;
+  // operators
+  double *frag_icub = nullptr, *frag_op2 = nullptr, *frag_ig = nullptr, *frag_aux = nullptr;
+  // control
+  StageCoef* d_coef = nullptr;
+  StageCoef* h_coef = nullptr;  // pinned
+  DevError* d_err = nullptr;
+  DevError* h_err = nullptr;  // pinned
+  GasParams gas{};
+  double* d_scratch = nullptr;  // reductions
+  std::vector<double> h_scratch;
+  int scratch_n = 0;
+  // graph cache for rk_steps
+  cudaGraphExec_t graph = nullptr;
+  int graph_riemann = -1;
+  double graph_gamma = 0.0;
+  // profiling
+  bool profiling = false;
+  double prof[3] = {0, 0, 0};
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  // halo
+  int n_send = 0, n_recv = 0;
+  int *d_send_idx = nullptr, *d_recv_idx = nullptr;
+  double *send_buf = nullptr, *recv_buf = nullptr;
+  double freestream[5] = {0, 0, 0, 0, 0};
+
+  int n_rows() const { return K * 5; }
+  int n_tiles() const { return (K + ks->E - 1) / ks->E; }
+  int grid(int tiles) const { return std::max(1, std::min(tiles, n_sms)); }
+};
+
+namespace {
+
+void check_device_error(cdg_gpu_level* lv) {
+  CUDA_OK(cudaMemcpyAsync(lv->h_err, lv->d_err, sizeof(DevError), cudaMemcpyDeviceToHost,
+                          lv->stream));
+  CUDA_OK(cudaStreamSynchronize(lv->stream));
+  if (lv->h_err->flag) {
+    const DevError e = *lv->h_err;
+    CUDA_OK(cudaMemsetAsync(lv->d_err, 0, sizeof(DevError), lv->stream));
+    CUDA_OK(cudaStreamSynchronize(lv->stream));
+    char buf[256];
+    if (e.kind == 1)
+      std::snprintf(buf, sizeof buf, "inadmissible state in element %d at cubature node %d (rho=%f)",
+                    e.elem, e.a, e.value);
+    else if (e.kind == 2)
+      std::snprintf(buf, sizeof buf, "inadmissible trace state in element %d face %d node %d",
+                    e.elem, e.a, e.b);
+    else if (e.kind == 3)
+      std::snprintf(buf, sizeof buf, "inadmissible state in compute_timestep: rho=%f", e.value);
+    else
+      std::snprintf(buf, sizeof buf, "compute_timestep: degenerate h or wavespeed in element %d",
+                    e.elem);
+    throw Status(CDG_GPU_ERR_NUMERICS, buf);
+  }
+}
+
+void launch_traces(cdg_gpu_level* lv, const double* u, double* traces) {
+  const int tiles = lv->n_tiles();
+  lv->ks->traces<<<lv->grid(tiles), kThreads, lv->ks->smem_traces, lv->stream>>>(
+      u, traces, lv->frag_ig, lv->n_rows(), tiles);
+  ++lv->launches;
+}
+
+RhsParams rhs_params(cdg_gpu_level* lv, int stage) {
+  RhsParams p{};
+  p.u = lv->u;
+  p.res = lv->res;
+  p.rhs_out = lv->rhs;
+  p.traces = lv->traces;
+  p.metric = lv->metric;
+  p.face = lv->face;
+  p.conn = lv->conn;
+  p.code_map = lv->code_map;
+  p.frag_icub = lv->frag_icub;
+  p.frag_op2 = lv->frag_op2;
+  p.coef = lv->d_coef;
+  p.stage = stage;
+  p.K = lv->K;
+  p.n_tiles = lv->n_tiles();
+  p.elem_offset = 0;
+  p.gas = lv->gas;
+  p.err = lv->d_err;
+  p.q = lv->q;
+  p.qtr = lv->qtr;
+  p.sqrt_eps = lv->sqrt_eps;
+  p.icub = lv->d_icub;
+  p.qtr_stride = (size_t)(lv->K + lv->n_halo) * 5 * lv->tb;
+  return p;
+}
+
+void launch_rhs(cdg_gpu_level* lv, bool update, bool viscous, int stage) {
+  RhsParams p = rhs_params(lv, stage);
+  const int tiles = lv->n_tiles();
+  auto fn = viscous ? (update ? lv->ks->visc_rhs_update : lv->ks->visc_rhs_only)
+                    : (update ? lv->ks->rhs_update : lv->ks->rhs_only);
+  fn<<<lv->grid(tiles), kThreads, lv->ks->smem_rhs, lv->stream>>>(p);
+  ++lv->launches;
+}
+
+// Viscosity phase: sensor -> eps, then (if any eps > 0) aux gradient q and its
+// traces (solver.cpp:239-321). Returns whether the viscous path is active.
+bool viscosity_phase(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg) {
+  if (!cfg->visc_enabled) return false;
+  if (cfg->eps0 < 0.0) throw Status(CDG_GPU_ERR_CONFIG, "viscosity_amount: eps0 must be >= 0");
+  if (cfg->jacobian_weighted)
+    throw Status(CDG_GPU_ERR_CONFIG, "jacobian_weighted indicator is not supported on the GPU path");
+  if (!lv->q) {
+    const size_t n = (size_t)lv->K * 5 * lv->bp;
+    const size_t nt = (size_t)(lv->K + lv->n_halo) * 5 * lv->tb;
+    CUDA_OK(cudaMalloc(&lv->q, 3 * n * sizeof(double)));
+    CUDA_OK(cudaMemset(lv->q, 0, 3 * n * sizeof(double)));
+    CUDA_OK(cudaMalloc(&lv->qtr, 3 * nt * sizeof(double)));
+    CUDA_OK(cudaMemset(lv->qtr, 0, 3 * nt * sizeof(double)));
+  }
+  CUDA_OK(cudaMemsetAsync(lv->d_maxeps, 0, sizeof(unsigned long long), lv->stream));
+  SensorParams sp{};
+  sp.u = lv->u;
+  sp.vinv = lv->d_vinv;
+  sp.eps = lv->eps;
+  sp.sqrt_eps = lv->sqrt_eps;
+  sp.maxeps = lv->d_maxeps;
+  sp.K = lv->K;
+  sp.np = lv->np;
+  sp.np_prev = lv->degree >= 1 ? (lv->degree) * (lv->degree + 1) * (lv->degree + 2) / 6 : 0;
+  sp.bp = lv->bp;
+  sp.comp = cfg->indicator_component;
+  sp.eps0 = cfg->eps0;
+  sp.kappa = cfg->kappa;
+  sp.s0 = std::log10(1.0 / std::pow((double)lv->degree, 4)) + cfg->s0_offset;
+  k_sensor<<<(lv->K + 7) / 8, 256, 0, lv->stream>>>(sp);
+  ++lv->launches;
+  unsigned long long bits = 0;
+  CUDA_OK(cudaMemcpyAsync(&bits, lv->d_maxeps, sizeof bits, cudaMemcpyDeviceToHost, lv->stream));
+  CUDA_OK(cudaStreamSynchronize(lv->stream));
+  double maxeps;
+  std::memcpy(&maxeps, &bits, sizeof maxeps);
+  if (!(maxeps > 0.0)) return false;
+  // aux gradient q_m (needs the U traces of all elements first)
+  launch_traces(lv, lv->u, lv->traces);
+  AuxParams ap{};
+  ap.u = lv->u;
+  ap.q = lv->q;
+  ap.traces = lv->traces;
+  ap.metric = lv->metric;
+  ap.face = lv->face;
+  ap.conn = lv->conn;
+  ap.code_map = lv->code_map;
+  ap.frag_icub = lv->frag_icub;
+  ap.frag_aux = lv->frag_aux;
+  ap.sqrt_eps = lv->sqrt_eps;
+  ap.K = lv->K;
+  ap.n_tiles = lv->n_tiles();
+  ap.gas = lv->gas;
+  lv->ks->aux_q<<<lv->grid(lv->n_tiles()), kThreads, lv->ks->smem_rhs, lv->stream>>>(ap);
+  ++lv->launches;
+  // q traces: 3 x (K*5 rows)
+  const size_t n = (size_t)lv->K * 5 * lv->bp;
+  const size_t nt = (size_t)(lv->K + lv->n_halo) * 5 * lv->tb;
+  for (int m = 0; m < 3; ++m) launch_traces(lv, lv->q + m * n, lv->qtr + m * nt);
+  return true;
+}
+
+}  // namespace
+
+namespace {
+int guarded(char* err, size_t errlen, const std::function<void()>& fn) {
+  try {
+    fn();
+    return CDG_GPU_OK;
+  } catch (const Status& s) {
+    set_err(err, errlen, s.what());
+    return s.code;
+  } catch (const std::exception& e) {
+    set_err(err, errlen, e.what());
+    return CDG_GPU_ERR_OTHER;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+const char* cdg_gpu_version(void) { return "cdg_gpu 0.1 (sm_100a, fp64 DMMA)"; }
+
+int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level** out, char* err,
+                         size_t errlen) {
+  *out = nullptr;
+  auto* lv = new cdg_gpu_level;
+  const int st = guarded(err, errlen, [&] {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      throw Status(CDG_GPU_ERR_CUDA, "no CUDA device available (the GPU path has no CPU fallback)");
+    if (device < 0 || device >= ndev) throw Status(CDG_GPU_ERR_CONFIG, "bad device index");
+    CUDA_OK(cudaSetDevice(device));
+    lv->device = device;
+    cudaDeviceProp prop{};
+    CUDA_OK(cudaGetDeviceProperties(&prop, device));
+    lv->n_sms = prop.multiProcessorCount;
+    if (d->degree < 1 || d->degree > 8) throw Status(CDG_GPU_ERR_CONFIG, "degree must be 1..8");
+    lv->degree = d->degree;
+    lv->np = d->n_basis;
+    lv->ncub = d->n_cub;
+    lv->ng = d->n_face_quad;
+    lv->nf = 4 * d->n_face_quad;
+    lv->K = d->n_elements;
+    lv->n_halo = d->n_halo;
+    if (lv->K < 1) throw Status(CDG_GPU_ERR_CONFIG, "level has no elements");
+    lv->ks = find_set(lv->np, lv->ncub, lv->ng);
+    if (!lv->ks)
+      throw Status(CDG_GPU_ERR_CONFIG, "no kernel instantiation for (N_p, N_cub, N_g) = (" +
+                                           std::to_string(lv->np) + ", " + std::to_string(lv->ncub) +
+                                           ", " + std::to_string(lv->ng) + ")");
+    lv->caller_padded = d->padded != 0;
+    lv->caller_block = lv->caller_padded ? pad16(lv->np) : lv->np;
+    lv->caller_tblock = lv->caller_padded ? pad16(lv->nf) : lv->nf;
+    lv->bp = pad16(lv->np);
+    lv->tb = pad16(lv->nf);
+    const int np = lv->np, ncub = lv->ncub, nf = lv->nf, ng = lv->ng, K = lv->K;
+
+    // ---- shared operators (operators.cpp:135-165, factored) ---------------
+    std::vector<double> icub(d->interp_cub, d->interp_cub + (size_t)ncub * np);
+    std::vector<double> ig(d->interp_face, d->interp_face + (size_t)nf * np);
+    const double* dm[3] = {d->deriv_r, d->deriv_s, d->deriv_t};
+    std::vector<double> mref((size_t)np * np, 0.0);
+    for (int i = 0; i < np; ++i)
+      for (int j = 0; j < np; ++j) {
+        double s = 0.0;
+        for (int q = 0; q < ncub; ++q) s += icub[(size_t)q * np + i] * d->cub_weights[q] * icub[(size_t)q * np + j];
+        mref[(size_t)i * np + j] = s;
+      }
+    const std::vector<double> minv = spd_inverse(mref, np);
+    // A_m = M^-1 D_m^T diag(W)  [np][ncub];   LIFT = M^-1 I_g^T diag(w)  [np][nf]
+    std::vector<double> amat[3];
+    for (int m = 0; m < 3; ++m) {
+      amat[m].assign((size_t)np * ncub, 0.0);
+      for (int i = 0; i < np; ++i)
+        for (int q = 0; q < ncub; ++q) {
+          double s = 0.0;
+          for (int j = 0; j < np; ++j) s += minv[(size_t)i * np + j] * dm[m][(size_t)q * np + j];
+          amat[m][(size_t)i * ncub + q] = s * d->cub_weights[q];
+        }
+    }
+    std::vector<double> lift((size_t)np * nf, 0.0);
+    for (int i = 0; i < np; ++i)
+      for (int fq = 0; fq < nf; ++fq) {
+        double s = 0.0;
+        for (int j = 0; j < np; ++j) s += minv[(size_t)i * np + j] * ig[(size_t)fq * np + j];
+        lift[(size_t)i * nf + fq] = s * d->face_weights[fq % ng];
+      }
+    const int kp = (np + 3) / 4 * 4, ncub8 = (ncub + 7) / 8 * 8, np8 = (np + 7) / 8 * 8,
+              nf8 = (nf + 7) / 8 * 8;
+    const int k2cub = 3 * ncub8, k2 = k2cub + nf;
+    // RHS operator rows i: [chunked (m, q) volume block | -LIFT]
+    std::vector<double> op2((size_t)np * k2, 0.0);
+    // aux operator (viscous gradient): same volume block, +LIFT (solver.cpp:283-309)
+    std::vector<double> opaux((size_t)np * k2, 0.0);
+    for (int q0 = 0; q0 < ncub8; q0 += 16) {
+      const int w = std::min(16, ncub8 - q0);
+      for (int m = 0; m < 3; ++m)
+        for (int ql = 0; ql < w; ++ql) {
+          const int q = q0 + ql;
+          if (q >= ncub) continue;
+          for (int i = 0; i < np; ++i) {
+            op2[(size_t)i * k2 + 3 * q0 + m * w + ql] = amat[m][(size_t)i * ncub + q];
+            opaux[(size_t)i * k2 + 3 * q0 + m * w + ql] = amat[m][(size_t)i * ncub + q];
+          }
+        }
+    }
+    for (int i = 0; i < np; ++i)
+      for (int fq = 0; fq < nf; ++fq) {
+        op2[(size_t)i * k2 + k2cub + fq] = -lift[(size_t)i * nf + fq];
+        opaux[(size_t)i * k2 + k2cub + fq] = lift[(size_t)i * nf + fq];
+      }
+    lv->frag_icub = dev_upload(make_frag(icub, ncub, np, ncub8, kp));
+    lv->d_icub = dev_upload(icub);
+    lv->frag_ig = dev_upload(make_frag(ig, nf, np, nf8, kp));
+    lv->frag_op2 = dev_upload(make_frag(op2, np, k2, np8, k2));
+    lv->frag_aux = dev_upload(make_frag(opaux, np, k2, np8, k2));
+    if (d->vandermonde_inv)
+      lv->d_vinv = dev_upload(std::vector<double>(d->vandermonde_inv, d->vandermonde_inv + (size_t)np * np));
+
+    // ---- per-element geometry + coupling -----------------------------------
+    std::vector<double> met(d->metric, d->metric + (size_t)K * 9);
+    std::vector<double4> face((size_t)K * 4);
+    std::vector<int2> conn((size_t)K * 4);
+    std::vector<int> codes;  // [n_codes][ng]
+    std::map<std::vector<int>, int> code_of;
+    if (d->face_code) {
+      if (!d->code_node_map || d->n_codes < 1) throw Status(CDG_GPU_ERR_CONFIG, "face_code needs code_node_map");
+      codes.assign(d->code_node_map, d->code_node_map + (size_t)d->n_codes * ng);
+    } else if (!d->node_map) {
+      throw Status(CDG_GPU_ERR_CONFIG, "level descriptor needs node_map or face_code");
+    }
+    for (int e = 0; e < K; ++e) {
+      const double jac = d->jac[e];
+      if (!(jac > 1e-14))
+        throw Status(CDG_GPU_ERR_NUMERICS, "inverted element " + std::to_string(e) + ": mapping Jacobian " +
+                                               std::to_string(jac) + " at quadrature node 0");
+      for (int f = 0; f < 4; ++f) {
+        const size_t i4 = (size_t)e * 4 + f;
+        face[i4] = make_double4(d->face_normal[i4 * 3 + 0], d->face_normal[i4 * 3 + 1],
+                                d->face_normal[i4 * 3 + 2], d->face_sjac[i4] / jac);
+        const int nb = d->neighbor[i4];
+        if (nb >= 0) {
+          if (nb >= K + lv->n_halo) throw Status(CDG_GPU_ERR_CONFIG, "neighbor index out of range");
+          int code = 0;
+          if (d->face_code) {
+            code = d->face_code[i4];
+          } else {
+            std::vector<int> row(d->node_map + i4 * ng, d->node_map + (i4 + 1) * ng);
+            auto it = code_of.find(row);
+            if (it == code_of.end()) {
+              code = (int)code_of.size();
+              code_of.emplace(row, code);
+              codes.insert(codes.end(), row.begin(), row.end());
+            } else {
+              code = it->second;
+            }
+          }
+          conn[i4] = make_int2(nb, pack_face(d->neighbor_face[i4], 0, 0, code));
+        } else {
+          const int bc = d->bc[i4];
+          if (bc < 0 || bc > 2) throw Status(CDG_GPU_ERR_CONFIG, "boundary_state: unknown kind");
+          conn[i4] = make_int2(-1, pack_face(0, bc, 1, 0));
+        }
+      }
+    }
+    if (codes.empty()) codes.assign(ng, 0);
+    lv->metric = dev_upload(met);
+    lv->face = dev_upload(face);
+    lv->conn = dev_upload(conn);
+    lv->code_map = dev_upload(codes);
+    if (d->h) lv->h = dev_upload(std::vector<double>(d->h, d->h + K));
+
+    // ---- state + workspace -------------------------------------------------
+    const size_t n = (size_t)K * 5 * lv->bp;
+    const size_t ntr = (size_t)(K + lv->n_halo) * 5 * lv->tb;
+    CUDA_OK(cudaMalloc(&lv->u, n * sizeof(double)));
+    CUDA_OK(cudaMalloc(&lv->res, n * sizeof(double)));
+    CUDA_OK(cudaMalloc(&lv->rhs, n * sizeof(double)));
+    CUDA_OK(cudaMalloc(&lv->traces, ntr * sizeof(double)));
+    CUDA_OK(cudaMemset(lv->u, 0, n * sizeof(double)));
+    CUDA_OK(cudaMemset(lv->res, 0, n * sizeof(double)));
+    CUDA_OK(cudaMemset(lv->rhs, 0, n * sizeof(double)));
+    CUDA_OK(cudaMemset(lv->traces, 0, ntr * sizeof(double)));
+    CUDA_OK(cudaMalloc(&lv->eps, K * sizeof(double)));
+    CUDA_OK(cudaMalloc(&lv->sqrt_eps, (K + lv->n_halo) * sizeof(double)));
+    CUDA_OK(cudaMemset(lv->eps, 0, K * sizeof(double)));
+    CUDA_OK(cudaMemset(lv->sqrt_eps, 0, (K + lv->n_halo) * sizeof(double)));
+    CUDA_OK(cudaMalloc(&lv->d_maxeps, sizeof(unsigned long long)));
+    CUDA_OK(cudaMalloc(&lv->d_coef, sizeof(StageCoef)));
+    CUDA_OK(cudaMallocHost(&lv->h_coef, sizeof(StageCoef)));
+    CUDA_OK(cudaMalloc(&lv->d_err, sizeof(DevError)));
+    CUDA_OK(cudaMemset(lv->d_err, 0, sizeof(DevError)));
+    CUDA_OK(cudaMallocHost(&lv->h_err, sizeof(DevError)));
+    lv->scratch_n = 1024;
+    CUDA_OK(cudaMalloc(&lv->d_scratch, lv->scratch_n * sizeof(double)));
+    lv->h_scratch.resize(lv->scratch_n);
+    CUDA_OK(cudaStreamCreateWithFlags(&lv->stream, cudaStreamNonBlocking));
+    for (auto& e : lv->ev) CUDA_OK(cudaEventCreate(&e));
+    std::memcpy(lv->freestream, d->freestream, sizeof(lv->freestream));
+    for (int c = 0; c < 5; ++c) lv->gas.fs[c] = d->freestream[c];
+    // opt in to > 48 KB dynamic shared memory
+    CUDA_OK(cudaFuncSetAttribute(lv->ks->rhs_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)lv->ks->smem_rhs));
+    CUDA_OK(cudaFuncSetAttribute(lv->ks->rhs_only, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)lv->ks->smem_rhs));
+    CUDA_OK(cudaFuncSetAttribute(lv->ks->visc_rhs_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)lv->ks->smem_rhs));
+    CUDA_OK(cudaFuncSetAttribute(lv->ks->visc_rhs_only, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)lv->ks->smem_rhs));
+    CUDA_OK(cudaFuncSetAttribute(lv->ks->aux_q, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)lv->ks->smem_rhs));
+    CUDA_OK(cudaFuncSetAttribute(lv->ks->traces, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)lv->ks->smem_traces));
+    CUDA_OK(cudaDeviceSynchronize());
+  });
+  if (st != CDG_GPU_OK) {
+    cdg_gpu_level_destroy(lv);
+    return st;
+  }
+  *out = lv;
+  return CDG_GPU_OK;
+}
+
+void cdg_gpu_level_destroy(cdg_gpu_level* lv) {
+  if (!lv) return;
+  cudaSetDevice(lv->device);
+  if (lv->graph) cudaGraphExecDestroy(lv->graph);
+  for (void* p : {(void*)lv->u, (void*)lv->res, (void*)lv->rhs, (void*)lv->traces, (void*)lv->before,
+                  (void*)lv->q, (void*)lv->qtr, (void*)lv->eps, (void*)lv->sqrt_eps, (void*)lv->d_vinv,
+                  (void*)lv->d_icub, (void*)lv->d_maxeps, (void*)lv->metric, (void*)lv->face, (void*)lv->conn,
+                  (void*)lv->code_map, (void*)lv->h, (void*)lv->frag_icub, (void*)lv->frag_op2,
+                  (void*)lv->frag_ig, (void*)lv->frag_aux, (void*)lv->d_coef, (void*)lv->d_err,
+                  (void*)lv->d_scratch, (void*)lv->d_send_idx, (void*)lv->d_recv_idx,
+                  (void*)lv->send_buf, (void*)lv->recv_buf})
+    if (p) cudaFree(p);
+  if (lv->h_coef) cudaFreeHost(lv->h_coef);
+  if (lv->h_err) cudaFreeHost(lv->h_err);
+  for (auto& e : lv->ev)
+    if (e) cudaEventDestroy(e);
+  if (lv->stream) cudaStreamDestroy(lv->stream);
+  delete lv;
+}
+
+void cdg_gpu_level_sizes(const cdg_gpu_level* lv, int* s) {
+  s[0] = lv->K;
+  s[1] = lv->np;
+  s[2] = lv->ncub;
+  s[3] = lv->ng;
+  s[4] = lv->caller_block;
+  s[5] = lv->caller_tblock;
+  s[6] = lv->bp;
+  s[7] = lv->n_halo;
+}
+
+void* cdg_gpu_stream(cdg_gpu_level* lv) { return lv->stream; }
+long long cdg_gpu_launch_count(const cdg_gpu_level* lv) { return lv->launches; }
+
+static void copy_rows(cdg_gpu_level* lv, double* dst, int dst_block, const double* src, int src_block,
+                      int values, int rows, cudaMemcpyKind kind) {
+  if (dst_block == src_block) {
+    CUDA_OK(cudaMemcpyAsync(dst, src, (size_t)rows * src_block * sizeof(double), kind, lv->stream));
+  } else {
+    CUDA_OK(cudaMemcpy2DAsync(dst, dst_block * sizeof(double), src, src_block * sizeof(double),
+                              values * sizeof(double), rows, kind, lv->stream));
+  }
+}
+
+int cdg_gpu_set_state(cdg_gpu_level* lv, const double* u, const double* res) {
+  return guarded(nullptr, 0, [&] {
+    CUDA_OK(cudaSetDevice(lv->device));
+    copy_rows(lv, lv->u, lv->bp, u, lv->caller_block, lv->np, lv->n_rows(), cudaMemcpyHostToDevice);
+    if (res)
+      copy_rows(lv, lv->res, lv->bp, res, lv->caller_block, lv->np, lv->n_rows(), cudaMemcpyHostToDevice);
+    else
+      CUDA_OK(cudaMemsetAsync(lv->res, 0, (size_t)lv->n_rows() * lv->bp * sizeof(double), lv->stream));
+    CUDA_OK(cudaStreamSynchronize(lv->stream));
+  });
+}
+
+int cdg_gpu_set_state_device(cdg_gpu_level* lv, const double* u, const double* res) {
+  return guarded(nullptr, 0, [&] {
+    CUDA_OK(cudaSetDevice(lv->device));
+    copy_rows(lv, lv->u, lv->bp, u, lv->caller_block, lv->np, lv->n_rows(), cudaMemcpyDeviceToDevice);
+    if (res)
+      copy_rows(lv, lv->res, lv->bp, res, lv->caller_block, lv->np, lv->n_rows(), cudaMemcpyDeviceToDevice);
+    else
+      CUDA_OK(cudaMemsetAsync(lv->res, 0, (size_t)lv->n_rows() * lv->bp * sizeof(double), lv->stream));
+    CUDA_OK(cudaStreamSynchronize(lv->stream));
+  });
+}
+
+int cdg_gpu_get_state(cdg_gpu_level* lv, double* u, double* res) {
+  return guarded(nullptr, 0, [&] {
+    CUDA_OK(cudaSetDevice(lv->device));
+    if (u) copy_rows(lv, u, lv->caller_block, lv->u, lv->bp, lv->np, lv->n_rows(), cudaMemcpyDeviceToHost);
+    if (res)
+      copy_rows(lv, res, lv->caller_block, lv->res, lv->bp, lv->np, lv->n_rows(), cudaMemcpyDeviceToHost);
+    CUDA_OK(cudaStreamSynchronize(lv->stream));
+  });
+}
+
+int cdg_gpu_device_buffers(cdg_gpu_level* lv, double** u, double** res, double** traces) {
+  if (u) *u = lv->u;
+  if (res) *res = lv->res;
+  if (traces) *traces = lv->traces;
+  return CDG_GPU_OK;
+}
+
+int cdg_gpu_interpolate_to_faces(cdg_gpu_level* lv, double* traces_out) {
+  return guarded(nullptr, 0, [&] {
+    CUDA_OK(cudaSetDevice(lv->device));
+    launch_traces(lv, lv->u, lv->traces);
+    CUDA_OK(cudaGetLastError());
+    if (traces_out)
+      copy_rows(lv, traces_out, lv->caller_tblock, lv->traces, lv->tb, lv->nf, lv->n_rows(),
+                cudaMemcpyDeviceToHost);
+    CUDA_OK(cudaStreamSynchronize(lv->stream));
+  });
+}
+
+int cdg_gpu_compute_rhs(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, double* rhs_out, char* err,
+                        size_t errlen) {
+  return guarded(err, errlen, [&] {
+    CUDA_OK(cudaSetDevice(lv->device));
+    if (cfg->riemann != 0 && cfg->riemann != 1)
+      throw Status(CDG_GPU_ERR_CONFIG, "unknown Riemann solver (llf|hllc)");
+    lv->gas.gamma = cfg->gamma;
+    lv->gas.riemann = cfg->riemann;
+    const bool viscous = viscosity_phase(lv, cfg);
+    lv->last_viscous = viscous;
+    if (!viscous) launch_traces(lv, lv->u, lv->traces);
+    launch_rhs(lv, false, viscous, 0);
+    CUDA_OK(cudaGetLastError());
+    check_device_error(lv);
+    if (rhs_out)
+      copy_rows(lv, rhs_out, lv->caller_block, lv->rhs, lv->bp, lv->np, lv->n_rows(), cudaMemcpyDeviceToHost);
+    CUDA_OK(cudaStreamSynchronize(lv->stream));
+  });
+}
+
+int cdg_gpu_rk_steps(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, int nsteps, double dt,
+                     const double a[5], const double b[5], char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    CUDA_OK(cudaSetDevice(lv->device));
+    if (cfg->riemann != 0 && cfg->riemann != 1)
+      throw Status(CDG_GPU_ERR_CONFIG, "unknown Riemann solver (llf|hllc)");
+    lv->gas.gamma = cfg->gamma;
+    lv->gas.riemann = cfg->riemann;
+    lv->h_coef->dt = dt;
+    for (int i = 0; i < 5; ++i) {
+      lv->h_coef->a[i] = a[i];
+      lv->h_coef->b[i] = b[i];
+    }
+    CUDA_OK(cudaMemcpyAsync(lv->d_coef, lv->h_coef, sizeof(StageCoef), cudaMemcpyHostToDevice, lv->stream));
+    if (cfg->visc_enabled) {
+      // viscous stages need a host decision per stage (viscous_active,
+      // solver.cpp:257-259): run eagerly.
+      for (int s = 0; s < nsteps; ++s)
+        for (int stage = 0; stage < 5; ++stage) {
+          const bool viscous = viscosity_phase(lv, cfg);
+          lv->last_viscous = viscous;
+          if (!viscous) launch_traces(lv, lv->u, lv->traces);
+          launch_rhs(lv, true, viscous, stage);
+        }
+      CUDA_OK(cudaGetLastError());
+      check_device_error(lv);
+      return;
+    }
+    if (lv->profiling) {
+      float t_tr = 0.f, t_rhs = 0.f;
+      for (int s = 0; s < nsteps; ++s)
+        for (int stage = 0; stage < 5; ++stage) {
+          CUDA_OK(cudaEventRecord(lv->ev[0], lv->stream));
+          launch_traces(lv, lv->u, lv->traces);
+          CUDA_OK(cudaEventRecord(lv->ev[1], lv->stream));
+          launch_rhs(lv, true, false, stage);
+          CUDA_OK(cudaEventRecord(lv->ev[2], lv->stream));
+          CUDA_OK(cudaEventSynchronize(lv->ev[2]));
+          float x, y;
+          CUDA_OK(cudaEventElapsedTime(&x, lv->ev[0], lv->ev[1]));
+          CUDA_OK(cudaEventElapsedTime(&y, lv->ev[1], lv->ev[2]));
+          t_tr += x;
+          t_rhs += y;
+        }
+      lv->prof[0] = t_tr;
+      lv->prof[1] = t_rhs;
+      lv->prof[2] = 10.0 * nsteps;
+      CUDA_OK(cudaGetLastError());
+      check_device_error(lv);
+      return;
+    }
+    // one RK step (5 x [traces, rhs+update]) captured once as a CUDA graph
+    if (!lv->graph || lv->graph_riemann != cfg->riemann || lv->graph_gamma != cfg->gamma) {
+      if (lv->graph) {
+        cudaGraphExecDestroy(lv->graph);
+        lv->graph = nullptr;
+      }
+      cudaGraph_t g;
+      CUDA_OK(cudaStreamBeginCapture(lv->stream, cudaStreamCaptureModeThreadLocal));
+      for (int stage = 0; stage < 5; ++stage) {
+        launch_traces(lv, lv->u, lv->traces);
+        launch_rhs(lv, true, false, stage);
+      }
+      lv->launches -= 10;  // counted at replay
+      CUDA_OK(cudaStreamEndCapture(lv->stream, &g));
+      CUDA_OK(cudaGraphInstantiate(&lv->graph, g, 0));
+      CUDA_OK(cudaGraphDestroy(g));
+      lv->graph_riemann = cfg->riemann;
+      lv->graph_gamma = cfg->gamma;
+    }
+    for (int s = 0; s < nsteps; ++s) {
+      CUDA_OK(cudaGraphLaunch(lv->graph, lv->stream));
+      lv->launches += 10;
+    }
+    CUDA_OK(cudaGetLastError());
+    check_device_error(lv);
+  });
+}
+
+int cdg_gpu_set_profiling(cdg_gpu_level* lv, int enabled) {
+  lv->profiling = enabled != 0;
+  return CDG_GPU_OK;
+}
+
+int cdg_gpu_last_profile(cdg_gpu_level* lv, double* out3) {
+  for (int i = 0; i < 3; ++i) out3[i] = lv->prof[i];
+  return CDG_GPU_OK;
+}
+
+int cdg_gpu_viscosity(cdg_gpu_level* lv, double* eps_out) {
+  return guarded(nullptr, 0, [&] {
+    CUDA_OK(cudaSetDevice(lv->device));
+    CUDA_OK(cudaMemcpyAsync(eps_out, lv->eps, lv->K * sizeof(double), cudaMemcpyDeviceToHost, lv->stream));
+    CUDA_OK(cudaStreamSynchronize(lv->stream));
+  });
+}
+
+int cdg_gpu_aux_gradient(cdg_gpu_level* lv, int m, double* q_out) {
+  return guarded(nullptr, 0, [&] {
+    if (!lv->q || !lv->last_viscous) throw Status(CDG_GPU_ERR_CONFIG, "no viscous RHS evaluated yet");
+    if (m < 0 || m > 2) throw Status(CDG_GPU_ERR_CONFIG, "aux_gradient: direction must be 0..2");
+    CUDA_OK(cudaSetDevice(lv->device));
+    const size_t n = (size_t)lv->K * 5 * lv->bp;
+    copy_rows(lv, q_out, lv->caller_block, lv->q + m * n, lv->bp, lv->np, lv->n_rows(),
+              cudaMemcpyDeviceToHost);
+    CUDA_OK(cudaStreamSynchronize(lv->stream));
+  });
+}
+
+int cdg_gpu_timestep(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, int use_viscosity, double* dt_out,
+                     char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (cfg->cfl <= 0.0) throw Status(CDG_GPU_ERR_CONFIG, "compute_timestep: CFL must be positive");
+    if (!lv->h) throw Status(CDG_GPU_ERR_CONFIG, "compute_timestep: level created without h");
+    CUDA_OK(cudaSetDevice(lv->device));
+    CUDA_OK(cudaMemsetAsync(lv->d_scratch, 0xff, sizeof(double), lv->stream));
+    TimestepParams tp{};
+    tp.u = lv->u;
+    tp.h = lv->h;
+    tp.eps = use_viscosity ? lv->eps : nullptr;
+    tp.K = lv->K;
+    tp.np = lv->np;
+    tp.bp = lv->bp;
+    tp.gamma = cfg->gamma;
+    tp.pfac = (lv->degree + 1.0) * (lv->degree + 1.0);
+    tp.out = reinterpret_cast<unsigned long long*>(lv->d_scratch);
+    tp.err = lv->d_err;
+    k_timestep<<<(lv->K + 255) / 256, 256, 0, lv->stream>>>(tp);
+    ++lv->launches;
+    CUDA_OK(cudaGetLastError());
+    check_device_error(lv);
+    unsigned long long bits;
+    CUDA_OK(cudaMemcpy(&bits, lv->d_scratch, sizeof bits, cudaMemcpyDeviceToHost));
+    double m;
+    std::memcpy(&m, &bits, sizeof m);
+    *dt_out = cfg->cfl * m;
+  });
+}
+
+int cdg_gpu_snapshot(cdg_gpu_level* lv) {
+  return guarded(nullptr, 0, [&] {
+    CUDA_OK(cudaSetDevice(lv->device));
+    const size_t n = (size_t)lv->K * 5 * lv->bp;
+    if (!lv->before) CUDA_OK(cudaMalloc(&lv->before, n * sizeof(double)));
+    CUDA_OK(cudaMemcpyAsync(lv->before, lv->u, n * sizeof(double), cudaMemcpyDeviceToDevice, lv->stream));
+  });
+}
+
+int cdg_gpu_residual(cdg_gpu_level* lv, int kind, double dt, double* out) {
+  return guarded(nullptr, 0, [&] {
+    if (!lv->before) throw Status(CDG_GPU_ERR_CONFIG, "residual: no snapshot taken");
+    CUDA_OK(cudaSetDevice(lv->device));
+    const size_t n = (size_t)lv->K * 5 * lv->bp;
+    const int blocks = 592;
+    k_residual<<<blocks, 256, 0, lv->stream>>>(lv->u, lv->before, n, kind, lv->d_scratch);
+    ++lv->launches;
+    CUDA_OK(cudaGetLastError());
+    CUDA_OK(cudaMemcpyAsync(lv->h_scratch.data(), lv->d_scratch, blocks * sizeof(double),
+                            cudaMemcpyDeviceToHost, lv->stream));
+    CUDA_OK(cudaStreamSynchronize(lv->stream));
+    double acc = 0.0;
+    for (int i = 0; i < blocks; ++i)
+      acc = kind == 1 ? acc + lv->h_scratch[i] : std::max(acc, lv->h_scratch[i]);
+    *out = (kind == 1 ? std::sqrt(acc) : acc) / dt;
+  });
+}
+
+// ---- multi-GPU halo plumbing -------------------------------------------------
+int cdg_gpu_halo_setup(cdg_gpu_level* lv, int n_send, const int* send_ef, int n_recv, const int* recv_ef,
+                       double** send_buf, double** recv_buf) {
+  return guarded(nullptr, 0, [&] {
+    CUDA_OK(cudaSetDevice(lv->device));
+    lv->n_send = n_send;
+    lv->n_recv = n_recv;
+    const size_t per = (size_t)5 * lv->ng;
+    if (n_send) {
+      lv->d_send_idx = dev_upload(std::vector<int>(send_ef, send_ef + n_send));
+      CUDA_OK(cudaMalloc(&lv->send_buf, n_send * per * sizeof(double)));
+    }
+    if (n_recv) {
+      lv->d_recv_idx = dev_upload(std::vector<int>(recv_ef, recv_ef + n_recv));
+      CUDA_OK(cudaMalloc(&lv->recv_buf, n_recv * per * sizeof(double)));
+    }
+    if (send_buf) *send_buf = lv->send_buf;
+    if (recv_buf) *recv_buf = lv->recv_buf;
+  });
+}
+
+int cdg_gpu_halo_pack(cdg_gpu_level* lv) {
+  return guarded(nullptr, 0, [&] {
+    if (!lv->n_send) return;
+    k_halo_copy<<<(lv->n_send + 7) / 8, 256, 0, lv->stream>>>(lv->traces, lv->send_buf, lv->d_send_idx,
+                                                               lv->n_send, lv->ng, lv->tb, 0);
+    ++lv->launches;
+    CUDA_OK(cudaGetLastError());
+  });
+}
+
+int cdg_gpu_halo_unpack(cdg_gpu_level* lv) {
+  return guarded(nullptr, 0, [&] {
+    if (!lv->n_recv) return;
+    k_halo_copy<<<(lv->n_recv + 7) / 8, 256, 0, lv->stream>>>(lv->traces, lv->recv_buf, lv->d_recv_idx,
+                                                               lv->n_recv, lv->ng, lv->tb, 1);
+    ++lv->launches;
+    CUDA_OK(cudaGetLastError());
+  });
+}
+
+int cdg_gpu_rk_stage_phase(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, int stage, int phase, double dt,
+                           const double a[5], const double b[5], char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    CUDA_OK(cudaSetDevice(lv->device));
+    if (cfg->visc_enabled)
+      throw Status(CDG_GPU_ERR_CONFIG, "split-phase stages support the inviscid path only");
+    lv->gas.gamma = cfg->gamma;
+    lv->gas.riemann = cfg->riemann;
+    if (phase == 0) {
+      if (stage == 0) {
+        lv->h_coef->dt = dt;
+        for (int i = 0; i < 5; ++i) {
+          lv->h_coef->a[i] = a[i];
+          lv->h_coef->b[i] = b[i];
+        }
+        CUDA_OK(cudaMemcpyAsync(lv->d_coef, lv->h_coef, sizeof(StageCoef), cudaMemcpyHostToDevice,
+                                lv->stream));
+      }
+      launch_traces(lv, lv->u, lv->traces);
+      if (lv->n_send)
+        k_halo_copy<<<(lv->n_send + 7) / 8, 256, 0, lv->stream>>>(lv->traces, lv->send_buf, lv->d_send_idx,
+                                                                   lv->n_send, lv->ng, lv->tb, 0);
+    } else {
+      if (lv->n_recv)
+        k_halo_copy<<<(lv->n_recv + 7) / 8, 256, 0, lv->stream>>>(lv->traces, lv->recv_buf, lv->d_recv_idx,
+                                                                   lv->n_recv, lv->ng, lv->tb, 1);
+      launch_rhs(lv, true, false, stage);
+      if (stage == 4) check_device_error(lv);
+    }
+    CUDA_OK(cudaGetLastError());
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,570 @@
+// cdg_kernels.cuh -- sm_100a kernels of the RKDG hot path (affine tets).
+//
+// Math (per element e, field c; reference: solver.cpp:325-492):
+//   U_cub   = I_cub U                                         (solver.cpp:362-363)
+//   F_d     = Euler flux at cubature nodes                    (solver.cpp:374-395)
+//   G_m     = sum_d (dr_m/dx_d) F_d        (contravariant flux; J cancels)
+//   F*      = LLF/HLLC(U-, U+, n) at face nodes               (solver.cpp:415-456)
+//   rhs     = sum_m A_m G_m - LIFT ((sjac_f / J) F*)
+// with the shared (per-level) operators
+//   A_m  = M_ref^-1 D_m^T diag(W),  LIFT = M_ref^-1 I_g^T diag(w_face),
+//   M_ref = I_cub^T diag(W) I_cub,
+// which is the reference's  M_e^-1 (sum S_m F_m - M_dOmega F*)  for affine
+// elements (M_e = J M_ref, S_m = J sum_k D_k^T diag(W r_{k,m}); operators.cpp:
+// 135-165) with the Cholesky solve folded into the operators.
+//
+// Layout: a "row" is one (element, field) pair; the tile's 5E rows are
+// contiguous rows of the SolutionStore matrix [K*5][block] (offset(e,c) =
+// (e*5+c)*block, solution_store.hpp:29-31). All three contractions are
+//   Out[rows x N] = In[rows x K] * Op^T
+// on the FP64 tensor pipe (DMMA, mma.sync.m16n8k4.f64): In (A operand) is
+// staged in shared memory, Op (B operand) is pre-swizzled on the host into
+// fragment order so each warp's B fragment is one coalesced 256-byte L1/L2 load.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace cdg_gpu {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+__host__ __device__ constexpr int round_up(int x, int m) { return (x + m - 1) / m * m; }
+__host__ __device__ constexpr int ceil_div(int x, int m) { return (x + m - 1) / m; }
+// leading dimension >= n with ld % 16 in {4, 12}: conflict-free A-fragment
+// loads (8 rows x 4 consecutive doubles per warp)
+__host__ __device__ constexpr int frag_ld(int n) {
+  return (n % 16 == 4 || n % 16 == 12) ? n : frag_ld(n + 4);
+}
+__host__ __device__ constexpr int imax(int a, int b) { return a > b ? a : b; }
+
+template <int NP_, int NCUB_, int NG_, int E_>
+struct Cfg {
+  static constexpr int NP = NP_, NCUB = NCUB_, NG = NG_, NF = 4 * NG_, E = E_;
+  static constexpr int R = 5 * E;                 // rows per tile
+  static constexpr int MT = R / 16;               // m16 tiles per tile
+  static constexpr int BP = round_up(NP, 16);     // device SolutionStore block (pad16)
+  static constexpr int TB = round_up(NF, 16);     // device trace block (pad16)
+  static constexpr int KP = round_up(NP, 4);      // K of the node->point GEMMs
+  static constexpr int KS1 = KP / 4;              // k-steps
+  static constexpr int NCUB8 = round_up(NCUB, 8);
+  static constexpr int NP8 = round_up(NP, 8);
+  static constexpr int NF8 = round_up(NF, 8);
+  static constexpr int NT2 = NP8 / 8;             // n-tiles of the RHS GEMM
+  static constexpr int CH = 16;                   // cubature nodes per chunk
+  static constexpr int NCH = ceil_div(NCUB8, CH);
+  static constexpr int FCH = 32;                  // face nodes per chunk
+  static constexpr int NFCH = ceil_div(NF, FCH);
+  static constexpr int K2CUB = 3 * NCUB8;         // volume part of the RHS K
+  static constexpr int K2 = K2CUB + NF;           // + face part (NF % 4 == 0)
+  static constexpr int KS2 = K2 / 4;
+  static constexpr int LDU = frag_ld(KP);
+  static constexpr int LDC = frag_ld(CH);
+  static constexpr int LDG = frag_ld(imax(3 * CH, FCH));
+  static constexpr int T2 = MT * NT2;             // RHS output tiles
+  static constexpr int MAXT2 = ceil_div(T2, kWarps);
+  static constexpr int SMEM_U = R * LDU;
+  static constexpr int SMEM_C = R * LDC;
+  static constexpr int SMEM_G = R * LDG;
+  static constexpr size_t SMEM_BYTES =
+      sizeof(double) * (SMEM_U + SMEM_C + SMEM_G + E * 9 + E * 4 * 4 + E) +
+      sizeof(int) * (E * 4 * 2);
+};
+
+// First-error record (the reference's RhsWorkspace::record_error,
+// solver.cpp:54-69, made device-side: first writer wins).
+struct DevError {
+  int flag;   // 0 none, 1 set
+  int kind;   // 1 cub-node state, 2 trace state, 3 timestep state
+  int elem;
+  int a;      // cub node / face
+  int b;      // face node
+  int pad;
+  double value;
+};
+
+__device__ __forceinline__ void record_error(DevError* err, int kind, int elem, int a, int b,
+                                             double value) {
+  if (atomicCAS(&err->flag, 0, 1) == 0) {
+    err->kind = kind;
+    err->elem = elem;
+    err->a = a;
+    err->b = b;
+    err->value = value;
+    __threadfence();
+  }
+}
+
+// Per-stage coefficients, read from global so that captured graphs stay valid
+// when dt / a / b change (solver.cpp:476-488).
+struct StageCoef {
+  double dt;
+  double a[5];
+  double b[5];
+};
+
+struct GasParams {
+  double gamma;
+  double fs[5];  // freestream
+  int riemann;   // 0 llf, 1 hllc
+};
+
+// ---------------------------------------------------------------------------
+// DMMA helper: D(16x8) += A(16x4, row) * B(4x8, col), fp64.
+// A frag: a0=(g, t) a1=(g+8, t); B frag: b0=(k=t, n=g); C: c0,c1=(g, 2t..2t+1),
+// c2,c3=(g+8, 2t..2t+1)   with g = lane/4, t = lane%4.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void dmma_k4(double (&d)[4], double a0, double a1, double b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 "
+      "{%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+      : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+      : "d"(a0), "d"(a1), "d"(b0));
+}
+
+// ---------------------------------------------------------------------------
+// Euler state algebra (euler.cpp:7-161), device versions.
+// ---------------------------------------------------------------------------
+struct State5 {
+  double r, mx, my, mz, E;
+};
+
+__device__ __forceinline__ bool admissible(const State5& u, double gamma) {
+  if (u.r <= 0.0) return false;
+  return (u.E - (u.mx * u.mx + u.my * u.my + u.mz * u.mz) / (2.0 * u.r)) > 0.0 && gamma > 1.0;
+}
+
+__device__ __forceinline__ double pressure(const State5& u, double gamma) {
+  return (gamma - 1.0) * (u.E - (u.mx * u.mx + u.my * u.my + u.mz * u.mz) / (2.0 * u.r));
+}
+
+// flux_dot_n (euler.cpp:42-50)
+__device__ __forceinline__ void flux_dot_n(const State5& u, double p, double nx, double ny,
+                                           double nz, double (&f)[5]) {
+  const double vn = (u.mx * nx + u.my * ny + u.mz * nz) / u.r;
+  f[0] = u.r * vn;
+  f[1] = u.mx * vn + p * nx;
+  f[2] = u.my * vn + p * ny;
+  f[3] = u.mz * vn + p * nz;
+  f[4] = vn * (u.E + p);
+}
+
+// llf_flux (euler.cpp:59-68)
+__device__ __forceinline__ void llf_flux(const State5& um, const State5& up, double nx, double ny,
+                                         double nz, double gamma, double (&out)[5]) {
+  const double pm = pressure(um, gamma), pp = pressure(up, gamma);
+  const double lm = fabs((um.mx * nx + um.my * ny + um.mz * nz) / um.r) + sqrt(gamma * pm / um.r);
+  const double lp = fabs((up.mx * nx + up.my * ny + up.mz * nz) / up.r) + sqrt(gamma * pp / up.r);
+  const double lambda = fmax(lm, lp);
+  double fm[5], fp[5];
+  flux_dot_n(um, pm, nx, ny, nz, fm);
+  flux_dot_n(up, pp, nx, ny, nz, fp);
+  const double dm[5] = {up.r - um.r, up.mx - um.mx, up.my - um.my, up.mz - um.mz, up.E - um.E};
+#pragma unroll
+  for (int c = 0; c < 5; ++c) out[c] = 0.5 * (fm[c] + fp[c]) - 0.5 * lambda * dm[c];
+}
+
+// hllc_flux with Einfeldt/Roe bounds and LLF fallback (euler.cpp:70-138)
+__device__ __forceinline__ void hllc_flux(const State5& um, const State5& up, double nx, double ny,
+                                          double nz, double g, double (&out)[5]) {
+  const double pl = pressure(um, g), pr = pressure(up, g);
+  const double vlx = um.mx / um.r, vly = um.my / um.r, vlz = um.mz / um.r;
+  const double vrx = up.mx / up.r, vry = up.my / up.r, vrz = up.mz / up.r;
+  const double unl = vlx * nx + vly * ny + vlz * nz;
+  const double unr = vrx * nx + vry * ny + vrz * nz;
+  const double cl = sqrt(g * pl / um.r), cr = sqrt(g * pr / up.r);
+  const double sl_ = sqrt(um.r), sr_ = sqrt(up.r);
+  const double den = sl_ + sr_;
+  const double vx = (sl_ * vlx + sr_ * vrx) / den, vy = (sl_ * vly + sr_ * vry) / den,
+               vz = (sl_ * vlz + sr_ * vrz) / den;
+  const double hl = (um.E + pl) / um.r, hr = (up.E + pr) / up.r;
+  const double h_roe = (sl_ * hl + sr_ * hr) / den;
+  const double c2_roe = (g - 1.0) * (h_roe - 0.5 * (vx * vx + vy * vy + vz * vz));
+  const double un_roe = vx * nx + vy * ny + vz * nz;
+  double s_left, s_right;
+  if (c2_roe <= 0.0) {
+    s_left = fmin(unl - cl, unr - cr);
+    s_right = fmax(unl + cl, unr + cr);
+  } else {
+    const double c_roe = sqrt(c2_roe);
+    s_left = fmin(unl - cl, un_roe - c_roe);
+    s_right = fmax(unr + cr, un_roe + c_roe);
+  }
+  if (!(s_left < s_right)) {
+    llf_flux(um, up, nx, ny, nz, g, out);
+    return;
+  }
+  const double s_star = (pr - pl + um.r * unl * (s_left - unl) - up.r * unr * (s_right - unr)) /
+                        (um.r * (s_left - unl) - up.r * (s_right - unr));
+  if (!isfinite(s_star)) {
+    llf_flux(um, up, nx, ny, nz, g, out);
+    return;
+  }
+  if (0.0 <= s_left) {
+    flux_dot_n(um, pl, nx, ny, nz, out);
+    return;
+  }
+  if (0.0 >= s_right) {
+    flux_dot_n(up, pr, nx, ny, nz, out);
+    return;
+  }
+  const bool left = 0.0 <= s_star;
+  const State5& u = left ? um : up;
+  const double un_k = left ? unl : unr, p_k = left ? pl : pr, s_k = left ? s_left : s_right;
+  const double factor = u.r * (s_k - un_k) / (s_k - s_star);
+  const double vx_ = u.mx / u.r, vy_ = u.my / u.r, vz_ = u.mz / u.r;
+  const double ds = s_star - un_k;
+  const double star[5] = {factor, factor * (vx_ + ds * nx), factor * (vy_ + ds * ny),
+                          factor * (vz_ + ds * nz),
+                          factor * (u.E / u.r + ds * (s_star + p_k / (u.r * (s_k - un_k))))};
+  double f[5];
+  flux_dot_n(u, p_k, nx, ny, nz, f);
+  const double uu[5] = {u.r, u.mx, u.my, u.mz, u.E};
+#pragma unroll
+  for (int c = 0; c < 5; ++c) out[c] = f[c] + s_k * (star[c] - uu[c]);
+}
+
+// boundary_state (euler.cpp:147-161)
+__device__ __forceinline__ State5 boundary_state(const State5& in, double nx, double ny, double nz,
+                                                 int kind, const GasParams& gp) {
+  if (kind == 1) return State5{gp.fs[0], gp.fs[1], gp.fs[2], gp.fs[3], gp.fs[4]};
+  State5 gh = in;
+  const double mn = in.mx * nx + in.my * ny + in.mz * nz;
+  gh.mx = in.mx - 2.0 * mn * nx;
+  gh.my = in.my - 2.0 * mn * ny;
+  gh.mz = in.mz - 2.0 * mn * nz;
+  return gh;
+}
+
+// Face coupling word: bits 0-1 neighbour face, 2-3 bc kind, 4 boundary flag,
+// 8-31 node-map code.
+__host__ __device__ constexpr int pack_face(int nface, int bc, int boundary, int code) {
+  return (nface & 3) | ((bc & 3) << 2) | ((boundary & 1) << 4) | (code << 8);
+}
+
+// ---------------------------------------------------------------------------
+// Kernel 1: traces  T[rows x NF] = U[rows x KP] * I_g^T   (solver.cpp:200-208)
+// ---------------------------------------------------------------------------
+template <class C>
+__global__ void __launch_bounds__(kThreads)
+k_traces(const double* __restrict__ u, double* __restrict__ traces,
+         const double* __restrict__ frag_ig, int n_rows, int n_tiles) {
+  extern __shared__ __align__(16) double smem[];
+  double* sU = smem;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  constexpr int NT = C::NF8 / 8;
+  constexpr int T = C::MT * NT;
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int row0 = tile * C::R;
+    // stage U rows (16-byte vector loads of KP doubles per row)
+    constexpr int V = C::KP / 2;
+    for (int idx = tid; idx < C::R * V; idx += kThreads) {
+      const int r = idx / V, v = idx % V;
+      double2 x = make_double2(0.0, 0.0);
+      if (row0 + r < n_rows)
+        x = __ldg(reinterpret_cast<const double2*>(u + (size_t)(row0 + r) * C::BP) + v);
+      *reinterpret_cast<double2*>(sU + r * C::LDU + 2 * v) = x;
+    }
+    __syncthreads();
+    for (int t = warp; t < T; t += kWarps) {
+      const int mt = t / NT, nt = t % NT;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      const double* a_ptr = sU + (mt * 16 + g) * C::LDU + tq;
+      const double* b_ptr = frag_ig + (size_t)nt * C::KS1 * 32 + lane;
+#pragma unroll 4
+      for (int ks = 0; ks < C::KS1; ++ks)
+        dmma_k4(acc, a_ptr[ks * 4], a_ptr[8 * C::LDU + ks * 4], __ldg(b_ptr + ks * 32));
+      const int col = nt * 8 + 2 * tq;
+      if (col < C::NF) {
+        const int r0 = row0 + mt * 16 + g;
+        if (r0 < n_rows)
+          *reinterpret_cast<double2*>(traces + (size_t)r0 * C::TB + col) = make_double2(acc[0], acc[1]);
+        if (r0 + 8 < n_rows)
+          *reinterpret_cast<double2*>(traces + (size_t)(r0 + 8) * C::TB + col) =
+              make_double2(acc[2], acc[3]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Kernel 2: fused volume + surface + lift (+ low-storage RK update)
+// ---------------------------------------------------------------------------
+struct RhsParams {
+  double* u;                  // [K*5][BP]    (updated in place when UPDATE)
+  double* res;                // [K*5][BP]
+  double* rhs_out;            // [K*5][BP]    (RHS-only mode)
+  const double* traces;       // [(K+halo)*5][TB]
+  const double* metric;       // [K][9]
+  const double4* face;        // [K][4] (nx, ny, nz, sjac/J)
+  const int2* conn;           // [K][4] (neighbour, packed word)
+  const int* code_map;        // [n_codes][NG]
+  const double* frag_icub;    // GEMM1 B fragments
+  const double* frag_op2;     // GEMM2 B fragments
+  const StageCoef* coef;
+  int stage;
+  int K;
+  int n_tiles;
+  int elem_offset;            // global element id of local element 0 (messages)
+  GasParams gas;
+  DevError* err;
+  // viscous extension (solver.cpp:364-369, 398-406, 438-453)
+  const double* q;            // [3][K*5][BP]   aux gradient q_m
+  const double* qtr;          // [3][(K+halo)*5][TB] its traces
+  const double* sqrt_eps;     // [K+halo]
+  const double* icub;         // [NCUB][NP] row-major (viscous volume term)
+  size_t qtr_stride;          // elements per direction of qtr
+};
+
+template <class C, bool UPDATE, bool VISC>
+__global__ void __launch_bounds__(kThreads, 1) k_rhs(RhsParams p) {
+  extern __shared__ __align__(16) double smem[];
+  double* sU = smem;                       // [R][LDU] nodal state
+  double* sC = sU + C::SMEM_U;             // [R][LDC] U at a cubature chunk
+  double* sG = sC + C::SMEM_C;             // [R][LDG] flux chunk (A operand)
+  double* sMet = sG + C::SMEM_G;           // [E][9]
+  double4* sFace = reinterpret_cast<double4*>(sMet + C::E * 9);  // [E][4]
+  double* sSe = reinterpret_cast<double*>(sFace + C::E * 4);      // [E] sqrt(eps)
+  int2* sConn = reinterpret_cast<int2*>(sSe + C::E);              // [E][4]
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const int n_rows = p.K * 5;
+  const double gamma = p.gas.gamma;
+  const size_t qstride = (size_t)p.K * 5 * C::BP;
+  // contiguous run of RHS output tiles for this warp (m-major order)
+  const int t_begin = (warp * C::T2) / kWarps, t_end = ((warp + 1) * C::T2) / kWarps;
+
+  for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+    if (*(volatile int*)&p.err->flag) return;
+    const int e0 = tile * C::E;
+    const int row0 = e0 * 5;
+    // ---- stage nodal state + per-element geometry --------------------------
+    constexpr int V = C::KP / 2;
+    for (int idx = tid; idx < C::R * V; idx += kThreads) {
+      const int r = idx / V, v = idx % V;
+      double2 x = make_double2(0.0, 0.0);
+      if (row0 + r < n_rows)
+        x = *(reinterpret_cast<const double2*>(p.u + (size_t)(row0 + r) * C::BP) + v);
+      *reinterpret_cast<double2*>(sU + r * C::LDU + 2 * v) = x;
+    }
+    for (int idx = tid; idx < C::E * 9; idx += kThreads) {
+      const int e = e0 + idx / 9;
+      sMet[idx] = e < p.K ? __ldg(p.metric + (size_t)e0 * 9 + idx) : 0.0;
+    }
+    for (int idx = tid; idx < C::E * 4; idx += kThreads) {
+      const int e = e0 + idx / 4;
+      sFace[idx] = e < p.K ? p.face[(size_t)e0 * 4 + idx] : make_double4(0, 0, 1, 0);
+      sConn[idx] = e < p.K ? p.conn[(size_t)e0 * 4 + idx] : make_int2(-1, pack_face(0, 0, 1, 0));
+    }
+    if (VISC)
+      for (int idx = tid; idx < C::E; idx += kThreads)
+        sSe[idx] = e0 + idx < p.K ? p.sqrt_eps[e0 + idx] : 0.0;
+    __syncthreads();
+
+    double acc[C::MAXT2][4];
+#pragma unroll
+    for (int i = 0; i < C::MAXT2; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.0;
+
+    // ---- volume: chunks of CH cubature nodes --------------------------------
+    for (int ch = 0; ch < C::NCH; ++ch) {
+      const int q0 = ch * C::CH;
+      const int w = (C::NCUB8 - q0) < C::CH ? (C::NCUB8 - q0) : C::CH;  // multiple of 8
+      // GEMM1: sC[:, 0:w] = sU * I_cub[q0:q0+w, :]^T
+      const int nt1 = w / 8, T1 = C::MT * nt1;
+      for (int t = warp; t < T1; t += kWarps) {
+        const int mt = t / nt1, nt = t % nt1;
+        double c1[4] = {0.0, 0.0, 0.0, 0.0};
+        const double* a_ptr = sU + (mt * 16 + g) * C::LDU + tq;
+        const double* b_ptr = p.frag_icub + ((size_t)(q0 / 8 + nt) * C::KS1) * 32 + lane;
+#pragma unroll 4
+        for (int ks = 0; ks < C::KS1; ++ks)
+          dmma_k4(c1, a_ptr[ks * 4], a_ptr[8 * C::LDU + ks * 4], __ldg(b_ptr + ks * 32));
+        double* o = sC + (mt * 16 + g) * C::LDC + nt * 8 + 2 * tq;
+        *reinterpret_cast<double2*>(o) = make_double2(c1[0], c1[1]);
+        *reinterpret_cast<double2*>(o + 8 * C::LDC) = make_double2(c1[2], c1[3]);
+      }
+      __syncthreads();
+      // pointwise Euler flux -> contravariant flux G_m = sum_d (dr_m/dx_d) F_d
+      for (int idx = tid; idx < C::E * w; idx += kThreads) {
+        const int e = idx / w, ql = idx % w, q = q0 + ql;
+        const double* uc = sC + (e * 5) * C::LDC + ql;
+        double* gout = sG + (e * 5) * C::LDG + ql;
+        if (q < C::NCUB && e0 + e < p.K) {
+          const State5 s{uc[0], uc[C::LDC], uc[2 * C::LDC], uc[3 * C::LDC], uc[4 * C::LDC]};
+          if (!admissible(s, gamma)) record_error(p.err, 1, p.elem_offset + e0 + e, q, 0, s.r);
+          const double pr = pressure(s, gamma);
+          const double vx = s.mx / s.r, vy = s.my / s.r, vz = s.mz / s.r;
+          const double ep = s.E + pr;
+          // F_d (d = x, y, z) for the 5 fields (solver.cpp:382-394)
+          double F[3][5] = {{s.mx, s.mx * vx + pr, s.my * vx, s.mz * vx, vx * ep},
+                            {s.my, s.mx * vy, s.my * vy + pr, s.mz * vy, vy * ep},
+                            {s.mz, s.mx * vz, s.my * vz, s.mz * vz + pr, vz * ep}};
+          if (VISC) {
+            // F_m <- F_m - sqrt(eps) I_cub q_m   (solver.cpp:398-406)
+            const double se = sSe[e];
+            if (se > 0.0) {
+              const double* irow = p.icub + (size_t)q * C::NP;
+#pragma unroll
+              for (int m = 0; m < 3; ++m)
+#pragma unroll
+                for (int c = 0; c < 5; ++c) {
+                  const double* qrow = p.q + m * qstride + (size_t)(row0 + e * 5 + c) * C::BP;
+                  double qc = 0.0;
+                  for (int j = 0; j < C::NP; ++j) qc += __ldg(irow + j) * __ldg(qrow + j);
+                  F[m][c] -= se * qc;
+                }
+            }
+          }
+          const double* met = sMet + e * 9;
+#pragma unroll
+          for (int m = 0; m < 3; ++m) {
+            const double r0 = met[m * 3 + 0], r1 = met[m * 3 + 1], r2 = met[m * 3 + 2];
+#pragma unroll
+            for (int c = 0; c < 5; ++c)
+              gout[c * C::LDG + m * w] = r0 * F[0][c] + r1 * F[1][c] + r2 * F[2][c];
+          }
+        } else {
+#pragma unroll
+          for (int m = 0; m < 3; ++m)
+#pragma unroll
+            for (int c = 0; c < 5; ++c) gout[c * C::LDG + m * w] = 0.0;
+        }
+      }
+      __syncthreads();
+      // GEMM2 (volume part): acc += G[:, 0:3w] * Op2[:, k0:k0+3w]^T
+      {
+        const int ks0 = (3 * q0) / 4, nks = (3 * w) / 4;
+#pragma unroll
+        for (int i = 0; i < C::MAXT2; ++i) {
+          const int t = t_begin + i;
+          if (t < t_end) {
+            const int mt = t / C::NT2, nt = t % C::NT2;
+            const double* a_ptr = sG + (mt * 16 + g) * C::LDG + tq;
+            const double* b_ptr = p.frag_op2 + ((size_t)nt * C::KS2 + ks0) * 32 + lane;
+            for (int ks = 0; ks < nks; ++ks)
+              dmma_k4(acc[i], a_ptr[ks * 4], a_ptr[8 * C::LDG + ks * 4], __ldg(b_ptr + ks * 32));
+          }
+        }
+      }
+      __syncthreads();
+    }
+
+    // ---- surface: chunks of FCH face nodes ---------------------------------
+    for (int fc = 0; fc < C::NFCH; ++fc) {
+      const int f0 = fc * C::FCH;
+      const int w = (C::NF - f0) < C::FCH ? (C::NF - f0) : C::FCH;  // multiple of 4
+      for (int idx = tid; idx < C::E * w; idx += kThreads) {
+        const int e = idx / w, fl = idx % w, fq = f0 + fl;
+        const int f = fq / C::NG, gq = fq - f * C::NG;
+        double* gout = sG + (e * 5) * C::LDG + fl;
+        const int eg = e0 + e;
+        if (eg >= p.K) {
+#pragma unroll
+          for (int c = 0; c < 5; ++c) gout[c * C::LDG] = 0.0;
+          continue;
+        }
+        const double* tm = p.traces + (size_t)eg * 5 * C::TB + fq;
+        const State5 um{tm[0], tm[C::TB], tm[2 * C::TB], tm[3 * C::TB], tm[4 * C::TB]};
+        const double4 fn = sFace[e * 4 + f];
+        const int2 cw = sConn[e * 4 + f];
+        State5 up;
+        if (cw.x >= 0) {
+          const int nface = cw.y & 3, code = cw.y >> 8;
+          const int h = __ldg(p.code_map + code * C::NG + gq);
+          const double* tp = p.traces + (size_t)cw.x * 5 * C::TB + nface * C::NG + h;
+          up = State5{tp[0], tp[C::TB], tp[2 * C::TB], tp[3 * C::TB], tp[4 * C::TB]};
+        } else {
+          up = boundary_state(um, fn.x, fn.y, fn.z, (cw.y >> 2) & 3, p.gas);
+        }
+        if (!admissible(um, gamma) || !admissible(up, gamma))
+          record_error(p.err, 2, p.elem_offset + eg, f, gq, um.r);
+        double fs[5];
+        if (p.gas.riemann == 1)
+          hllc_flux(um, up, fn.x, fn.y, fn.z, gamma, fs);
+        else
+          llf_flux(um, up, fn.x, fn.y, fn.z, gamma, fs);
+        if (VISC) {
+          // BR1 central viscous flux with per-side sqrt(eps) (solver.cpp:438-453)
+          const double se = sSe[e];
+          const bool has_nb = cw.x >= 0;
+          const double snb = has_nb ? p.sqrt_eps[cw.x] : se;
+          const int h = has_nb ? __ldg(p.code_map + (cw.y >> 8) * C::NG + gq) : 0;
+          const double nrm[3] = {fn.x, fn.y, fn.z};
+#pragma unroll
+          for (int c = 0; c < 5; ++c) {
+            double visc = 0.0;
+#pragma unroll
+            for (int m = 0; m < 3; ++m) {
+              const double* qt = p.qtr + m * p.qtr_stride;
+              const double qs = qt[((size_t)eg * 5 + c) * C::TB + fq];
+              const double qn =
+                  has_nb ? qt[((size_t)cw.x * 5 + c) * C::TB + (cw.y & 3) * C::NG + h] : qs;
+              visc += 0.5 * (se * qs + snb * qn) * nrm[m];
+            }
+            fs[c] -= visc;
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 5; ++c) gout[c * C::LDG] = fn.w * fs[c];
+      }
+      __syncthreads();
+      {
+        const int ks0 = (C::K2CUB + f0) / 4, nks = w / 4;
+#pragma unroll
+        for (int i = 0; i < C::MAXT2; ++i) {
+          const int t = t_begin + i;
+          if (t < t_end) {
+            const int mt = t / C::NT2, nt = t % C::NT2;
+            const double* a_ptr = sG + (mt * 16 + g) * C::LDG + tq;
+            const double* b_ptr = p.frag_op2 + ((size_t)nt * C::KS2 + ks0) * 32 + lane;
+            for (int ks = 0; ks < nks; ++ks)
+              dmma_k4(acc[i], a_ptr[ks * 4], a_ptr[8 * C::LDG + ks * 4], __ldg(b_ptr + ks * 32));
+          }
+        }
+      }
+      __syncthreads();
+    }
+
+    // ---- epilogue: rhs -> (res, u) update or rhs store ---------------------
+    double a_c = 0.0, b_c = 0.0, dt = 0.0;
+    if (UPDATE) {
+      a_c = p.coef->a[p.stage];
+      b_c = p.coef->b[p.stage];
+      dt = p.coef->dt;
+    }
+#pragma unroll
+    for (int i = 0; i < C::MAXT2; ++i) {
+      const int t = t_begin + i;
+      if (t < t_end) {
+        const int mt = t / C::NT2, nt = t % C::NT2;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int r = mt * 16 + g + 8 * hh;
+          const int grow = row0 + r;
+          if (grow >= n_rows) continue;
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int col = nt * 8 + 2 * tq + v;
+            if (col >= C::NP) continue;
+            const double rhs = acc[i][2 * hh + v];
+            const size_t gi = (size_t)grow * C::BP + col;
+            if (UPDATE) {
+              const double rn = a_c * p.res[gi] + dt * rhs;
+              p.res[gi] = rn;
+              p.u[gi] = sU[r * C::LDU + col] + b_c * rn;
+            } else {
+              p.rhs_out[gi] = rhs;
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace cdg_gpu

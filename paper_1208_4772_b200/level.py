@@ -1,0 +1,115 @@
+"""Level setup for the GPU path: affine geometry, face coupling, node maps.
+
+Host-side restatement of the parts of ``DgLevel`` (solver.cpp:97-179) the
+kernels need, in compact per-element form (SURVEY.md §7 "Memory layout at
+scale": 26 doubles per affine element instead of ~125 KB of per-element
+operator matrices):
+
+* ``affine_geometry`` -- compute_mapping (operators.cpp:32-121) for a straight
+  tet: dx/dr = (v1-v0, v2-v0, v3-v0)/2, J = det, dr_m/dx_i = inverse, face
+  normal/sjac from the face-chart tangents (operators.cpp:98-118),
+  h = 6V/A (operators.hpp:37).
+* ``perm_node_maps`` -- the face-node pairing. The reference pairs nodes by
+  nearest physical point (solver.cpp:144-172); on conforming faces with the
+  symmetric face rules (quadrature.hpp:33-36) that pairing is the barycentric
+  permutation induced by FaceLink.perm (mesh.hpp:23-27), so one table per
+  vertex permutation replaces the per-face node_map (verified against the
+  reference's node_map in tests/test_level_vs_reference.py).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .mesh import PERMS, Mesh
+from .refelem import FACE_VERTS, TET_VERTS, ReferenceElement, pad16, tri_quadrature
+
+BC_KINDS = {"slip_wall": 0, "wall": 0, "farfield": 1, "symmetry": 2}
+
+
+def affine_geometry(vertices: np.ndarray, tets: np.ndarray, re: ReferenceElement):
+    v = vertices[tets]                                   # [K,4,3]
+    fwd = np.stack([(v[:, 1] - v[:, 0]) * 0.5, (v[:, 2] - v[:, 0]) * 0.5, (v[:, 3] - v[:, 0]) * 0.5],
+                   axis=2)                               # f[i][m] = dx_i/dr_m
+    jac = np.linalg.det(fwd)
+    if np.any(jac <= 1e-14):
+        e = int(np.argmax(jac <= 1e-14))
+        raise ArithmeticError(f"inverted element {e}: mapping Jacobian {jac[e]} at quadrature node 0")
+    inv = np.linalg.inv(fwd)                             # inv[m][i] = dr_m/dx_i
+    metric = inv.reshape(-1, 9)
+    normals = np.empty((tets.shape[0], 4, 3))
+    sjac = np.empty((tets.shape[0], 4))
+    for f, (a, b, c) in enumerate(FACE_VERTS):
+        ra = 0.5 * (TET_VERTS[b] - TET_VERTS[a])
+        rb = 0.5 * (TET_VERTS[c] - TET_VERTS[a])
+        xa = fwd @ ra
+        xb = fwd @ rb
+        nraw = np.cross(xa, xb)
+        s = np.linalg.norm(nraw, axis=1)
+        sjac[:, f] = s
+        normals[:, f] = nraw / s[:, None]
+    volume = jac * re.cub_weights.sum()
+    area = (sjac * re.face_weights.sum()).sum(axis=1)
+    return metric, jac, normals, sjac, 6.0 * volume / area
+
+
+def perm_node_maps(re: ReferenceElement) -> np.ndarray:
+    """[6][N_g] node maps, one per face-vertex permutation (PERMS order)."""
+    ng = re.n_face_quad
+    # barycentric coordinates of the 2D rule on (A, B, C): (1-u-v, u, v)
+    a, b = _face_rule_ab(re)
+    u, w = (a + 1.0) / 2.0, (b + 1.0) / 2.0
+    lam = np.stack([1.0 - u - w, u, w], axis=1)          # [ng,3]
+    maps = np.empty((len(PERMS), ng), np.int32)
+    for code, p in enumerate(PERMS):
+        theirs = np.empty_like(lam)
+        for i in range(3):
+            theirs[:, p[i]] = lam[:, i]
+        d = np.linalg.norm(theirs[:, None, :] - lam[None, :, :], axis=2)
+        maps[code] = np.argmin(d, axis=1)
+        if np.max(np.min(d, axis=1)) > 1e-10:
+            raise ArithmeticError("face rule is not invariant under the vertex permutation")
+    return maps
+
+
+def _face_rule_ab(re: ReferenceElement):
+    # recover (a, b) of face 0's chart from the embedded nodes: x = A + u(B-A) + v(C-A)
+    A, B, C = (TET_VERTS[i] for i in FACE_VERTS[0])
+    x = re.face_nodes[: re.n_face_quad]
+    m = np.stack([B - A, C - A], axis=1)
+    uv, *_ = np.linalg.lstsq(m, (x - A).T, rcond=None)
+    return 2.0 * uv[0] - 1.0, 2.0 * uv[1] - 1.0
+
+
+class LevelArrays:
+    """All host arrays behind one cdg_gpu_level_desc (kept alive by the owner)."""
+
+    def __init__(self, mesh: Mesh, re: ReferenceElement, bc: dict | int = 0, freestream=None,
+                 padded: bool = True):
+        K = mesh.n_owned
+        self.re = re
+        self.K = K
+        self.n_halo = mesh.n_halo
+        self.padded = padded
+        self.block = pad16(re.n_basis) if padded else re.n_basis
+        self.trace_block = pad16(4 * re.n_face_quad) if padded else 4 * re.n_face_quad
+        metric, jac, normals, sjac, h = affine_geometry(mesh.vertices, mesh.tets[:K], re)
+        self.metric = np.ascontiguousarray(metric)
+        self.jac = np.ascontiguousarray(jac)
+        self.face_normal = np.ascontiguousarray(normals)
+        self.face_sjac = np.ascontiguousarray(sjac)
+        self.h = np.ascontiguousarray(h)
+        self.neighbor = np.ascontiguousarray(mesh.neighbor[:K], np.int32)
+        self.neighbor_face = np.ascontiguousarray(np.maximum(mesh.neighbor_face[:K], 0), np.int32)
+        self.face_code = np.ascontiguousarray(np.maximum(mesh.perm_code[:K], 0), np.int32)
+        self.code_node_map = np.ascontiguousarray(perm_node_maps(re))
+        if isinstance(bc, (int, np.integer)):
+            kinds = np.full(K * 4, int(bc), np.int32).reshape(K, 4)
+        else:
+            kinds = np.zeros((K, 4), np.int32)
+            for tag_id, tag in enumerate(mesh.tags):
+                kinds[mesh.boundary_tag[:K] == tag_id] = BC_KINDS[bc[tag]] if isinstance(bc[tag], str) else bc[tag]
+        self.bc = np.ascontiguousarray(np.where(self.neighbor < 0, kinds, 0), np.int32)
+        self.freestream = np.zeros(5) if freestream is None else np.asarray(freestream, float)
+        self.tables = {k: np.ascontiguousarray(getattr(re, k)) for k in
+                       ("interp_cub", "interp_face", "deriv_r", "deriv_s", "deriv_t", "cub_weights",
+                        "face_weights", "vandermonde_inv")}

@@ -1,0 +1,190 @@
+"""GPU parity: the sm_100a path through the C ABI vs the oracle on the same
+seeded inputs (tolerances per north_star: conserved variables within 1e-12
+normwise-relative L_inf per RK step, bounded drift over N steps).
+
+RHS values are compared normwise-relative with a 1e-11 budget: the RHS is a
+discrete derivative (~h^-1 p^2 amplification of the 1e-15 rounding differences
+between the factored M^-1 operators and the reference's per-element Cholesky
+solve, operators.cpp:8-22)."""
+import numpy as np
+import pytest
+
+from oracle import port
+from paper_1208_4772_b200 import mesh as M
+from paper_1208_4772_b200 import refelem as R
+
+pytestmark = pytest.mark.gpu
+
+FS = None
+
+
+def _fs(gpu):
+    return gpu.make_state(1.0, [0.4, 0.05, -0.1], 1.0)
+
+
+def _pair(gpu, m, p, bc=1, curved=False):
+    fs = _fs(gpu)
+    re = R.level_reference_element(p, curved)
+    lv = gpu.GpuLevel(m, p, bc=bc, freestream=fs, re=re)
+    ol = port.OracleLevel(m, re, bc=bc, freestream=fs)
+    return lv, ol, fs
+
+
+def rel(a, b):
+    return np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300)
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("riemann", ["llf", "hllc"])
+def test_rhs_matches_oracle(gpu_lib, p, riemann):
+    gpu = gpu_lib
+    m = M.cube_mesh(2 if p <= 5 else 1, scale=4.0)
+    lv, ol, fs = _pair(gpu, m, p, bc=1)
+    cfg = gpu.run_config(riemann)
+    u = gpu.random_admissible_store(lv, seed=100 + p)
+    r_gpu = lv.compute_rhs(cfg, u)
+    r_ref = ol.compute_rhs(u, cfg)
+    assert rel(r_gpu, r_ref) < 1e-11
+    # padding slots stay zero (padded layout, solution_store.hpp:37-46)
+    assert np.all(r_gpu.reshape(lv.K, 5, lv.block)[:, :, lv.n_basis:] == 0.0)
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+@pytest.mark.parametrize("bc", [0, 1, 2])
+def test_rk_steps_match_oracle(gpu_lib, p, bc):
+    gpu = gpu_lib
+    m = M.cube_mesh(3, scale=2.0)
+    lv, ol, fs = _pair(gpu, m, p, bc=bc)
+    cfg = gpu.run_config("llf")
+    u0 = gpu.random_admissible_store(lv, seed=7)
+    lv.set_state(u0)
+    dt = 0.25 * lv.compute_timestep(cfg)
+    assert dt == pytest.approx(0.25 * ol.compute_timestep(u0, cfg), rel=1e-12)
+    res = np.zeros_like(u0)
+    u_ref = u0.copy()
+    worst = 0.0
+    for step in range(10):
+        lv.rk_steps(cfg, dt, 1)
+        u_ref, res = ol.rk_steps(u_ref, res, cfg, dt, 1)
+        u_gpu, res_gpu = lv.get_state()
+        e = rel(u_gpu, u_ref)
+        worst = max(worst, e)
+        if step == 0:
+            assert e < 1e-12, f"first step rel err {e:.2e}"
+    assert worst < 1e-11, f"drift over 10 steps {worst:.2e}"
+
+
+def test_traces_match_oracle(gpu_lib):
+    gpu = gpu_lib
+    m = M.cube_mesh(2)
+    lv, ol, fs = _pair(gpu, m, 3)
+    u = gpu.random_admissible_store(lv, seed=3)
+    lv.set_state(u)
+    t_gpu = lv.interpolate_to_faces()
+    t_ref = ol.interpolate_to_faces(u)
+    assert rel(t_gpu, t_ref) < 1e-13
+    tb = t_gpu.reshape(lv.K, 5, lv.trace_block)
+    assert np.all(tb[:, :, 4 * lv.n_face_quad:] == 0.0)
+
+
+def test_freestream_preservation(gpu_lib):
+    """test_solver.cpp:115-133 on the GPU path."""
+    gpu = gpu_lib
+    m = M.cube_mesh(2, scale=4.0)
+    fs = _fs(gpu)
+    cfg = gpu.run_config("llf")
+    for p, tol in ((1, 1e-12), (2, 1e-12), (3, 1e-12), (4, 2e-11)):
+        lv = gpu.GpuLevel(m, p, bc=1, freestream=fs)
+        r = lv.compute_rhs(cfg, gpu.freestream_store(lv, fs))
+        assert np.max(np.abs(r)) < tol, (p, np.max(np.abs(r)))
+
+
+def test_stationary_closed_element(gpu_lib):
+    """test_solver.cpp:135-142: single tet, slip walls, gas at rest."""
+    gpu = gpu_lib
+    rest = gpu.make_state(1.3, [0, 0, 0], 0.8)
+    lv = gpu.GpuLevel(M.single_tet(), 2, bc=0, freestream=rest)
+    r = lv.compute_rhs(gpu.run_config("llf"), gpu.freestream_store(lv, rest))
+    assert np.max(np.abs(r)) < 1e-12
+
+
+def test_inadmissible_abort_names_element_and_node(gpu_lib):
+    """test_solver.cpp:460-479."""
+    gpu = gpu_lib
+    m = M.cube_mesh(1)
+    fs = _fs(gpu)
+    lv = gpu.GpuLevel(m, 2, bc=1, freestream=fs)
+    u = gpu.freestream_store(lv, fs).reshape(lv.K, 5, lv.block)
+    u[3, 0, : lv.n_basis] = -1.0
+    with pytest.raises(gpu.NumericsError) as ei:
+        lv.compute_rhs(gpu.run_config("llf"), u.reshape(-1))
+    msg = str(ei.value)
+    assert "inadmissible" in msg and "element" in msg and "node" in msg
+    # the level stays usable after the error
+    r = lv.compute_rhs(gpu.run_config("llf"), gpu.freestream_store(lv, fs))
+    assert np.max(np.abs(r)) < 1e-11
+
+
+def test_determinism_bitwise(gpu_lib):
+    """test_solver.cpp:413-437: repeated runs are bitwise identical."""
+    gpu = gpu_lib
+    m = M.cube_mesh(3)
+    fs = _fs(gpu)
+    cfg = gpu.run_config("hllc")
+    outs = []
+    for _ in range(2):
+        lv = gpu.GpuLevel(m, 3, bc=1, freestream=fs)
+        u0 = gpu.random_admissible_store(lv, seed=11)
+        lv.set_state(u0)
+        dt = 0.25 * lv.compute_timestep(cfg)
+        lv.rk_steps(cfg, dt, 5)
+        outs.append(lv.get_state()[0])
+    assert np.array_equal(outs[0], outs[1])
+
+
+def test_padded_unpadded_bitwise(gpu_lib):
+    """test_solver.cpp:439-458."""
+    gpu = gpu_lib
+    m = M.cube_mesh(2)
+    fs = _fs(gpu)
+    cfg = gpu.run_config("llf")
+    res = []
+    for padded in (True, False):
+        lv = gpu.GpuLevel(m, 2, bc=1, freestream=fs, padded=padded)
+        u0 = gpu.random_admissible_store(lv, seed=5) if padded else None
+        if padded:
+            base = u0.reshape(lv.K, 5, lv.block)[:, :, : lv.n_basis].copy()
+        lv.set_state(base.reshape(-1) if not padded else u0)
+        dt = 0.01
+        lv.rk_steps(cfg, dt, 3)
+        u = lv.get_state()[0].reshape(lv.K, 5, lv.block)[:, :, : lv.n_basis]
+        res.append(u.copy())
+    assert np.array_equal(res[0], res[1])
+
+
+def test_zero_rhs_rk_step_keeps_freestream(gpu_lib):
+    """test_solver.cpp:230-244."""
+    gpu = gpu_lib
+    fs = _fs(gpu)
+    lv = gpu.GpuLevel(M.cube_mesh(1), 2, bc=1, freestream=fs)
+    u0 = gpu.freestream_store(lv, fs)
+    lv.set_state(u0)
+    lv.rk_steps(gpu.run_config("llf"), 1e-3, 1)
+    assert np.max(np.abs(lv.get_state()[0] - u0)) < 1e-13
+
+
+def test_residual_and_timestep(gpu_lib):
+    gpu = gpu_lib
+    m = M.cube_mesh(2)
+    lv, ol, fs = _pair(gpu, m, 2)
+    cfg = gpu.run_config("llf")
+    u0 = gpu.random_admissible_store(lv, seed=9)
+    lv.set_state(u0)
+    dt = lv.compute_timestep(cfg)
+    lv.snapshot()
+    lv.rk_steps(cfg, 0.2 * dt, 1)
+    u1 = lv.get_state()[0]
+    r_inf = lv.residual(0.2 * dt, "inf")
+    r_l2 = lv.residual(0.2 * dt, "l2")
+    assert r_inf == pytest.approx(np.max(np.abs(u1 - u0)) / (0.2 * dt), rel=1e-14)
+    assert r_l2 == pytest.approx(np.sqrt(np.sum((u1 - u0) ** 2)) / (0.2 * dt), rel=1e-12)
