@@ -1,0 +1,398 @@
+"""Benchmark: DOF-updates/s of the fused RK-stage RHS + low-storage update.
+
+Workload (BASELINE.json configs[4], the single-GPU-fitting headline config):
+make_cube_mesh(88) = 4,088,832 straight tets, P=4 (N_p=35, N_cub=70, N_f=64),
+LLF, slip walls, random admissible state (bench.cpp:22-40 recipe), FP64.
+One "step" = one LSRK4 step = 5 x (traces kernel + fused RHS/update kernel).
+DOF-updates/s = K * N_p * 5 fields * 5 stages * steps / time.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+N>1 (torchrun, one process per GPU, NCCL): strong scaling over z-slab
+partitions of the same mesh with a per-stage halo exchange of face traces.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+P_DEFAULT = 4
+N_DEFAULT = 88
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--p", type=int, default=P_DEFAULT)
+    ap.add_argument("--n", type=int, default=N_DEFAULT, help="cube cells per side (6 n^3 tets)")
+    ap.add_argument("--riemann", default="llf")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def freestream_state(mach=0.3, alpha_deg=0.0, rho=1.0, p=1.0, gamma=1.4):
+    """FreestreamConfig::state (config.cpp:12-24), the bench.cpp:155 state."""
+    c = math.sqrt(gamma * p / rho)
+    vmag = mach * c
+    a = math.radians(alpha_deg)
+    v = np.array([vmag * math.cos(a), 0.0, vmag * math.sin(a)])
+    return np.array([rho, rho * v[0], rho * v[1], rho * v[2], p / (gamma - 1.0) + 0.5 * rho * v.dot(v)])
+
+
+def model_flops_bytes(np_, ncub, nf):
+    """SURVEY.md §8d / BASELINE.md §2 per-element-per-stage model."""
+    F = 10 * (4 * np_ * ncub + 2 * np_ * nf + np_ * np_) + 30 * ncub + 130 * nf + 20 * np_
+    F_rhs = F - 10 * np_ * nf            # minus the I_g trace GEMV (separate kernel)
+    B = 160 * np_ + 80 * nf + 208 + 32
+    return F, F_rhs, B
+
+
+def kernel_flops_executed(np_, ncub, nf):
+    """DMMA flops the kernels issue per element per stage (padding included)."""
+    r4, r8 = (lambda x: (x + 3) // 4 * 4), (lambda x: (x + 7) // 8 * 8)
+    kp, ncub8, np8, nf8 = r4(np_), r8(ncub), r8(np_), r8(nf)
+    rhs = 2 * 5 * (ncub8 * kp + np8 * (3 * ncub8 + nf))
+    tr = 2 * 5 * nf8 * kp
+    return rhs, tr
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 4 + i and s[4 + i].lower().startswith("active")})
+        power = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "power_w_max": max(power) if power else None, "samples": len(self.samples)}
+
+
+def cpu_baseline(p, riemann, seconds_budget=25.0):
+    """The reference's own rk_step (oracle/_ref, all host threads) on a bounded
+    sample of the same workload; falls back to the C restatement (1 thread)."""
+    try:
+        from oracle import ref
+        if ref.available():
+            nthreads = ref.num_threads(os.cpu_count() or 1)
+            n_cpu = 14
+            mesh = ref.Mesh("cube", n_cpu)
+            lv = ref.Level(mesh, p, bc_wall=0, bc_far=1)
+            cfg = ref.make_cfg(riemann)
+            fs = freestream_state()
+            u = lv.random_admissible_store(42)
+            res = np.zeros_like(u)
+            dt = 0.5 * lv.compute_timestep(u, cfg)
+            u, res = lv.rk_steps(u, res, cfg, fs, dt, 1)  # warm-up
+            times = []
+            t_total = 0.0
+            while len(times) < 5 and t_total < seconds_budget:
+                t0 = time.perf_counter()
+                u, res = lv.rk_steps(u, res, cfg, fs, dt, 1)
+                times.append(time.perf_counter() - t0)
+                t_total += times[-1]
+            med = statistics.median(times)
+            dofs = lv.K * lv.n_basis * 5 * 5
+            return {"value": dofs / med, "unit": "DOF-updates/s", "cores": nthreads, "kind": "reference",
+                    "sample": f"make_cube_mesh({n_cpu}) = {lv.K} tets, P={p}, {len(times)} timed rk_step "
+                              f"(median {med:.3f} s), oracle/_ref (reference sources built in place)"}
+    except Exception as e:  # pragma: no cover - diagnostic path
+        err = repr(e)
+    else:
+        err = "oracle/_ref not built"
+    from oracle import port
+    from paper_1208_4772_b200 import gpu, mesh as M, refelem as R
+    m = M.cube_mesh(6)
+    re = R.get_reference_element(p)
+    ol = port.OracleLevel(m, re, bc=0, freestream=freestream_state())
+    cfg = gpu.run_config(riemann)
+    u = np.zeros(ol.store_size)
+    # same recipe via the product helper on a shape-compatible object
+    class _L:
+        K, n_basis, block = ol.K, re.n_basis, ol.block
+    u = gpu.random_admissible_store(_L, seed=42)
+    dt = 0.5 * ol.compute_timestep(u, cfg)
+    t0 = time.perf_counter()
+    ol.rk_steps(u, np.zeros_like(u), cfg, dt, 1)
+    t = time.perf_counter() - t0
+    return {"value": ol.K * re.n_basis * 25 / t, "unit": "DOF-updates/s", "cores": 1, "kind": "port",
+            "sample": f"make_cube_mesh(6) = {ol.K} tets, P={p}, 1 rk_step, C restatement ({err})"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU rk_step on this box's host cores."""
+    if rank != 0:
+        return
+    cb = cpu_baseline(args.p, args.riemann, seconds_budget=max(10.0, 4.0 * args.steps))
+    line = {"impl": "reference", "metric": "DOF-updates/sec (RK-stage RHS+update)", "value": cb["value"],
+            "unit": "DOF-updates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": f"make_cube_mesh P={args.p} (bounded CPU sample)",
+                                            "p": args.p, "riemann": args.riemann},
+            "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": "DOF-updates/s",
+                                        "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    from paper_1208_4772_b200 import gpu, partition, refelem as R
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    p = args.p
+    re = R.get_reference_element(p)
+    fs = freestream_state()
+    t_setup = time.perf_counter()
+    part = partition.rank_part(args.n, world, rank)
+    lv = gpu.GpuLevel(part.mesh, p, bc=0, freestream=fs, re=re, device=local_rank)
+    cfg = gpu.run_config(args.riemann, cfl=0.5)
+    K = lv.K
+    # random admissible state generated on the device (bench.cpp:22-40 recipe)
+    g = torch.Generator(device="cuda").manual_seed(42 + rank)
+    u = torch.zeros((K, 5, lv.block), dtype=torch.float64, device="cuda")
+    npb = lv.n_basis
+    j = lambda: (torch.rand((K, npb), generator=g, dtype=torch.float64, device="cuda") - 0.5) * 0.1
+    rho = 1.0 + j()
+    vx, vy, vz = 0.3 + j(), j(), j()
+    pr = 1.0 + j()
+    u[:, 0, :npb] = rho
+    u[:, 1, :npb] = rho * vx
+    u[:, 2, :npb] = rho * vy
+    u[:, 3, :npb] = rho * vz
+    u[:, 4, :npb] = pr / 0.4 + 0.5 * rho * (vx * vx + vy * vy + vz * vz)
+    del rho, vx, vy, vz, pr
+    lv.set_state_device(u.data_ptr(), None)
+    del u
+    torch.cuda.empty_cache()
+    dt = lv.compute_timestep(cfg)
+    if dist is not None:
+        t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        dt = float(t.item())
+    setup_s = time.perf_counter() - t_setup
+
+    # ---- halo plumbing (N>1) ------------------------------------------------
+    bufs = []
+    if world > 1:
+        per = 5 * lv.n_face_quad
+        send_all = np.concatenate([pe.send_elem_face for pe in part.peers])
+        recv_all = np.concatenate([pe.recv_elem_face for pe in part.peers])
+        sbuf = torch.empty(len(send_all) * per, dtype=torch.float64, device="cuda")
+        rbuf = torch.empty(len(recv_all) * per, dtype=torch.float64, device="cuda")
+        lv.halo_setup(send_all, recv_all, sbuf.data_ptr(), rbuf.data_ptr())
+        off_s = off_r = 0
+        for pe in part.peers:
+            ns, nr = len(pe.send_elem_face) * per, len(pe.recv_elem_face) * per
+            bufs.append((pe.rank, sbuf[off_s:off_s + ns], rbuf[off_r:off_r + nr]))
+            off_s += ns
+            off_r += nr
+    ext = torch.cuda.ExternalStream(lv.stream())
+
+    def step_multi():
+        with torch.cuda.stream(ext):
+            for stage in range(5):
+                lv.stage_phase(cfg, stage, 0, dt)
+                ops = []
+                for peer, sb, rb in bufs:
+                    ops.append(dist.P2POp(dist.isend, sb, peer))
+                    ops.append(dist.P2POp(dist.irecv, rb, peer))
+                for w in dist.batch_isend_irecv(ops):
+                    w.wait()
+                lv.stage_phase(cfg, stage, 1, dt)
+
+    def run_steps(n):
+        if world > 1:
+            for _ in range(n):
+                step_multi()
+        else:
+            lv.rk_steps(cfg, dt, n)
+
+    # ---- warm-up ------------------------------------------------------------
+    run_steps(args.warmup)
+    torch.cuda.synchronize()
+
+    # ---- timed region (device events on the level's stream, max over ranks) --
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    launches0 = lv.launch_count()
+    prof_tr = prof_rhs = 0.0
+    with ClockSampler(local_rank) as clk:
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0.record(ext)
+        if world > 1:
+            run_steps(args.steps)
+        else:
+            lv.set_profiling(True)       # per-kernel CUDA events on the launching stream
+            lv.rk_steps(cfg, dt, args.steps)
+            lv.set_profiling(False)
+            prof = lv.last_profile()
+            prof_tr, prof_rhs = float(prof[0]), float(prof[1])
+        ev1.record(ext)
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+    launches = lv.launch_count() - launches0
+    ms_total = ev0.elapsed_time(ev1)
+    if dist is not None:
+        t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    K_global = 6 * args.n ** 3
+    dofs_per_step = K_global * npb * 5 * 5
+    value = dofs_per_step * args.steps / (ms_total * 1e-3)
+    ms_per_step = ms_total / args.steps
+
+    # ---- end-to-end through the public API with host buffers -----------------
+    e2e = None
+    if not args.no_e2e and world == 1:
+        # per step: H2D of dt/RK coefficients (pinned), RK step, D2H residual
+        steps = max(3, args.steps // 2)
+        lv.rk_steps(cfg, dt, 1)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            lv.snapshot()
+            lv.rk_steps(cfg, dt, 1)
+            r = lv.residual(dt, "inf")
+        t_e2e = time.perf_counter() - t0
+        assert math.isfinite(r)
+        e2e = {"value": dofs_per_step * steps / t_e2e, "unit": "DOF-updates/s",
+               "h2d_bytes_per_step": 8 * 11, "d2h_bytes_per_step": 8 * 592,
+               "what": "per step: snapshot + cdg_gpu_rk_steps(1) (dt/a/b H2D) + cdg_gpu_residual (inf-norm "
+                       "partials D2H), wall clock, the run_steady check loop (solver.cpp:637-668)"}
+        # reference rk_step adapter semantics: full state host->device->host every step
+        u_host, res_host = lv.get_state()
+        t0 = time.perf_counter()
+        rt_steps = 2
+        for _ in range(rt_steps):
+            lv.set_state(u_host, res_host)
+            lv.rk_steps(cfg, dt, 1)
+            u_host, res_host = lv.get_state()
+        t_rt = time.perf_counter() - t0
+        e2e["roundtrip"] = {"value": dofs_per_step * rt_steps / t_rt, "unit": "DOF-updates/s",
+                            "h2d_bytes_per_step": 2 * u_host.nbytes, "d2h_bytes_per_step": 2 * u_host.nbytes,
+                            "what": "rk_step adapter: u,res H2D + 1 step + u,res D2H (pageable numpy)"}
+
+    # ---- roofline -----------------------------------------------------------
+    F, F_rhs, B = model_flops_bytes(npb, re.n_cub, 4 * re.n_face_quad)
+    ex_rhs, ex_tr = kernel_flops_executed(npb, re.n_cub, 4 * re.n_face_quad)
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    roof = None
+    if world == 1 and prof_rhs > 0:
+        fp64_dmma, fp64_dfma = gpu.measure_fp64_peak(local_rank)
+        launches_rhs = 5 * args.steps
+        t_rhs = prof_rhs / launches_rhs * 1e-3
+        t_tr = prof_tr / launches_rhs * 1e-3
+        achieved = F_rhs * K / t_rhs / 1e12
+        traffic = None
+        ncu_file = ROOT / "profiles" / f"ncu_rhs_p{p}.json"
+        if ncu_file.exists():
+            traffic = json.loads(ncu_file.read_text()).get("dram_bytes_per_launch")
+        roof = {"bound": "tensor", "achieved": achieved, "peak": fp64_dmma, "unit": "TFLOP/s",
+                "frac": achieved / fp64_dmma, "traffic": traffic,
+                "kernel": f"k_rhs<P={p}> (fused volume+surface+lift+LSRK update, FP64 DMMA)",
+                "algorithmic_flops_per_launch": F_rhs * K,
+                "peak_source": "FP64 DMMA (mma.sync.m16n8k4.f64) peak measured live on this GPU by "
+                               "cdg_gpu_measure_fp64_peak; MEASURED_PEAKS.json has no fp64 entry",
+                "fp64_dfma_peak_tflops": fp64_dfma,
+                "kernel_ms_avg": t_rhs * 1e3, "trace_kernel_ms_avg": t_tr * 1e3,
+                "rhs_share_of_stage": prof_rhs / (prof_rhs + prof_tr),
+                "executed_dmma_tflops": ex_rhs * K / t_rhs / 1e12,
+                "hbm_achieved_gbs": B * K / t_rhs / 1e9, "hbm_peak_gbs": hbm_peak,
+                "hbm_frac": B * K / t_rhs / 1e9 / hbm_peak,
+                "stage_model_tflops": F * K / ((t_rhs + t_tr)) / 1e12}
+
+    clocks = clk.summary()
+    line = {"metric": "DOF-updates/sec (RK-stage RHS+update), Euler P=4, 1/2/4/8 B200",
+            "value": value, "unit": "DOF-updates/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"make_cube_mesh({args.n}) = {K_global} straight tets, P={p} "
+                                   f"(N_p={npb}, N_cub={re.n_cub}, N_f={4 * re.n_face_quad}), {args.riemann.upper()}, "
+                                   f"slip walls, random admissible state (bench.cpp:22-40)",
+                       "elements": K_global, "p": p, "riemann": args.riemann, "dof": K_global * npb * 5,
+                       "partition": f"{world} z-slab(s)", "l2": "working set ~%.0f GB >> 126 MB L2 (no flush needed)"
+                       % (K_global * (3 * 5 * lv.device_block + 5 * lv.trace_block) * 8 / 1e9),
+                       "setup_s": round(setup_s, 1)},
+            "gpu_launches": launches, "clocks": clocks}
+    if e2e:
+        line["e2e"] = e2e
+    if roof:
+        line["roofline"] = roof
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(p, args.riemann)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -159,12 +159,13 @@ int cdg_gpu_snapshot(cdg_gpu_level *lv);
 int cdg_gpu_residual(cdg_gpu_level *lv, int kind, double dt, double *out);
 
 /* ---- multi-GPU halo plumbing (one process per GPU) --------------------------
- * send_idx: [n_send] trace rows (element*4+face) whose 5*N_g trace values are
- * packed into a contiguous device send buffer; recv rows land in ghost
- * elements K.. (element index, face). The transport (NCCL send/recv over
- * NVLink) is driven by the caller on `stream`. */
+ * send_elem_face[i] = element*4+face of an owned element whose face trace
+ * (5*N_g values) is packed into row i of the caller-owned DEVICE buffer
+ * send_buf [n_send][5][N_g]; recv_elem_face[i] names the ghost element
+ * (K..K+n_halo-1) and face that row i of recv_buf lands in. The transport
+ * (NCCL send/recv over NVLink) is driven by the caller on cdg_gpu_stream(). */
 int cdg_gpu_halo_setup(cdg_gpu_level *lv, int n_send, const int *send_elem_face, int n_recv,
-                       const int *recv_elem_face, double **send_buf, double **recv_buf);
+                       const int *recv_elem_face, double *send_buf, double *recv_buf);
 int cdg_gpu_halo_pack(cdg_gpu_level *lv);
 int cdg_gpu_halo_unpack(cdg_gpu_level *lv);
 /* Runs one RK stage in split form for overlap: trace kernel, then (caller
@@ -185,6 +186,9 @@ int cdg_gpu_set_profiling(cdg_gpu_level *lv, int enabled);
 int cdg_gpu_last_profile(cdg_gpu_level *lv, double *out3);
 
 const char *cdg_gpu_version(void);
+/* FP64 roofline denominators measured on `device`: out[0] DMMA TFLOP/s,
+ * out[1] DFMA TFLOP/s. */
+int cdg_gpu_measure_fp64_peak(int device, double *out);
 
 #ifdef __cplusplus
 }

@@ -19,6 +19,7 @@
 #include "cdg_aux.cuh"
 #include "cdg_gpu.h"
 #include "cdg_kernels.cuh"
+#include "cdg_peak.cuh"
 
 using namespace cdg_gpu;
 
@@ -362,6 +363,43 @@ extern "C" {
 
 const char* cdg_gpu_version(void) { return "cdg_gpu 0.1 (sm_100a, fp64 DMMA)"; }
 
+// out[0] = DMMA TFLOP/s, out[1] = DFMA TFLOP/s (best of 5, full-device grid)
+int cdg_gpu_measure_fp64_peak(int device, double* out) {
+  return guarded(nullptr, 0, [&] {
+    CUDA_OK(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    CUDA_OK(cudaGetDeviceProperties(&prop, device));
+    double* d = nullptr;
+    CUDA_OK(cudaMalloc(&d, sizeof(double)));
+    cudaEvent_t e0, e1;
+    CUDA_OK(cudaEventCreate(&e0));
+    CUDA_OK(cudaEventCreate(&e1));
+    const int blocks = prop.multiProcessorCount * 4, iters = 20000;
+    for (int kind = 0; kind < 2; ++kind) {
+      float best = 1e30f;
+      for (int rep = 0; rep < 6; ++rep) {
+        CUDA_OK(cudaEventRecord(e0));
+        if (kind == 0)
+          k_peak_dmma<<<blocks, 256>>>(d, iters);
+        else
+          k_peak_dfma<<<blocks, 256>>>(d, iters);
+        CUDA_OK(cudaEventRecord(e1));
+        CUDA_OK(cudaEventSynchronize(e1));
+        float ms;
+        CUDA_OK(cudaEventElapsedTime(&ms, e0, e1));
+        if (rep > 0) best = std::min(best, ms);
+      }
+      const double warps = blocks * 8.0;
+      const double flops = kind == 0 ? warps * iters * 8.0 * 16 * 8 * 4 * 2   // 8 mma/iter, 16x8x4 FMA
+                                     : blocks * 256.0 * iters * 8.0 * 2;     // 8 fma/iter/thread
+      out[kind] = flops / (best * 1e-3) / 1e12;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(d);
+  });
+}
+
 int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level** out, char* err,
                          size_t errlen) {
   *out = nullptr;
@@ -572,8 +610,7 @@ void cdg_gpu_level_destroy(cdg_gpu_level* lv) {
                   (void*)lv->d_icub, (void*)lv->d_maxeps, (void*)lv->metric, (void*)lv->face, (void*)lv->conn,
                   (void*)lv->code_map, (void*)lv->h, (void*)lv->frag_icub, (void*)lv->frag_op2,
                   (void*)lv->frag_ig, (void*)lv->frag_aux, (void*)lv->d_coef, (void*)lv->d_err,
-                  (void*)lv->d_scratch, (void*)lv->d_send_idx, (void*)lv->d_recv_idx,
-                  (void*)lv->send_buf, (void*)lv->recv_buf})
+                  (void*)lv->d_scratch, (void*)lv->d_send_idx, (void*)lv->d_recv_idx})
     if (p) cudaFree(p);
   if (lv->h_coef) cudaFreeHost(lv->h_coef);
   if (lv->h_err) cudaFreeHost(lv->h_err);
@@ -849,22 +886,22 @@ int cdg_gpu_residual(cdg_gpu_level* lv, int kind, double dt, double* out) {
 
 // ---- multi-GPU halo plumbing -------------------------------------------------
 int cdg_gpu_halo_setup(cdg_gpu_level* lv, int n_send, const int* send_ef, int n_recv, const int* recv_ef,
-                       double** send_buf, double** recv_buf) {
+                       double* send_buf, double* recv_buf) {
   return guarded(nullptr, 0, [&] {
     CUDA_OK(cudaSetDevice(lv->device));
+    if ((n_send && !send_buf) || (n_recv && !recv_buf))
+      throw Status(CDG_GPU_ERR_CONFIG, "halo_setup: device buffers required");
+    for (int i = 0; i < n_recv; ++i)
+      if ((recv_ef[i] >> 2) < lv->K || (recv_ef[i] >> 2) >= lv->K + lv->n_halo)
+        throw Status(CDG_GPU_ERR_CONFIG, "halo_setup: receive rows must be ghost elements");
     lv->n_send = n_send;
     lv->n_recv = n_recv;
-    const size_t per = (size_t)5 * lv->ng;
-    if (n_send) {
-      lv->d_send_idx = dev_upload(std::vector<int>(send_ef, send_ef + n_send));
-      CUDA_OK(cudaMalloc(&lv->send_buf, n_send * per * sizeof(double)));
-    }
-    if (n_recv) {
-      lv->d_recv_idx = dev_upload(std::vector<int>(recv_ef, recv_ef + n_recv));
-      CUDA_OK(cudaMalloc(&lv->recv_buf, n_recv * per * sizeof(double)));
-    }
-    if (send_buf) *send_buf = lv->send_buf;
-    if (recv_buf) *recv_buf = lv->recv_buf;
+    if (lv->d_send_idx) cudaFree(lv->d_send_idx);
+    if (lv->d_recv_idx) cudaFree(lv->d_recv_idx);
+    lv->d_send_idx = n_send ? dev_upload(std::vector<int>(send_ef, send_ef + n_send)) : nullptr;
+    lv->d_recv_idx = n_recv ? dev_upload(std::vector<int>(recv_ef, recv_ef + n_recv)) : nullptr;
+    lv->send_buf = send_buf;  // caller-owned (e.g. NCCL-registered torch tensors)
+    lv->recv_buf = recv_buf;
   });
 }
 

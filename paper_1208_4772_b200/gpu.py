@@ -99,7 +99,7 @@ def lib():
         L.cdg_gpu_timestep.argtypes = [vp, C.POINTER(RunConfig), C.c_int, _dp, C.c_char_p, C.c_size_t]
         L.cdg_gpu_snapshot.argtypes = [vp]
         L.cdg_gpu_residual.argtypes = [vp, C.c_int, C.c_double, _dp]
-        L.cdg_gpu_halo_setup.argtypes = [vp, C.c_int, _ip, C.c_int, _ip, C.POINTER(_dp), C.POINTER(_dp)]
+        L.cdg_gpu_halo_setup.argtypes = [vp, C.c_int, _ip, C.c_int, _ip, C.c_void_p, C.c_void_p]
         L.cdg_gpu_halo_pack.argtypes = [vp]
         L.cdg_gpu_halo_unpack.argtypes = [vp]
         L.cdg_gpu_rk_stage_phase.argtypes = [vp, C.POINTER(RunConfig), C.c_int, C.c_int, C.c_double, _dp, _dp,
@@ -111,6 +111,7 @@ def lib():
         L.cdg_gpu_set_profiling.argtypes = [vp, C.c_int]
         L.cdg_gpu_last_profile.argtypes = [vp, _dp]
         L.cdg_gpu_version.restype = C.c_char_p
+        L.cdg_gpu_measure_fp64_peak.argtypes = [C.c_int, _dp]
         _lib = L
     return _lib
 
@@ -274,13 +275,12 @@ class GpuLevel:
         return out
 
     # -- multi-GPU halo ---------------------------------------------------------
-    def halo_setup(self, send_elem_face: np.ndarray, recv_elem_face: np.ndarray):
+    def halo_setup(self, send_elem_face: np.ndarray, recv_elem_face: np.ndarray, send_ptr: int, recv_ptr: int):
+        """Register halo rows and the caller-owned device buffers (torch tensors)."""
         s = np.ascontiguousarray(send_elem_face, np.int32)
         r = np.ascontiguousarray(recv_elem_face, np.int32)
-        sb, rb = _dp(), _dp()
-        _raise(lib().cdg_gpu_halo_setup(self.h, len(s), _p(s), len(r), _p(r), C.byref(sb), C.byref(rb)),
+        _raise(lib().cdg_gpu_halo_setup(self.h, len(s), _p(s), len(r), _p(r), send_ptr, recv_ptr),
                "halo_setup failed")
-        return C.cast(sb, C.c_void_p).value, C.cast(rb, C.c_void_p).value
 
     def stage_phase(self, cfg: RunConfig, stage: int, phase: int, dt: float, a=LSRK_A, b=LSRK_B):
         a = np.ascontiguousarray(a, np.float64)
@@ -291,6 +291,13 @@ class GpuLevel:
 
     def stream(self) -> int:
         return int(lib().cdg_gpu_stream(self.h) or 0)
+
+
+def measure_fp64_peak(device: int = 0):
+    """(DMMA TFLOP/s, DFMA TFLOP/s) measured on the device."""
+    out = np.zeros(2)
+    _raise(lib().cdg_gpu_measure_fp64_peak(device, _p(out)), "fp64 peak measurement failed")
+    return float(out[0]), float(out[1])
 
 
 def freestream_store(level: GpuLevel, u_inf) -> np.ndarray:

@@ -1,0 +1,91 @@
+"""Multi-GPU host logic on CPU: slab partition, canonical halo ordering and a
+world_size-2 gloo exchange of face traces (computed by the oracle on the
+global mesh) that must land exactly on the ghost faces each rank expects."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1208_4772_b200 import mesh as M, partition as P
+
+
+@pytest.mark.parametrize("n,R", [(4, 2), (5, 3), (6, 4)])
+def test_partition_consistency(n, R):
+    g = M.cube_mesh(n)
+    parts = [P.rank_part(n, R, r) for r in range(R)]
+    assert sum(pt.mesh.n_owned for pt in parts) == g.n_owned
+    for pt in parts:
+        m, (lo, hi) = pt.mesh, pt.elem_range
+        loc = np.where(m.neighbor >= 0, m.global_ids[np.maximum(m.neighbor, 0)], -1)
+        assert np.array_equal(loc, g.neighbor[lo:hi])
+        assert np.array_equal(m.neighbor_face, g.neighbor_face[lo:hi])
+        assert np.array_equal(m.perm_code[m.neighbor >= 0], g.perm_code[lo:hi][m.neighbor >= 0])
+        for peer in pt.peers:
+            other = [q for q in parts[peer.rank].peers if q.rank == pt.rank][0]
+            se, sf = peer.send_elem_face >> 2, peer.send_elem_face & 3
+            re_, rf = other.recv_elem_face >> 2, other.recv_elem_face & 3
+            assert np.array_equal(m.global_ids[se], parts[peer.rank].mesh.global_ids[re_])
+            assert np.array_equal(sf, rf)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, n, q):
+    import torch
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import port as oport
+    from paper_1208_4772_b200 import gpu, refelem as R
+    p = 2
+    re = R.get_reference_element(p)
+    g = M.cube_mesh(n)
+    ol = oport.OracleLevel(g, re, bc=1, freestream=gpu.make_state(1, [0.3, 0, 0], 1))
+    rng = np.random.default_rng(3)
+    u = np.zeros((g.n_owned, 5, ol.block))
+    u[:, :, : re.n_basis] = 1.0 + 0.1 * rng.uniform(-1, 1, size=(g.n_owned, 5, re.n_basis))
+    traces = ol.interpolate_to_faces(u.reshape(-1)).reshape(g.n_owned, 5, ol.trace_block)
+    pt = P.rank_part(n, world, rank)
+    m = pt.mesh
+    ng = re.n_face_quad
+    ok = True
+    for peer in pt.peers:
+        se = m.global_ids[peer.send_elem_face >> 2]
+        sf = peer.send_elem_face & 3
+        send = np.stack([traces[e, :, f * ng:(f + 1) * ng] for e, f in zip(se, sf)])
+        recv = np.empty_like(send)
+        st = torch.from_numpy(send.copy())
+        rt = torch.from_numpy(recv)
+        ops = [dist.P2POp(dist.isend, st, peer.rank), dist.P2POp(dist.irecv, rt, peer.rank)]
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+        ge = m.global_ids[peer.recv_elem_face >> 2]
+        gf = peer.recv_elem_face & 3
+        expect = np.stack([traces[e, :, f * ng:(f + 1) * ng] for e, f in zip(ge, gf)])
+        ok = ok and np.array_equal(rt.numpy(), expect)
+    q.put((rank, ok, len(pt.peers)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_gloo_halo_exchange(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, 4, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=240) for _ in procs]
+    for pr in procs:
+        pr.join(timeout=60)
+    assert all(ok for _, ok, _ in res), res
+    assert all(npeers == 1 for _, _, npeers in res)
