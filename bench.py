@@ -225,6 +225,7 @@ def main():
     u[:, 3, :npb] = rho * vz
     u[:, 4, :npb] = pr / 0.4 + 0.5 * rho * (vx * vx + vy * vy + vz * vz)
     del rho, vx, vy, vz, pr
+    torch.cuda.synchronize()  # the level copies on its own (non-blocking) stream
     lv.set_state_device(u.data_ptr(), None)
     del u
     torch.cuda.empty_cache()
@@ -346,7 +347,7 @@ def main():
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     roof = None
     if world == 1 and prof_rhs > 0:
-        fp64_dmma, fp64_dfma = gpu.measure_fp64_peak(local_rank)
+        fp64_dmma, fp64_dfma, fp64_k8, fp64_k16 = gpu.measure_fp64_peak(local_rank)
         launches_rhs = 5 * args.steps
         t_rhs = prof_rhs / launches_rhs * 1e-3
         t_tr = prof_tr / launches_rhs * 1e-3
@@ -361,7 +362,8 @@ def main():
                 "algorithmic_flops_per_launch": F_rhs * K,
                 "peak_source": "FP64 DMMA (mma.sync.m16n8k4.f64) peak measured live on this GPU by "
                                "cdg_gpu_measure_fp64_peak; MEASURED_PEAKS.json has no fp64 entry",
-                "fp64_dfma_peak_tflops": fp64_dfma,
+                "fp64_dfma_peak_tflops": fp64_dfma, "fp64_dmma_k8_tflops": fp64_k8,
+                "fp64_dmma_k16_tflops": fp64_k16,
                 "kernel_ms_avg": t_rhs * 1e3, "trace_kernel_ms_avg": t_tr * 1e3,
                 "rhs_share_of_stage": prof_rhs / (prof_rhs + prof_tr),
                 "executed_dmma_tflops": ex_rhs * K / t_rhs / 1e12,

@@ -175,6 +175,10 @@ int cdg_gpu_rk_stage_phase(cdg_gpu_level *lv, const cdg_gpu_run_config *cfg, int
                            double dt, const double a[5], const double b[5], char *err,
                            size_t errlen);
 
+/* Replace the farfield ghost state (compute_rhs/rk_step take it per call,
+ * solver.hpp:94-109). */
+int cdg_gpu_set_freestream(cdg_gpu_level *lv, const double *freestream5);
+
 /* CUDA stream (cudaStream_t) the level launches on. */
 void *cdg_gpu_stream(cdg_gpu_level *lv);
 /* Kernel launches issued by this level since creation (evidence counter). */
@@ -186,8 +190,8 @@ int cdg_gpu_set_profiling(cdg_gpu_level *lv, int enabled);
 int cdg_gpu_last_profile(cdg_gpu_level *lv, double *out3);
 
 const char *cdg_gpu_version(void);
-/* FP64 roofline denominators measured on `device`: out[0] DMMA TFLOP/s,
- * out[1] DFMA TFLOP/s. */
+/* FP64 roofline denominators measured on `device` (TFLOP/s): out[0] DMMA
+ * m16n8k4, out[1] DFMA, out[2] DMMA m16n8k8, out[3] DMMA m16n8k16. */
 int cdg_gpu_measure_fp64_peak(int device, double *out);
 
 #ifdef __cplusplus

@@ -1,0 +1,195 @@
+// cdg_gpu_adapter.cpp -- the reference-side binding: implements the reference
+// solver kernel API (proj/core/include/cdg/solver.hpp:83-109) on top of the
+// C ABI in include/cdg_gpu.h, so reference code (run_steady, the CLI, the
+// reference's own unit tests) calls the B200 path unchanged.
+//
+//   cdg::make_workspace        solver.hpp:84   -> cdg_gpu_level_create
+//   cdg::interpolate_to_faces  solver.hpp:87   -> cdg_gpu_interpolate_to_faces
+//   cdg::compute_rhs           solver.hpp:94   -> cdg_gpu_compute_rhs
+//   cdg::current_viscosity     solver.hpp:100  -> cdg_gpu_viscosity
+//   cdg::aux_gradient          solver.hpp:103  -> cdg_gpu_aux_gradient
+//   cdg::rk_step               solver.hpp:107  -> cdg_gpu_rk_steps (1 step)
+//
+// Build (reference side): compile this file against proj/core/include, link
+// libcdg_gpu.so, and compile solver.cpp with the six names above renamed
+// (e.g. -Dcompute_rhs=compute_rhs_cpu ...; oracle/Makefile target
+// test_solver_gpu does exactly this to run the reference's test_solver.cpp on
+// the GPU). Exceptions and messages are the reference's: status 3 ->
+// NumericsError, 2 -> ConfigError.
+#include <cmath>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "cdg/solver.hpp"
+#include "cdg_gpu.h"
+
+namespace cdg {
+
+struct RhsWorkspace {
+  const DgLevel* level = nullptr;
+  cdg_gpu_level* lv = nullptr;
+  std::vector<double> eps;
+  std::array<SolutionStore, 3> q;
+  ~RhsWorkspace() {
+    if (lv) cdg_gpu_level_destroy(lv);
+  }
+};
+
+namespace {
+
+void throw_status(int st, const char* msg) {
+  if (st == 0) return;
+  if (st == CDG_GPU_ERR_NUMERICS) throw NumericsError(msg);
+  if (st == CDG_GPU_ERR_CONFIG) throw ConfigError(msg);
+  throw std::runtime_error(std::string("cdg_gpu: ") + msg);
+}
+
+std::vector<double> row_major(const Eigen::MatrixXd& m) {
+  std::vector<double> out(static_cast<size_t>(m.rows() * m.cols()));
+  for (Eigen::Index i = 0; i < m.rows(); ++i)
+    for (Eigen::Index j = 0; j < m.cols(); ++j) out[static_cast<size_t>(i * m.cols() + j)] = m(i, j);
+  return out;
+}
+
+cdg_gpu_level* create_level(const DgLevel& level, const ConservedState& fs) {
+  const auto& re = level.refelem();
+  const int K = level.n_elements(), np = re.n_basis(), ncub = re.n_cub(), ng = re.n_face_quad();
+  std::vector<double> icub = row_major(re.interp_cub()), ig = row_major(re.interp_face()),
+                      dr = row_major(re.deriv_r()), ds = row_major(re.deriv_s()),
+                      dt = row_major(re.deriv_t()), vinv = row_major(re.vandermonde_inv());
+  std::vector<double> metric(9 * (size_t)K), jac(K), normal(12 * (size_t)K), sjac(4 * (size_t)K), h(K);
+  std::vector<int> nb(4 * (size_t)K), nbf(4 * (size_t)K), bc(4 * (size_t)K), nmap(4 * (size_t)K * ng);
+  for (int e = 0; e < K; ++e) {
+    const auto& g = level.geom(e);
+    // the GPU path consumes affine (constant) geometry; curved elements carry
+    // per-node metrics that this adapter does not forward yet
+    for (int q = 1; q < ncub; ++q)
+      if (std::abs(g.cub_jac[q] - g.cub_jac[0]) > 1e-10 * std::abs(g.cub_jac[0]))
+        throw ConfigError("cdg_gpu adapter: curved element " + std::to_string(e) +
+                          " (per-node metrics) is not supported by this build");
+    for (int k = 0; k < 9; ++k) metric[9 * (size_t)e + k] = g.cub_dr[0][k];
+    jac[e] = g.cub_jac[0];
+    h[e] = g.h();
+    for (int f = 0; f < 4; ++f) {
+      for (int d = 0; d < 3; ++d) normal[12 * (size_t)e + 3 * f + d] = g.face_normal[f * ng][d];
+      sjac[4 * (size_t)e + f] = g.face_sjac[f * ng];
+      const auto& fc = level.coupling(e, f);
+      nb[4 * (size_t)e + f] = fc.neighbor;
+      nbf[4 * (size_t)e + f] = fc.neighbor >= 0 ? fc.neighbor_face : 0;
+      bc[4 * (size_t)e + f] = static_cast<int>(fc.bc);
+      for (int gg = 0; gg < ng; ++gg)
+        nmap[(4 * (size_t)e + f) * ng + gg] = fc.neighbor >= 0 ? fc.node_map[gg] : 0;
+    }
+  }
+  cdg_gpu_level_desc d{};
+  d.degree = re.degree();
+  d.n_basis = np;
+  d.n_cub = ncub;
+  d.n_face_quad = ng;
+  d.n_elements = K;
+  d.n_halo = 0;
+  d.padded = level.padded() ? 1 : 0;
+  d.interp_cub = icub.data();
+  d.interp_face = ig.data();
+  d.deriv_r = dr.data();
+  d.deriv_s = ds.data();
+  d.deriv_t = dt.data();
+  d.cub_weights = re.cub_weights().data();
+  d.face_weights = re.face_weights().data();
+  d.vandermonde_inv = vinv.data();
+  d.metric = metric.data();
+  d.jac = jac.data();
+  d.face_normal = normal.data();
+  d.face_sjac = sjac.data();
+  d.h = h.data();
+  d.neighbor = nb.data();
+  d.neighbor_face = nbf.data();
+  d.bc = bc.data();
+  d.node_map = nmap.data();
+  for (int c = 0; c < 5; ++c) d.freestream[c] = fs[c];
+  cdg_gpu_level* lv = nullptr;
+  char err[512] = {0};
+  throw_status(cdg_gpu_level_create(&d, 0, &lv, err, sizeof err), err);
+  return lv;
+}
+
+cdg_gpu_run_config to_cfg(const RunConfig& cfg) {
+  cdg_gpu_run_config c{};
+  if (cfg.riemann == "llf")
+    c.riemann = CDG_GPU_RIEMANN_LLF;
+  else if (cfg.riemann == "hllc")
+    c.riemann = CDG_GPU_RIEMANN_HLLC;
+  else
+    throw ConfigError("unknown Riemann solver '" + cfg.riemann + "' (llf|hllc)");
+  c.gamma = cfg.gas.gamma;
+  c.visc_enabled = cfg.viscosity.enabled;
+  c.eps0 = cfg.viscosity.eps0;
+  c.kappa = cfg.viscosity.kappa;
+  c.s0_offset = cfg.viscosity.s0_offset;
+  c.indicator_component = cfg.viscosity.indicator_component;
+  c.jacobian_weighted = cfg.viscosity.jacobian_weighted;
+  c.cfl = cfg.cfl;
+  return c;
+}
+
+void ensure_level(RhsWorkspace& ws, const ConservedState& fs) {
+  if (!ws.lv) ws.lv = create_level(*ws.level, fs);
+  double f[5] = {fs[0], fs[1], fs[2], fs[3], fs[4]};
+  throw_status(cdg_gpu_set_freestream(ws.lv, f), "set_freestream failed");
+}
+
+}  // namespace
+
+std::shared_ptr<RhsWorkspace> make_workspace(const DgLevel& level) {
+  auto ws = std::make_shared<RhsWorkspace>();
+  ws->level = &level;
+  ws->eps.assign(level.n_elements(), 0.0);
+  return ws;
+}
+
+void interpolate_to_faces(const DgLevel& level, const SolutionStore& u, SolutionStore& traces) {
+  RhsWorkspace ws;
+  ws.level = &level;
+  ensure_level(ws, ConservedState{});
+  throw_status(cdg_gpu_set_state(ws.lv, u.raw().data(), nullptr), "set_state failed");
+  throw_status(cdg_gpu_interpolate_to_faces(ws.lv, traces.raw().data()), "interpolate_to_faces failed");
+}
+
+void compute_rhs(const DgLevel& level, const SolutionStore& u, const RunConfig& cfg,
+                 const ConservedState& freestream, SolutionStore& rhs, RhsWorkspace& ws) {
+  (void)level;
+  ensure_level(ws, freestream);
+  const cdg_gpu_run_config c = to_cfg(cfg);
+  char err[512] = {0};
+  throw_status(cdg_gpu_set_state(ws.lv, u.raw().data(), nullptr), "set_state failed");
+  throw_status(cdg_gpu_compute_rhs(ws.lv, &c, rhs.raw().data(), err, sizeof err), err);
+  if (cfg.viscosity.enabled) {
+    throw_status(cdg_gpu_viscosity(ws.lv, ws.eps.data()), "viscosity failed");
+    for (int m = 0; m < 3; ++m) {
+      if (ws.q[m].n_elements() == 0) ws.q[m] = ws.level->make_store();
+      if (cdg_gpu_aux_gradient(ws.lv, m, ws.q[m].raw().data()) != 0) break;  // inviscid evaluation
+    }
+  }
+}
+
+const std::vector<double>& current_viscosity(const RhsWorkspace& ws) { return ws.eps; }
+
+const SolutionStore& aux_gradient(const RhsWorkspace& ws, int direction) { return ws.q[direction]; }
+
+void rk_step(const DgLevel& level, SolutionStore& u, SolutionStore& res, const RunConfig& cfg,
+             const ConservedState& freestream, double dt, const RKScheme& scheme, RhsWorkspace& ws) {
+  (void)level;
+  ensure_level(ws, freestream);
+  const cdg_gpu_run_config c = to_cfg(cfg);
+  char err[512] = {0};
+  throw_status(cdg_gpu_set_state(ws.lv, u.raw().data(), res.raw().data()), "set_state failed");
+  throw_status(cdg_gpu_rk_steps(ws.lv, &c, 1, dt, scheme.a.data(), scheme.b.data(), err, sizeof err), err);
+  throw_status(cdg_gpu_get_state(ws.lv, u.raw().data(), res.raw().data()), "get_state failed");
+  if (cfg.viscosity.enabled) throw_status(cdg_gpu_viscosity(ws.lv, ws.eps.data()), "viscosity failed");
+}
+
+}  // namespace cdg

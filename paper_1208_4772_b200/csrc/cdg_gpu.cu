@@ -363,7 +363,8 @@ extern "C" {
 
 const char* cdg_gpu_version(void) { return "cdg_gpu 0.1 (sm_100a, fp64 DMMA)"; }
 
-// out[0] = DMMA TFLOP/s, out[1] = DFMA TFLOP/s (best of 5, full-device grid)
+// out[0] = DMMA m16n8k4, out[1] = DFMA, out[2] = DMMA m16n8k8, out[3] = DMMA m16n8k16 TFLOP/s
+// (best of 5, 4 CTAs x 8 warps per SM)
 int cdg_gpu_measure_fp64_peak(int device, double* out) {
   return guarded(nullptr, 0, [&] {
     CUDA_OK(cudaSetDevice(device));
@@ -375,14 +376,18 @@ int cdg_gpu_measure_fp64_peak(int device, double* out) {
     CUDA_OK(cudaEventCreate(&e0));
     CUDA_OK(cudaEventCreate(&e1));
     const int blocks = prop.multiProcessorCount * 4, iters = 20000;
-    for (int kind = 0; kind < 2; ++kind) {
+    for (int kind = 0; kind < 4; ++kind) {
       float best = 1e30f;
       for (int rep = 0; rep < 6; ++rep) {
         CUDA_OK(cudaEventRecord(e0));
         if (kind == 0)
           k_peak_dmma<<<blocks, 256>>>(d, iters);
-        else
+        else if (kind == 1)
           k_peak_dfma<<<blocks, 256>>>(d, iters);
+        else if (kind == 2)
+          k_peak_dmma8<<<blocks, 256>>>(d, iters / 2);
+        else
+          k_peak_dmma16<<<blocks, 256>>>(d, iters / 4);
         CUDA_OK(cudaEventRecord(e1));
         CUDA_OK(cudaEventSynchronize(e1));
         float ms;
@@ -390,8 +395,8 @@ int cdg_gpu_measure_fp64_peak(int device, double* out) {
         if (rep > 0) best = std::min(best, ms);
       }
       const double warps = blocks * 8.0;
-      const double flops = kind == 0 ? warps * iters * 8.0 * 16 * 8 * 4 * 2   // 8 mma/iter, 16x8x4 FMA
-                                     : blocks * 256.0 * iters * 8.0 * 2;     // 8 fma/iter/thread
+      double flops = warps * iters * 8.0 * 16 * 8 * 4 * 2;  // 8 mma/iter, 16x8x4 FMA (k8: iters/2, k16: iters/4)
+      if (kind == 1) flops = blocks * 256.0 * iters * 8.0 * 2;  // 8 fma/iter/thread
       out[kind] = flops / (best * 1e-3) / 1e12;
     }
     cudaEventDestroy(e0);
@@ -794,6 +799,20 @@ int cdg_gpu_rk_steps(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, int nstep
     CUDA_OK(cudaGetLastError());
     check_device_error(lv);
   });
+}
+
+int cdg_gpu_set_freestream(cdg_gpu_level* lv, const double* fs) {
+  bool same = true;
+  for (int c = 0; c < 5; ++c) same = same && lv->gas.fs[c] == fs[c];
+  if (!same && lv->graph) {  // kernel params are baked into the captured graph
+    cudaGraphExecDestroy(lv->graph);
+    lv->graph = nullptr;
+  }
+  for (int c = 0; c < 5; ++c) {
+    lv->freestream[c] = fs[c];
+    lv->gas.fs[c] = fs[c];
+  }
+  return CDG_GPU_OK;
 }
 
 int cdg_gpu_set_profiling(cdg_gpu_level* lv, int enabled) {

@@ -294,10 +294,10 @@ class GpuLevel:
 
 
 def measure_fp64_peak(device: int = 0):
-    """(DMMA TFLOP/s, DFMA TFLOP/s) measured on the device."""
-    out = np.zeros(2)
+    """(DMMA m16n8k4, DFMA, DMMA m16n8k8, DMMA m16n8k16) TFLOP/s measured on the device."""
+    out = np.zeros(4)
     _raise(lib().cdg_gpu_measure_fp64_peak(device, _p(out)), "fp64 peak measurement failed")
-    return float(out[0]), float(out[1])
+    return tuple(float(x) for x in out)
 
 
 def freestream_store(level: GpuLevel, u_inf) -> np.ndarray:

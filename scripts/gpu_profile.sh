@@ -1,4 +1,5 @@
 set -x
+python -c "from paper_1208_4772_b200 import gpu; gpu.lib(); print(gpu.measure_fp64_peak())"
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv
 timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_r1.json 2> gpurun_out/bench_r1.err
 tail -3 gpurun_out/bench_r1.err; cat gpurun_out/bench_r1.json
