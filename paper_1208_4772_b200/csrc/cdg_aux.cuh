@@ -79,7 +79,7 @@ struct AuxParams {
 };
 
 template <class C>
-__global__ void __launch_bounds__(kThreads, 1) k_aux_q(AuxParams p) {
+__global__ void __launch_bounds__(kThreads, C::MINB) k_aux_q(AuxParams p) {
   extern __shared__ __align__(16) double smem[];
   double* sU = smem;
   double* sC = sU + C::SMEM_U;
@@ -93,16 +93,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_aux_q(AuxParams p) {
   const int n_rows = p.K * 5;
   const size_t qstride = (size_t)p.K * 5 * C::BP;
   const int t_begin = (warp * C::T2) / kWarps, t_end = ((warp + 1) * C::T2) / kWarps;
+  const double2* fb1 = reinterpret_cast<const double2*>(p.frag_icub);
+  const double2* fba = reinterpret_cast<const double2*>(p.frag_aux);
 
   for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
     const int e0 = tile * C::E, row0 = e0 * 5;
-    constexpr int V = C::KP / 2;
-    for (int idx = tid; idx < C::R * V; idx += kThreads) {
-      const int r = idx / V, v = idx % V;
-      double2 x = make_double2(0.0, 0.0);
-      if (row0 + r < n_rows) x = *(reinterpret_cast<const double2*>(p.u + (size_t)(row0 + r) * C::BP) + v);
-      *reinterpret_cast<double2*>(sU + r * C::LDU + 2 * v) = x;
-    }
+    stage_rows<C>(p.u, row0, n_rows, sU, tid);
     for (int idx = tid; idx < C::E * 9; idx += kThreads)
       sMet[idx] = e0 + idx / 9 < p.K ? p.metric[(size_t)e0 * 9 + idx] : 0.0;
     for (int idx = tid; idx < C::E * 4; idx += kThreads) {
@@ -120,54 +116,33 @@ __global__ void __launch_bounds__(kThreads, 1) k_aux_q(AuxParams p) {
       for (int ch = 0; ch < C::NCH; ++ch) {
         const int q0 = ch * C::CH;
         const int w = (C::NCUB8 - q0) < C::CH ? (C::NCUB8 - q0) : C::CH;
-        const int nt1 = w / 8, T1 = C::MT * nt1;
-        for (int t = warp; t < T1; t += kWarps) {
-          const int mt = t / nt1, nt = t % nt1;
-          double c1[4] = {0.0, 0.0, 0.0, 0.0};
-          const double* a_ptr = sU + (mt * 16 + g) * C::LDU + tq;
-          const double* b_ptr = p.frag_icub + ((size_t)(q0 / 8 + nt) * C::KS1) * 32 + lane;
-          for (int ks = 0; ks < C::KS1; ++ks)
-            dmma_k4(c1, a_ptr[ks * 4], a_ptr[8 * C::LDU + ks * 4], __ldg(b_ptr + ks * 32));
-          double* o = sC + (mt * 16 + g) * C::LDC + nt * 8 + 2 * tq;
-          *reinterpret_cast<double2*>(o) = make_double2(c1[0], c1[1]);
-          *reinterpret_cast<double2*>(o + 8 * C::LDC) = make_double2(c1[2], c1[3]);
-        }
+        gemm1_chunk<C>(sU, sC, fb1, q0, w, warp, lane);
         __syncthreads();
-        // G_k = -se * r_{k,m} * U_cub  for every field
+        // G_k = -se * r_{k,m} * U_cub  for every field (solver.cpp:283-289)
         for (int idx = tid; idx < C::R * w; idx += kThreads) {
           const int r = idx / w, ql = idx % w, e = r / 5;
           const double uc = (q0 + ql < C::NCUB) ? sC[r * C::LDC + ql] : 0.0;
           const double se = sSe[e];
 #pragma unroll
-          for (int k = 0; k < 3; ++k) sG[r * C::LDG + k * w + ql] = -se * (sMet[e * 9 + k * 3 + m] * uc);
+          for (int k = 0; k < 3; ++k) sG[r * C::LDG + pcol(k * w + ql)] = -se * (sMet[e * 9 + k * 3 + m] * uc);
         }
         __syncthreads();
-        const int ks0 = (3 * q0) / 4, nks = (3 * w) / 4;
-#pragma unroll
-        for (int i = 0; i < C::MAXT2; ++i) {
-          const int t = t_begin + i;
-          if (t < t_end) {
-            const int mt = t / C::NT2, nt = t % C::NT2;
-            const double* a_ptr = sG + (mt * 16 + g) * C::LDG + tq;
-            const double* b_ptr = p.frag_aux + ((size_t)nt * C::KS2 + ks0) * 32 + lane;
-            for (int ks = 0; ks < nks; ++ks)
-              dmma_k4(acc[i], a_ptr[ks * 4], a_ptr[8 * C::LDG + ks * 4], __ldg(b_ptr + ks * 32));
-          }
-        }
+        gemm2_partial<C>(acc, sG, fba, (3 * q0) / 8, (3 * w) / 8, t_begin, t_end, lane);
         __syncthreads();
       }
       for (int fc = 0; fc < C::NFCH; ++fc) {
         const int f0 = fc * C::FCH;
-        const int w = (C::NF - f0) < C::FCH ? (C::NF - f0) : C::FCH;
-        for (int idx = tid; idx < C::E * w; idx += kThreads) {
-          const int e = idx / w, fl = idx % w, fq = f0 + fl;
-          const int f = fq / C::NG, gq = fq - f * C::NG;
+        const int wr = (C::NF - f0) < C::FCH ? (C::NF - f0) : C::FCH;
+        const int wp = round_up(wr, 8);
+        for (int idx = tid; idx < C::E * wp; idx += kThreads) {
+          const int e = idx / wp, fl = idx % wp, fq = f0 + fl;
           const int eg = e0 + e;
-          double* gout = sG + (e * 5) * C::LDG + fl;
-          if (eg >= p.K) {
+          double* gout = sG + (e * 5) * C::LDG + pcol(fl);
+          if (eg >= p.K || fl >= wr) {
             for (int c = 0; c < 5; ++c) gout[c * C::LDG] = 0.0;
             continue;
           }
+          const int f = fq / C::NG, gq = fq - f * C::NG;
           const double* tm = p.traces + (size_t)eg * 5 * C::TB + fq;
           const State5 um{tm[0], tm[C::TB], tm[2 * C::TB], tm[3 * C::TB], tm[4 * C::TB]};
           const double4 fn = sFace[e * 4 + f];
@@ -190,18 +165,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_aux_q(AuxParams p) {
           for (int c = 0; c < 5; ++c) gout[c * C::LDG] = fn.w * (0.5 * (se * umv[c] + snb * upv[c]) * nm);
         }
         __syncthreads();
-        const int ks0 = (C::K2CUB + f0) / 4, nks = w / 4;
-#pragma unroll
-        for (int i = 0; i < C::MAXT2; ++i) {
-          const int t = t_begin + i;
-          if (t < t_end) {
-            const int mt = t / C::NT2, nt = t % C::NT2;
-            const double* a_ptr = sG + (mt * 16 + g) * C::LDG + tq;
-            const double* b_ptr = p.frag_aux + ((size_t)nt * C::KS2 + ks0) * 32 + lane;
-            for (int ks = 0; ks < nks; ++ks)
-              dmma_k4(acc[i], a_ptr[ks * 4], a_ptr[8 * C::LDG + ks * 4], __ldg(b_ptr + ks * 32));
-          }
-        }
+        gemm2_partial<C>(acc, sG, fba, (C::K2CUB + f0) / 8, wp / 8, t_begin, t_end, lane);
         __syncthreads();
       }
 #pragma unroll

@@ -49,7 +49,7 @@ int pad16(int n) { return 16 * ((n + 15) / 16); }
 
 // ---- kernel dispatch per (N_p, N_cub, N_g) ---------------------------------
 struct KernelSet {
-  int np, ncub, ng, E;
+  int np, ncub, ng, E, minb, ch;
   size_t smem_traces, smem_rhs;
   void (*traces)(const double*, double*, const double*, int, int);
   void (*rhs_update)(RhsParams);
@@ -59,14 +59,16 @@ struct KernelSet {
   void (*visc_rhs_only)(RhsParams);
 };
 
-template <int NP, int NCUB, int NG, int E>
+template <int NP, int NCUB, int NG, int E, int CH = 16, int MINB = 1>
 KernelSet make_set() {
-  using C = Cfg<NP, NCUB, NG, E>;
+  using C = Cfg<NP, NCUB, NG, E, CH, MINB>;
   KernelSet k;
   k.np = NP;
   k.ncub = NCUB;
   k.ng = NG;
   k.E = E;
+  k.minb = MINB;
+  k.ch = CH;
   k.smem_traces = sizeof(double) * C::R * C::LDU;
   k.smem_rhs = C::SMEM_BYTES;
   k.traces = &k_traces<C>;
@@ -81,11 +83,12 @@ KernelSet make_set() {
 const std::vector<KernelSet>& kernel_sets() {
   static const std::vector<KernelSet> sets = {
       // straight-sided strengths (2p+1 / 2p): refelem.cpp:311-317
-      make_set<4, 5, 3, 32>(), make_set<10, 15, 6, 32>(), make_set<20, 35, 12, 32>(),
-      make_set<35, 70, 16, 32>(), make_set<56, 126, 56, 32>(), make_set<84, 210, 84, 16>(),
+      // <N_p, N_cub, N_g, E elements/tile, CH cubature chunk, CTAs/SM>
+      make_set<4, 5, 3, 16, 8, 2>(), make_set<10, 15, 6, 16, 16, 2>(), make_set<20, 35, 12, 16, 16, 2>(),
+      make_set<35, 70, 16, 16, 24, 2>(), make_set<56, 126, 56, 16, 16, 2>(), make_set<84, 210, 84, 16>(),
       make_set<120, 330, 120, 16>(), make_set<165, 495, 165, 16>(),
       // curved-mesh strengths (3p-3 / 3p-2): refelem.hpp:118-119
-      make_set<20, 35, 16, 32>(), make_set<35, 70, 56, 32>(), make_set<56, 210, 84, 32>(),
+      make_set<20, 35, 16, 16, 16, 2>(), make_set<35, 70, 56, 16, 24, 2>(), make_set<56, 210, 84, 16, 16, 2>(),
       make_set<84, 330, 165, 16>(), make_set<120, 715, 220, 16>(),
       make_set<165, 1001, 364, 16>()};
   return sets;
@@ -131,18 +134,20 @@ std::vector<double> spd_inverse(const std::vector<double>& m, int n) {
   return inv;
 }
 
-// B-operand fragments for mma.m16n8k4 (.col): frag[nt][ks][lane] =
-// op[nt*8 + lane/4][ks*4 + lane%4], zero outside [rows x cols].
+// B-operand fragments for mma.m16n8k8 (.col): frag[nt][ks][lane] = the pair
+// (op[nt*8 + lane/4][ks*8 + lane%4], op[nt*8 + lane/4][ks*8 + lane%4 + 4]),
+// zero outside [rows x cols]: one coalesced 16-byte load per thread per step.
 std::vector<double> make_frag(const std::vector<double>& op, int rows, int cols, int rows8,
-                              int cols4) {
-  std::vector<double> f((size_t)rows8 / 8 * (cols4 / 4) * 32, 0.0);
+                              int cols8) {
+  std::vector<double> f((size_t)rows8 / 8 * (cols8 / 8) * 64, 0.0);
   for (int nt = 0; nt < rows8 / 8; ++nt)
-    for (int ks = 0; ks < cols4 / 4; ++ks)
-      for (int lane = 0; lane < 32; ++lane) {
-        const int r = nt * 8 + lane / 4, c = ks * 4 + lane % 4;
-        if (r < rows && c < cols)
-          f[((size_t)nt * (cols4 / 4) + ks) * 32 + lane] = op[(size_t)r * cols + c];
-      }
+    for (int ks = 0; ks < cols8 / 8; ++ks)
+      for (int lane = 0; lane < 32; ++lane)
+        for (int v = 0; v < 2; ++v) {
+          const int r = nt * 8 + lane / 4, c = ks * 8 + lane % 4 + 4 * v;
+          if (r < rows && c < cols)
+            f[(((size_t)nt * (cols8 / 8) + ks) * 32 + lane) * 2 + v] = op[(size_t)r * cols + c];
+        }
   return f;
 }
 
@@ -207,7 +212,7 @@ struct cdg_gpu_level {
 
   int n_rows() const { return K * 5; }
   int n_tiles() const { return (K + ks->E - 1) / ks->E; }
-  int grid(int tiles) const { return std::max(1, std::min(tiles, n_sms)); }
+  int grid(int tiles) const { return std::max(1, std::min(tiles, n_sms * ks->minb)); }
 };
 
 namespace {
@@ -238,7 +243,7 @@ void check_device_error(cdg_gpu_level* lv) {
 
 void launch_traces(cdg_gpu_level* lv, const double* u, double* traces) {
   const int tiles = lv->n_tiles();
-  lv->ks->traces<<<lv->grid(tiles), kThreads, lv->ks->smem_traces, lv->stream>>>(
+  lv->ks->traces<<<tiles, kThreads, lv->ks->smem_traces, lv->stream>>>(
       u, traces, lv->frag_ig, lv->n_rows(), tiles);
   ++lv->launches;
 }
@@ -470,15 +475,16 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
         for (int j = 0; j < np; ++j) s += minv[(size_t)i * np + j] * ig[(size_t)fq * np + j];
         lift[(size_t)i * nf + fq] = s * d->face_weights[fq % ng];
       }
-    const int kp = (np + 3) / 4 * 4, ncub8 = (ncub + 7) / 8 * 8, np8 = (np + 7) / 8 * 8,
+    const int kp = (np + 7) / 8 * 8, ncub8 = (ncub + 7) / 8 * 8, np8 = (np + 7) / 8 * 8,
               nf8 = (nf + 7) / 8 * 8;
-    const int k2cub = 3 * ncub8, k2 = k2cub + nf;
+    const int k2cub = 3 * ncub8, k2 = k2cub + nf8;
     // RHS operator rows i: [chunked (m, q) volume block | -LIFT]
     std::vector<double> op2((size_t)np * k2, 0.0);
     // aux operator (viscous gradient): same volume block, +LIFT (solver.cpp:283-309)
     std::vector<double> opaux((size_t)np * k2, 0.0);
-    for (int q0 = 0; q0 < ncub8; q0 += 16) {
-      const int w = std::min(16, ncub8 - q0);
+    const int CH = lv->ks->ch;
+    for (int q0 = 0; q0 < ncub8; q0 += CH) {
+      const int w = std::min(CH, ncub8 - q0);
       for (int m = 0; m < 3; ++m)
         for (int ql = 0; ql < w; ++ql) {
           const int q = q0 + ql;

@@ -39,31 +39,40 @@ __host__ __device__ constexpr int frag_ld(int n) {
 }
 __host__ __device__ constexpr int imax(int a, int b) { return a > b ? a : b; }
 
-template <int NP_, int NCUB_, int NG_, int E_>
+// leading dimension >= n with ld % 16 == 8: conflict-free 128-bit A-fragment
+// loads from the k8-permuted layout (see pcol)
+__host__ __device__ constexpr int frag_ld8(int n) { return (n % 16 == 8) ? n : frag_ld8(n + 8); }
+
+template <int NP_, int NCUB_, int NG_, int E_, int CH_ = 16, int MINB_ = 1>
 struct Cfg {
   static constexpr int NP = NP_, NCUB = NCUB_, NG = NG_, NF = 4 * NG_, E = E_;
+  static constexpr int MINB = MINB_;              // resident CTAs per SM (launch bounds)
   static constexpr int R = 5 * E;                 // rows per tile
   static constexpr int MT = R / 16;               // m16 tiles per tile
   static constexpr int BP = round_up(NP, 16);     // device SolutionStore block (pad16)
   static constexpr int TB = round_up(NF, 16);     // device trace block (pad16)
-  static constexpr int KP = round_up(NP, 4);      // K of the node->point GEMMs
-  static constexpr int KS1 = KP / 4;              // k-steps
+  static constexpr int KP = round_up(NP, 8);      // K of the node->point GEMMs (k8 steps)
+  static constexpr int KS1 = KP / 8;
   static constexpr int NCUB8 = round_up(NCUB, 8);
   static constexpr int NP8 = round_up(NP, 8);
   static constexpr int NF8 = round_up(NF, 8);
   static constexpr int NT2 = NP8 / 8;             // n-tiles of the RHS GEMM
-  static constexpr int CH = 16;                   // cubature nodes per chunk
+  static constexpr int CH = CH_;                  // cubature nodes per chunk (multiple of 8)
   static constexpr int NCH = ceil_div(NCUB8, CH);
   static constexpr int FCH = 32;                  // face nodes per chunk
   static constexpr int NFCH = ceil_div(NF, FCH);
   static constexpr int K2CUB = 3 * NCUB8;         // volume part of the RHS K
-  static constexpr int K2 = K2CUB + NF;           // + face part (NF % 4 == 0)
-  static constexpr int KS2 = K2 / 4;
-  static constexpr int LDU = frag_ld(KP);
-  static constexpr int LDC = frag_ld(CH);
-  static constexpr int LDG = frag_ld(imax(3 * CH, FCH));
+  static constexpr int K2 = K2CUB + NF8;          // + face part (padded to 8)
+  static constexpr int KS2 = K2 / 8;
+  static constexpr int LDU = frag_ld8(KP);
+  static constexpr int LDC = CH + 4;
+  static constexpr int LDG = frag_ld8(imax(3 * CH, FCH));
   static constexpr int T2 = MT * NT2;             // RHS output tiles
   static constexpr int MAXT2 = ceil_div(T2, kWarps);
+  static constexpr int T1MAX = MT * (CH / 8);     // GEMM1 tiles per chunk
+  static constexpr int MAXT1 = ceil_div(T1MAX, kWarps);
+  static constexpr int IT_P = ceil_div(E * CH, kThreads);   // pointwise pairs per thread
+  static constexpr int IT_F = ceil_div(E * FCH, kThreads);  // face pairs per thread
   static constexpr int SMEM_U = R * LDU;
   static constexpr int SMEM_C = R * LDC;
   static constexpr int SMEM_G = R * LDG;
@@ -71,6 +80,10 @@ struct Cfg {
       sizeof(double) * (SMEM_U + SMEM_C + SMEM_G + E * 9 + E * 4 * 4 + E) +
       sizeof(int) * (E * 4 * 2);
 };
+
+// Column permutation inside each 8-column group so that a thread's two k8
+// A-fragment values (k = t and t+4) are adjacent: one 128-bit shared load.
+__host__ __device__ __forceinline__ int pcol(int k) { return (k & ~7) | ((k & 3) << 1) | ((k >> 2) & 1); }
 
 // First-error record (the reference's RhsWorkspace::record_error,
 // solver.cpp:54-69, made device-side: first writer wins).
@@ -123,6 +136,51 @@ __device__ __forceinline__ void dmma_k4(double (&d)[4], double a0, double a1, do
       : "d"(a0), "d"(a1), "d"(b0));
 }
 
+// D(16x8) += A(16x8, row) * B(8x8, col), fp64: the native DMMA shape on
+// sm_100 (m16n8k4 lowers to two DMMA.8x8x4 and reaches only ~80% of the
+// measured FP64 peak; profiles/r1). A: a0=(g,t) a1=(g+8,t) a2=(g,t+4)
+// a3=(g+8,t+4); B: b0=(k=t,n=g) b1=(k=t+4,n=g).
+__device__ __forceinline__ void dmma_k8(double (&d)[4], double a0, double a1, double a2, double a3,
+                                        double b0, double b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 "
+      "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+      : "d"(a0), "d"(a1), "d"(a2), "d"(a3), "d"(b0), "d"(b1));
+}
+
+struct AFrag {
+  double a0, a1, a2, a3;
+};
+// A fragment of m-tile rows [r0, r0+16) at k8 step k0 from a pcol-permuted panel
+__device__ __forceinline__ AFrag load_afrag(const double* s, int ld, int r0, int k0, int g, int tq) {
+  const double2 x = *reinterpret_cast<const double2*>(s + (r0 + g) * ld + k0 + 2 * tq);
+  const double2 y = *reinterpret_cast<const double2*>(s + (r0 + g + 8) * ld + k0 + 2 * tq);
+  return AFrag{x.x, y.x, x.y, y.y};
+}
+__device__ __forceinline__ void mma_frag(double (&d)[4], const AFrag& a, const double2 b) {
+  dmma_k8(d, a.a0, a.a1, a.a2, a.a3, b.x, b.y);
+}
+
+// Stage rows [row0, row0+R) of a [*][BP] store into a pcol-permuted panel.
+template <class C>
+__device__ __forceinline__ void stage_rows(const double* __restrict__ src, int row0, int n_rows, double* s,
+                                           int tid) {
+  constexpr int V8 = C::KP / 8;
+  for (int idx = tid; idx < C::R * V8 * 2; idx += kThreads) {
+    const int h = idx & 1, j = (idx >> 1) % V8, r = (idx >> 1) / V8;
+    double2 x = make_double2(0.0, 0.0), y = make_double2(0.0, 0.0);
+    if (row0 + r < n_rows) {
+      const double* p = src + (size_t)(row0 + r) * C::BP + 8 * j + 2 * h;
+      x = *reinterpret_cast<const double2*>(p);
+      y = *reinterpret_cast<const double2*>(p + 4);
+    }
+    double* o = s + r * C::LDU + 8 * j + 4 * h;
+    *reinterpret_cast<double2*>(o) = make_double2(x.x, y.x);
+    *reinterpret_cast<double2*>(o + 2) = make_double2(x.y, y.y);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Euler state algebra (euler.cpp:7-161), device versions.
 // ---------------------------------------------------------------------------
@@ -160,6 +218,25 @@ __device__ __forceinline__ void llf_flux(const State5& um, const State5& up, dou
   double fm[5], fp[5];
   flux_dot_n(um, pm, nx, ny, nz, fm);
   flux_dot_n(up, pp, nx, ny, nz, fp);
+  const double dm[5] = {up.r - um.r, up.mx - um.mx, up.my - um.my, up.mz - um.mz, up.E - um.E};
+#pragma unroll
+  for (int c = 0; c < 5; ++c) out[c] = 0.5 * (fm[c] + fp[c]) - 0.5 * lambda * dm[c];
+}
+
+// llf_flux with one reciprocal per side (rounding differs from the reference's
+// divisions at the 1-ulp level; parity budget 1e-12)
+__device__ __forceinline__ void llf_flux_fast(const State5& um, const State5& up, double nx, double ny,
+                                              double nz, double gamma, double (&out)[5]) {
+  const double im = 1.0 / um.r, ip = 1.0 / up.r;
+  const double pm = (gamma - 1.0) * (um.E - 0.5 * im * (um.mx * um.mx + um.my * um.my + um.mz * um.mz));
+  const double pp = (gamma - 1.0) * (up.E - 0.5 * ip * (up.mx * up.mx + up.my * up.my + up.mz * up.mz));
+  const double vm = (um.mx * nx + um.my * ny + um.mz * nz) * im;
+  const double vp = (up.mx * nx + up.my * ny + up.mz * nz) * ip;
+  const double lambda = fmax(fabs(vm) + sqrt(gamma * pm * im), fabs(vp) + sqrt(gamma * pp * ip));
+  const double fm[5] = {um.r * vm, um.mx * vm + pm * nx, um.my * vm + pm * ny, um.mz * vm + pm * nz,
+                        vm * (um.E + pm)};
+  const double fp[5] = {up.r * vp, up.mx * vp + pp * nx, up.my * vp + pp * ny, up.mz * vp + pp * nz,
+                        vp * (up.E + pp)};
   const double dm[5] = {up.r - um.r, up.mx - um.mx, up.my - um.my, up.mz - um.mz, up.E - um.E};
 #pragma unroll
   for (int c = 0; c < 5; ++c) out[c] = 0.5 * (fm[c] + fp[c]) - 0.5 * lambda * dm[c];
@@ -245,6 +322,7 @@ __host__ __device__ constexpr int pack_face(int nface, int bc, int boundary, int
 
 // ---------------------------------------------------------------------------
 // Kernel 1: traces  T[rows x NF] = U[rows x KP] * I_g^T   (solver.cpp:200-208)
+// Non-persistent (one tile per CTA, several CTAs per SM): memory-bound.
 // ---------------------------------------------------------------------------
 template <class C>
 __global__ void __launch_bounds__(kThreads)
@@ -256,26 +334,17 @@ k_traces(const double* __restrict__ u, double* __restrict__ traces,
   const int g = lane >> 2, tq = lane & 3;
   constexpr int NT = C::NF8 / 8;
   constexpr int T = C::MT * NT;
+  const double2* fb = reinterpret_cast<const double2*>(frag_ig);
   for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const int row0 = tile * C::R;
-    // stage U rows (16-byte vector loads of KP doubles per row)
-    constexpr int V = C::KP / 2;
-    for (int idx = tid; idx < C::R * V; idx += kThreads) {
-      const int r = idx / V, v = idx % V;
-      double2 x = make_double2(0.0, 0.0);
-      if (row0 + r < n_rows)
-        x = __ldg(reinterpret_cast<const double2*>(u + (size_t)(row0 + r) * C::BP) + v);
-      *reinterpret_cast<double2*>(sU + r * C::LDU + 2 * v) = x;
-    }
+    stage_rows<C>(u, row0, n_rows, sU, tid);
     __syncthreads();
     for (int t = warp; t < T; t += kWarps) {
       const int mt = t / NT, nt = t % NT;
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      const double* a_ptr = sU + (mt * 16 + g) * C::LDU + tq;
-      const double* b_ptr = frag_ig + (size_t)nt * C::KS1 * 32 + lane;
-#pragma unroll 4
+#pragma unroll
       for (int ks = 0; ks < C::KS1; ++ks)
-        dmma_k4(acc, a_ptr[ks * 4], a_ptr[8 * C::LDU + ks * 4], __ldg(b_ptr + ks * 32));
+        mma_frag(acc, load_afrag(sU, C::LDU, mt * 16, ks * 8, g, tq), __ldg(fb + ((size_t)nt * C::KS1 + ks) * 32 + lane));
       const int col = nt * 8 + 2 * tq;
       if (col < C::NF) {
         const int r0 = row0 + mt * 16 + g;
@@ -319,12 +388,64 @@ struct RhsParams {
   size_t qtr_stride;          // elements per direction of qtr
 };
 
+// GEMM1 for one cubature chunk: sC[:, 0:w] = U * I_cub[q0:q0+w, :]^T
+template <class C>
+__device__ __forceinline__ void gemm1_chunk(const double* sU, double* sC, const double2* fb, int q0, int w,
+                                            int warp, int lane) {
+  const int g = lane >> 2, tq = lane & 3;
+  const int nt1 = w / 8, T1 = C::MT * nt1;
+  double c[C::MAXT1][4];
+#pragma unroll
+  for (int i = 0; i < C::MAXT1; ++i) c[i][0] = c[i][1] = c[i][2] = c[i][3] = 0.0;
+#pragma unroll
+  for (int ks = 0; ks < C::KS1; ++ks) {
+#pragma unroll
+    for (int i = 0; i < C::MAXT1; ++i) {
+      const int t = warp + i * kWarps;
+      if (t < T1) {
+        const int mt = t / nt1, nt = t % nt1;
+        mma_frag(c[i], load_afrag(sU, C::LDU, mt * 16, ks * 8, g, tq),
+                 __ldg(fb + ((size_t)(q0 / 8 + nt) * C::KS1 + ks) * 32 + lane));
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < C::MAXT1; ++i) {
+    const int t = warp + i * kWarps;
+    if (t < T1) {
+      const int mt = t / nt1, nt = t % nt1;
+      double* o = sC + (mt * 16 + g) * C::LDC + nt * 8 + 2 * tq;
+      *reinterpret_cast<double2*>(o) = make_double2(c[i][0], c[i][1]);
+      *reinterpret_cast<double2*>(o + 8 * C::LDC) = make_double2(c[i][2], c[i][3]);
+    }
+  }
+}
+
+// GEMM2 partial: acc[warp tiles] += sG[:, 0:8*nks] * Op2[:, k0:...]^T
+// (k-steps outer, the warp's independent output tiles inner for ILP)
+template <class C>
+__device__ __forceinline__ void gemm2_partial(double (&acc)[C::MAXT2][4], const double* sG, const double2* fb,
+                                              int ks0, int nks, int t_begin, int t_end, int lane) {
+  const int g = lane >> 2, tq = lane & 3;
+  for (int ks = 0; ks < nks; ++ks) {
+#pragma unroll
+    for (int i = 0; i < C::MAXT2; ++i) {
+      const int t = t_begin + i;
+      if (t < t_end) {
+        const int mt = t / C::NT2, nt = t % C::NT2;
+        mma_frag(acc[i], load_afrag(sG, C::LDG, mt * 16, ks * 8, g, tq),
+                 __ldg(fb + ((size_t)nt * C::KS2 + ks0 + ks) * 32 + lane));
+      }
+    }
+  }
+}
+
 template <class C, bool UPDATE, bool VISC>
-__global__ void __launch_bounds__(kThreads, 1) k_rhs(RhsParams p) {
+__global__ void __launch_bounds__(kThreads, C::MINB) k_rhs(RhsParams p) {
   extern __shared__ __align__(16) double smem[];
-  double* sU = smem;                       // [R][LDU] nodal state
+  double* sU = smem;                       // [R][LDU] nodal state (pcol-permuted)
   double* sC = sU + C::SMEM_U;             // [R][LDC] U at a cubature chunk
-  double* sG = sC + C::SMEM_C;             // [R][LDG] flux chunk (A operand)
+  double* sG = sC + C::SMEM_C;             // [R][LDG] flux chunk (A operand, pcol-permuted)
   double* sMet = sG + C::SMEM_G;           // [E][9]
   double4* sFace = reinterpret_cast<double4*>(sMet + C::E * 9);  // [E][4]
   double* sSe = reinterpret_cast<double*>(sFace + C::E * 4);      // [E] sqrt(eps)
@@ -335,6 +456,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_rhs(RhsParams p) {
   const int n_rows = p.K * 5;
   const double gamma = p.gas.gamma;
   const size_t qstride = (size_t)p.K * 5 * C::BP;
+  const double2* fb1 = reinterpret_cast<const double2*>(p.frag_icub);
+  const double2* fb2 = reinterpret_cast<const double2*>(p.frag_op2);
   // contiguous run of RHS output tiles for this warp (m-major order)
   const int t_begin = (warp * C::T2) / kWarps, t_end = ((warp + 1) * C::T2) / kWarps;
 
@@ -343,14 +466,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rhs(RhsParams p) {
     const int e0 = tile * C::E;
     const int row0 = e0 * 5;
     // ---- stage nodal state + per-element geometry --------------------------
-    constexpr int V = C::KP / 2;
-    for (int idx = tid; idx < C::R * V; idx += kThreads) {
-      const int r = idx / V, v = idx % V;
-      double2 x = make_double2(0.0, 0.0);
-      if (row0 + r < n_rows)
-        x = *(reinterpret_cast<const double2*>(p.u + (size_t)(row0 + r) * C::BP) + v);
-      *reinterpret_cast<double2*>(sU + r * C::LDU + 2 * v) = x;
-    }
+    stage_rows<C>(p.u, row0, n_rows, sU, tid);
     for (int idx = tid; idx < C::E * 9; idx += kThreads) {
       const int e = e0 + idx / 9;
       sMet[idx] = e < p.K ? __ldg(p.metric + (size_t)e0 * 9 + idx) : 0.0;
@@ -372,109 +488,98 @@ __global__ void __launch_bounds__(kThreads, 1) k_rhs(RhsParams p) {
     // ---- volume: chunks of CH cubature nodes --------------------------------
     for (int ch = 0; ch < C::NCH; ++ch) {
       const int q0 = ch * C::CH;
-      const int w = (C::NCUB8 - q0) < C::CH ? (C::NCUB8 - q0) : C::CH;  // multiple of 8
-      // GEMM1: sC[:, 0:w] = sU * I_cub[q0:q0+w, :]^T
-      const int nt1 = w / 8, T1 = C::MT * nt1;
-      for (int t = warp; t < T1; t += kWarps) {
-        const int mt = t / nt1, nt = t % nt1;
-        double c1[4] = {0.0, 0.0, 0.0, 0.0};
-        const double* a_ptr = sU + (mt * 16 + g) * C::LDU + tq;
-        const double* b_ptr = p.frag_icub + ((size_t)(q0 / 8 + nt) * C::KS1) * 32 + lane;
-#pragma unroll 4
-        for (int ks = 0; ks < C::KS1; ++ks)
-          dmma_k4(c1, a_ptr[ks * 4], a_ptr[8 * C::LDU + ks * 4], __ldg(b_ptr + ks * 32));
-        double* o = sC + (mt * 16 + g) * C::LDC + nt * 8 + 2 * tq;
-        *reinterpret_cast<double2*>(o) = make_double2(c1[0], c1[1]);
-        *reinterpret_cast<double2*>(o + 8 * C::LDC) = make_double2(c1[2], c1[3]);
-      }
+      const int w = (C::NCUB8 - q0) < C::CH ? (C::NCUB8 - q0) : C::CH;  // 16 or 8
+      gemm1_chunk<C>(sU, sC, fb1, q0, w, warp, lane);
       __syncthreads();
       // pointwise Euler flux -> contravariant flux G_m = sum_d (dr_m/dx_d) F_d
-      for (int idx = tid; idx < C::E * w; idx += kThreads) {
-        const int e = idx / w, ql = idx % w, q = q0 + ql;
-        const double* uc = sC + (e * 5) * C::LDC + ql;
-        double* gout = sG + (e * 5) * C::LDG + ql;
-        if (q < C::NCUB && e0 + e < p.K) {
-          const State5 s{uc[0], uc[C::LDC], uc[2 * C::LDC], uc[3 * C::LDC], uc[4 * C::LDC]};
-          if (!admissible(s, gamma)) record_error(p.err, 1, p.elem_offset + e0 + e, q, 0, s.r);
-          const double pr = pressure(s, gamma);
-          const double vx = s.mx / s.r, vy = s.my / s.r, vz = s.mz / s.r;
-          const double ep = s.E + pr;
-          // F_d (d = x, y, z) for the 5 fields (solver.cpp:382-394)
-          double F[3][5] = {{s.mx, s.mx * vx + pr, s.my * vx, s.mz * vx, vx * ep},
-                            {s.my, s.mx * vy, s.my * vy + pr, s.mz * vy, vy * ep},
-                            {s.mz, s.mx * vz, s.my * vz, s.mz * vz + pr, vz * ep}};
-          if (VISC) {
-            // F_m <- F_m - sqrt(eps) I_cub q_m   (solver.cpp:398-406)
-            const double se = sSe[e];
-            if (se > 0.0) {
-              const double* irow = p.icub + (size_t)q * C::NP;
 #pragma unroll
-              for (int m = 0; m < 3; ++m)
+      for (int it = 0; it < C::IT_P; ++it) {
+        const int idx = tid + it * kThreads;
+        if (idx < C::E * w) {
+          const int e = idx / w, ql = idx - e * w, q = q0 + ql;
+          const double* uc = sC + (e * 5) * C::LDC + ql;
+          double* gout = sG + (e * 5) * C::LDG;
+          double G[3][5];
+          if (q < C::NCUB && e0 + e < p.K) {
+            const State5 s{uc[0], uc[C::LDC], uc[2 * C::LDC], uc[3 * C::LDC], uc[4 * C::LDC]};
+            if (!admissible(s, gamma)) record_error(p.err, 1, p.elem_offset + e0 + e, q, 0, s.r);
+            const double ir = 1.0 / s.r;
+            const double pr = (gamma - 1.0) * (s.E - 0.5 * ir * (s.mx * s.mx + s.my * s.my + s.mz * s.mz));
+            const double vx = s.mx * ir, vy = s.my * ir, vz = s.mz * ir;
+            const double ep = s.E + pr;
+            // F_d (d = x, y, z) for the 5 fields (solver.cpp:382-394)
+            double F[3][5] = {{s.mx, s.mx * vx + pr, s.my * vx, s.mz * vx, vx * ep},
+                              {s.my, s.mx * vy, s.my * vy + pr, s.mz * vy, vy * ep},
+                              {s.mz, s.mx * vz, s.my * vz, s.mz * vz + pr, vz * ep}};
+            if (VISC) {
+              // F_m <- F_m - sqrt(eps) I_cub q_m   (solver.cpp:398-406)
+              const double se = sSe[e];
+              if (se > 0.0) {
+                const double* irow = p.icub + (size_t)q * C::NP;
 #pragma unroll
-                for (int c = 0; c < 5; ++c) {
-                  const double* qrow = p.q + m * qstride + (size_t)(row0 + e * 5 + c) * C::BP;
-                  double qc = 0.0;
-                  for (int j = 0; j < C::NP; ++j) qc += __ldg(irow + j) * __ldg(qrow + j);
-                  F[m][c] -= se * qc;
-                }
+                for (int m = 0; m < 3; ++m)
+#pragma unroll
+                  for (int c = 0; c < 5; ++c) {
+                    const double* qrow = p.q + m * qstride + (size_t)(row0 + e * 5 + c) * C::BP;
+                    double qc = 0.0;
+                    for (int j = 0; j < C::NP; ++j) qc += __ldg(irow + j) * __ldg(qrow + j);
+                    F[m][c] -= se * qc;
+                  }
+              }
             }
+            const double* met = sMet + e * 9;
+#pragma unroll
+            for (int m = 0; m < 3; ++m) {
+              const double r0 = met[m * 3 + 0], r1 = met[m * 3 + 1], r2 = met[m * 3 + 2];
+#pragma unroll
+              for (int c = 0; c < 5; ++c) G[m][c] = r0 * F[0][c] + r1 * F[1][c] + r2 * F[2][c];
+            }
+          } else {
+#pragma unroll
+            for (int m = 0; m < 3; ++m)
+#pragma unroll
+              for (int c = 0; c < 5; ++c) G[m][c] = 0.0;
           }
-          const double* met = sMet + e * 9;
 #pragma unroll
           for (int m = 0; m < 3; ++m) {
-            const double r0 = met[m * 3 + 0], r1 = met[m * 3 + 1], r2 = met[m * 3 + 2];
+            const int col = pcol(m * w + ql);
 #pragma unroll
-            for (int c = 0; c < 5; ++c)
-              gout[c * C::LDG + m * w] = r0 * F[0][c] + r1 * F[1][c] + r2 * F[2][c];
+            for (int c = 0; c < 5; ++c) gout[c * C::LDG + col] = G[m][c];
           }
-        } else {
-#pragma unroll
-          for (int m = 0; m < 3; ++m)
-#pragma unroll
-            for (int c = 0; c < 5; ++c) gout[c * C::LDG + m * w] = 0.0;
         }
       }
       __syncthreads();
-      // GEMM2 (volume part): acc += G[:, 0:3w] * Op2[:, k0:k0+3w]^T
-      {
-        const int ks0 = (3 * q0) / 4, nks = (3 * w) / 4;
-#pragma unroll
-        for (int i = 0; i < C::MAXT2; ++i) {
-          const int t = t_begin + i;
-          if (t < t_end) {
-            const int mt = t / C::NT2, nt = t % C::NT2;
-            const double* a_ptr = sG + (mt * 16 + g) * C::LDG + tq;
-            const double* b_ptr = p.frag_op2 + ((size_t)nt * C::KS2 + ks0) * 32 + lane;
-            for (int ks = 0; ks < nks; ++ks)
-              dmma_k4(acc[i], a_ptr[ks * 4], a_ptr[8 * C::LDG + ks * 4], __ldg(b_ptr + ks * 32));
-          }
-        }
-      }
+      gemm2_partial<C>(acc, sG, fb2, (3 * q0) / 8, (3 * w) / 8, t_begin, t_end, lane);
       __syncthreads();
     }
 
     // ---- surface: chunks of FCH face nodes ---------------------------------
     for (int fc = 0; fc < C::NFCH; ++fc) {
       const int f0 = fc * C::FCH;
-      const int w = (C::NF - f0) < C::FCH ? (C::NF - f0) : C::FCH;  // multiple of 4
-      for (int idx = tid; idx < C::E * w; idx += kThreads) {
-        const int e = idx / w, fl = idx % w, fq = f0 + fl;
-        const int f = fq / C::NG, gq = fq - f * C::NG;
-        double* gout = sG + (e * 5) * C::LDG + fl;
+      const int wr = (C::NF - f0) < C::FCH ? (C::NF - f0) : C::FCH;  // real nodes (multiple of 4)
+      const int wp = round_up(wr, 8);                                 // padded to the k8 step
+#pragma unroll
+      for (int it = 0; it < C::IT_F; ++it) {
+        const int idx = tid + it * kThreads;
+        if (idx >= C::E * wp) continue;
+        const int e = idx / wp, fl = idx - e * wp, fq = f0 + fl;
+        double* gout = sG + (e * 5) * C::LDG + pcol(fl);
         const int eg = e0 + e;
-        if (eg >= p.K) {
+        if (eg >= p.K || fl >= wr) {
 #pragma unroll
           for (int c = 0; c < 5; ++c) gout[c * C::LDG] = 0.0;
           continue;
         }
+        const int f = fq / C::NG, gq = fq - f * C::NG;
         const double* tm = p.traces + (size_t)eg * 5 * C::TB + fq;
         const State5 um{tm[0], tm[C::TB], tm[2 * C::TB], tm[3 * C::TB], tm[4 * C::TB]};
         const double4 fn = sFace[e * 4 + f];
         const int2 cw = sConn[e * 4 + f];
         State5 up;
+        int h = 0;
         if (cw.x >= 0) {
           const int nface = cw.y & 3, code = cw.y >> 8;
-          const int h = __ldg(p.code_map + code * C::NG + gq);
+          h = __ldg(p.code_map + code * C::NG + gq);
           const double* tp = p.traces + (size_t)cw.x * 5 * C::TB + nface * C::NG + h;
           up = State5{tp[0], tp[C::TB], tp[2 * C::TB], tp[3 * C::TB], tp[4 * C::TB]};
         } else {
@@ -486,13 +591,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_rhs(RhsParams p) {
         if (p.gas.riemann == 1)
           hllc_flux(um, up, fn.x, fn.y, fn.z, gamma, fs);
         else
-          llf_flux(um, up, fn.x, fn.y, fn.z, gamma, fs);
+          llf_flux_fast(um, up, fn.x, fn.y, fn.z, gamma, fs);
         if (VISC) {
           // BR1 central viscous flux with per-side sqrt(eps) (solver.cpp:438-453)
           const double se = sSe[e];
           const bool has_nb = cw.x >= 0;
           const double snb = has_nb ? p.sqrt_eps[cw.x] : se;
-          const int h = has_nb ? __ldg(p.code_map + (cw.y >> 8) * C::NG + gq) : 0;
           const double nrm[3] = {fn.x, fn.y, fn.z};
 #pragma unroll
           for (int c = 0; c < 5; ++c) {
@@ -512,20 +616,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rhs(RhsParams p) {
         for (int c = 0; c < 5; ++c) gout[c * C::LDG] = fn.w * fs[c];
       }
       __syncthreads();
-      {
-        const int ks0 = (C::K2CUB + f0) / 4, nks = w / 4;
-#pragma unroll
-        for (int i = 0; i < C::MAXT2; ++i) {
-          const int t = t_begin + i;
-          if (t < t_end) {
-            const int mt = t / C::NT2, nt = t % C::NT2;
-            const double* a_ptr = sG + (mt * 16 + g) * C::LDG + tq;
-            const double* b_ptr = p.frag_op2 + ((size_t)nt * C::KS2 + ks0) * 32 + lane;
-            for (int ks = 0; ks < nks; ++ks)
-              dmma_k4(acc[i], a_ptr[ks * 4], a_ptr[8 * C::LDG + ks * 4], __ldg(b_ptr + ks * 32));
-          }
-        }
-      }
+      gemm2_partial<C>(acc, sG, fb2, (C::K2CUB + f0) / 8, wp / 8, t_begin, t_end, lane);
       __syncthreads();
     }
 
@@ -545,19 +636,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_rhs(RhsParams p) {
         for (int hh = 0; hh < 2; ++hh) {
           const int r = mt * 16 + g + 8 * hh;
           const int grow = row0 + r;
-          if (grow >= n_rows) continue;
-#pragma unroll
-          for (int v = 0; v < 2; ++v) {
-            const int col = nt * 8 + 2 * tq + v;
-            if (col >= C::NP) continue;
-            const double rhs = acc[i][2 * hh + v];
-            const size_t gi = (size_t)grow * C::BP + col;
+          const int col = nt * 8 + 2 * tq;
+          if (grow >= n_rows || col >= C::NP) continue;
+          const size_t gi = (size_t)grow * C::BP + col;
+          const double r0 = acc[i][2 * hh], r1 = acc[i][2 * hh + 1];
+          if (col + 1 < C::NP) {
             if (UPDATE) {
-              const double rn = a_c * p.res[gi] + dt * rhs;
-              p.res[gi] = rn;
-              p.u[gi] = sU[r * C::LDU + col] + b_c * rn;
+              const double2 rs = *reinterpret_cast<const double2*>(p.res + gi);
+              const double n0 = a_c * rs.x + dt * r0, n1 = a_c * rs.y + dt * r1;
+              *reinterpret_cast<double2*>(p.res + gi) = make_double2(n0, n1);
+              *reinterpret_cast<double2*>(p.u + gi) =
+                  make_double2(sU[r * C::LDU + pcol(col)] + b_c * n0, sU[r * C::LDU + pcol(col + 1)] + b_c * n1);
             } else {
-              p.rhs_out[gi] = rhs;
+              *reinterpret_cast<double2*>(p.rhs_out + gi) = make_double2(r0, r1);
+            }
+          } else {
+            if (UPDATE) {
+              const double n0 = a_c * p.res[gi] + dt * r0;
+              p.res[gi] = n0;
+              p.u[gi] = sU[r * C::LDU + pcol(col)] + b_c * n0;
+            } else {
+              p.rhs_out[gi] = r0;
             }
           }
         }

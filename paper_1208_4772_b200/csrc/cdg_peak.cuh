@@ -23,14 +23,6 @@ __global__ void __launch_bounds__(256) k_peak_dmma(double* out, int iters) {
   if (s == 1234.5) out[0] = s;
 }
 
-__device__ __forceinline__ void dmma_k8(double (&d)[4], double a0, double a1, double a2, double a3,
-                                        double b0, double b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 "
-      "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
-      : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
-      : "d"(a0), "d"(a1), "d"(a2), "d"(a3), "d"(b0), "d"(b1));
-}
 __device__ __forceinline__ void dmma_k16(double (&d)[4], const double (&a)[8], const double (&b)[4]) {
   asm volatile(
       "mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 "
