@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(kThreads, C::MINB) k_aux_q(AuxParams p) {
       for (int i = 0; i < C::MAXT2; ++i) {
         const int t = t_begin + i;
         if (t < t_end) {
-          const int mt = t / C::NT2, nt = t % C::NT2;
+          const int nt = t / C::MT, mt = t % C::MT;
           for (int hh = 0; hh < 2; ++hh) {
             const int grow = row0 + mt * 16 + g + 8 * hh;
             if (grow >= n_rows) continue;
@@ -201,21 +201,34 @@ struct TimestepParams {
   DevError* err;
 };
 
-__global__ void k_timestep(TimestepParams p) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+// one warp per element, lanes over nodes (coalesced rows), shuffle max
+__global__ void __launch_bounds__(256) k_timestep(TimestepParams p) {
+  const int lane = threadIdx.x & 31;
+  const int e = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (e >= p.K) return;
   const double* f = p.u + (size_t)e * 5 * p.bp;
   double lambda = 0.0;
-  for (int i = 0; i < p.np; ++i) {
+  int bad = -1;
+  double bad_rho = 0.0;
+  for (int i = lane; i < p.np; i += 32) {
     const State5 s{f[i], f[p.bp + i], f[2 * p.bp + i], f[3 * p.bp + i], f[4 * p.bp + i]};
     if (!admissible(s, p.gamma)) {
-      record_error(p.err, 3, e, i, 0, s.r);
-      return;
+      bad = i;
+      bad_rho = s.r;
+      continue;
     }
     const double pres = pressure(s, p.gamma);
     const double c = sqrt(p.gamma * pres / s.r);
     lambda = fmax(lambda, sqrt(s.mx * s.mx + s.my * s.my + s.mz * s.mz) / s.r + c);
   }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) lambda = fmax(lambda, __shfl_xor_sync(0xffffffffu, lambda, off));
+  const unsigned badmask = __ballot_sync(0xffffffffu, bad >= 0);
+  if (badmask) {
+    if (lane == __ffs(badmask) - 1) record_error(p.err, 3, e, bad, 0, bad_rho);
+    return;
+  }
+  if (lane != 0) return;
   const double h = p.h[e];
   if (h <= 0.0 || lambda <= 0.0) {
     record_error(p.err, 4, e, 0, 0, 0.0);

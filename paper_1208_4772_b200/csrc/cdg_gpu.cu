@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -20,6 +21,8 @@
 #include "cdg_gpu.h"
 #include "cdg_kernels.cuh"
 #include "cdg_peak.cuh"
+#include "cdg_sp.cuh"
+#include "cdg_ws.cuh"
 
 using namespace cdg_gpu;
 
@@ -50,6 +53,8 @@ int pad16(int n) { return 16 * ((n + 15) / 16); }
 // ---- kernel dispatch per (N_p, N_cub, N_g) ---------------------------------
 struct KernelSet {
   int np, ncub, ng, E, minb, ch;
+  bool ws = false, rhs_only_ws = false;
+  size_t smem_ws = 0;
   size_t smem_traces, smem_rhs;
   void (*traces)(const double*, double*, const double*, int, int);
   void (*rhs_update)(RhsParams);
@@ -57,11 +62,12 @@ struct KernelSet {
   void (*aux_q)(AuxParams);
   void (*visc_rhs_update)(RhsParams);
   void (*visc_rhs_only)(RhsParams);
+  void (*dbg_rhs[2])(RhsParams);  // timing experiments (CDG_KDBG=1|2)
 };
 
-template <int NP, int NCUB, int NG, int E, int CH = 16, int MINB = 1>
+template <int NP, int NCUB, int NG, int E, int CH = 16, int MINB = 1, int FCH = 32, int MODE = 0>
 KernelSet make_set() {
-  using C = Cfg<NP, NCUB, NG, E, CH, MINB>;
+  using C = Cfg<NP, NCUB, NG, E, CH, MINB, FCH>;
   KernelSet k;
   k.np = NP;
   k.ncub = NCUB;
@@ -73,10 +79,22 @@ KernelSet make_set() {
   k.smem_rhs = C::SMEM_BYTES;
   k.traces = &k_traces<C>;
   k.rhs_update = &k_rhs<C, true, false>;
+  k.ws = MODE != 0;  // MODE 1: warp-specialised, 2: software-pipelined (inviscid kernels)
+  if constexpr (MODE == 1) {
+    k.rhs_update = &k_rhs_ws<C>;
+    k.smem_ws = WsLayout<C>::SMEM_BYTES;
+  } else if constexpr (MODE == 2) {
+    k.rhs_update = &k_rhs_sp<C, true>;
+    k.rhs_only = &k_rhs_sp<C, false>;
+    k.rhs_only_ws = true;
+    k.smem_ws = SpLayout<C>::SMEM_BYTES;
+  }
   k.rhs_only = &k_rhs<C, false, false>;
   k.aux_q = &k_aux_q<C>;
   k.visc_rhs_update = &k_rhs<C, true, true>;
   k.visc_rhs_only = &k_rhs<C, false, true>;
+  k.dbg_rhs[0] = &k_rhs<C, true, false, 1>;
+  k.dbg_rhs[1] = &k_rhs<C, true, false, 2>;
   return k;
 }
 
@@ -85,19 +103,28 @@ const std::vector<KernelSet>& kernel_sets() {
       // straight-sided strengths (2p+1 / 2p): refelem.cpp:311-317
       // <N_p, N_cub, N_g, E elements/tile, CH cubature chunk, CTAs/SM>
       make_set<4, 5, 3, 16, 8, 2>(), make_set<10, 15, 6, 16, 16, 2>(), make_set<20, 35, 12, 16, 16, 2>(),
-      make_set<35, 70, 16, 16, 24, 2>(), make_set<56, 126, 56, 16, 16, 2>(), make_set<84, 210, 84, 16>(),
+      make_set<35, 70, 16, 16, 24, 2, 64>(), make_set<56, 126, 56, 16, 16, 2>(), make_set<84, 210, 84, 16>(),
       make_set<120, 330, 120, 16>(), make_set<165, 495, 165, 16>(),
       // curved-mesh strengths (3p-3 / 3p-2): refelem.hpp:118-119
       make_set<20, 35, 16, 16, 16, 2>(), make_set<35, 70, 56, 16, 24, 2>(), make_set<56, 210, 84, 16, 16, 2>(),
       make_set<84, 330, 165, 16>(), make_set<120, 715, 220, 16>(),
-      make_set<165, 1001, 364, 16>()};
+      make_set<165, 1001, 364, 16>(),
+      // P=4 straight tuning variants, selected with CDG_KCFG=<n> (bench sweeps)
+      make_set<35, 70, 16, 16, 8, 2, 16, 1>(), make_set<35, 70, 16, 16, 8, 2, 16, 2>(),
+      make_set<35, 70, 16, 16, 24, 2, 32>(), make_set<35, 70, 16, 32, 24, 1, 32>()};
   return sets;
 }
 
 const KernelSet* find_set(int np, int ncub, int ng) {
+  const char* v = std::getenv("CDG_KCFG");
+  int want = v ? std::atoi(v) : 0, seen = 0;
+  const KernelSet* first = nullptr;
   for (const auto& k : kernel_sets())
-    if (k.np == np && k.ncub == ncub && k.ng == ng) return &k;
-  return nullptr;
+    if (k.np == np && k.ncub == ncub && k.ng == ng) {
+      if (!first) first = &k;
+      if (seen++ == want) return &k;
+    }
+  return first;
 }
 
 // ---- small dense host linear algebra (setup only) --------------------------
@@ -280,7 +307,11 @@ void launch_rhs(cdg_gpu_level* lv, bool update, bool viscous, int stage) {
   const int tiles = lv->n_tiles();
   auto fn = viscous ? (update ? lv->ks->visc_rhs_update : lv->ks->visc_rhs_only)
                     : (update ? lv->ks->rhs_update : lv->ks->rhs_only);
-  fn<<<lv->grid(tiles), kThreads, lv->ks->smem_rhs, lv->stream>>>(p);
+  static const int dbg = std::getenv("CDG_KDBG") ? std::atoi(std::getenv("CDG_KDBG")) : 0;
+  if (update && !viscous && (dbg == 1 || dbg == 2)) fn = lv->ks->dbg_rhs[dbg - 1];
+  const size_t smem = (!viscous && lv->ks->ws && (update || lv->ks->rhs_only_ws)) ? lv->ks->smem_ws
+                                                                                  : lv->ks->smem_rhs;
+  fn<<<lv->grid(tiles), kThreads, smem, lv->stream>>>(p);
   ++lv->launches;
 }
 
@@ -591,15 +622,26 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
     for (int c = 0; c < 5; ++c) lv->gas.fs[c] = d->freestream[c];
     // opt in to > 48 KB dynamic shared memory
     CUDA_OK(cudaFuncSetAttribute(lv->ks->rhs_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)lv->ks->smem_rhs));
+                                 (int)std::max(lv->ks->smem_rhs, lv->ks->smem_ws)));
+    if (std::getenv("CDG_CARVEOUT")) {
+      // leave the rest of the 256 KB L1/smem array to L1, where the B-operand
+      // fragments of the shared operators stream from
+      const int pct = std::min(100, (int)std::ceil(100.0 * lv->ks->minb * (lv->ks->smem_rhs + 1024) /
+                                                   (double)prop.sharedMemPerMultiprocessor));
+      for (auto fn : {lv->ks->rhs_update, lv->ks->rhs_only, lv->ks->visc_rhs_update, lv->ks->visc_rhs_only,
+                      lv->ks->dbg_rhs[0], lv->ks->dbg_rhs[1]})
+        CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+    }
     CUDA_OK(cudaFuncSetAttribute(lv->ks->rhs_only, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)lv->ks->smem_rhs));
+                                 (int)std::max(lv->ks->smem_rhs, lv->ks->smem_ws)));
     CUDA_OK(cudaFuncSetAttribute(lv->ks->visc_rhs_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)lv->ks->smem_rhs));
     CUDA_OK(cudaFuncSetAttribute(lv->ks->visc_rhs_only, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)lv->ks->smem_rhs));
     CUDA_OK(cudaFuncSetAttribute(lv->ks->aux_q, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)lv->ks->smem_rhs));
+    for (auto fn : {lv->ks->dbg_rhs[0], lv->ks->dbg_rhs[1]})
+      CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lv->ks->smem_rhs));
     CUDA_OK(cudaFuncSetAttribute(lv->ks->traces, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)lv->ks->smem_traces));
     CUDA_OK(cudaDeviceSynchronize());
@@ -869,7 +911,7 @@ int cdg_gpu_timestep(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, int use_v
     tp.pfac = (lv->degree + 1.0) * (lv->degree + 1.0);
     tp.out = reinterpret_cast<unsigned long long*>(lv->d_scratch);
     tp.err = lv->d_err;
-    k_timestep<<<(lv->K + 255) / 256, 256, 0, lv->stream>>>(tp);
+    k_timestep<<<(lv->K + 7) / 8, 256, 0, lv->stream>>>(tp);
     ++lv->launches;
     CUDA_OK(cudaGetLastError());
     check_device_error(lv);

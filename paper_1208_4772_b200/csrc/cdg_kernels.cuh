@@ -43,7 +43,7 @@ __host__ __device__ constexpr int imax(int a, int b) { return a > b ? a : b; }
 // loads from the k8-permuted layout (see pcol)
 __host__ __device__ constexpr int frag_ld8(int n) { return (n % 16 == 8) ? n : frag_ld8(n + 8); }
 
-template <int NP_, int NCUB_, int NG_, int E_, int CH_ = 16, int MINB_ = 1>
+template <int NP_, int NCUB_, int NG_, int E_, int CH_ = 16, int MINB_ = 1, int FCH_ = 32>
 struct Cfg {
   static constexpr int NP = NP_, NCUB = NCUB_, NG = NG_, NF = 4 * NG_, E = E_;
   static constexpr int MINB = MINB_;              // resident CTAs per SM (launch bounds)
@@ -59,7 +59,7 @@ struct Cfg {
   static constexpr int NT2 = NP8 / 8;             // n-tiles of the RHS GEMM
   static constexpr int CH = CH_;                  // cubature nodes per chunk (multiple of 8)
   static constexpr int NCH = ceil_div(NCUB8, CH);
-  static constexpr int FCH = 32;                  // face nodes per chunk
+  static constexpr int FCH = FCH_;                // face nodes per chunk (multiple of 8)
   static constexpr int NFCH = ceil_div(NF, FCH);
   static constexpr int K2CUB = 3 * NCUB8;         // volume part of the RHS K
   static constexpr int K2 = K2CUB + NF8;          // + face part (padded to 8)
@@ -423,6 +423,24 @@ __device__ __forceinline__ void gemm1_chunk(const double* sU, double* sC, const 
 
 // GEMM2 partial: acc[warp tiles] += sG[:, 0:8*nks] * Op2[:, k0:...]^T
 // (k-steps outer, the warp's independent output tiles inner for ILP)
+template <class C, int NKS>
+__device__ __forceinline__ void gemm2_fixed(double (&acc)[C::MAXT2][4], const double* sG, const double2* fb,
+                                            int ks0, int t_begin, int t_end, int lane) {
+  const int g = lane >> 2, tq = lane & 3;
+#pragma unroll
+  for (int ks = 0; ks < NKS; ++ks) {
+#pragma unroll
+    for (int i = 0; i < C::MAXT2; ++i) {
+      const int t = t_begin + i;
+      if (t < t_end) {
+        const int nt = t / C::MT, mt = t % C::MT;
+        mma_frag(acc[i], load_afrag(sG, C::LDG, mt * 16, ks * 8, g, tq),
+                 __ldg(fb + ((size_t)nt * C::KS2 + ks0 + ks) * 32 + lane));
+      }
+    }
+  }
+}
+
 template <class C>
 __device__ __forceinline__ void gemm2_partial(double (&acc)[C::MAXT2][4], const double* sG, const double2* fb,
                                               int ks0, int nks, int t_begin, int t_end, int lane) {
@@ -432,7 +450,7 @@ __device__ __forceinline__ void gemm2_partial(double (&acc)[C::MAXT2][4], const 
     for (int i = 0; i < C::MAXT2; ++i) {
       const int t = t_begin + i;
       if (t < t_end) {
-        const int mt = t / C::NT2, nt = t % C::NT2;
+        const int nt = t / C::MT, mt = t % C::MT;  // n-major: a warp's run reuses B fragments
         mma_frag(acc[i], load_afrag(sG, C::LDG, mt * 16, ks * 8, g, tq),
                  __ldg(fb + ((size_t)nt * C::KS2 + ks0 + ks) * 32 + lane));
       }
@@ -440,7 +458,9 @@ __device__ __forceinline__ void gemm2_partial(double (&acc)[C::MAXT2][4], const 
   }
 }
 
-template <class C, bool UPDATE, bool VISC>
+// DBG (timing experiments only): 1 = skip the SIMT pointwise/face work,
+// 2 = skip the tensor-core GEMMs. Never used for results.
+template <class C, bool UPDATE, bool VISC, int DBG = 0>
 __global__ void __launch_bounds__(kThreads, C::MINB) k_rhs(RhsParams p) {
   extern __shared__ __align__(16) double smem[];
   double* sU = smem;                       // [R][LDU] nodal state (pcol-permuted)
@@ -461,8 +481,12 @@ __global__ void __launch_bounds__(kThreads, C::MINB) k_rhs(RhsParams p) {
   // contiguous run of RHS output tiles for this warp (m-major order)
   const int t_begin = (warp * C::T2) / kWarps, t_end = ((warp + 1) * C::T2) / kWarps;
 
+  __shared__ int s_stop;
   for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
-    if (*(volatile int*)&p.err->flag) return;
+    // block-uniform early exit after a recorded error (no divergent barriers)
+    if (tid == 0) s_stop = *(volatile int*)&p.err->flag;
+    __syncthreads();
+    if (s_stop) return;
     const int e0 = tile * C::E;
     const int row0 = e0 * 5;
     // ---- stage nodal state + per-element geometry --------------------------
@@ -489,29 +513,44 @@ __global__ void __launch_bounds__(kThreads, C::MINB) k_rhs(RhsParams p) {
     for (int ch = 0; ch < C::NCH; ++ch) {
       const int q0 = ch * C::CH;
       const int w = (C::NCUB8 - q0) < C::CH ? (C::NCUB8 - q0) : C::CH;  // 16 or 8
-      gemm1_chunk<C>(sU, sC, fb1, q0, w, warp, lane);
+      if (DBG != 2) gemm1_chunk<C>(sU, sC, fb1, q0, w, warp, lane);
       __syncthreads();
       // pointwise Euler flux -> contravariant flux G_m = sum_d (dr_m/dx_d) F_d
 #pragma unroll
       for (int it = 0; it < C::IT_P; ++it) {
         const int idx = tid + it * kThreads;
-        if (idx < C::E * w) {
+        if (DBG != 1 && idx < C::E * w) {
           const int e = idx / w, ql = idx - e * w, q = q0 + ql;
           const double* uc = sC + (e * 5) * C::LDC + ql;
           double* gout = sG + (e * 5) * C::LDG;
           double G[3][5];
           if (q < C::NCUB && e0 + e < p.K) {
             const State5 s{uc[0], uc[C::LDC], uc[2 * C::LDC], uc[3 * C::LDC], uc[4 * C::LDC]};
-            if (!admissible(s, gamma)) record_error(p.err, 1, p.elem_offset + e0 + e, q, 0, s.r);
+            if (DBG == 0 && !admissible(s, gamma)) record_error(p.err, 1, p.elem_offset + e0 + e, q, 0, s.r);
             const double ir = 1.0 / s.r;
             const double pr = (gamma - 1.0) * (s.E - 0.5 * ir * (s.mx * s.mx + s.my * s.my + s.mz * s.mz));
             const double vx = s.mx * ir, vy = s.my * ir, vz = s.mz * ir;
             const double ep = s.E + pr;
-            // F_d (d = x, y, z) for the 5 fields (solver.cpp:382-394)
-            double F[3][5] = {{s.mx, s.mx * vx + pr, s.my * vx, s.mz * vx, vx * ep},
-                              {s.my, s.mx * vy, s.my * vy + pr, s.mz * vy, vy * ep},
-                              {s.mz, s.mx * vz, s.my * vz, s.mz * vz + pr, vz * ep}};
-            if (VISC) {
+            const double* met = sMet + e * 9;
+            if (!VISC) {
+              // contravariant flux directly: with U_m = sum_d r_md v_d,
+              // G_m = (rho U_m, m U_m + p r_m, (E+p) U_m)  ==  sum_d r_md F_d
+              // (solver.cpp:382-394 contracted with S_m, operators.cpp:139-147)
+#pragma unroll
+              for (int m = 0; m < 3; ++m) {
+                const double r0 = met[m * 3 + 0], r1 = met[m * 3 + 1], r2 = met[m * 3 + 2];
+                const double um = r0 * vx + r1 * vy + r2 * vz;
+                G[m][0] = s.r * um;
+                G[m][1] = s.mx * um + pr * r0;
+                G[m][2] = s.my * um + pr * r1;
+                G[m][3] = s.mz * um + pr * r2;
+                G[m][4] = ep * um;
+              }
+            } else {
+              // F_d (d = x, y, z) for the 5 fields (solver.cpp:382-394)
+              double F[3][5] = {{s.mx, s.mx * vx + pr, s.my * vx, s.mz * vx, vx * ep},
+                                {s.my, s.mx * vy, s.my * vy + pr, s.mz * vy, vy * ep},
+                                {s.mz, s.mx * vz, s.my * vz, s.mz * vz + pr, vz * ep}};
               // F_m <- F_m - sqrt(eps) I_cub q_m   (solver.cpp:398-406)
               const double se = sSe[e];
               if (se > 0.0) {
@@ -526,13 +565,12 @@ __global__ void __launch_bounds__(kThreads, C::MINB) k_rhs(RhsParams p) {
                     F[m][c] -= se * qc;
                   }
               }
-            }
-            const double* met = sMet + e * 9;
 #pragma unroll
-            for (int m = 0; m < 3; ++m) {
-              const double r0 = met[m * 3 + 0], r1 = met[m * 3 + 1], r2 = met[m * 3 + 2];
+              for (int m = 0; m < 3; ++m) {
+                const double r0 = met[m * 3 + 0], r1 = met[m * 3 + 1], r2 = met[m * 3 + 2];
 #pragma unroll
-              for (int c = 0; c < 5; ++c) G[m][c] = r0 * F[0][c] + r1 * F[1][c] + r2 * F[2][c];
+                for (int c = 0; c < 5; ++c) G[m][c] = r0 * F[0][c] + r1 * F[1][c] + r2 * F[2][c];
+              }
             }
           } else {
 #pragma unroll
@@ -549,7 +587,12 @@ __global__ void __launch_bounds__(kThreads, C::MINB) k_rhs(RhsParams p) {
         }
       }
       __syncthreads();
-      gemm2_partial<C>(acc, sG, fb2, (3 * q0) / 8, (3 * w) / 8, t_begin, t_end, lane);
+      if (DBG != 2) {
+        if (w == C::CH)
+          gemm2_fixed<C, 3 * C::CH / 8>(acc, sG, fb2, (3 * q0) / 8, t_begin, t_end, lane);
+        else
+          gemm2_partial<C>(acc, sG, fb2, (3 * q0) / 8, (3 * w) / 8, t_begin, t_end, lane);
+      }
       __syncthreads();
     }
 
@@ -561,7 +604,7 @@ __global__ void __launch_bounds__(kThreads, C::MINB) k_rhs(RhsParams p) {
 #pragma unroll
       for (int it = 0; it < C::IT_F; ++it) {
         const int idx = tid + it * kThreads;
-        if (idx >= C::E * wp) continue;
+        if (DBG == 1 || idx >= C::E * wp) continue;
         const int e = idx / wp, fl = idx - e * wp, fq = f0 + fl;
         double* gout = sG + (e * 5) * C::LDG + pcol(fl);
         const int eg = e0 + e;
@@ -585,7 +628,7 @@ __global__ void __launch_bounds__(kThreads, C::MINB) k_rhs(RhsParams p) {
         } else {
           up = boundary_state(um, fn.x, fn.y, fn.z, (cw.y >> 2) & 3, p.gas);
         }
-        if (!admissible(um, gamma) || !admissible(up, gamma))
+        if (DBG == 0 && (!admissible(um, gamma) || !admissible(up, gamma)))
           record_error(p.err, 2, p.elem_offset + eg, f, gq, um.r);
         double fs[5];
         if (p.gas.riemann == 1)
@@ -616,7 +659,12 @@ __global__ void __launch_bounds__(kThreads, C::MINB) k_rhs(RhsParams p) {
         for (int c = 0; c < 5; ++c) gout[c * C::LDG] = fn.w * fs[c];
       }
       __syncthreads();
-      gemm2_partial<C>(acc, sG, fb2, (C::K2CUB + f0) / 8, wp / 8, t_begin, t_end, lane);
+      if (DBG != 2) {
+        if (wp == C::FCH)
+          gemm2_fixed<C, C::FCH / 8>(acc, sG, fb2, (C::K2CUB + f0) / 8, t_begin, t_end, lane);
+        else
+          gemm2_partial<C>(acc, sG, fb2, (C::K2CUB + f0) / 8, wp / 8, t_begin, t_end, lane);
+      }
       __syncthreads();
     }
 
@@ -631,7 +679,7 @@ __global__ void __launch_bounds__(kThreads, C::MINB) k_rhs(RhsParams p) {
     for (int i = 0; i < C::MAXT2; ++i) {
       const int t = t_begin + i;
       if (t < t_end) {
-        const int mt = t / C::NT2, nt = t % C::NT2;
+        const int nt = t / C::MT, mt = t % C::MT;
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
           const int r = mt * 16 + g + 8 * hh;
