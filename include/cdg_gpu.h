@@ -105,6 +105,15 @@ typedef struct cdg_gpu_level_desc {
   int n_codes;
 
   double freestream[5];          /* farfield ghost state (euler.cpp:157-158) */
+
+  /* Curved (isoparametric) elements, CurvedMesh::is_curved (curved_mesh.hpp:
+   * 14-51): their affine entries above are ignored; per-node geometry from
+   * compute_mapping (operators.cpp:32-121) and the element mass inverse. */
+  int n_curved;
+  const int *curved_ids;         /* [Kc] element indices */
+  const double *curved_jwr;      /* [Kc][N_cub][9] cub_jac*W*cub_dr (m*3+d) */
+  const double *curved_face;     /* [Kc][4N_g][4] face_normal xyz, face_sjac*w */
+  const double *curved_minv;     /* [Kc][N_p][N_p] (I_cub^T diag(JW) I_cub)^-1 */
 } cdg_gpu_level_desc;
 
 typedef struct cdg_gpu_level cdg_gpu_level;

@@ -57,6 +57,9 @@ def lib():
         L.ref_mesh_sphere_shell.restype = C.c_void_p
         L.ref_mesh_sphere_shell.argtypes = [C.c_double, C.c_double, C.c_int, C.c_int]
         L.ref_mesh_free.argtypes = [C.c_void_p]
+        L.ref_mesh_sphere_curved.restype = C.c_void_p
+        L.ref_mesh_sphere_curved.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_size_t]
+        L.ref_level_nodes.argtypes = [C.c_void_p, _dp, _ip]
         L.ref_mesh_sizes.argtypes = [C.c_void_p, _ip]
         L.ref_mesh_export.argtypes = [C.c_void_p, _dp, _ip, _ip, _ip, _ip, _ip]
         L.ref_level_create.restype = C.c_void_p
@@ -123,6 +126,12 @@ class Mesh:
             self.h = L.ref_mesh_two_tets()
         elif kind == "sphere":
             self.h = L.ref_mesh_sphere_shell(*sphere)
+        elif kind == "sphere_curved":
+            # sphere=(subdiv, layers, p_curve, p_fem)
+            err = C.create_string_buffer(512)
+            self.h = L.ref_mesh_sphere_curved(*sphere, err, 512)
+            if not self.h:
+                raise RefError(3, err.value.decode())
         else:
             raise ValueError(kind)
         sz = np.zeros(3, np.int32)
@@ -175,6 +184,12 @@ class Level:
                  bc=np.zeros((K, 4), np.int32), node_map=np.zeros((K, 4, ng), np.int32))
         lib().ref_level_geometry(self.h, *[_p(g[k]) for k in g])
         return g
+
+    def nodes(self):
+        x = np.zeros((self.K, self.n_basis, 3))
+        cv = np.zeros(self.K, np.int32)
+        lib().ref_level_nodes(self.h, _p(x), _p(cv))
+        return x, cv.astype(bool)
 
     def operators(self, e: int) -> dict:
         np_, ncub, nf = self.n_basis, self.n_cub, 4 * self.n_face_quad

@@ -26,7 +26,9 @@
 #include <vector>
 
 #include "cdg/curved_mesh.hpp"
+#include "cdg/elasticity.hpp"
 #include "cdg/meshgen.hpp"
+#include "cdg/nurbs.hpp"
 #include "cdg/refelem.hpp"
 #include "cdg/solver.hpp"
 
@@ -36,6 +38,7 @@ namespace {
 
 struct RefMesh {
   Mesh mesh;
+  std::unique_ptr<CurvedMesh> curved;  // set by ref_mesh_sphere_curved
 };
 
 struct RefLevel {
@@ -170,6 +173,29 @@ void* ref_mesh_sphere_shell(double r_in, double r_out, int subdiv, int layers) {
   m->mesh = make_sphere_shell_mesh(r_in, r_out, subdiv, layers, "sphere", "farfield");
   return m;
 }
+// The acceptance fixture pipeline (acceptance_main.cpp:82-120 / cmd_curve,
+// cli_ops.cpp:16-76) in memory: sphere shell, box [-1.5,1.5]^3 sub-mesh,
+// elasticity with E=1 nu=0.45 and the exact sphere displacement, curve_mesh at
+// degree p_curve. Returns null on failure (err filled).
+void* ref_mesh_sphere_curved(int subdiv, int layers, int p_curve, int p_fem, char* err, size_t errn) {
+  try {
+    auto* m = new RefMesh;
+    m->mesh = make_sphere_shell_mesh(1.0, 8.0, subdiv, layers, "sphere", "farfield");
+    const Box box{{-1.5, -1.5, -1.5}, {1.5, 1.5, 1.5}};
+    const SubMesh sub = extract_submesh(m->mesh, box, "sphere", {});
+    const Vec3 center{0, 0, 0};
+    auto g = [center](const Vec3& x) { return sphere_displacement(center, 1.0, x); };
+    const auto material = ElasticMaterial::from_E_nu(1.0, 0.45);
+    const DeformationField field = solve_elasticity(sub, material, g, p_fem);
+    auto re = get_reference_element(p_curve);
+    m->curved = std::make_unique<CurvedMesh>(curve_mesh(m->mesh, sub, field, *re));
+    return m;
+  } catch (const std::exception& e) {
+    copy_err(e, err, errn);
+    return nullptr;
+  }
+}
+
 void ref_mesh_free(void* h) { delete static_cast<RefMesh*>(h); }
 
 // sizes: [0]=n_vertices [1]=n_elements [2]=n_boundary_faces
@@ -217,7 +243,8 @@ void* ref_level_create(void* mesh_h, int p, int bc_wall, int bc_far, int padded,
   try {
     auto* lv = new RefLevel;
     lv->mesh = static_cast<RefMesh*>(mesh_h);
-    lv->cmesh = std::make_unique<CurvedMesh>(lv->mesh->mesh, p);
+    lv->cmesh = lv->mesh->curved ? std::make_unique<CurvedMesh>(*lv->mesh->curved)
+                                 : std::make_unique<CurvedMesh>(lv->mesh->mesh, p);
     RunConfig cfg;
     cfg.curved_quadrature = curved_quadrature != 0;
     auto re = level_reference_element(*lv->cmesh, p, cfg);
@@ -283,6 +310,20 @@ void ref_level_geometry(void* h, double* cub_dr, double* cub_jac, double* face_n
           node_map[(static_cast<size_t>(e) * 4 + f) * ng + gg] =
               fc.neighbor >= 0 ? fc.node_map[gg] : -1;
     }
+  }
+}
+
+// Element collocation nodes at the level degree (ElementGeometry::phys_nodes,
+// from CurvedMesh::element_nodes_for_degree) [K][np][3] and curved flags [K].
+void ref_level_nodes(void* h, double* nodes, int* curved) {
+  auto* lvh = static_cast<RefLevel*>(h);
+  const DgLevel& lv = *lvh->level;
+  const int np = lv.refelem().n_basis();
+  for (int e = 0; e < lv.n_elements(); ++e) {
+    const auto& pn = lv.geom(e).phys_nodes;
+    for (int i = 0; i < np; ++i)
+      for (int d = 0; d < 3; ++d) nodes[(static_cast<size_t>(e) * np + i) * 3 + d] = pn[i][d];
+    if (curved) curved[e] = lvh->cmesh->is_curved(e) ? 1 : 0;
   }
 }
 

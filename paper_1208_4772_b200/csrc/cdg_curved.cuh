@@ -1,0 +1,211 @@
+// cdg_curved.cuh -- RHS + LSRK kernel for CURVED (isoparametric) elements.
+//
+// Reference math (operators.cpp:32-167, solver.cpp:362-464) for an element
+// whose map is not affine: per cubature node the metric terms vary, so
+//   vol  = sum_m D_m^T ( JW r_m . F )  -  I_g^T ( (sjac w) F* )
+//   rhs  = M_e^-1 vol,     M_e = I_cub^T diag(J W) I_cub
+// G_m(q) = sum_d (J W dr_m/dx_d)(q) F_d(q) is formed pointwise from per-node
+// metrics; the shared operator [D_r^T D_s^T D_t^T | -I_g^T] runs on the DMMA
+// pipe exactly like k_rhs; M_e^-1 (dense, per element, precomputed on the
+// host -- a GEMV instead of the reference's two triangular solves,
+// operators.cpp:8-22) is applied in the epilogue. Curved elements are a
+// list (ids); the affine kernels skip them (curved flag in the coupling word).
+#pragma once
+
+#include "cdg_kernels.cuh"
+
+namespace cdg_gpu {
+
+struct CurvedParams {
+  RhsParams base;
+  const int* ids;          // [Kc] element ids
+  const double* jwr;       // [Kc][NCUB][9]  J W dr_m/dx_d  (m*3+d)
+  const double4* face;     // [Kc][NF]       (nx, ny, nz, sjac*w)
+  const double* minv;      // [Kc][NP][NP]
+  const double* frag_opc;  // B fragments of [D^T | -I_g^T]
+  int Kc;
+};
+
+template <class C>
+struct CurvedLayout {
+  static constexpr int LDV = C::NP8 + 1;
+  static constexpr size_t SMEM_BYTES =
+      sizeof(double) * (C::SMEM_U + C::SMEM_C + C::SMEM_G + (size_t)C::R * LDV) + sizeof(int) * (C::E * 4 * 2 + C::E);
+};
+
+template <class C, bool UPDATE>
+__global__ void __launch_bounds__(kThreads, 1) k_rhs_curved(CurvedParams cp) {
+  using L = CurvedLayout<C>;
+  const RhsParams& p = cp.base;
+  extern __shared__ __align__(16) double smem[];
+  double* sU = smem;
+  double* sC = sU + C::SMEM_U;
+  double* sG = sC + C::SMEM_C;
+  double* sV = sG + C::SMEM_G;  // [R][LDV] vol (epilogue)
+  int2* sConn = reinterpret_cast<int2*>(sV + (size_t)C::R * L::LDV);
+  int* sId = reinterpret_cast<int*>(sConn + C::E * 4);
+  __shared__ int s_stop;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const double gamma = p.gas.gamma;
+  const double2* fb1 = reinterpret_cast<const double2*>(p.frag_icub);
+  const double2* fbc = reinterpret_cast<const double2*>(cp.frag_opc);
+  const int t_begin = (warp * C::T2) / kWarps, t_end = ((warp + 1) * C::T2) / kWarps;
+  const int n_tiles = (cp.Kc + C::E - 1) / C::E;
+
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    if (tid == 0) s_stop = *(volatile int*)&p.err->flag;
+    __syncthreads();
+    if (s_stop) return;
+    const int c0 = tile * C::E;  // index into the curved list
+    for (int idx = tid; idx < C::E; idx += kThreads) sId[idx] = c0 + idx < cp.Kc ? cp.ids[c0 + idx] : -1;
+    __syncthreads();
+    // stage U rows of the listed elements (pcol-permuted panel)
+    constexpr int V8 = C::KP / 8;
+    for (int idx = tid; idx < C::R * V8 * 2; idx += kThreads) {
+      const int h = idx & 1, j = (idx >> 1) % V8, r = (idx >> 1) / V8;
+      const int e = sId[r / 5];
+      double2 x = make_double2(0.0, 0.0), y = make_double2(0.0, 0.0);
+      if (e >= 0) {
+        const double* src = p.u + ((size_t)e * 5 + r % 5) * C::BP + 8 * j + 2 * h;
+        x = *reinterpret_cast<const double2*>(src);
+        y = *reinterpret_cast<const double2*>(src + 4);
+      }
+      double* o = sU + r * C::LDU + 8 * j + 4 * h;
+      *reinterpret_cast<double2*>(o) = make_double2(x.x, y.x);
+      *reinterpret_cast<double2*>(o + 2) = make_double2(x.y, y.y);
+    }
+    for (int idx = tid; idx < C::E * 4; idx += kThreads) {
+      const int e = sId[idx / 4];
+      sConn[idx] = e >= 0 ? p.conn[(size_t)e * 4 + idx % 4] : make_int2(-1, pack_face(0, 0, 1, 0));
+    }
+    __syncthreads();
+
+    double acc[C::MAXT2][4];
+#pragma unroll
+    for (int i = 0; i < C::MAXT2; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.0;
+
+    for (int ch = 0; ch < C::NCH; ++ch) {
+      const int q0 = ch * C::CH;
+      const int w = (C::NCUB8 - q0) < C::CH ? (C::NCUB8 - q0) : C::CH;
+      gemm1_chunk<C>(sU, sC, fb1, q0, w, warp, lane);
+      __syncthreads();
+      for (int idx = tid; idx < C::E * w; idx += kThreads) {
+        const int e = idx / w, ql = idx - e * w, q = q0 + ql;
+        const double* uc = sC + (e * 5) * C::LDC + ql;
+        double G[3][5];
+        const int ce = c0 + e;
+        if (q < C::NCUB && ce < cp.Kc) {
+          const State5 s{uc[0], uc[C::LDC], uc[2 * C::LDC], uc[3 * C::LDC], uc[4 * C::LDC]};
+          if (!admissible(s, gamma)) record_error(p.err, 1, p.elem_offset + sId[e], q, 0, s.r);
+          const double pr = pressure(s, gamma);
+          const double vx = s.mx / s.r, vy = s.my / s.r, vz = s.mz / s.r;
+          const double ep = s.E + pr;
+          const double F[3][5] = {{s.mx, s.mx * vx + pr, s.my * vx, s.mz * vx, vx * ep},
+                                  {s.my, s.mx * vy, s.my * vy + pr, s.mz * vy, vy * ep},
+                                  {s.mz, s.mx * vz, s.my * vz, s.mz * vz + pr, vz * ep}};
+          const double* met = cp.jwr + ((size_t)ce * C::NCUB + q) * 9;
+#pragma unroll
+          for (int m = 0; m < 3; ++m) {
+            const double r0 = __ldg(met + m * 3), r1 = __ldg(met + m * 3 + 1), r2 = __ldg(met + m * 3 + 2);
+#pragma unroll
+            for (int c = 0; c < 5; ++c) G[m][c] = r0 * F[0][c] + r1 * F[1][c] + r2 * F[2][c];
+          }
+        } else {
+#pragma unroll
+          for (int m = 0; m < 3; ++m)
+#pragma unroll
+            for (int c = 0; c < 5; ++c) G[m][c] = 0.0;
+        }
+        double* gout = sG + (e * 5) * C::LDG;
+#pragma unroll
+        for (int m = 0; m < 3; ++m)
+#pragma unroll
+          for (int c = 0; c < 5; ++c) gout[c * C::LDG + pcol(m * w + ql)] = G[m][c];
+      }
+      __syncthreads();
+      gemm2_partial<C>(acc, sG, fbc, (3 * q0) / 8, (3 * w) / 8, t_begin, t_end, lane);
+      __syncthreads();
+    }
+    for (int fc = 0; fc < C::NFCH; ++fc) {
+      const int f0 = fc * C::FCH;
+      const int wr = (C::NF - f0) < C::FCH ? (C::NF - f0) : C::FCH;
+      const int wp = round_up(wr, 8);
+      for (int idx = tid; idx < C::E * wp; idx += kThreads) {
+        const int e = idx / wp, fl = idx - e * wp, fq = f0 + fl;
+        double* gout = sG + (e * 5) * C::LDG + pcol(fl);
+        const int ce = c0 + e, eg = sId[e];
+        if (ce >= cp.Kc || fl >= wr) {
+#pragma unroll
+          for (int c = 0; c < 5; ++c) gout[c * C::LDG] = 0.0;
+          continue;
+        }
+        const int f = fq / C::NG, gq = fq - f * C::NG;
+        const double* tm = p.traces + (size_t)eg * 5 * C::TB + fq;
+        const State5 um{tm[0], tm[C::TB], tm[2 * C::TB], tm[3 * C::TB], tm[4 * C::TB]};
+        const double4 fn = cp.face[(size_t)ce * C::NF + fq];
+        const int2 cw = sConn[e * 4 + f];
+        State5 up;
+        if (cw.x >= 0) {
+          const int h = __ldg(p.code_map + (cw.y >> 8) * C::NG + gq);
+          const double* tp = p.traces + (size_t)cw.x * 5 * C::TB + (cw.y & 3) * C::NG + h;
+          up = State5{tp[0], tp[C::TB], tp[2 * C::TB], tp[3 * C::TB], tp[4 * C::TB]};
+        } else {
+          up = boundary_state(um, fn.x, fn.y, fn.z, (cw.y >> 2) & 3, p.gas);
+        }
+        if (!admissible(um, gamma) || !admissible(up, gamma))
+          record_error(p.err, 2, p.elem_offset + eg, f, gq, um.r);
+        double fs[5];
+        if (p.gas.riemann == 1)
+          hllc_flux(um, up, fn.x, fn.y, fn.z, gamma, fs);
+        else
+          llf_flux(um, up, fn.x, fn.y, fn.z, gamma, fs);
+#pragma unroll
+        for (int c = 0; c < 5; ++c) gout[c * C::LDG] = fn.w * fs[c];
+      }
+      __syncthreads();
+      gemm2_partial<C>(acc, sG, fbc, (C::K2CUB + f0) / 8, wp / 8, t_begin, t_end, lane);
+      __syncthreads();
+    }
+    // vol -> smem, then rhs = M_e^-1 vol (per element dense GEMV), update
+#pragma unroll
+    for (int i = 0; i < C::MAXT2; ++i) {
+      const int t = t_begin + i;
+      if (t < t_end) {
+        const int nt = t / C::MT, mt = t % C::MT;
+        for (int hh = 0; hh < 2; ++hh) {
+          const int r = mt * 16 + g + 8 * hh;
+          sV[r * L::LDV + nt * 8 + 2 * tq] = acc[i][2 * hh];
+          sV[r * L::LDV + nt * 8 + 2 * tq + 1] = acc[i][2 * hh + 1];
+        }
+      }
+    }
+    __syncthreads();
+    double a_c = 0.0, b_c = 0.0, dt = 0.0;
+    if (UPDATE) {
+      a_c = p.coef->a[p.stage];
+      b_c = p.coef->b[p.stage];
+      dt = p.coef->dt;
+    }
+    for (int idx = tid; idx < C::R * C::NP; idx += kThreads) {
+      const int r = idx / C::NP, i = idx - r * C::NP, e = r / 5;
+      const int ce = c0 + e;
+      if (ce >= cp.Kc) continue;
+      const double* mrow = cp.minv + ((size_t)ce * C::NP + i) * C::NP;
+      const double* v = sV + r * L::LDV;
+      double rhs = 0.0;
+      for (int j = 0; j < C::NP; ++j) rhs += __ldg(mrow + j) * v[j];
+      const size_t gi = ((size_t)sId[e] * 5 + r % 5) * C::BP + i;
+      if (UPDATE) {
+        const double rn = a_c * p.res[gi] + dt * rhs;
+        p.res[gi] = rn;
+        p.u[gi] = sU[r * C::LDU + pcol(i)] + b_c * rn;
+      } else {
+        p.rhs_out[gi] = rhs;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace cdg_gpu

@@ -21,6 +21,7 @@
 #include "cdg_gpu.h"
 #include "cdg_kernels.cuh"
 #include "cdg_peak.cuh"
+#include "cdg_curved.cuh"
 #include "cdg_sp.cuh"
 #include "cdg_ws.cuh"
 
@@ -63,6 +64,9 @@ struct KernelSet {
   void (*visc_rhs_update)(RhsParams);
   void (*visc_rhs_only)(RhsParams);
   void (*dbg_rhs[2])(RhsParams);  // timing experiments (CDG_KDBG=1|2)
+  void (*curved_update)(CurvedParams);
+  void (*curved_only)(CurvedParams);
+  size_t smem_curved;
 };
 
 template <int NP, int NCUB, int NG, int E, int CH = 16, int MINB = 1, int FCH = 32, int MODE = 0>
@@ -95,6 +99,9 @@ KernelSet make_set() {
   k.visc_rhs_only = &k_rhs<C, false, true>;
   k.dbg_rhs[0] = &k_rhs<C, true, false, 1>;
   k.dbg_rhs[1] = &k_rhs<C, true, false, 2>;
+  k.curved_update = &k_rhs_curved<C, true>;
+  k.curved_only = &k_rhs_curved<C, false>;
+  k.smem_curved = CurvedLayout<C>::SMEM_BYTES;
   return k;
 }
 
@@ -214,6 +221,11 @@ struct cdg_gpu_level {
   double* h = nullptr;
   // operators
   double *frag_icub = nullptr, *frag_op2 = nullptr, *frag_ig = nullptr, *frag_aux = nullptr;
+  // curved elements
+  int n_curved = 0;
+  int* curved_ids = nullptr;
+  double *curved_jwr = nullptr, *curved_minv = nullptr, *frag_opc = nullptr;
+  double4* curved_face = nullptr;
   // control
   StageCoef* d_coef = nullptr;
   StageCoef* h_coef = nullptr;  // pinned
@@ -302,6 +314,22 @@ RhsParams rhs_params(cdg_gpu_level* lv, int stage) {
   return p;
 }
 
+void launch_curved(cdg_gpu_level* lv, bool update, int stage) {
+  if (!lv->n_curved) return;
+  CurvedParams cp{};
+  cp.base = rhs_params(lv, stage);
+  cp.ids = lv->curved_ids;
+  cp.jwr = lv->curved_jwr;
+  cp.face = lv->curved_face;
+  cp.minv = lv->curved_minv;
+  cp.frag_opc = lv->frag_opc;
+  cp.Kc = lv->n_curved;
+  const int tiles = (lv->n_curved + lv->ks->E - 1) / lv->ks->E;
+  auto fn = update ? lv->ks->curved_update : lv->ks->curved_only;
+  fn<<<std::max(1, std::min(tiles, lv->n_sms)), kThreads, lv->ks->smem_curved, lv->stream>>>(cp);
+  ++lv->launches;
+}
+
 void launch_rhs(cdg_gpu_level* lv, bool update, bool viscous, int stage) {
   RhsParams p = rhs_params(lv, stage);
   const int tiles = lv->n_tiles();
@@ -313,12 +341,15 @@ void launch_rhs(cdg_gpu_level* lv, bool update, bool viscous, int stage) {
                                                                                   : lv->ks->smem_rhs;
   fn<<<lv->grid(tiles), kThreads, smem, lv->stream>>>(p);
   ++lv->launches;
+  launch_curved(lv, update, stage);
 }
 
 // Viscosity phase: sensor -> eps, then (if any eps > 0) aux gradient q and its
 // traces (solver.cpp:239-321). Returns whether the viscous path is active.
 bool viscosity_phase(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg) {
   if (!cfg->visc_enabled) return false;
+  if (lv->n_curved)
+    throw Status(CDG_GPU_ERR_CONFIG, "artificial viscosity on curved elements is not supported by this build");
   if (cfg->eps0 < 0.0) throw Status(CDG_GPU_ERR_CONFIG, "viscosity_amount: eps0 must be >= 0");
   if (cfg->jacobian_weighted)
     throw Status(CDG_GPU_ERR_CONFIG, "jacobian_weighted indicator is not supported on the GPU path");
@@ -551,8 +582,11 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
     } else if (!d->node_map) {
       throw Status(CDG_GPU_ERR_CONFIG, "level descriptor needs node_map or face_code");
     }
+    std::vector<char> is_curved(K, 0);
+    for (int i = 0; i < d->n_curved; ++i)
+      if (d->curved_ids && d->curved_ids[i] >= 0 && d->curved_ids[i] < K) is_curved[d->curved_ids[i]] = 1;
     for (int e = 0; e < K; ++e) {
-      const double jac = d->jac[e];
+      const double jac = is_curved[e] ? 1.0 : d->jac[e];
       if (!(jac > 1e-14))
         throw Status(CDG_GPU_ERR_NUMERICS, "inverted element " + std::to_string(e) + ": mapping Jacobian " +
                                                std::to_string(jac) + " at quadrature node 0");
@@ -586,6 +620,39 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
       }
     }
     if (codes.empty()) codes.assign(ng, 0);
+    if (d->n_curved > 0) {
+      if (!d->curved_ids || !d->curved_jwr || !d->curved_face || !d->curved_minv)
+        throw Status(CDG_GPU_ERR_CONFIG, "curved elements need curved_ids/jwr/face/minv");
+      for (int i = 0; i < d->n_curved; ++i) {
+        const int e = d->curved_ids[i];
+        if (e < 0 || e >= K) throw Status(CDG_GPU_ERR_CONFIG, "curved element id out of range");
+        conn[(size_t)e * 4].y |= kCurvedBit;
+      }
+      lv->n_curved = d->n_curved;
+      lv->curved_ids = dev_upload(std::vector<int>(d->curved_ids, d->curved_ids + d->n_curved));
+      lv->curved_jwr = dev_upload(std::vector<double>(d->curved_jwr, d->curved_jwr + (size_t)d->n_curved * ncub * 9));
+      std::vector<double4> cf((size_t)d->n_curved * nf);
+      for (size_t i = 0; i < cf.size(); ++i)
+        cf[i] = make_double4(d->curved_face[4 * i], d->curved_face[4 * i + 1], d->curved_face[4 * i + 2],
+                             d->curved_face[4 * i + 3]);
+      lv->curved_face = dev_upload(cf);
+      lv->curved_minv = dev_upload(std::vector<double>(d->curved_minv, d->curved_minv + (size_t)d->n_curved * np * np));
+      // [D_r^T D_s^T D_t^T | -I_g^T] in the chunked K layout of op2
+      std::vector<double> opc((size_t)np * k2, 0.0);
+      const int CHc = lv->ks->ch;
+      for (int q0 = 0; q0 < ncub8; q0 += CHc) {
+        const int w = std::min(CHc, ncub8 - q0);
+        for (int m = 0; m < 3; ++m)
+          for (int ql = 0; ql < w; ++ql) {
+            const int q = q0 + ql;
+            if (q >= ncub) continue;
+            for (int i = 0; i < np; ++i) opc[(size_t)i * k2 + 3 * q0 + m * w + ql] = dm[m][(size_t)q * np + i];
+          }
+      }
+      for (int i = 0; i < np; ++i)
+        for (int fq = 0; fq < nf; ++fq) opc[(size_t)i * k2 + k2cub + fq] = -ig[(size_t)fq * np + i];
+      lv->frag_opc = dev_upload(make_frag(opc, np, k2, np8, k2));
+    }
     lv->metric = dev_upload(met);
     lv->face = dev_upload(face);
     lv->conn = dev_upload(conn);
@@ -640,6 +707,8 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
                                  (int)lv->ks->smem_rhs));
     CUDA_OK(cudaFuncSetAttribute(lv->ks->aux_q, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)lv->ks->smem_rhs));
+    for (auto fn : {lv->ks->curved_update, lv->ks->curved_only})
+      CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lv->ks->smem_curved));
     for (auto fn : {lv->ks->dbg_rhs[0], lv->ks->dbg_rhs[1]})
       CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lv->ks->smem_rhs));
     CUDA_OK(cudaFuncSetAttribute(lv->ks->traces, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -662,7 +731,9 @@ void cdg_gpu_level_destroy(cdg_gpu_level* lv) {
                   (void*)lv->q, (void*)lv->qtr, (void*)lv->eps, (void*)lv->sqrt_eps, (void*)lv->d_vinv,
                   (void*)lv->d_icub, (void*)lv->d_maxeps, (void*)lv->metric, (void*)lv->face, (void*)lv->conn,
                   (void*)lv->code_map, (void*)lv->h, (void*)lv->frag_icub, (void*)lv->frag_op2,
-                  (void*)lv->frag_ig, (void*)lv->frag_aux, (void*)lv->d_coef, (void*)lv->d_err,
+                  (void*)lv->frag_ig, (void*)lv->frag_aux,
+                  (void*)lv->curved_ids, (void*)lv->curved_jwr, (void*)lv->curved_minv, (void*)lv->frag_opc,
+                  (void*)lv->curved_face, (void*)lv->d_coef, (void*)lv->d_err,
                   (void*)lv->d_scratch, (void*)lv->d_send_idx, (void*)lv->d_recv_idx})
     if (p) cudaFree(p);
   if (lv->h_coef) cudaFreeHost(lv->h_coef);

@@ -315,7 +315,8 @@ __device__ __forceinline__ State5 boundary_state(const State5& in, double nx, do
 }
 
 // Face coupling word: bits 0-1 neighbour face, 2-3 bc kind, 4 boundary flag,
-// 8-31 node-map code.
+// 5 (face 0 only) element is curved -> handled by k_rhs_curved, 8-31 node-map code.
+constexpr int kCurvedBit = 1 << 5;
 __host__ __device__ constexpr int pack_face(int nface, int bc, int boundary, int code) {
   return (nface & 3) | ((bc & 3) << 2) | ((boundary & 1) << 4) | (code << 8);
 }
@@ -686,6 +687,7 @@ __global__ void __launch_bounds__(kThreads, C::MINB) k_rhs(RhsParams p) {
           const int grow = row0 + r;
           const int col = nt * 8 + 2 * tq;
           if (grow >= n_rows || col >= C::NP) continue;
+          if (sConn[(r / 5) * 4].y & kCurvedBit) continue;  // written by k_rhs_curved
           const size_t gi = (size_t)grow * C::BP + col;
           const double r0 = acc[i][2 * hh], r1 = acc[i][2 * hh + 1];
           if (col + 1 < C::NP) {

@@ -234,6 +234,7 @@ __global__ void __launch_bounds__(kThreads, C::MINB) k_rhs_sp(RhsParams p) {
           const int grow = row0 + r;
           const int col = nt * 8 + 2 * tq;
           if (grow >= n_rows || col >= C::NP) continue;
+          if (sConn[(r / 5) * 4].y & kCurvedBit) continue;
           const size_t gi = (size_t)grow * C::BP + col;
           const double r0 = acc[i][2 * hh], r1 = acc[i][2 * hh + 1];
           if (col + 1 < C::NP) {

@@ -68,7 +68,9 @@ class LevelDesc(C.Structure):
                 ("metric", _dp), ("jac", _dp), ("face_normal", _dp), ("face_sjac", _dp), ("h", _dp),
                 ("neighbor", _ip), ("neighbor_face", _ip), ("bc", _ip), ("node_map", _ip),
                 ("face_code", _ip), ("code_node_map", _ip), ("n_codes", C.c_int),
-                ("freestream", C.c_double * 5)]
+                ("freestream", C.c_double * 5),
+                ("n_curved", C.c_int), ("curved_ids", _ip), ("curved_jwr", _dp), ("curved_face", _dp),
+                ("curved_minv", _dp)]
 
 
 _lib = None
@@ -139,9 +141,16 @@ class GpuLevel:
     DgLevel + RhsWorkspace + the solver kernels (solver.hpp:52-116)."""
 
     def __init__(self, mesh: Mesh, p: int, bc=0, freestream=None, curved_quadrature: bool = False,
-                 padded: bool = True, device: int = 0, re: R.ReferenceElement | None = None):
+                 padded: bool = True, device: int = 0, re: R.ReferenceElement | None = None,
+                 curved: tuple | None = None):
+        """curved = (element ids, physical collocation nodes [Kc, N_p, 3]) of the
+        isoparametric elements (CurvedMesh); a mesh with curved elements uses the
+        raised quadrature for every element (solver.cpp:551-557)."""
+        if curved is not None and len(curved[0]):
+            curved_quadrature = True
         self.re = re or R.level_reference_element(p, curved_quadrature)
-        self.arrays = a = LevelArrays(mesh, self.re, bc=bc, freestream=freestream, padded=padded)
+        self.arrays = a = LevelArrays(mesh, self.re, bc=bc, freestream=freestream, padded=padded,
+                                      curved=curved)
         re = self.re
         d = LevelDesc()
         d.degree, d.n_basis, d.n_cub, d.n_face_quad = re.degree, re.n_basis, re.n_cub, re.n_face_quad
@@ -158,6 +167,10 @@ class GpuLevel:
         d.face_code, d.code_node_map, d.n_codes = _p(a.face_code), _p(a.code_node_map), a.code_node_map.shape[0]
         for c in range(5):
             d.freestream[c] = a.freestream[c]
+        if a.curved_ids is not None:
+            d.n_curved = len(a.curved_ids)
+            d.curved_ids, d.curved_jwr = _p(a.curved_ids), _p(a.curved_jwr)
+            d.curved_face, d.curved_minv = _p(a.curved_face), _p(a.curved_minv)
         self._desc = d
         h = C.c_void_p()
         err = C.create_string_buffer(1024)

@@ -52,6 +52,47 @@ def affine_geometry(vertices: np.ndarray, tets: np.ndarray, re: ReferenceElement
     return metric, jac, normals, sjac, 6.0 * volume / area
 
 
+def curved_geometry(nodes: np.ndarray, re: ReferenceElement):
+    """compute_mapping + build_operators (operators.cpp:32-167) for curved
+    elements from their physical collocation nodes [Kc, N_p, 3]:
+    per-cubature-node J*W*dr_m/dx_d [Kc, N_cub, 9], per-face-node
+    (n, sjac*w) [Kc, 4N_g, 4], M_e^-1 [Kc, N_p, N_p] and h = 6V/A [Kc]."""
+    X = np.asarray(nodes, float)
+    ng = re.n_face_quad
+
+    def fwd_at(dr, ds, dt):
+        return np.stack([np.einsum("qj,kjd->kqd", dr, X), np.einsum("qj,kjd->kqd", ds, X),
+                         np.einsum("qj,kjd->kqd", dt, X)], axis=3)  # [Kc, n, i, m]
+
+    f = fwd_at(re.deriv_r, re.deriv_s, re.deriv_t)
+    jac = np.linalg.det(f)
+    if np.any(jac <= 1e-14):
+        k, q = np.argwhere(jac <= 1e-14)[0]
+        raise ArithmeticError(f"inverted curved element (list index {k}): mapping Jacobian {jac[k, q]} "
+                              f"at quadrature node {q}")
+    inv = np.linalg.inv(f)                                   # [Kc, q, m, i]
+    jw = jac * re.cub_weights[None, :]
+    jwr = (jw[:, :, None, None] * inv).reshape(X.shape[0], re.n_cub, 9)
+    ff = fwd_at(re.face_deriv_r, re.face_deriv_s, re.face_deriv_t)  # [Kc, nf, i, m]
+    face = np.empty((X.shape[0], 4 * ng, 4))
+    area = np.zeros(X.shape[0])
+    for fi, (a, b, c) in enumerate(FACE_VERTS):
+        ra = 0.5 * (TET_VERTS[b] - TET_VERTS[a])
+        rb = 0.5 * (TET_VERTS[c] - TET_VERTS[a])
+        sl = slice(fi * ng, (fi + 1) * ng)
+        xa = ff[:, sl] @ ra
+        xb = ff[:, sl] @ rb
+        nraw = np.cross(xa, xb)
+        s = np.linalg.norm(nraw, axis=2)
+        face[:, sl, :3] = nraw / s[..., None]
+        face[:, sl, 3] = s * re.face_weights[None, :]
+        area += (s * re.face_weights[None, :]).sum(axis=1)
+    mass = np.einsum("qi,kq,qj->kij", re.interp_cub, jw, re.interp_cub)
+    minv = np.linalg.inv(mass)
+    h = 6.0 * jw.sum(axis=1) / area
+    return np.ascontiguousarray(jwr), np.ascontiguousarray(face), np.ascontiguousarray(minv), h
+
+
 def perm_node_maps(re: ReferenceElement) -> np.ndarray:
     """[6][N_g] node maps, one per face-vertex permutation (PERMS order)."""
     ng = re.n_face_quad
@@ -84,7 +125,8 @@ class LevelArrays:
     """All host arrays behind one cdg_gpu_level_desc (kept alive by the owner)."""
 
     def __init__(self, mesh: Mesh, re: ReferenceElement, bc: dict | int = 0, freestream=None,
-                 padded: bool = True):
+                 padded: bool = True, curved: tuple | None = None):
+        """curved = (ids [Kc], nodes [Kc, N_p, 3]) for isoparametric elements."""
         K = mesh.n_owned
         self.re = re
         self.K = K
@@ -110,6 +152,12 @@ class LevelArrays:
                 kinds[mesh.boundary_tag[:K] == tag_id] = BC_KINDS[bc[tag]] if isinstance(bc[tag], str) else bc[tag]
         self.bc = np.ascontiguousarray(np.where(self.neighbor < 0, kinds, 0), np.int32)
         self.freestream = np.zeros(5) if freestream is None else np.asarray(freestream, float)
+        self.curved_ids = None
+        if curved is not None and len(curved[0]):
+            ids = np.ascontiguousarray(curved[0], np.int32)
+            self.curved_ids = ids
+            self.curved_jwr, self.curved_face, self.curved_minv, hc = curved_geometry(curved[1], re)
+            self.h[ids] = hc
         self.tables = {k: np.ascontiguousarray(getattr(re, k)) for k in
                        ("interp_cub", "interp_face", "deriv_r", "deriv_s", "deriv_t", "cub_weights",
                         "face_weights", "vandermonde_inv")}

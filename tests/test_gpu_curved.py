@@ -1,0 +1,85 @@
+"""Curved (isoparametric) elements on the GPU vs the reference itself: the
+acceptance sphere-shell fixture curved through the reference's own
+elasticity pipeline (acceptance_main.cpp:82-120), mixed affine + curved
+level with the raised quadrature (solver.cpp:551-557). Needs oracle/_ref."""
+import numpy as np
+import pytest
+
+from paper_1208_4772_b200 import mesh as M
+
+pytestmark = pytest.mark.gpu
+
+_CACHE = {}
+
+
+def sphere_case(ref, p):
+    key = p
+    if key not in _CACHE:
+        rm = ref.Mesh("sphere_curved", sphere=(2, 5, p, p))
+        rl = ref.Level(rm, p, bc_wall=0, bc_far=1)
+        ex = rm.export()
+        nodes, curved = rl.nodes()
+        perm = ex["perm"]
+        # reference FaceLink.perm packed p0+3p1+9p2 -> PERMS index
+        lut = {q[0] + 3 * q[1] + 9 * q[2]: i for i, q in enumerate(M.PERMS)}
+        code = np.where(perm >= 0, np.vectorize(lambda x: lut.get(int(x), 0))(perm), -1)
+        mesh = M.from_arrays(ex["vertices"], ex["tets"], ex["neighbor"], ex["neighbor_face"], code,
+                             np.where(ex["neighbor"] >= 0, -1, ex["bnd_tag"]))
+        mesh.tags = ["sphere", "farfield"]
+        ids = np.nonzero(curved)[0]
+        _CACHE[key] = (rm, rl, mesh, ids, nodes)
+    return _CACHE[key]
+
+
+def rel(a, b):
+    return np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300)
+
+
+FS = None
+
+
+def _fs(gpu):
+    # sphere_m038.json-like freestream: M=0.38, rho=p=1, alpha=0
+    c = np.sqrt(1.4)
+    return gpu.make_state(1.0, [0.38 * c, 0.0, 0.0], 1.0)
+
+
+@pytest.mark.parametrize("p", [2, 3, 4])
+def test_curved_sphere_rhs_and_steps_match_reference(gpu_lib, refmod, p):
+    gpu, ref = gpu_lib, refmod
+    rm, rl, mesh, ids, nodes = sphere_case(ref, p)
+    assert len(ids) > 0 and rl.n_cub > 0
+    fs = _fs(gpu)
+    lv = gpu.GpuLevel(mesh, p, bc={"sphere": 0, "farfield": 1}, freestream=fs, curved=(ids, nodes[ids]))
+    assert (lv.n_cub, lv.n_face_quad) == (rl.n_cub, rl.n_face_quad)
+    # node pairing identical to the reference's nearest-point pairing
+    g = rl.geometry()
+    a = lv.arrays
+    nm = a.code_node_map[a.face_code]
+    mask = a.neighbor >= 0
+    assert np.array_equal(nm[mask], g["node_map"][mask])
+    for riem in ("llf", "hllc"):
+        cfg = gpu.run_config(riem)
+        u = rl.random_admissible_store(5)
+        r_ref = rl.compute_rhs(u, ref.make_cfg(riem), fs)
+        r_gpu = lv.compute_rhs(cfg, u)
+        assert rel(r_gpu, r_ref) < 1e-10, (riem, rel(r_gpu, r_ref))
+    dt = 0.2 * rl.compute_timestep(u, ref.make_cfg("llf"))
+    lv.set_state(u)
+    assert 0.2 * lv.compute_timestep(gpu.run_config("llf")) == pytest.approx(dt, rel=1e-10)
+    lv.rk_steps(gpu.run_config("llf"), dt, 2)
+    u_ref, _ = rl.rk_steps(u, np.zeros_like(u), ref.make_cfg("llf"), fs, dt, 2)
+    assert rel(lv.get_state()[0], u_ref) < 1e-12
+
+
+@pytest.mark.parametrize("p", [2, 3, 4])
+def test_curved_sphere_freestream_preservation(gpu_lib, refmod, p):
+    """Acceptance C03 (acceptance_main.cpp:264-298): ||RHS||_inf < 1e-8."""
+    gpu, ref = gpu_lib, refmod
+    rm, rl, mesh, ids, nodes = sphere_case(ref, p)
+    fs = _fs(gpu)
+    lv = gpu.GpuLevel(mesh, p, bc={"sphere": 0, "farfield": 1}, freestream=fs, curved=(ids, nodes[ids]))
+    # farfield everywhere (as C03) -- freestream ghost on the sphere too
+    lv2 = gpu.GpuLevel(mesh, p, bc={"sphere": 1, "farfield": 1}, freestream=fs, curved=(ids, nodes[ids]))
+    r = lv2.compute_rhs(gpu.run_config("llf"), gpu.freestream_store(lv2, fs))
+    assert np.max(np.abs(r)) < 1e-8, np.max(np.abs(r))

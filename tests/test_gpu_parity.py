@@ -188,3 +188,77 @@ def test_residual_and_timestep(gpu_lib):
     r_l2 = lv.residual(0.2 * dt, "l2")
     assert r_inf == pytest.approx(np.max(np.abs(u1 - u0)) / (0.2 * dt), rel=1e-14)
     assert r_l2 == pytest.approx(np.sqrt(np.sum((u1 - u0) ** 2)) / (0.2 * dt), rel=1e-12)
+
+
+# ---- artificial viscosity (solver.cpp:239-321, 364-453) ----------------------
+VISC_FORCED = dict(enabled=True, eps0=0.04, kappa=4.0, s0_offset=-100.0)
+VISC_RAMP = dict(enabled=True, eps0=0.3, kappa=4.0, s0_offset=0.0)
+
+
+def _golden(name):
+    from pathlib import Path
+    return np.load(Path(__file__).resolve().parent / "golden" / name)
+
+
+def test_viscous_forced_matches_reference_golden(gpu_lib):
+    gpu = gpu_lib
+    gold = _golden("viscous_cube3_p2.npz")
+    m = M.cube_mesh(3)
+    lv = gpu.GpuLevel(m, 2, bc=1, freestream=gold["freestream"])
+    cfg = gpu.run_config("llf", viscosity=VISC_FORCED)
+    rhs = lv.compute_rhs(cfg, gold["forced_u"])
+    assert np.allclose(lv.viscosity(), gold["forced_eps"], rtol=1e-13, atol=0)
+    q = np.stack([lv.aux_gradient(mm) for mm in range(3)])
+    assert rel(q, gold["forced_q"]) < 1e-11
+    assert rel(rhs, gold["forced_rhs"]) < 1e-11
+
+
+def test_viscous_ramp_matches_reference_golden(gpu_lib):
+    gpu = gpu_lib
+    gold = _golden("viscous_cube3_p2.npz")
+    lv = gpu.GpuLevel(M.cube_mesh(3), 2, bc=1, freestream=gold["freestream"])
+    cfg = gpu.run_config("hllc", viscosity=VISC_RAMP)
+    rhs = lv.compute_rhs(cfg, gold["ramp_u"])
+    eps = lv.viscosity()
+    assert np.max(np.abs(eps - gold["ramp_eps"])) < 1e-12
+    assert (eps > 0).any() and (eps == 0).any()
+    assert rel(rhs, gold["ramp_rhs"]) < 1e-11
+
+
+@pytest.mark.parametrize("p", [2, 3, 4])
+def test_viscous_rk_steps_match_oracle(gpu_lib, p):
+    gpu = gpu_lib
+    m = M.cube_mesh(2, scale=2.0)
+    lv, ol, fs = _pair(gpu, m, p, bc=1)
+    cfg = gpu.run_config("llf", viscosity=VISC_FORCED)
+    u0 = gpu.random_admissible_store(lv, seed=13)
+    lv.set_state(u0)
+    dt = 0.1 * lv.compute_timestep(cfg)
+    lv.rk_steps(cfg, dt, 2)
+    u_ref, _ = ol.rk_steps(u0, np.zeros_like(u0), cfg, dt, 2)
+    assert rel(lv.get_state()[0], u_ref) < 1e-12
+    eps_ref, _ = ol.last_viscosity(with_q=False)
+    assert np.allclose(lv.viscosity(), eps_ref, rtol=1e-12, atol=0)
+
+
+def test_viscosity_off_is_bitwise_inviscid(gpu_lib):
+    """test_solver.cpp:334-352: eps0 = 0 gives the inviscid RHS bit for bit."""
+    gpu = gpu_lib
+    m = M.cube_mesh(2)
+    fs = _fs(gpu)
+    lv = gpu.GpuLevel(m, 2, bc=1, freestream=fs)
+    u = gpu.random_admissible_store(lv, seed=4)
+    r1 = lv.compute_rhs(gpu.run_config("llf"), u)
+    r2 = lv.compute_rhs(gpu.run_config("llf", viscosity=dict(enabled=True, eps0=0.0)), u)
+    assert np.array_equal(r1, r2)
+
+
+def test_viscous_timestep_limit(gpu_lib):
+    gpu = gpu_lib
+    m = M.cube_mesh(2)
+    lv, ol, fs = _pair(gpu, m, 3, bc=1)
+    cfg = gpu.run_config("llf", viscosity=VISC_FORCED)
+    u = gpu.random_admissible_store(lv, seed=8)
+    lv.compute_rhs(cfg, u)
+    eps = lv.viscosity()
+    assert lv.compute_timestep(cfg, use_viscosity=True) == pytest.approx(ol.compute_timestep(u, cfg, eps), rel=1e-12)
