@@ -63,14 +63,43 @@ cdg_gpu_level* create_level(const DgLevel& level, const ConservedState& fs) {
                       dt = row_major(re.deriv_t()), vinv = row_major(re.vandermonde_inv());
   std::vector<double> metric(9 * (size_t)K), jac(K), normal(12 * (size_t)K), sjac(4 * (size_t)K), h(K);
   std::vector<int> nb(4 * (size_t)K), nbf(4 * (size_t)K), bc(4 * (size_t)K), nmap(4 * (size_t)K * ng);
+  // curved (isoparametric) elements: per-node geometry + M_e^-1
+  std::vector<int> cids;
+  std::vector<double> cjwr, cface, cminv;
   for (int e = 0; e < K; ++e) {
     const auto& g = level.geom(e);
-    // the GPU path consumes affine (constant) geometry; curved elements carry
-    // per-node metrics that this adapter does not forward yet
-    for (int q = 1; q < ncub; ++q)
-      if (std::abs(g.cub_jac[q] - g.cub_jac[0]) > 1e-10 * std::abs(g.cub_jac[0]))
-        throw ConfigError("cdg_gpu adapter: curved element " + std::to_string(e) +
-                          " (per-node metrics) is not supported by this build");
+    bool curved = false;
+    for (int q = 1; q < ncub && !curved; ++q) {
+      curved = std::abs(g.cub_jac[q] - g.cub_jac[0]) > 1e-12 * std::abs(g.cub_jac[0]);
+      for (int k = 0; k < 9 && !curved; ++k)
+        curved = std::abs(g.cub_dr[q][k] - g.cub_dr[0][k]) > 1e-12 * (1.0 + std::abs(g.cub_dr[0][k]));
+    }
+    if (curved) {
+      cids.push_back(e);
+      for (int q = 0; q < ncub; ++q)
+        for (int k = 0; k < 9; ++k) cjwr.push_back(g.cub_jac[q] * re.cub_weights()[q] * g.cub_dr[q][k]);
+      for (int q = 0; q < 4 * ng; ++q) {
+        for (int d = 0; d < 3; ++d) cface.push_back(g.face_normal[q][d]);
+        cface.push_back(g.face_sjac[q] * re.face_weights()[q % ng]);
+      }
+      // M^-1 = L^-T L^-1 from the reference's Cholesky factor (operators.cpp:151-158)
+      const auto& l = level.ops(e).mass_chol;
+      std::vector<double> inv((size_t)np * np), y(np), x(np);
+      for (int col = 0; col < np; ++col) {
+        for (int i = 0; i < np; ++i) {
+          double s2 = (i == col) ? 1.0 : 0.0;
+          for (int j = 0; j < i; ++j) s2 -= l[j * np + i] * y[j];
+          y[i] = s2 / l[i * np + i];
+        }
+        for (int i = np - 1; i >= 0; --i) {
+          double s2 = y[i];
+          for (int j = i + 1; j < np; ++j) s2 -= l[i * np + j] * x[j];
+          x[i] = s2 / l[i * np + i];
+        }
+        for (int i = 0; i < np; ++i) inv[(size_t)i * np + col] = x[i];
+      }
+      cminv.insert(cminv.end(), inv.begin(), inv.end());
+    }
     for (int k = 0; k < 9; ++k) metric[9 * (size_t)e + k] = g.cub_dr[0][k];
     jac[e] = g.cub_jac[0];
     h[e] = g.h();
@@ -111,6 +140,11 @@ cdg_gpu_level* create_level(const DgLevel& level, const ConservedState& fs) {
   d.bc = bc.data();
   d.node_map = nmap.data();
   for (int c = 0; c < 5; ++c) d.freestream[c] = fs[c];
+  d.n_curved = static_cast<int>(cids.size());
+  d.curved_ids = cids.data();
+  d.curved_jwr = cjwr.data();
+  d.curved_face = cface.data();
+  d.curved_minv = cminv.data();
   cdg_gpu_level* lv = nullptr;
   char err[512] = {0};
   throw_status(cdg_gpu_level_create(&d, 0, &lv, err, sizeof err), err);
