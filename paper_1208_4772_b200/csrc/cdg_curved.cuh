@@ -23,14 +23,19 @@ struct CurvedParams {
   const double4* face;     // [Kc][NF]       (nx, ny, nz, sjac*w)
   const double* minv;      // [Kc][NP][NP]
   const double* frag_opc;  // B fragments of [D^T | -I_g^T]
+  double* vol;             // [Kc*5][NP8] epilogue scratch when the tile's vol does not fit smem
   int Kc;
 };
 
 template <class C>
 struct CurvedLayout {
   static constexpr int LDV = C::NP8 + 1;
-  static constexpr size_t SMEM_BYTES =
-      sizeof(double) * (C::SMEM_U + C::SMEM_C + C::SMEM_G + (size_t)C::R * LDV) + sizeof(int) * (C::E * 4 * 2 + C::E);
+  static constexpr size_t SMEM_NO_V =
+      sizeof(double) * (C::SMEM_U + C::SMEM_C + C::SMEM_G) + sizeof(int) * (C::E * 4 * 2 + C::E);
+  // p=8: the [R][NP8] vol panel does not fit next to the GEMM panels (227 KB
+  // opt-in limit); it then goes through a global scratch (GV).
+  static constexpr bool GV = SMEM_NO_V + sizeof(double) * (size_t)C::R * LDV > 232448;
+  static constexpr size_t SMEM_BYTES = SMEM_NO_V + (GV ? 0 : sizeof(double) * (size_t)C::R * LDV);
 };
 
 template <class C, bool UPDATE>
@@ -41,8 +46,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_rhs_curved(CurvedParams cp) {
   double* sU = smem;
   double* sC = sU + C::SMEM_U;
   double* sG = sC + C::SMEM_C;
-  double* sV = sG + C::SMEM_G;  // [R][LDV] vol (epilogue)
-  int2* sConn = reinterpret_cast<int2*>(sV + (size_t)C::R * L::LDV);
+  double* sV = sG + C::SMEM_G;  // [R][LDV] vol (epilogue), unless GV
+  int2* sConn = reinterpret_cast<int2*>(sV + (L::GV ? 0 : (size_t)C::R * L::LDV));
   int* sId = reinterpret_cast<int*>(sConn + C::E * 4);
   __shared__ int s_stop;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -167,7 +172,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_rhs_curved(CurvedParams cp) {
       gemm2_partial<C>(acc, sG, fbc, (C::K2CUB + f0) / 8, wp / 8, t_begin, t_end, lane);
       __syncthreads();
     }
-    // vol -> smem, then rhs = M_e^-1 vol (per element dense GEMV), update
+    // vol -> smem (or the global scratch), then rhs = M_e^-1 vol (per element
+    // dense GEMV), update
+    double* vbase = L::GV ? cp.vol + (size_t)c0 * 5 * L::LDV : sV;
 #pragma unroll
     for (int i = 0; i < C::MAXT2; ++i) {
       const int t = t_begin + i;
@@ -175,8 +182,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_rhs_curved(CurvedParams cp) {
         const int nt = t / C::MT, mt = t % C::MT;
         for (int hh = 0; hh < 2; ++hh) {
           const int r = mt * 16 + g + 8 * hh;
-          sV[r * L::LDV + nt * 8 + 2 * tq] = acc[i][2 * hh];
-          sV[r * L::LDV + nt * 8 + 2 * tq + 1] = acc[i][2 * hh + 1];
+          if (L::GV && c0 + r / 5 >= cp.Kc) continue;
+          vbase[r * L::LDV + nt * 8 + 2 * tq] = acc[i][2 * hh];
+          vbase[r * L::LDV + nt * 8 + 2 * tq + 1] = acc[i][2 * hh + 1];
         }
       }
     }
@@ -192,7 +200,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rhs_curved(CurvedParams cp) {
       const int ce = c0 + e;
       if (ce >= cp.Kc) continue;
       const double* mrow = cp.minv + ((size_t)ce * C::NP + i) * C::NP;
-      const double* v = sV + r * L::LDV;
+      const double* v = vbase + r * L::LDV;
       double rhs = 0.0;
       for (int j = 0; j < C::NP; ++j) rhs += __ldg(mrow + j) * v[j];
       const size_t gi = ((size_t)sId[e] * 5 + r % 5) * C::BP + i;

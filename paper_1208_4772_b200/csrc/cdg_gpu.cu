@@ -224,7 +224,7 @@ struct cdg_gpu_level {
   // curved elements
   int n_curved = 0;
   int* curved_ids = nullptr;
-  double *curved_jwr = nullptr, *curved_minv = nullptr, *frag_opc = nullptr;
+  double *curved_jwr = nullptr, *curved_minv = nullptr, *frag_opc = nullptr, *curved_vol = nullptr;
   double4* curved_face = nullptr;
   // control
   StageCoef* d_coef = nullptr;
@@ -323,6 +323,7 @@ void launch_curved(cdg_gpu_level* lv, bool update, int stage) {
   cp.face = lv->curved_face;
   cp.minv = lv->curved_minv;
   cp.frag_opc = lv->frag_opc;
+  cp.vol = lv->curved_vol;
   cp.Kc = lv->n_curved;
   const int tiles = (lv->n_curved + lv->ks->E - 1) / lv->ks->E;
   auto fn = update ? lv->ks->curved_update : lv->ks->curved_only;
@@ -652,6 +653,8 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
       for (int i = 0; i < np; ++i)
         for (int fq = 0; fq < nf; ++fq) opc[(size_t)i * k2 + k2cub + fq] = -ig[(size_t)fq * np + i];
       lv->frag_opc = dev_upload(make_frag(opc, np, k2, np8, k2));
+      // epilogue scratch for configurations whose vol panel does not fit smem (p=8)
+      CUDA_OK(cudaMalloc(&lv->curved_vol, sizeof(double) * (size_t)d->n_curved * 5 * (np8 + 1)));
     }
     lv->metric = dev_upload(met);
     lv->face = dev_upload(face);
@@ -707,8 +710,9 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
                                  (int)lv->ks->smem_rhs));
     CUDA_OK(cudaFuncSetAttribute(lv->ks->aux_q, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)lv->ks->smem_rhs));
-    for (auto fn : {lv->ks->curved_update, lv->ks->curved_only})
-      CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lv->ks->smem_curved));
+    if (lv->n_curved)
+      for (auto fn : {lv->ks->curved_update, lv->ks->curved_only})
+        CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lv->ks->smem_curved));
     for (auto fn : {lv->ks->dbg_rhs[0], lv->ks->dbg_rhs[1]})
       CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lv->ks->smem_rhs));
     CUDA_OK(cudaFuncSetAttribute(lv->ks->traces, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -733,7 +737,7 @@ void cdg_gpu_level_destroy(cdg_gpu_level* lv) {
                   (void*)lv->code_map, (void*)lv->h, (void*)lv->frag_icub, (void*)lv->frag_op2,
                   (void*)lv->frag_ig, (void*)lv->frag_aux,
                   (void*)lv->curved_ids, (void*)lv->curved_jwr, (void*)lv->curved_minv, (void*)lv->frag_opc,
-                  (void*)lv->curved_face, (void*)lv->d_coef, (void*)lv->d_err,
+                  (void*)lv->curved_vol, (void*)lv->curved_face, (void*)lv->d_coef, (void*)lv->d_err,
                   (void*)lv->d_scratch, (void*)lv->d_send_idx, (void*)lv->d_recv_idx})
     if (p) cudaFree(p);
   if (lv->h_coef) cudaFreeHost(lv->h_coef);

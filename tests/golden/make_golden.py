@@ -81,6 +81,8 @@ def viscous_cases():
     u2 = u.copy().reshape(lv.K, 5, lv.block)
     rng = np.random.default_rng(0)
     u2[::3, 0, : lv.n_basis] *= 1.0 + 0.2 * rng.uniform(-1, 1, size=u2[::3, 0, : lv.n_basis].shape)
+    # elements 1::3 constant (only the mean mode): indicator 0 -> eps = 0 branch
+    u2[1::3, :, : lv.n_basis] = u2[1::3, :, : lv.n_basis].mean(axis=2, keepdims=True)
     u2 = u2.reshape(-1)
     out["ramp_u"] = u2
     out["ramp_rhs"] = lv.compute_rhs(u2, cfg2, FS)
