@@ -17,8 +17,6 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libcdg_gpu.so"
-NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared", "-ccbin", "/usr/bin/g++"]
 
 
 def _nvcc() -> str:
@@ -36,9 +34,29 @@ def _stale(target: Path, sources) -> bool:
 
 
 def build_gpu(force: bool = False, verbose: bool = False) -> Path:
-    sources = sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "cdg_gpu.h"]
-    if force or _stale(LIB, sources):
-        cmd = [_nvcc(), *NVCC_FLAGS, "-I", str(ROOT / "include"), "-o", str(LIB), str(CSRC / "cdg_gpu.cu")]
+    """Compile every translation unit (cdg_gpu.cu + the kernel-set TUs
+    sets_*.cu) to an object in parallel, then link libcdg_gpu.so."""
+    headers = sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "cdg_gpu.h"]
+    units = sorted(CSRC.glob("*.cu"))
+    objdir = PKG / "build"
+    objdir.mkdir(exist_ok=True)
+    comp = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+            "-Xcompiler", "-fPIC", "-ccbin", "/usr/bin/g++", "-I", str(ROOT / "include")]
+    procs, objs = [], []
+    for cu in units:
+        obj = objdir / (cu.stem + ".o")
+        objs.append(obj)
+        if force or _stale(obj, [cu] + headers):
+            cmd = comp + ["-c", "-o", str(obj), str(cu)]
+            if verbose:
+                print(" ".join(cmd), flush=True)
+            procs.append((cu, subprocess.Popen(cmd)))
+    for cu, p in procs:
+        if p.wait() != 0:
+            raise subprocess.CalledProcessError(p.returncode, f"nvcc {cu.name}")
+    if force or procs or _stale(LIB, objs):
+        cmd = [_nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-ccbin", "/usr/bin/g++",
+               "-o", str(LIB), *map(str, objs)]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

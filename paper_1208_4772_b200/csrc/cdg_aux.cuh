@@ -21,6 +21,7 @@ struct SensorParams {
   double eps0, kappa, s0;
 };
 
+#ifndef CDG_SET_TU  // non-template kernels: defined once, in cdg_gpu.cu
 __global__ void __launch_bounds__(256) k_sensor(SensorParams p) {
   const int lane = threadIdx.x & 31;
   const int e = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -57,6 +58,7 @@ __global__ void __launch_bounds__(256) k_sensor(SensorParams p) {
     atomicMax(p.maxeps, (unsigned long long)__double_as_longlong(eps));
   }
 }
+#endif  // CDG_SET_TU
 
 // ---------------------------------------------------------------------------
 // Auxiliary gradient (compute_aux_gradient, solver.cpp:264-312), affine form:
@@ -201,6 +203,7 @@ struct TimestepParams {
   DevError* err;
 };
 
+#ifndef CDG_SET_TU
 // one warp per element, lanes over nodes (coalesced rows), shuffle max
 __global__ void __launch_bounds__(256) k_timestep(TimestepParams p) {
   const int lane = threadIdx.x & 31;
@@ -280,5 +283,6 @@ __global__ void k_halo_copy(double* traces, double* buf, const int* idx, int n, 
       *t = *s;
   }
 }
+#endif  // CDG_SET_TU
 
 }  // namespace cdg_gpu

@@ -17,13 +17,9 @@
 #include <string>
 #include <vector>
 
-#include "cdg_aux.cuh"
 #include "cdg_gpu.h"
-#include "cdg_kernels.cuh"
 #include "cdg_peak.cuh"
-#include "cdg_curved.cuh"
-#include "cdg_sp.cuh"
-#include "cdg_ws.cuh"
+#include "cdg_sets.cuh"
 
 using namespace cdg_gpu;
 
@@ -51,74 +47,13 @@ void set_err(char* err, size_t n, const std::string& msg) {
 
 int pad16(int n) { return 16 * ((n + 15) / 16); }
 
-// ---- kernel dispatch per (N_p, N_cub, N_g) ---------------------------------
-struct KernelSet {
-  int np, ncub, ng, E, minb, ch;
-  bool ws = false, rhs_only_ws = false;
-  size_t smem_ws = 0;
-  size_t smem_traces, smem_rhs;
-  void (*traces)(const double*, double*, const double*, int, int);
-  void (*rhs_update)(RhsParams);
-  void (*rhs_only)(RhsParams);
-  void (*aux_q)(AuxParams);
-  void (*visc_rhs_update)(RhsParams);
-  void (*visc_rhs_only)(RhsParams);
-  void (*dbg_rhs[2])(RhsParams);  // timing experiments (CDG_KDBG=1|2)
-  void (*curved_update)(CurvedParams);
-  void (*curved_only)(CurvedParams);
-  size_t smem_curved;
-};
-
-template <int NP, int NCUB, int NG, int E, int CH = 16, int MINB = 1, int FCH = 32, int MODE = 0>
-KernelSet make_set() {
-  using C = Cfg<NP, NCUB, NG, E, CH, MINB, FCH>;
-  KernelSet k;
-  k.np = NP;
-  k.ncub = NCUB;
-  k.ng = NG;
-  k.E = E;
-  k.minb = MINB;
-  k.ch = CH;
-  k.smem_traces = sizeof(double) * C::R * C::LDU;
-  k.smem_rhs = C::SMEM_BYTES;
-  k.traces = &k_traces<C>;
-  k.rhs_update = &k_rhs<C, true, false>;
-  k.ws = MODE != 0;  // MODE 1: warp-specialised, 2: software-pipelined (inviscid kernels)
-  if constexpr (MODE == 1) {
-    k.rhs_update = &k_rhs_ws<C>;
-    k.smem_ws = WsLayout<C>::SMEM_BYTES;
-  } else if constexpr (MODE == 2) {
-    k.rhs_update = &k_rhs_sp<C, true>;
-    k.rhs_only = &k_rhs_sp<C, false>;
-    k.rhs_only_ws = true;
-    k.smem_ws = SpLayout<C>::SMEM_BYTES;
-  }
-  k.rhs_only = &k_rhs<C, false, false>;
-  k.aux_q = &k_aux_q<C>;
-  k.visc_rhs_update = &k_rhs<C, true, true>;
-  k.visc_rhs_only = &k_rhs<C, false, true>;
-  k.dbg_rhs[0] = &k_rhs<C, true, false, 1>;
-  k.dbg_rhs[1] = &k_rhs<C, true, false, 2>;
-  k.curved_update = &k_rhs_curved<C, true>;
-  k.curved_only = &k_rhs_curved<C, false>;
-  k.smem_curved = CurvedLayout<C>::SMEM_BYTES;
-  return k;
-}
-
 const std::vector<KernelSet>& kernel_sets() {
-  static const std::vector<KernelSet> sets = {
-      // straight-sided strengths (2p+1 / 2p): refelem.cpp:311-317
-      // <N_p, N_cub, N_g, E elements/tile, CH cubature chunk, CTAs/SM>
-      make_set<4, 5, 3, 16, 8, 2>(), make_set<10, 15, 6, 16, 16, 2>(), make_set<20, 35, 12, 16, 16, 2>(),
-      make_set<35, 70, 16, 16, 24, 2, 64>(), make_set<56, 126, 56, 16, 16, 2>(), make_set<84, 210, 84, 16>(),
-      make_set<120, 330, 120, 16>(), make_set<165, 495, 165, 16>(),
-      // curved-mesh strengths (3p-3 / 3p-2): refelem.hpp:118-119
-      make_set<20, 35, 16, 16, 16, 2>(), make_set<35, 70, 56, 16, 24, 2>(), make_set<56, 210, 84, 16, 16, 2>(),
-      make_set<84, 330, 165, 16>(), make_set<120, 715, 220, 16>(),
-      make_set<165, 1001, 364, 16>(),
-      // P=4 straight tuning variants, selected with CDG_KCFG=<n> (bench sweeps)
-      make_set<35, 70, 16, 16, 8, 2, 16, 1>(), make_set<35, 70, 16, 16, 8, 2, 16, 2>(),
-      make_set<35, 70, 16, 16, 24, 2, 32>(), make_set<35, 70, 16, 32, 24, 1, 32>()};
+  static const std::vector<KernelSet> sets = [] {
+    std::vector<KernelSet> all;
+    for (auto part : {kernel_sets_p1_3(), kernel_sets_p4(), kernel_sets_p5_6(), kernel_sets_p7_8()})
+      all.insert(all.end(), part.begin(), part.end());
+    return all;
+  }();
   return sets;
 }
 
@@ -185,6 +120,16 @@ std::vector<double> make_frag(const std::vector<double>& op, int rows, int cols,
   return f;
 }
 
+// B fragments for the warp-tile kernel (cdg_warp.cuh): lane (g, t) of
+// (n-tile nt, k-step ks) holds (op[8nt+g][8ks+2t], op[8nt+g][8ks+2t+1]).
+void frag_nat(std::vector<double>& out, const std::vector<double>& op, int rows, int cols, int nt, int ks) {
+  for (int lane = 0; lane < 32; ++lane)
+    for (int v = 0; v < 2; ++v) {
+      const int r = nt * 8 + lane / 4, c = ks * 8 + 2 * (lane % 4) + v;
+      out.push_back(r < rows && c < cols ? op[(size_t)r * cols + c] : 0.0);
+    }
+}
+
 template <typename T>
 T* dev_upload(const std::vector<T>& h) {
   T* d = nullptr;
@@ -221,6 +166,10 @@ struct cdg_gpu_level {
   double* h = nullptr;
   // operators
   double *frag_icub = nullptr, *frag_op2 = nullptr, *frag_ig = nullptr, *frag_aux = nullptr;
+  double *wfrag1 = nullptr, *wfrag2v = nullptr, *wfrag2f = nullptr;  // warp-tile kernel
+  bool use_warp = false;
+  double* rfrag2 = nullptr;  // row kernel (its I_cub fragments are wfrag1)
+  bool use_row = false;
   // curved elements
   int n_curved = 0;
   int* curved_ids = nullptr;
@@ -311,6 +260,8 @@ RhsParams rhs_params(cdg_gpu_level* lv, int stage) {
   p.sqrt_eps = lv->sqrt_eps;
   p.icub = lv->d_icub;
   p.qtr_stride = (size_t)(lv->K + lv->n_halo) * 5 * lv->tb;
+  static const int pf = std::getenv("CDG_PREFETCH") ? std::atoi(std::getenv("CDG_PREFETCH")) : 15;
+  p.prefetch = pf;
   return p;
 }
 
@@ -331,16 +282,61 @@ void launch_curved(cdg_gpu_level* lv, bool update, int stage) {
   ++lv->launches;
 }
 
+void launch_rhs_warp(cdg_gpu_level* lv, bool update, int stage) {
+  WarpParams w{};
+  w.u = lv->u;
+  w.res = lv->res;
+  w.rhs_out = lv->rhs;
+  w.traces = lv->traces;
+  w.metric = lv->metric;
+  w.face = lv->face;
+  w.conn = lv->conn;
+  w.code_map = lv->code_map;
+  w.frag1 = reinterpret_cast<const double2*>(lv->wfrag1);
+  w.frag2v = reinterpret_cast<const double2*>(lv->wfrag2v);
+  w.frag2f = reinterpret_cast<const double2*>(lv->wfrag2f);
+  w.coef = lv->d_coef;
+  w.stage = stage;
+  w.K = lv->K;
+  w.elem_offset = 0;
+  w.gas = lv->gas;
+  w.err = lv->d_err;
+  const int tiles = (lv->K + 15) / 16;
+  const int ctas = std::max(1, std::min((tiles + lv->ks->warp_warps - 1) / lv->ks->warp_warps,
+                                        lv->n_sms * lv->ks->warp_minb));
+  const int rm = lv->gas.riemann == 1 ? 1 : 0;
+  auto fn = update ? lv->ks->warp_update[rm] : lv->ks->warp_only[rm];
+  fn<<<ctas, 32 * lv->ks->warp_warps, lv->ks->smem_warp, lv->stream>>>(w);
+  ++lv->launches;
+  launch_curved(lv, update, stage);
+}
+
+void launch_rhs_row(cdg_gpu_level* lv, bool update, int stage) {
+  RhsParams p = rhs_params(lv, stage);
+  p.frag_icub = lv->wfrag1;
+  p.frag_op2 = lv->rfrag2;
+  const int rm = lv->gas.riemann == 1 ? 1 : 0;
+  auto fn = update ? lv->ks->row_update[rm] : lv->ks->row_only[rm];
+  const int tiles = (lv->K + 15) / 16;
+  fn<<<std::max(1, std::min(tiles, lv->n_sms * lv->ks->row_minb)), 160, lv->ks->smem_row, lv->stream>>>(p);
+  ++lv->launches;
+  launch_curved(lv, update, stage);
+}
+
 void launch_rhs(cdg_gpu_level* lv, bool update, bool viscous, int stage) {
+  if (!viscous && lv->use_row) {
+    launch_rhs_row(lv, update, stage);
+    return;
+  }
+  if (!viscous && lv->use_warp) {
+    launch_rhs_warp(lv, update, stage);
+    return;
+  }
   RhsParams p = rhs_params(lv, stage);
   const int tiles = lv->n_tiles();
   auto fn = viscous ? (update ? lv->ks->visc_rhs_update : lv->ks->visc_rhs_only)
                     : (update ? lv->ks->rhs_update : lv->ks->rhs_only);
-  static const int dbg = std::getenv("CDG_KDBG") ? std::atoi(std::getenv("CDG_KDBG")) : 0;
-  if (update && !viscous && (dbg == 1 || dbg == 2)) fn = lv->ks->dbg_rhs[dbg - 1];
-  const size_t smem = (!viscous && lv->ks->ws && (update || lv->ks->rhs_only_ws)) ? lv->ks->smem_ws
-                                                                                  : lv->ks->smem_rhs;
-  fn<<<lv->grid(tiles), kThreads, smem, lv->stream>>>(p);
+  fn<<<lv->grid(tiles), lv->ks->nth, lv->ks->smem_rhs, lv->stream>>>(p);
   ++lv->launches;
   launch_curved(lv, update, stage);
 }
@@ -401,7 +397,7 @@ bool viscosity_phase(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg) {
   ap.K = lv->K;
   ap.n_tiles = lv->n_tiles();
   ap.gas = lv->gas;
-  lv->ks->aux_q<<<lv->grid(lv->n_tiles()), kThreads, lv->ks->smem_rhs, lv->stream>>>(ap);
+  lv->ks->aux_q<<<lv->grid(lv->n_tiles()), kThreads, lv->ks->smem_aux, lv->stream>>>(ap);
   ++lv->launches;
   // q traces: 3 x (K*5 rows)
   const size_t n = (size_t)lv->K * 5 * lv->bp;
@@ -541,33 +537,58 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
     const int kp = (np + 7) / 8 * 8, ncub8 = (ncub + 7) / 8 * 8, np8 = (np + 7) / 8 * 8,
               nf8 = (nf + 7) / 8 * 8;
     const int k2cub = 3 * ncub8, k2 = k2cub + nf8;
-    // RHS operator rows i: [chunked (m, q) volume block | -LIFT]
-    std::vector<double> op2((size_t)np * k2, 0.0);
-    // aux operator (viscous gradient): same volume block, +LIFT (solver.cpp:283-309)
-    std::vector<double> opaux((size_t)np * k2, 0.0);
-    const int CH = lv->ks->ch;
-    for (int q0 = 0; q0 < ncub8; q0 += CH) {
-      const int w = std::min(CH, ncub8 - q0);
-      for (int m = 0; m < 3; ++m)
-        for (int ql = 0; ql < w; ++ql) {
-          const int q = q0 + ql;
-          if (q >= ncub) continue;
-          for (int i = 0; i < np; ++i) {
-            op2[(size_t)i * k2 + 3 * q0 + m * w + ql] = amat[m][(size_t)i * ncub + q];
-            opaux[(size_t)i * k2 + 3 * q0 + m * w + ql] = amat[m][(size_t)i * ncub + q];
+    // RHS operator rows i: [chunked (m, q) volume block | -LIFT]; the aux
+    // operator (viscous gradient) has the same volume block and +LIFT
+    // (solver.cpp:283-309). The K order follows the kernel's cubature chunk.
+    auto build_op2 = [&](int CH, double lift_sign) {
+      std::vector<double> op((size_t)np * k2, 0.0);
+      for (int q0 = 0; q0 < ncub8; q0 += CH) {
+        const int w = std::min(CH, ncub8 - q0);
+        for (int m = 0; m < 3; ++m)
+          for (int ql = 0; ql < w; ++ql) {
+            const int q = q0 + ql;
+            if (q >= ncub) continue;
+            for (int i = 0; i < np; ++i) op[(size_t)i * k2 + 3 * q0 + m * w + ql] = amat[m][(size_t)i * ncub + q];
           }
-        }
-    }
-    for (int i = 0; i < np; ++i)
-      for (int fq = 0; fq < nf; ++fq) {
-        op2[(size_t)i * k2 + k2cub + fq] = -lift[(size_t)i * nf + fq];
-        opaux[(size_t)i * k2 + k2cub + fq] = lift[(size_t)i * nf + fq];
       }
+      for (int i = 0; i < np; ++i)
+        for (int fq = 0; fq < nf; ++fq) op[(size_t)i * k2 + k2cub + fq] = lift_sign * lift[(size_t)i * nf + fq];
+      return op;
+    };
+    const std::vector<double> op2 = build_op2(lv->ks->ch, -1.0), opaux = build_op2(lv->ks->ch, 1.0);
     lv->frag_icub = dev_upload(make_frag(icub, ncub, np, ncub8, kp));
     lv->d_icub = dev_upload(icub);
     lv->frag_ig = dev_upload(make_frag(ig, nf, np, nf8, kp));
     lv->frag_op2 = dev_upload(make_frag(op2, np, k2, np8, k2));
     lv->frag_aux = dev_upload(make_frag(opaux, np, k2, np8, k2));
+    if (lv->ks->row_update[0]) {
+      const std::vector<double> op2r = build_op2(lv->ks->row_ch, -1.0);
+      std::vector<double> f2;
+      for (int k = 0; k < k2 / 8; ++k)
+        for (int n = 0; n < np8 / 8; ++n) frag_nat(f2, op2r, np, k2, n, k);
+      lv->rfrag2 = dev_upload(f2);
+      const char* nr = std::getenv("CDG_NOROW");
+      lv->use_row = !(nr && std::atoi(nr));
+    }
+    if (lv->ks->warp_update[0] || lv->ks->row_update[0]) {
+      const int nch = (ncub + 7) / 8, nfch = (nf + 7) / 8, ks1 = kp / 8, nt = np8 / 8;
+      std::vector<double> f1, f2v, f2f;
+      std::vector<double> neg_lift(lift.size());
+      for (size_t i = 0; i < lift.size(); ++i) neg_lift[i] = -lift[i];
+      for (int ch = 0; ch < nch; ++ch)
+        for (int k = 0; k < ks1; ++k) frag_nat(f1, icub, ncub, np, ch, k);
+      for (int ch = 0; ch < nch; ++ch)
+        for (int m = 0; m < 3; ++m)
+          for (int n = 0; n < nt; ++n) frag_nat(f2v, amat[m], np, ncub, n, ch);
+      for (int fc = 0; fc < nfch; ++fc)
+        for (int n = 0; n < nt; ++n) frag_nat(f2f, neg_lift, np, nf, n, fc);
+      lv->wfrag1 = dev_upload(f1);
+      if (!lv->ks->warp_update[0]) f2v.clear(), f2f.clear();
+      lv->wfrag2v = dev_upload(f2v);
+      lv->wfrag2f = dev_upload(f2f);
+      const char* nw = std::getenv("CDG_NOWARP");
+      lv->use_warp = lv->ks->warp_update[0] && !(nw && std::atoi(nw));
+    }
     if (d->vandermonde_inv)
       lv->d_vinv = dev_upload(std::vector<double>(d->vandermonde_inv, d->vandermonde_inv + (size_t)np * np));
 
@@ -691,30 +712,19 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
     std::memcpy(lv->freestream, d->freestream, sizeof(lv->freestream));
     for (int c = 0; c < 5; ++c) lv->gas.fs[c] = d->freestream[c];
     // opt in to > 48 KB dynamic shared memory
-    CUDA_OK(cudaFuncSetAttribute(lv->ks->rhs_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)std::max(lv->ks->smem_rhs, lv->ks->smem_ws)));
-    if (std::getenv("CDG_CARVEOUT")) {
-      // leave the rest of the 256 KB L1/smem array to L1, where the B-operand
-      // fragments of the shared operators stream from
-      const int pct = std::min(100, (int)std::ceil(100.0 * lv->ks->minb * (lv->ks->smem_rhs + 1024) /
-                                                   (double)prop.sharedMemPerMultiprocessor));
-      for (auto fn : {lv->ks->rhs_update, lv->ks->rhs_only, lv->ks->visc_rhs_update, lv->ks->visc_rhs_only,
-                      lv->ks->dbg_rhs[0], lv->ks->dbg_rhs[1]})
-        CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
-    }
-    CUDA_OK(cudaFuncSetAttribute(lv->ks->rhs_only, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)std::max(lv->ks->smem_rhs, lv->ks->smem_ws)));
-    CUDA_OK(cudaFuncSetAttribute(lv->ks->visc_rhs_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)lv->ks->smem_rhs));
-    CUDA_OK(cudaFuncSetAttribute(lv->ks->visc_rhs_only, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)lv->ks->smem_rhs));
+    for (auto fn : {lv->ks->rhs_update, lv->ks->rhs_only, lv->ks->visc_rhs_update, lv->ks->visc_rhs_only})
+      CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lv->ks->smem_rhs));
     CUDA_OK(cudaFuncSetAttribute(lv->ks->aux_q, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)lv->ks->smem_rhs));
+                                 (int)lv->ks->smem_aux));
+    if (lv->ks->row_update[0])
+      for (auto fn : {lv->ks->row_update[0], lv->ks->row_update[1], lv->ks->row_only[0], lv->ks->row_only[1]})
+        CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lv->ks->smem_row));
+    if (lv->ks->warp_update[0])
+      for (auto fn : {lv->ks->warp_update[0], lv->ks->warp_update[1], lv->ks->warp_only[0], lv->ks->warp_only[1]})
+        CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lv->ks->smem_warp));
     if (lv->n_curved)
       for (auto fn : {lv->ks->curved_update, lv->ks->curved_only})
         CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lv->ks->smem_curved));
-    for (auto fn : {lv->ks->dbg_rhs[0], lv->ks->dbg_rhs[1]})
-      CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lv->ks->smem_rhs));
     CUDA_OK(cudaFuncSetAttribute(lv->ks->traces, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)lv->ks->smem_traces));
     CUDA_OK(cudaDeviceSynchronize());
@@ -735,7 +745,7 @@ void cdg_gpu_level_destroy(cdg_gpu_level* lv) {
                   (void*)lv->q, (void*)lv->qtr, (void*)lv->eps, (void*)lv->sqrt_eps, (void*)lv->d_vinv,
                   (void*)lv->d_icub, (void*)lv->d_maxeps, (void*)lv->metric, (void*)lv->face, (void*)lv->conn,
                   (void*)lv->code_map, (void*)lv->h, (void*)lv->frag_icub, (void*)lv->frag_op2,
-                  (void*)lv->frag_ig, (void*)lv->frag_aux,
+                  (void*)lv->frag_ig, (void*)lv->frag_aux, (void*)lv->wfrag1, (void*)lv->wfrag2v, (void*)lv->wfrag2f, (void*)lv->rfrag2,
                   (void*)lv->curved_ids, (void*)lv->curved_jwr, (void*)lv->curved_minv, (void*)lv->frag_opc,
                   (void*)lv->curved_vol, (void*)lv->curved_face, (void*)lv->d_coef, (void*)lv->d_err,
                   (void*)lv->d_scratch, (void*)lv->d_send_idx, (void*)lv->d_recv_idx})

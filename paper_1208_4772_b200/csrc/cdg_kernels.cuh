@@ -43,9 +43,10 @@ __host__ __device__ constexpr int imax(int a, int b) { return a > b ? a : b; }
 // loads from the k8-permuted layout (see pcol)
 __host__ __device__ constexpr int frag_ld8(int n) { return (n % 16 == 8) ? n : frag_ld8(n + 8); }
 
-template <int NP_, int NCUB_, int NG_, int E_, int CH_ = 16, int MINB_ = 1, int FCH_ = 32>
+template <int NP_, int NCUB_, int NG_, int E_, int CH_ = 16, int MINB_ = 1, int FCH_ = 32, int NW_ = 8>
 struct Cfg {
   static constexpr int NP = NP_, NCUB = NCUB_, NG = NG_, NF = 4 * NG_, E = E_;
+  static constexpr int NW = NW_, NTH = 32 * NW_;  // warps / threads per CTA (k_rhs)
   static constexpr int MINB = MINB_;              // resident CTAs per SM (launch bounds)
   static constexpr int R = 5 * E;                 // rows per tile
   static constexpr int MT = R / 16;               // m16 tiles per tile
@@ -68,11 +69,14 @@ struct Cfg {
   static constexpr int LDC = CH + 4;
   static constexpr int LDG = frag_ld8(imax(3 * CH, FCH));
   static constexpr int T2 = MT * NT2;             // RHS output tiles
-  static constexpr int MAXT2 = ceil_div(T2, kWarps);
+  static constexpr int MAXT2 = ceil_div(T2, NW);
+  // one m-tile row per warp (NW == MT): the warp's A fragment is loaded once
+  // per k-step and reused across all NT2 n-tiles
+  static constexpr bool WROW = (NW == MT);
   static constexpr int T1MAX = MT * (CH / 8);     // GEMM1 tiles per chunk
-  static constexpr int MAXT1 = ceil_div(T1MAX, kWarps);
-  static constexpr int IT_P = ceil_div(E * CH, kThreads);   // pointwise pairs per thread
-  static constexpr int IT_F = ceil_div(E * FCH, kThreads);  // face pairs per thread
+  static constexpr int MAXT1 = (NW == MT) ? CH / 8 : ceil_div(T1MAX, NW);
+  static constexpr int IT_P = ceil_div(E * CH, NTH);   // pointwise pairs per thread
+  static constexpr int IT_F = ceil_div(E * FCH, NTH);  // face pairs per thread
   static constexpr int SMEM_U = R * LDU;
   static constexpr int SMEM_C = R * LDC;
   static constexpr int SMEM_G = R * LDG;
@@ -163,11 +167,11 @@ __device__ __forceinline__ void mma_frag(double (&d)[4], const AFrag& a, const d
 }
 
 // Stage rows [row0, row0+R) of a [*][BP] store into a pcol-permuted panel.
-template <class C>
+template <class C, int NTH = kThreads>
 __device__ __forceinline__ void stage_rows(const double* __restrict__ src, int row0, int n_rows, double* s,
                                            int tid) {
   constexpr int V8 = C::KP / 8;
-  for (int idx = tid; idx < C::R * V8 * 2; idx += kThreads) {
+  for (int idx = tid; idx < C::R * V8 * 2; idx += NTH) {
     const int h = idx & 1, j = (idx >> 1) % V8, r = (idx >> 1) / V8;
     double2 x = make_double2(0.0, 0.0), y = make_double2(0.0, 0.0);
     if (row0 + r < n_rows) {
@@ -387,7 +391,16 @@ struct RhsParams {
   const double* sqrt_eps;     // [K+halo]
   const double* icub;         // [NCUB][NP] row-major (viscous volume term)
   size_t qtr_stride;          // elements per direction of qtr
+  int prefetch;               // L2 prefetch mask: 1 res, 2 next-tile u, 4 own traces, 8 neighbour traces
 };
+
+__device__ __forceinline__ void l2_prefetch(const void* ptr) { asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr)); }
+
+// Touch `bytes` bytes from `base` (128-byte lines) into L2, lines spread over the CTA.
+__device__ __forceinline__ void l2_prefetch_range(const void* base, size_t bytes, int tid, int nthreads) {
+  const char* b = reinterpret_cast<const char*>(base);
+  for (size_t off = (size_t)tid * 128; off < bytes; off += (size_t)nthreads * 128) l2_prefetch(b + off);
+}
 
 // GEMM1 for one cubature chunk: sC[:, 0:w] = U * I_cub[q0:q0+w, :]^T
 template <class C>
@@ -398,23 +411,41 @@ __device__ __forceinline__ void gemm1_chunk(const double* sU, double* sC, const 
   double c[C::MAXT1][4];
 #pragma unroll
   for (int i = 0; i < C::MAXT1; ++i) c[i][0] = c[i][1] = c[i][2] = c[i][3] = 0.0;
+  // tile i of this warp: WROW -> (m-tile warp, n-tile i), else round robin
 #pragma unroll
   for (int ks = 0; ks < C::KS1; ++ks) {
+    if constexpr (C::WROW) {
+      const AFrag a = load_afrag(sU, C::LDU, warp * 16, ks * 8, g, tq);
 #pragma unroll
-    for (int i = 0; i < C::MAXT1; ++i) {
-      const int t = warp + i * kWarps;
-      if (t < T1) {
-        const int mt = t / nt1, nt = t % nt1;
-        mma_frag(c[i], load_afrag(sU, C::LDU, mt * 16, ks * 8, g, tq),
-                 __ldg(fb + ((size_t)(q0 / 8 + nt) * C::KS1 + ks) * 32 + lane));
+      for (int i = 0; i < C::MAXT1; ++i)
+        if (i < nt1) mma_frag(c[i], a, __ldg(fb + ((size_t)(q0 / 8 + i) * C::KS1 + ks) * 32 + lane));
+    } else {
+#pragma unroll
+      for (int i = 0; i < C::MAXT1; ++i) {
+        const int t = warp + i * C::NW;
+        if (t < T1) {
+          const int mt = t / nt1, nt = t % nt1;
+          mma_frag(c[i], load_afrag(sU, C::LDU, mt * 16, ks * 8, g, tq),
+                   __ldg(fb + ((size_t)(q0 / 8 + nt) * C::KS1 + ks) * 32 + lane));
+        }
       }
     }
   }
 #pragma unroll
   for (int i = 0; i < C::MAXT1; ++i) {
-    const int t = warp + i * kWarps;
-    if (t < T1) {
-      const int mt = t / nt1, nt = t % nt1;
+    int mt, nt;
+    bool ok;
+    if constexpr (C::WROW) {
+      mt = warp;
+      nt = i;
+      ok = i < nt1;
+    } else {
+      const int t = warp + i * C::NW;
+      ok = t < T1;
+      mt = ok ? t / nt1 : 0;
+      nt = ok ? t % nt1 : 0;
+    }
+    if (ok) {
       double* o = sC + (mt * 16 + g) * C::LDC + nt * 8 + 2 * tq;
       *reinterpret_cast<double2*>(o) = make_double2(c[i][0], c[i][1]);
       *reinterpret_cast<double2*>(o + 8 * C::LDC) = make_double2(c[i][2], c[i][3]);
@@ -428,15 +459,25 @@ template <class C, int NKS>
 __device__ __forceinline__ void gemm2_fixed(double (&acc)[C::MAXT2][4], const double* sG, const double2* fb,
                                             int ks0, int t_begin, int t_end, int lane) {
   const int g = lane >> 2, tq = lane & 3;
+  if constexpr (C::WROW) {
+    const int mt = t_begin / C::NT2;
 #pragma unroll
-  for (int ks = 0; ks < NKS; ++ks) {
+    for (int ks = 0; ks < NKS; ++ks) {
+      const AFrag a = load_afrag(sG, C::LDG, mt * 16, ks * 8, g, tq);
 #pragma unroll
-    for (int i = 0; i < C::MAXT2; ++i) {
-      const int t = t_begin + i;
-      if (t < t_end) {
-        const int nt = t / C::MT, mt = t % C::MT;
-        mma_frag(acc[i], load_afrag(sG, C::LDG, mt * 16, ks * 8, g, tq),
-                 __ldg(fb + ((size_t)nt * C::KS2 + ks0 + ks) * 32 + lane));
+      for (int i = 0; i < C::NT2; ++i) mma_frag(acc[i], a, __ldg(fb + ((size_t)i * C::KS2 + ks0 + ks) * 32 + lane));
+    }
+  } else {
+#pragma unroll
+    for (int ks = 0; ks < NKS; ++ks) {
+#pragma unroll
+      for (int i = 0; i < C::MAXT2; ++i) {
+        const int t = t_begin + i;
+        if (t < t_end) {
+          const int nt = t / C::MT, mt = t % C::MT;
+          mma_frag(acc[i], load_afrag(sG, C::LDG, mt * 16, ks * 8, g, tq),
+                   __ldg(fb + ((size_t)nt * C::KS2 + ks0 + ks) * 32 + lane));
+        }
       }
     }
   }
@@ -446,23 +487,47 @@ template <class C>
 __device__ __forceinline__ void gemm2_partial(double (&acc)[C::MAXT2][4], const double* sG, const double2* fb,
                                               int ks0, int nks, int t_begin, int t_end, int lane) {
   const int g = lane >> 2, tq = lane & 3;
-  for (int ks = 0; ks < nks; ++ks) {
+  if constexpr (C::WROW) {
+    const int mt = t_begin / C::NT2;
+    for (int ks = 0; ks < nks; ++ks) {
+      const AFrag a = load_afrag(sG, C::LDG, mt * 16, ks * 8, g, tq);
 #pragma unroll
-    for (int i = 0; i < C::MAXT2; ++i) {
-      const int t = t_begin + i;
-      if (t < t_end) {
-        const int nt = t / C::MT, mt = t % C::MT;  // n-major: a warp's run reuses B fragments
-        mma_frag(acc[i], load_afrag(sG, C::LDG, mt * 16, ks * 8, g, tq),
-                 __ldg(fb + ((size_t)nt * C::KS2 + ks0 + ks) * 32 + lane));
+      for (int i = 0; i < C::NT2; ++i) mma_frag(acc[i], a, __ldg(fb + ((size_t)i * C::KS2 + ks0 + ks) * 32 + lane));
+    }
+  } else {
+    for (int ks = 0; ks < nks; ++ks) {
+#pragma unroll
+      for (int i = 0; i < C::MAXT2; ++i) {
+        const int t = t_begin + i;
+        if (t < t_end) {
+          const int nt = t / C::MT, mt = t % C::MT;  // n-major: a warp's run reuses B fragments
+          mma_frag(acc[i], load_afrag(sG, C::LDG, mt * 16, ks * 8, g, tq),
+                   __ldg(fb + ((size_t)nt * C::KS2 + ks0 + ks) * 32 + lane));
+        }
       }
     }
   }
 }
 
+// output tile i of this warp -> (m-tile, n-tile)
+template <class C>
+__device__ __forceinline__ void tile_coords(int t_begin, int i, int& mt, int& nt) {
+  if constexpr (C::WROW) {
+    mt = t_begin / C::NT2;
+    nt = i;
+  } else {
+    const int t = t_begin + i;
+    nt = t / C::MT;
+    mt = t % C::MT;
+  }
+}
+
 // DBG (timing experiments only): 1 = skip the SIMT pointwise/face work,
 // 2 = skip the tensor-core GEMMs. Never used for results.
-template <class C, bool UPDATE, bool VISC, int DBG = 0>
-__global__ void __launch_bounds__(kThreads, C::MINB) k_rhs(RhsParams p) {
+// RM: Riemann solver baked in at compile time (0 LLF, 1 HLLC, -1 runtime
+// p.gas.riemann): the LLF-only instantiation needs far fewer registers.
+template <class C, bool UPDATE, bool VISC, int DBG = 0, int RM = -1>
+__global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs(RhsParams p) {
   extern __shared__ __align__(16) double smem[];
   double* sU = smem;                       // [R][LDU] nodal state (pcol-permuted)
   double* sC = sU + C::SMEM_U;             // [R][LDC] U at a cubature chunk
@@ -480,7 +545,7 @@ __global__ void __launch_bounds__(kThreads, C::MINB) k_rhs(RhsParams p) {
   const double2* fb1 = reinterpret_cast<const double2*>(p.frag_icub);
   const double2* fb2 = reinterpret_cast<const double2*>(p.frag_op2);
   // contiguous run of RHS output tiles for this warp (m-major order)
-  const int t_begin = (warp * C::T2) / kWarps, t_end = ((warp + 1) * C::T2) / kWarps;
+  const int t_begin = (warp * C::T2) / C::NW, t_end = ((warp + 1) * C::T2) / C::NW;
 
   __shared__ int s_stop;
   for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
@@ -490,21 +555,44 @@ __global__ void __launch_bounds__(kThreads, C::MINB) k_rhs(RhsParams p) {
     if (s_stop) return;
     const int e0 = tile * C::E;
     const int row0 = e0 * 5;
+    // ---- L2 prefetch of what this tile reads late (res in the epilogue, traces
+    // in the face phase) and of the next tile's state: their HBM latency then
+    // overlaps the volume phase instead of stalling the whole CTA.
+    if (p.prefetch) {
+      const int rows = min(C::R, n_rows - row0);
+      if (UPDATE && (p.prefetch & 1)) l2_prefetch_range(p.res + (size_t)row0 * C::BP, (size_t)rows * C::BP * 8, tid, C::NTH);
+      if (p.prefetch & 4) l2_prefetch_range(p.traces + (size_t)row0 * C::TB, (size_t)rows * C::TB * 8, tid, C::NTH);
+      const int nrow0 = (tile + gridDim.x) * C::R;
+      if ((p.prefetch & 2) && nrow0 < n_rows)
+        l2_prefetch_range(p.u + (size_t)nrow0 * C::BP, (size_t)min(C::R, n_rows - nrow0) * C::BP * 8, tid, C::NTH);
+    }
     // ---- stage nodal state + per-element geometry --------------------------
-    stage_rows<C>(p.u, row0, n_rows, sU, tid);
-    for (int idx = tid; idx < C::E * 9; idx += kThreads) {
+    stage_rows<C, C::NTH>(p.u, row0, n_rows, sU, tid);
+    for (int idx = tid; idx < C::E * 9; idx += C::NTH) {
       const int e = e0 + idx / 9;
       sMet[idx] = e < p.K ? __ldg(p.metric + (size_t)e0 * 9 + idx) : 0.0;
     }
-    for (int idx = tid; idx < C::E * 4; idx += kThreads) {
+    for (int idx = tid; idx < C::E * 4; idx += C::NTH) {
       const int e = e0 + idx / 4;
       sFace[idx] = e < p.K ? p.face[(size_t)e0 * 4 + idx] : make_double4(0, 0, 1, 0);
       sConn[idx] = e < p.K ? p.conn[(size_t)e0 * 4 + idx] : make_int2(-1, pack_face(0, 0, 1, 0));
     }
     if (VISC)
-      for (int idx = tid; idx < C::E; idx += kThreads)
+      for (int idx = tid; idx < C::E; idx += C::NTH)
         sSe[idx] = e0 + idx < p.K ? p.sqrt_eps[e0 + idx] : 0.0;
     __syncthreads();
+    if (p.prefetch & 8) {
+      // neighbour trace segments (5 fields x one face of N_g nodes each)
+      for (int idx = tid; idx < C::E * 4 * 5; idx += C::NTH) {
+        const int ef = idx / 5, c = idx - ef * 5;
+        const int2 cw = sConn[ef];
+        if (cw.x >= 0) {
+          const double* seg = p.traces + ((size_t)cw.x * 5 + c) * C::TB + (cw.y & 3) * C::NG;
+          l2_prefetch(seg);
+          if (C::NG * 8 > 128) l2_prefetch(seg + C::NG - 1);
+        }
+      }
+    }
 
     double acc[C::MAXT2][4];
 #pragma unroll
@@ -519,7 +607,7 @@ __global__ void __launch_bounds__(kThreads, C::MINB) k_rhs(RhsParams p) {
       // pointwise Euler flux -> contravariant flux G_m = sum_d (dr_m/dx_d) F_d
 #pragma unroll
       for (int it = 0; it < C::IT_P; ++it) {
-        const int idx = tid + it * kThreads;
+        const int idx = tid + it * C::NTH;
         if (DBG != 1 && idx < C::E * w) {
           const int e = idx / w, ql = idx - e * w, q = q0 + ql;
           const double* uc = sC + (e * 5) * C::LDC + ql;
@@ -602,9 +690,9 @@ __global__ void __launch_bounds__(kThreads, C::MINB) k_rhs(RhsParams p) {
       const int f0 = fc * C::FCH;
       const int wr = (C::NF - f0) < C::FCH ? (C::NF - f0) : C::FCH;  // real nodes (multiple of 4)
       const int wp = round_up(wr, 8);                                 // padded to the k8 step
-#pragma unroll
+#pragma unroll 1
       for (int it = 0; it < C::IT_F; ++it) {
-        const int idx = tid + it * kThreads;
+        const int idx = tid + it * C::NTH;
         if (DBG == 1 || idx >= C::E * wp) continue;
         const int e = idx / wp, fl = idx - e * wp, fq = f0 + fl;
         double* gout = sG + (e * 5) * C::LDG + pcol(fl);
@@ -632,7 +720,7 @@ __global__ void __launch_bounds__(kThreads, C::MINB) k_rhs(RhsParams p) {
         if (DBG == 0 && (!admissible(um, gamma) || !admissible(up, gamma)))
           record_error(p.err, 2, p.elem_offset + eg, f, gq, um.r);
         double fs[5];
-        if (p.gas.riemann == 1)
+        if (RM == 1 || (RM == -1 && p.gas.riemann == 1))
           hllc_flux(um, up, fn.x, fn.y, fn.z, gamma, fs);
         else
           llf_flux_fast(um, up, fn.x, fn.y, fn.z, gamma, fs);
@@ -678,9 +766,9 @@ __global__ void __launch_bounds__(kThreads, C::MINB) k_rhs(RhsParams p) {
     }
 #pragma unroll
     for (int i = 0; i < C::MAXT2; ++i) {
-      const int t = t_begin + i;
-      if (t < t_end) {
-        const int nt = t / C::MT, mt = t % C::MT;
+      if (C::WROW || t_begin + i < t_end) {
+        int mt, nt;
+        tile_coords<C>(t_begin, i, mt, nt);
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
           const int r = mt * 16 + g + 8 * hh;

@@ -1,0 +1,292 @@
+// cdg_row.cuh -- RHS + LSRK kernel with one m-tile ROW per warp (affine tets,
+// inviscid; p = 4 and the curved-mesh p = 3/4 levels' affine elements).
+//
+// Same math and evaluation order as k_rhs (cdg_kernels.cuh; reference
+// solver.cpp:325-492). What changes is the mapping onto the SM:
+//
+//  * A CTA is 5 warps on a tile of 16 elements = 80 (element, field) rows =
+//    5 m16 tiles; warp w owns rows [16w, 16w+16) in EVERY contraction. Its
+//    GEMM output is one full row of n-tiles, so each A fragment (2 x LDS.128)
+//    is reused across all N_p/8 n-tiles.
+//  * The nodal state U never goes to shared memory: the warp keeps its rows
+//    of U as the A fragments of the nodal->cubature GEMM in registers (with
+//    logical k = t <-> node 8ks+2t and k = t+4 <-> node 8ks+2t+1, the
+//    fragment of k-step ks holds exactly the (row, 8ks+2t..+1) values the
+//    accumulator of output n-tile ks holds), so the same registers are the
+//    old u of the LSRK update in the epilogue.
+//  * Without the U panel a CTA needs ~46 KB of shared memory (double-buffered
+//    U_cub / flux chunks, then reused for the face fluxes), so 3 CTAs share
+//    an SM with ~90 KB left to L1 -- enough to keep the shared operators'
+//    B fragments (115 KB at p = 4, read by every CTA) mostly L1-resident.
+//  * Two CTA barriers per cubature chunk (U_cub ready, flux ready); the
+//    double buffers remove the third.
+#pragma once
+
+#include "cdg_kernels.cuh"
+
+namespace cdg_gpu {
+
+template <int NP_, int NCUB_, int NG_, int CH_ = 8, int FCH_ = 64, int MINB_ = 3>
+struct RCfg {
+  static constexpr int NP = NP_, NCUB = NCUB_, NG = NG_, NF = 4 * NG_;
+  static constexpr int E = 16, R = 80, NW = 5, NTH = 160, MINB = MINB_;
+  static constexpr int BP = round_up(NP, 16), TB = round_up(NF, 16);
+  static constexpr int KP = round_up(NP, 8), KS1 = KP / 8, NT2 = KS1;
+  static constexpr int NCUB8 = round_up(NCUB, 8), NF8 = round_up(NF, 8);
+  static constexpr int CH = CH_, NCH = ceil_div(NCUB8, CH);
+  static constexpr int FCH = FCH_, NFCH = ceil_div(NF, FCH);
+  static constexpr int K2CUB = 3 * NCUB8, K2 = K2CUB + NF8, KS2 = K2 / 8;
+  static constexpr int LDC = CH + 4;                  // U_cub chunk (pointwise reads columns)
+  static constexpr int LDG = frag_ld8(3 * CH);        // flux chunk, conflict-free 128-bit A loads
+  static constexpr int LDF = frag_ld8(FCH);           // face-flux chunk
+  static constexpr int VOL = 2 * R * LDC + 2 * R * LDG;  // doubles, volume phase
+  static constexpr int FACE = R * LDF;                    // doubles, face phase (aliases VOL)
+  static constexpr int WORK = VOL > FACE ? VOL : FACE;
+  static constexpr int IT_P = ceil_div(E * CH, NTH);
+  static constexpr int IT_F = ceil_div(E * FCH, NTH);
+  static constexpr size_t SMEM_BYTES =
+      sizeof(double) * ((size_t)WORK + E * 9 + E * 4 * 4) + sizeof(int) * (E * 4 * 2);
+};
+
+// B fragments (natural pairing, see cdg_warp.cuh): frag1[(qt*KS1 + ks)*32 + lane]
+// for I_cub n-tile qt; frag2[(ks*NT2 + nt)*32 + lane] for the chunked
+// [A_r A_s A_t | -LIFT] operator (k-step-major: one k-step's n-tiles adjacent).
+template <class C, bool UPDATE, int RM>
+__global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_row(RhsParams p) {
+  extern __shared__ __align__(16) double smem[];
+  double* sWork = smem;
+  double* sMet = sWork + C::WORK;                                 // [E][9]
+  double4* sFace = reinterpret_cast<double4*>(sMet + C::E * 9);    // [E][4]
+  int2* sConn = reinterpret_cast<int2*>(sFace + C::E * 4);         // [E][4]
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const int n_rows = p.K * 5;
+  const double gamma = p.gas.gamma;
+  const double2* fb1 = reinterpret_cast<const double2*>(p.frag_icub);
+  const double2* fb2 = reinterpret_cast<const double2*>(p.frag_op2);
+  const int n_tiles = (p.K + C::E - 1) / C::E;
+  __shared__ int s_stop;
+
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    // block-uniform early exit after a recorded error (no divergent barriers)
+    if (tid == 0) s_stop = *(volatile int*)&p.err->flag;
+    __syncthreads();
+    if (s_stop) return;
+    const int e0 = tile * C::E, row0 = e0 * 5;
+    const int r_lo = row0 + warp * 16 + g, r_hi = r_lo + 8;  // this thread's two rows
+    if (p.prefetch) {
+      const int rows = min(C::R, n_rows - row0);
+      if (UPDATE && (p.prefetch & 1)) l2_prefetch_range(p.res + (size_t)row0 * C::BP, (size_t)rows * C::BP * 8, tid, C::NTH);
+      if (p.prefetch & 4) l2_prefetch_range(p.traces + (size_t)row0 * C::TB, (size_t)rows * C::TB * 8, tid, C::NTH);
+      const int nrow0 = (tile + gridDim.x) * C::R;
+      if ((p.prefetch & 2) && nrow0 < n_rows)
+        l2_prefetch_range(p.u + (size_t)nrow0 * C::BP, (size_t)min(C::R, n_rows - nrow0) * C::BP * 8, tid, C::NTH);
+    }
+    // ---- U rows -> registers (A fragments of the nodal->cubature GEMM) ------
+    double uA[C::KS1][4];
+#pragma unroll
+    for (int ks = 0; ks < C::KS1; ++ks) {
+      double2 x = make_double2(0.0, 0.0), y = make_double2(0.0, 0.0);
+      if (r_lo < n_rows) x = *reinterpret_cast<const double2*>(p.u + (size_t)r_lo * C::BP + ks * 8 + 2 * tq);
+      if (r_hi < n_rows) y = *reinterpret_cast<const double2*>(p.u + (size_t)r_hi * C::BP + ks * 8 + 2 * tq);
+      uA[ks][0] = x.x;
+      uA[ks][1] = y.x;
+      uA[ks][2] = x.y;
+      uA[ks][3] = y.y;
+    }
+    for (int idx = tid; idx < C::E * 9; idx += C::NTH)
+      sMet[idx] = e0 + idx / 9 < p.K ? __ldg(p.metric + (size_t)e0 * 9 + idx) : 0.0;
+    for (int idx = tid; idx < C::E * 4; idx += C::NTH) {
+      const bool ok = e0 + idx / 4 < p.K;
+      sFace[idx] = ok ? p.face[(size_t)e0 * 4 + idx] : make_double4(0, 0, 1, 0);
+      sConn[idx] = ok ? p.conn[(size_t)e0 * 4 + idx] : make_int2(-1, pack_face(0, 0, 1, 0));
+    }
+    __syncthreads();
+    if (p.prefetch & 8) {
+      for (int idx = tid; idx < C::E * 4 * 5; idx += C::NTH) {
+        const int ef = idx / 5, c = idx - ef * 5;
+        const int2 cw = sConn[ef];
+        if (cw.x >= 0) {
+          const double* seg = p.traces + ((size_t)cw.x * 5 + c) * C::TB + (cw.y & 3) * C::NG;
+          l2_prefetch(seg);
+          if (C::NG * 8 > 128) l2_prefetch(seg + C::NG - 1);
+        }
+      }
+    }
+
+    double acc[C::NT2][4];
+#pragma unroll
+    for (int i = 0; i < C::NT2; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.0;
+
+    // ---- volume: chunks of CH cubature nodes ----------------------------------
+#pragma unroll 1
+    for (int ch = 0; ch < C::NCH; ++ch) {
+      const int q0 = ch * C::CH;
+      const int w = (C::NCUB8 - q0) < C::CH ? (C::NCUB8 - q0) : C::CH;  // multiple of 8
+      double* sC = sWork + (ch & 1) * (C::R * C::LDC);
+      double* sG = sWork + 2 * C::R * C::LDC + (ch & 1) * (C::R * C::LDG);
+      // GEMM1: U_cub[rows, q0:q0+w] for this warp's 16 rows
+      {
+        double c1[C::CH / 8][4];
+#pragma unroll
+        for (int j = 0; j < C::CH / 8; ++j) c1[j][0] = c1[j][1] = c1[j][2] = c1[j][3] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < C::KS1; ++ks)
+#pragma unroll
+          for (int j = 0; j < C::CH / 8; ++j)
+            if (j * 8 < w) {
+              const double2 b = __ldg(fb1 + ((size_t)(q0 / 8 + j) * C::KS1 + ks) * 32 + lane);
+              dmma_k8(c1[j], uA[ks][0], uA[ks][1], uA[ks][2], uA[ks][3], b.x, b.y);
+            }
+#pragma unroll
+        for (int j = 0; j < C::CH / 8; ++j)
+          if (j * 8 < w) {
+            double* o = sC + (warp * 16 + g) * C::LDC + j * 8 + 2 * tq;
+            *reinterpret_cast<double2*>(o) = make_double2(c1[j][0], c1[j][1]);
+            *reinterpret_cast<double2*>(o + 8 * C::LDC) = make_double2(c1[j][2], c1[j][3]);
+          }
+      }
+      __syncthreads();
+      // pointwise Euler flux -> contravariant flux G_m = sum_d (dr_m/dx_d) F_d
+#pragma unroll 1
+      for (int it = 0; it < C::IT_P; ++it) {
+        const int idx = tid + it * C::NTH;
+        if (idx < C::E * w) {
+          const int e = idx / w, ql = idx - e * w, q = q0 + ql;
+          const double* uc = sC + (e * 5) * C::LDC + ql;
+          double* gout = sG + (e * 5) * C::LDG + ql;
+          if (q < C::NCUB && e0 + e < p.K) {
+            const State5 s{uc[0], uc[C::LDC], uc[2 * C::LDC], uc[3 * C::LDC], uc[4 * C::LDC]};
+            if (!admissible(s, gamma)) record_error(p.err, 1, p.elem_offset + e0 + e, q, 0, s.r);
+            const double ir = 1.0 / s.r;
+            const double pr = (gamma - 1.0) * (s.E - 0.5 * ir * (s.mx * s.mx + s.my * s.my + s.mz * s.mz));
+            const double vx = s.mx * ir, vy = s.my * ir, vz = s.mz * ir;
+            const double ep = s.E + pr;
+            const double* met = sMet + e * 9;
+            // G_m = (rho U_m, m U_m + p r_m, (E+p) U_m), U_m = sum_d r_md v_d
+            // (solver.cpp:382-394 contracted with S_m, operators.cpp:139-147)
+#pragma unroll
+            for (int m = 0; m < 3; ++m) {
+              const double r0 = met[m * 3 + 0], r1 = met[m * 3 + 1], r2 = met[m * 3 + 2];
+              const double um = r0 * vx + r1 * vy + r2 * vz;
+              double* o = gout + m * w;
+              o[0] = s.r * um;
+              o[C::LDG] = s.mx * um + pr * r0;
+              o[2 * C::LDG] = s.my * um + pr * r1;
+              o[3 * C::LDG] = s.mz * um + pr * r2;
+              o[4 * C::LDG] = ep * um;
+            }
+          } else {
+#pragma unroll
+            for (int m = 0; m < 3; ++m)
+#pragma unroll
+              for (int c = 0; c < 5; ++c) gout[m * w + c * C::LDG] = 0.0;
+          }
+        }
+      }
+      __syncthreads();
+      // GEMM2 (volume part of K): acc += G[rows, 3w] * Op2[:, 3 q0 : 3 q0 + 3w]^T
+      {
+        const int ks0 = (3 * q0) / 8, nks = (3 * w) / 8;
+#pragma unroll 1
+        for (int ks = 0; ks < nks; ++ks) {
+          const AFrag a = load_afrag(sG, C::LDG, warp * 16, ks * 8, g, tq);
+#pragma unroll
+          for (int n = 0; n < C::NT2; ++n)
+            mma_frag(acc[n], a, __ldg(fb2 + ((size_t)(ks0 + ks) * C::NT2 + n) * 32 + lane));
+        }
+      }
+    }
+    __syncthreads();  // the face phase reuses the volume buffers
+
+    // ---- surface: chunks of FCH face nodes -------------------------------------
+    double* sF = sWork;
+#pragma unroll 1
+    for (int fc = 0; fc < C::NFCH; ++fc) {
+      const int f0 = fc * C::FCH;
+      const int wr = (C::NF - f0) < C::FCH ? (C::NF - f0) : C::FCH;
+      const int wp = round_up(wr, 8);
+#pragma unroll 1
+      for (int it = 0; it < C::IT_F; ++it) {
+        const int idx = tid + it * C::NTH;
+        if (idx >= C::E * wp) continue;
+        const int e = idx / wp, fl = idx - e * wp, fq = f0 + fl;
+        double* gout = sF + (e * 5) * C::LDF + fl;
+        const int eg = e0 + e;
+        if (eg >= p.K || fl >= wr) {
+#pragma unroll
+          for (int c = 0; c < 5; ++c) gout[c * C::LDF] = 0.0;
+          continue;
+        }
+        const int f = fq / C::NG, gq = fq - f * C::NG;
+        const double* tm = p.traces + (size_t)eg * 5 * C::TB + fq;
+        const State5 um{tm[0], tm[C::TB], tm[2 * C::TB], tm[3 * C::TB], tm[4 * C::TB]};
+        const double4 fn = sFace[e * 4 + f];
+        const int2 cw = sConn[e * 4 + f];
+        State5 up;
+        if (cw.x >= 0) {
+          const int h = __ldg(p.code_map + (cw.y >> 8) * C::NG + gq);
+          const double* tp = p.traces + (size_t)cw.x * 5 * C::TB + (cw.y & 3) * C::NG + h;
+          up = State5{tp[0], tp[C::TB], tp[2 * C::TB], tp[3 * C::TB], tp[4 * C::TB]};
+        } else {
+          up = boundary_state(um, fn.x, fn.y, fn.z, (cw.y >> 2) & 3, p.gas);
+        }
+        if (!admissible(um, gamma) || !admissible(up, gamma)) record_error(p.err, 2, p.elem_offset + eg, f, gq, um.r);
+        double fs[5];
+        if (RM == 1)
+          hllc_flux(um, up, fn.x, fn.y, fn.z, gamma, fs);
+        else
+          llf_flux_fast(um, up, fn.x, fn.y, fn.z, gamma, fs);
+#pragma unroll
+        for (int c = 0; c < 5; ++c) gout[c * C::LDF] = fn.w * fs[c];
+      }
+      __syncthreads();
+      {
+        const int ks0 = (C::K2CUB + f0) / 8, nks = wp / 8;
+#pragma unroll 1
+        for (int ks = 0; ks < nks; ++ks) {
+          const AFrag a = load_afrag(sF, C::LDF, warp * 16, ks * 8, g, tq);
+#pragma unroll
+          for (int n = 0; n < C::NT2; ++n)
+            mma_frag(acc[n], a, __ldg(fb2 + ((size_t)(ks0 + ks) * C::NT2 + n) * 32 + lane));
+        }
+      }
+      if (fc + 1 < C::NFCH) __syncthreads();
+    }
+
+    // ---- epilogue: rhs -> (res, u) update or rhs store ---------------------------
+    double a_c = 0.0, b_c = 0.0, dt = 0.0;
+    if (UPDATE) {
+      a_c = p.coef->a[p.stage];
+      b_c = p.coef->b[p.stage];
+      dt = p.coef->dt;
+    }
+    const bool cur_lo = (sConn[((warp * 16 + g) / 5) * 4].y & kCurvedBit) != 0;
+    const bool cur_hi = (sConn[((warp * 16 + g + 8) / 5) * 4].y & kCurvedBit) != 0;
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const int grow = hh ? r_hi : r_lo;
+      if (grow >= n_rows || (hh ? cur_hi : cur_lo)) continue;  // curved rows: k_rhs_curved
+      const size_t rowoff = (size_t)grow * C::BP;
+#pragma unroll
+      for (int n = 0; n < C::NT2; ++n) {
+        const int col = n * 8 + 2 * tq;  // < KP <= BP; padded columns carry exact zeros
+        const double r0 = acc[n][2 * hh], r1 = acc[n][2 * hh + 1];
+        if (UPDATE) {
+          const double2 rs = *reinterpret_cast<const double2*>(p.res + rowoff + col);
+          const double n0 = a_c * rs.x + dt * r0, n1 = a_c * rs.y + dt * r1;
+          *reinterpret_cast<double2*>(p.res + rowoff + col) = make_double2(n0, n1);
+          // old u: the A fragment of k-step n holds (row, 8n+2t) / (row, 8n+2t+1)
+          const double u0 = hh ? uA[n][1] : uA[n][0], u1 = hh ? uA[n][3] : uA[n][2];
+          *reinterpret_cast<double2*>(p.u + rowoff + col) = make_double2(u0 + b_c * n0, u1 + b_c * n1);
+        } else {
+          *reinterpret_cast<double2*>(p.rhs_out + rowoff + col) = make_double2(r0, r1);
+        }
+      }
+    }
+    __syncthreads();  // sConn / sWork are restaged next tile
+  }
+}
+
+}  // namespace cdg_gpu

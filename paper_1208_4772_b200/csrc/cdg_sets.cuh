@@ -1,0 +1,103 @@
+// cdg_sets.cuh -- kernel-set table types: one KernelSet per (N_p, N_cub, N_g)
+// level shape, holding the instantiated sm_100a kernels. The instantiations
+// are spread over several translation units (sets_*.cu) so that nvcc builds
+// them in parallel.
+#pragma once
+
+#include <vector>
+
+#include "cdg_aux.cuh"
+#include "cdg_curved.cuh"
+#include "cdg_kernels.cuh"
+#include "cdg_row.cuh"
+#include "cdg_warp.cuh"
+
+namespace cdg_gpu {
+
+struct KernelSet {
+  int np, ncub, ng, E, minb, ch, nth;
+  size_t smem_traces, smem_rhs, smem_aux;
+  void (*traces)(const double*, double*, const double*, int, int);
+  void (*rhs_update)(RhsParams);
+  void (*rhs_only)(RhsParams);
+  void (*aux_q)(AuxParams);
+  void (*visc_rhs_update)(RhsParams);
+  void (*visc_rhs_only)(RhsParams);
+  void (*curved_update)(CurvedParams);
+  void (*curved_only)(CurvedParams);
+  size_t smem_curved;
+  // warp-tile inviscid kernel (cdg_warp.cuh), p <= 3
+  void (*warp_update[2])(WarpParams) = {nullptr, nullptr};  // [riemann]
+  void (*warp_only[2])(WarpParams) = {nullptr, nullptr};
+  size_t smem_warp = 0;
+  int warp_warps = 0, warp_minb = 0;
+  // row-per-warp inviscid kernel (cdg_row.cuh), p = 4
+  void (*row_update[2])(RhsParams) = {nullptr, nullptr};  // [riemann]
+  void (*row_only[2])(RhsParams) = {nullptr, nullptr};
+  size_t smem_row = 0;
+  int row_minb = 0, row_ch = 0;
+};
+
+template <int NP, int NCUB, int NG, int CH = 8, int FCH = 64, int MINB = 3>
+KernelSet with_row(KernelSet k) {
+  using RC = RCfg<NP, NCUB, NG, CH, FCH, MINB>;
+  k.row_update[0] = &k_rhs_row<RC, true, 0>;
+  k.row_update[1] = &k_rhs_row<RC, true, 1>;
+  k.row_only[0] = &k_rhs_row<RC, false, 0>;
+  k.row_only[1] = &k_rhs_row<RC, false, 1>;
+  k.smem_row = RC::SMEM_BYTES;
+  k.row_minb = MINB;
+  k.row_ch = CH;
+  return k;
+}
+
+template <int NP, int NCUB, int NG, int WARPS = 4, int MINB = 2>
+KernelSet with_warp(KernelSet k) {
+  using W = WCfg<NP, NCUB, NG, WARPS, MINB>;
+  k.warp_update[0] = &k_rhs_warp<W, true, 0>;
+  k.warp_update[1] = &k_rhs_warp<W, true, 1>;
+  k.warp_only[0] = &k_rhs_warp<W, false, 0>;
+  k.warp_only[1] = &k_rhs_warp<W, false, 1>;
+  k.smem_warp = W::SMEM_BYTES;
+  k.warp_warps = WARPS;
+  k.warp_minb = MINB;
+  return k;
+}
+
+// <N_p, N_cub, N_g, E elements/tile, CH cubature chunk, CTAs/SM, FCH face
+// chunk, NW warps/CTA of k_rhs>. The aux-gradient and curved kernels always
+// run with 8 warps on the same tile shape (same host operator layout).
+template <int NP, int NCUB, int NG, int E, int CH = 16, int MINB = 1, int FCH = 32, int NW = 8>
+KernelSet make_set() {
+  using C = Cfg<NP, NCUB, NG, E, CH, MINB, FCH, NW>;
+  using C8 = Cfg<NP, NCUB, NG, E, CH, (NW == 8 ? MINB : 1), FCH, 8>;
+  KernelSet k;
+  k.np = NP;
+  k.ncub = NCUB;
+  k.ng = NG;
+  k.E = E;
+  k.minb = MINB;
+  k.ch = CH;
+  k.nth = C::NTH;
+  k.smem_traces = sizeof(double) * C8::R * C8::LDU;
+  k.smem_rhs = C::SMEM_BYTES;
+  k.smem_aux = C8::SMEM_BYTES;
+  k.traces = &k_traces<C8>;
+  k.rhs_update = &k_rhs<C, true, false>;
+  k.rhs_only = &k_rhs<C, false, false>;
+  k.aux_q = &k_aux_q<C8>;
+  k.visc_rhs_update = &k_rhs<C, true, true>;
+  k.visc_rhs_only = &k_rhs<C, false, true>;
+  k.curved_update = &k_rhs_curved<C8, true>;
+  k.curved_only = &k_rhs_curved<C8, false>;
+  k.smem_curved = CurvedLayout<C8>::SMEM_BYTES;
+  return k;
+}
+
+// one function per translation unit (sets_*.cu)
+std::vector<KernelSet> kernel_sets_p1_3();
+std::vector<KernelSet> kernel_sets_p4();
+std::vector<KernelSet> kernel_sets_p5_6();
+std::vector<KernelSet> kernel_sets_p7_8();
+
+}  // namespace cdg_gpu

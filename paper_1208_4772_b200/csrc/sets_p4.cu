@@ -1,0 +1,18 @@
+// sets_p4.cu -- kernel instantiations for one group of level shapes
+// <N_p, N_cub, N_g, ...> (see cdg_sets.cuh); compiled as its own translation unit.
+#define CDG_SET_TU
+#include "cdg_sets.cuh"
+
+namespace cdg_gpu {
+
+std::vector<KernelSet> kernel_sets_p4() {
+  return {
+      with_row<35, 70, 16>(make_set<35, 70, 16, 16, 24, 2, 64>()),
+      with_row<35, 70, 56>(make_set<35, 70, 56, 16, 24, 2>()),
+      // P=4 straight tuning variants, selected with CDG_KCFG=<n> (bench sweeps)
+      make_set<35, 70, 16, 16, 24, 2, 64>(), make_set<35, 70, 16, 16, 8, 4, 24, 5>(),
+      with_row<35, 70, 16, 16, 64, 2>(make_set<35, 70, 16, 16, 24, 2, 64>()),
+      with_row<35, 70, 16, 8, 32, 3>(make_set<35, 70, 16, 16, 24, 2, 64>())};
+}
+
+}  // namespace cdg_gpu

@@ -1,0 +1,14 @@
+// sets_p5_6.cu -- kernel instantiations for one group of level shapes
+// <N_p, N_cub, N_g, ...> (see cdg_sets.cuh); compiled as its own translation unit.
+#define CDG_SET_TU
+#include "cdg_sets.cuh"
+
+namespace cdg_gpu {
+
+std::vector<KernelSet> kernel_sets_p5_6() {
+  return {
+      make_set<56, 126, 56, 16, 16, 2>(), make_set<84, 210, 84, 16>(),
+      make_set<56, 210, 84, 16, 16, 2>(), make_set<84, 330, 165, 16>()};
+}
+
+}  // namespace cdg_gpu
