@@ -14,10 +14,13 @@
 //    fragment of k-step ks holds exactly the (row, 8ks+2t..+1) values the
 //    accumulator of output n-tile ks holds), so the same registers are the
 //    old u of the LSRK update in the epilogue.
-//  * Without the U panel a CTA needs ~46 KB of shared memory (double-buffered
-//    U_cub / flux chunks, then reused for the face fluxes), so 3 CTAs share
-//    an SM with ~90 KB left to L1 -- enough to keep the shared operators'
-//    B fragments (115 KB at p = 4, read by every CTA) mostly L1-resident.
+//  * The B fragments of the shared operators (115 KB at p = 4) are streamed
+//    chunk by chunk into a double-buffered shared-memory ring by the bulk-copy
+//    (TMA) engine, one elected thread per CTA issuing cp.async.bulk with an
+//    mbarrier transaction count; the copy of chunk n+1 overlaps chunk n.
+//  * Without the U panel a CTA needs ~69 KB of shared memory (double-buffered
+//    U_cub / flux chunks, reused for the face fluxes and the staged res of the
+//    epilogue, plus the operator ring), so 3 CTAs share an SM.
 //  * Two CTA barriers per cubature chunk (U_cub ready, flux ready); the
 //    double buffers remove the third.
 #pragma once
@@ -26,10 +29,14 @@
 
 namespace cdg_gpu {
 
-template <int NP_, int NCUB_, int NG_, int CH_ = 8, int FCH_ = 64, int MINB_ = 3>
+// MODE bits: 1 operator ring (bulk-copy staged B fragments; else __ldg from
+// L1/L2), 2 U fragments register-resident for the whole tile (else reloaded
+// per chunk, which frees ~40 registers), 4 res staged to smem for the epilogue.
+template <int NP_, int NCUB_, int NG_, int CH_ = 8, int FCH_ = 32, int MINB_ = 3, int MODE_ = 7>
 struct RCfg {
   static constexpr int NP = NP_, NCUB = NCUB_, NG = NG_, NF = 4 * NG_;
   static constexpr int E = 16, R = 80, NW = 5, NTH = 160, MINB = MINB_;
+  static constexpr bool OPRING = MODE_ & 1, UREG = MODE_ & 2, RESS = MODE_ & 4;
   static constexpr int BP = round_up(NP, 16), TB = round_up(NF, 16);
   static constexpr int KP = round_up(NP, 8), KS1 = KP / 8, NT2 = KS1;
   static constexpr int NCUB8 = round_up(NCUB, 8), NF8 = round_up(NF, 8);
@@ -39,14 +46,79 @@ struct RCfg {
   static constexpr int LDC = CH + 4;                  // U_cub chunk (pointwise reads columns)
   static constexpr int LDG = frag_ld8(3 * CH);        // flux chunk, conflict-free 128-bit A loads
   static constexpr int LDF = frag_ld8(FCH);           // face-flux chunk
-  static constexpr int VOL = 2 * R * LDC + 2 * R * LDG;  // doubles, volume phase
-  static constexpr int FACE = R * LDF;                    // doubles, face phase (aliases VOL)
+  // volume phase: one U_cub chunk (rewritten only after the barrier that
+  // follows the pointwise pass) + two flux chunks (double buffer)
+  static constexpr int VOL = R * LDC + 2 * R * LDG;
+  static constexpr int RES = RESS ? NTH * 2 * NT2 * 2 : 0;  // doubles: each thread's epilogue res values
+  static constexpr int FACE = R * LDF + RES;              // doubles, face phase (aliases VOL)
   static constexpr int WORK = VOL > FACE ? VOL : FACE;
   static constexpr int IT_P = ceil_div(E * CH, NTH);
   static constexpr int IT_F = ceil_div(E * FCH, NTH);
-  static constexpr size_t SMEM_BYTES =
-      sizeof(double) * ((size_t)WORK + E * 9 + E * 4 * 4) + sizeof(int) * (E * 4 * 2);
+  // operator chunks staged by the bulk-copy engine: a cubature chunk needs the
+  // I_cub fragments of its CH/8 n-tiles and the [A_r A_s A_t] fragments of
+  // its 3CH/8 k-steps; a face chunk the -LIFT fragments of its FCH/8 k-steps
+  static constexpr int OPV = (CH / 8) * KS1 * 64 + (3 * CH / 8) * NT2 * 64;  // doubles
+  static constexpr int OPF = (FCH / 8) * NT2 * 64;
+  static constexpr int OPB = !OPRING ? 0 : (OPV > OPF ? OPV : OPF);
+  static constexpr int NCHT = NCH + NFCH;  // operator chunks per tile
+  static constexpr size_t SMEM_BYTES = sizeof(double) * ((size_t)WORK + 2 * OPB + E * 9 + E * 4 * 4) +
+                                       sizeof(int) * (E * 4 * 2) + 2 * sizeof(unsigned long long);
 };
+
+// ---- bulk-copy (TMA engine) + mbarrier helpers -----------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred P;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared.b64 P, [%0], %1;\n"
+      " @!P bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async16_sh(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// Issue the operator chunk with global index n (per CTA, counting over its
+// tiles) into buffer n & 1. Chunk k = n % NCHT of a tile: k < NCH cubature
+// chunk k, else face chunk k - NCH.
+template <class C>
+__device__ __forceinline__ void issue_op_chunk(int n, double* sOp, unsigned long long* bars, const double* f1,
+                                               const double* f2) {
+  const int k = n % C::NCHT, b = n & 1;
+  double* dst = sOp + b * C::OPB;
+  if (k < C::NCH) {
+    const int q0 = k * C::CH, w = min(C::CH, C::NCUB8 - q0);
+    const unsigned b1 = (unsigned)((w / 8) * C::KS1 * 64 * sizeof(double));
+    const unsigned b2 = (unsigned)((3 * w / 8) * C::NT2 * 64 * sizeof(double));
+    mbar_expect_tx(&bars[b], b1 + b2);
+    bulk_g2s(dst, f1 + (size_t)(q0 / 8) * C::KS1 * 64, b1, &bars[b]);
+    bulk_g2s(dst + (C::CH / 8) * C::KS1 * 64, f2 + (size_t)(3 * q0 / 8) * C::NT2 * 64, b2, &bars[b]);
+  } else {
+    const int f0 = (k - C::NCH) * C::FCH;
+    const int wp = round_up(min(C::FCH, C::NF - f0), 8);
+    const unsigned b2 = (unsigned)((wp / 8) * C::NT2 * 64 * sizeof(double));
+    mbar_expect_tx(&bars[b], b2);
+    bulk_g2s(dst, f2 + (size_t)((C::K2CUB + f0) / 8) * C::NT2 * 64, b2, &bars[b]);
+  }
+}
 
 // B fragments (natural pairing, see cdg_warp.cuh): frag1[(qt*KS1 + ks)*32 + lane]
 // for I_cub n-tile qt; frag2[(ks*NT2 + nt)*32 + lane] for the chunked
@@ -55,18 +127,31 @@ template <class C, bool UPDATE, int RM>
 __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_row(RhsParams p) {
   extern __shared__ __align__(16) double smem[];
   double* sWork = smem;
-  double* sMet = sWork + C::WORK;                                 // [E][9]
+  double* sOp = sWork + C::WORK;                                  // [2][OPB] operator chunks
+  double* sMet = sOp + 2 * C::OPB;                                // [E][9]
   double4* sFace = reinterpret_cast<double4*>(sMet + C::E * 9);    // [E][4]
   int2* sConn = reinterpret_cast<int2*>(sFace + C::E * 4);         // [E][4]
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(sConn + C::E * 4);  // [2]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, tq = lane & 3;
   const int n_rows = p.K * 5;
   const double gamma = p.gas.gamma;
-  const double2* fb1 = reinterpret_cast<const double2*>(p.frag_icub);
-  const double2* fb2 = reinterpret_cast<const double2*>(p.frag_op2);
   const int n_tiles = (p.K + C::E - 1) / C::E;
   __shared__ int s_stop;
+  // operator chunk pipeline: chunk n of this CTA lives in buffer n & 1
+  const int my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int n_chunks = my_tiles * C::NCHT;
+  int n = 0;  // current chunk
+  if (C::OPRING) {
+    if (tid == 0) {
+      mbar_init(&bars[0], 1);
+      mbar_init(&bars[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0 && n_chunks > 0) issue_op_chunk<C>(0, sOp, bars, p.frag_icub, p.frag_op2);
+  }
 
   for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     // block-uniform early exit after a recorded error (no divergent barriers)
@@ -78,23 +163,30 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_row(RhsParams p) {
     if (p.prefetch) {
       const int rows = min(C::R, n_rows - row0);
       if (UPDATE && (p.prefetch & 1)) l2_prefetch_range(p.res + (size_t)row0 * C::BP, (size_t)rows * C::BP * 8, tid, C::NTH);
+      (void)rows;
       if (p.prefetch & 4) l2_prefetch_range(p.traces + (size_t)row0 * C::TB, (size_t)rows * C::TB * 8, tid, C::NTH);
       const int nrow0 = (tile + gridDim.x) * C::R;
       if ((p.prefetch & 2) && nrow0 < n_rows)
         l2_prefetch_range(p.u + (size_t)nrow0 * C::BP, (size_t)min(C::R, n_rows - nrow0) * C::BP * 8, tid, C::NTH);
     }
     // ---- U rows -> registers (A fragments of the nodal->cubature GEMM) ------
+    const double* u_lo = p.u + (size_t)min(r_lo, n_rows - 1) * C::BP + 2 * tq;
+    const double* u_hi = p.u + (size_t)min(r_hi, n_rows - 1) * C::BP + 2 * tq;
+    const bool ok_lo = r_lo < n_rows, ok_hi = r_hi < n_rows;
     double uA[C::KS1][4];
+    auto load_u = [&]() {
 #pragma unroll
-    for (int ks = 0; ks < C::KS1; ++ks) {
-      double2 x = make_double2(0.0, 0.0), y = make_double2(0.0, 0.0);
-      if (r_lo < n_rows) x = *reinterpret_cast<const double2*>(p.u + (size_t)r_lo * C::BP + ks * 8 + 2 * tq);
-      if (r_hi < n_rows) y = *reinterpret_cast<const double2*>(p.u + (size_t)r_hi * C::BP + ks * 8 + 2 * tq);
-      uA[ks][0] = x.x;
-      uA[ks][1] = y.x;
-      uA[ks][2] = x.y;
-      uA[ks][3] = y.y;
-    }
+      for (int ks = 0; ks < C::KS1; ++ks) {
+        double2 x = make_double2(0.0, 0.0), y = make_double2(0.0, 0.0);
+        if (ok_lo) x = *reinterpret_cast<const double2*>(u_lo + ks * 8);
+        if (ok_hi) y = *reinterpret_cast<const double2*>(u_hi + ks * 8);
+        uA[ks][0] = x.x;
+        uA[ks][1] = y.x;
+        uA[ks][2] = x.y;
+        uA[ks][3] = y.y;
+      }
+    };
+    if (C::UREG) load_u();
     for (int idx = tid; idx < C::E * 9; idx += C::NTH)
       sMet[idx] = e0 + idx / 9 < p.K ? __ldg(p.metric + (size_t)e0 * 9 + idx) : 0.0;
     for (int idx = tid; idx < C::E * 4; idx += C::NTH) {
@@ -124,8 +216,18 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_row(RhsParams p) {
     for (int ch = 0; ch < C::NCH; ++ch) {
       const int q0 = ch * C::CH;
       const int w = (C::NCUB8 - q0) < C::CH ? (C::NCUB8 - q0) : C::CH;  // multiple of 8
-      double* sC = sWork + (ch & 1) * (C::R * C::LDC);
-      double* sG = sWork + 2 * C::R * C::LDC + (ch & 1) * (C::R * C::LDG);
+      double* sC = sWork;
+      double* sG = sWork + C::R * C::LDC + (ch & 1) * (C::R * C::LDG);
+      const double2 *fb1, *fb2;  // [CH/8][KS1][32], [3CH/8][NT2][32]
+      if (C::OPRING) {
+        fb1 = reinterpret_cast<const double2*>(sOp + (n & 1) * C::OPB);
+        fb2 = fb1 + (C::CH / 8) * C::KS1 * 32;
+        mbar_wait(&bars[n & 1], (n >> 1) & 1);
+      } else {
+        fb1 = reinterpret_cast<const double2*>(p.frag_icub) + (size_t)(q0 / 8) * C::KS1 * 32;
+        fb2 = reinterpret_cast<const double2*>(p.frag_op2) + (size_t)(3 * q0 / 8) * C::NT2 * 32;
+      }
+      if (!C::UREG) load_u();
       // GEMM1: U_cub[rows, q0:q0+w] for this warp's 16 rows
       {
         double c1[C::CH / 8][4];
@@ -136,7 +238,7 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_row(RhsParams p) {
 #pragma unroll
           for (int j = 0; j < C::CH / 8; ++j)
             if (j * 8 < w) {
-              const double2 b = __ldg(fb1 + ((size_t)(q0 / 8 + j) * C::KS1 + ks) * 32 + lane);
+              const double2 b = C::OPRING ? fb1[(j * C::KS1 + ks) * 32 + lane] : __ldg(fb1 + (j * C::KS1 + ks) * 32 + lane);
               dmma_k8(c1[j], uA[ks][0], uA[ks][1], uA[ks][2], uA[ks][3], b.x, b.y);
             }
 #pragma unroll
@@ -148,6 +250,11 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_row(RhsParams p) {
           }
       }
       __syncthreads();
+      // every warp is past GEMM2 of chunk n-1: its buffer takes chunk n+1
+      if (C::OPRING && tid == 0 && n + 1 < n_chunks) {
+        fence_proxy_async();
+        issue_op_chunk<C>(n + 1, sOp, bars, p.frag_icub, p.frag_op2);
+      }
       // pointwise Euler flux -> contravariant flux G_m = sum_d (dr_m/dx_d) F_d
 #pragma unroll 1
       for (int it = 0; it < C::IT_P; ++it) {
@@ -188,20 +295,33 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_row(RhsParams p) {
       __syncthreads();
       // GEMM2 (volume part of K): acc += G[rows, 3w] * Op2[:, 3 q0 : 3 q0 + 3w]^T
       {
-        const int ks0 = (3 * q0) / 8, nks = (3 * w) / 8;
+        const int nks = (3 * w) / 8;
 #pragma unroll 1
         for (int ks = 0; ks < nks; ++ks) {
           const AFrag a = load_afrag(sG, C::LDG, warp * 16, ks * 8, g, tq);
 #pragma unroll
-          for (int n = 0; n < C::NT2; ++n)
-            mma_frag(acc[n], a, __ldg(fb2 + ((size_t)(ks0 + ks) * C::NT2 + n) * 32 + lane));
+          for (int nt = 0; nt < C::NT2; ++nt)
+            mma_frag(acc[nt], a, C::OPRING ? fb2[(ks * C::NT2 + nt) * 32 + lane] : __ldg(fb2 + (ks * C::NT2 + nt) * 32 + lane));
         }
       }
+      ++n;
     }
     __syncthreads();  // the face phase reuses the volume buffers
 
     // ---- surface: chunks of FCH face nodes -------------------------------------
     double* sF = sWork;
+    // this thread's epilogue res values -> smem while the face phase runs
+    double* sRes = sWork + C::R * C::LDF + tid * (2 * C::NT2 * 2);
+    if (UPDATE && C::RESS) {
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int grow = hh ? r_hi : r_lo;
+        if (grow < n_rows)
+#pragma unroll
+          for (int nt = 0; nt < C::NT2; ++nt)
+            cp_async16_sh(sRes + (hh * C::NT2 + nt) * 2, p.res + (size_t)grow * C::BP + nt * 8 + 2 * tq);
+      }
+    }
 #pragma unroll 1
     for (int fc = 0; fc < C::NFCH; ++fc) {
       const int f0 = fc * C::FCH;
@@ -242,18 +362,32 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_row(RhsParams p) {
         for (int c = 0; c < 5; ++c) gout[c * C::LDF] = fn.w * fs[c];
       }
       __syncthreads();
+      if (C::OPRING && tid == 0 && n + 1 < n_chunks) {  // every warp is past the GEMM of chunk n-1
+        fence_proxy_async();
+        issue_op_chunk<C>(n + 1, sOp, bars, p.frag_icub, p.frag_op2);
+      }
       {
-        const int ks0 = (C::K2CUB + f0) / 8, nks = wp / 8;
+        const double2* fb2;
+        if (C::OPRING) {
+          fb2 = reinterpret_cast<const double2*>(sOp + (n & 1) * C::OPB);
+          mbar_wait(&bars[n & 1], (n >> 1) & 1);
+        } else {
+          fb2 = reinterpret_cast<const double2*>(p.frag_op2) + (size_t)((C::K2CUB + f0) / 8) * C::NT2 * 32;
+        }
+        const int nks = wp / 8;
 #pragma unroll 1
         for (int ks = 0; ks < nks; ++ks) {
           const AFrag a = load_afrag(sF, C::LDF, warp * 16, ks * 8, g, tq);
 #pragma unroll
-          for (int n = 0; n < C::NT2; ++n)
-            mma_frag(acc[n], a, __ldg(fb2 + ((size_t)(ks0 + ks) * C::NT2 + n) * 32 + lane));
+          for (int nt = 0; nt < C::NT2; ++nt)
+            mma_frag(acc[nt], a, C::OPRING ? fb2[(ks * C::NT2 + nt) * 32 + lane] : __ldg(fb2 + (ks * C::NT2 + nt) * 32 + lane));
         }
       }
+      ++n;
       if (fc + 1 < C::NFCH) __syncthreads();
     }
+    if (UPDATE && C::RESS) cp_async_wait0();
+    if (UPDATE && !C::UREG) load_u();  // old u for the update
 
     // ---- epilogue: rhs -> (res, u) update or rhs store ---------------------------
     double a_c = 0.0, b_c = 0.0, dt = 0.0;
@@ -270,15 +404,16 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_row(RhsParams p) {
       if (grow >= n_rows || (hh ? cur_hi : cur_lo)) continue;  // curved rows: k_rhs_curved
       const size_t rowoff = (size_t)grow * C::BP;
 #pragma unroll
-      for (int n = 0; n < C::NT2; ++n) {
-        const int col = n * 8 + 2 * tq;  // < KP <= BP; padded columns carry exact zeros
-        const double r0 = acc[n][2 * hh], r1 = acc[n][2 * hh + 1];
+      for (int j = 0; j < C::NT2; ++j) {
+        const int col = j * 8 + 2 * tq;  // < KP <= BP; padded columns carry exact zeros
+        const double r0 = acc[j][2 * hh], r1 = acc[j][2 * hh + 1];
         if (UPDATE) {
-          const double2 rs = *reinterpret_cast<const double2*>(p.res + rowoff + col);
+          const double2 rs = C::RESS ? *reinterpret_cast<const double2*>(sRes + (hh * C::NT2 + j) * 2)
+                                     : *reinterpret_cast<const double2*>(p.res + rowoff + col);
           const double n0 = a_c * rs.x + dt * r0, n1 = a_c * rs.y + dt * r1;
           *reinterpret_cast<double2*>(p.res + rowoff + col) = make_double2(n0, n1);
-          // old u: the A fragment of k-step n holds (row, 8n+2t) / (row, 8n+2t+1)
-          const double u0 = hh ? uA[n][1] : uA[n][0], u1 = hh ? uA[n][3] : uA[n][2];
+          // old u: the A fragment of k-step j holds (row, 8j+2t) / (row, 8j+2t+1)
+          const double u0 = hh ? uA[j][1] : uA[j][0], u1 = hh ? uA[j][3] : uA[j][2];
           *reinterpret_cast<double2*>(p.u + rowoff + col) = make_double2(u0 + b_c * n0, u1 + b_c * n1);
         } else {
           *reinterpret_cast<double2*>(p.rhs_out + rowoff + col) = make_double2(r0, r1);

@@ -38,9 +38,9 @@ struct KernelSet {
   int row_minb = 0, row_ch = 0;
 };
 
-template <int NP, int NCUB, int NG, int CH = 8, int FCH = 64, int MINB = 3>
+template <int NP, int NCUB, int NG, int CH = 8, int FCH = 32, int MINB = 3, int MODE = 7>
 KernelSet with_row(KernelSet k) {
-  using RC = RCfg<NP, NCUB, NG, CH, FCH, MINB>;
+  using RC = RCfg<NP, NCUB, NG, CH, FCH, MINB, MODE>;
   k.row_update[0] = &k_rhs_row<RC, true, 0>;
   k.row_update[1] = &k_rhs_row<RC, true, 1>;
   k.row_only[0] = &k_rhs_row<RC, false, 0>;

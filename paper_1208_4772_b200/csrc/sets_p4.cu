@@ -7,12 +7,15 @@ namespace cdg_gpu {
 
 std::vector<KernelSet> kernel_sets_p4() {
   return {
-      with_row<35, 70, 16>(make_set<35, 70, 16, 16, 24, 2, 64>()),
-      with_row<35, 70, 56>(make_set<35, 70, 56, 16, 24, 2>()),
+      with_row<35, 70, 16, 8, 32, 4, 0>(make_set<35, 70, 16, 16, 24, 2, 64>()),
+      with_row<35, 70, 56, 8, 32, 4, 0>(make_set<35, 70, 56, 16, 24, 2>()),
       // P=4 straight tuning variants, selected with CDG_KCFG=<n> (bench sweeps)
       make_set<35, 70, 16, 16, 24, 2, 64>(), make_set<35, 70, 16, 16, 8, 4, 24, 5>(),
-      with_row<35, 70, 16, 16, 64, 2>(make_set<35, 70, 16, 16, 24, 2, 64>()),
-      with_row<35, 70, 16, 8, 32, 3>(make_set<35, 70, 16, 16, 24, 2, 64>())};
+      with_row<35, 70, 16, 8, 32, 3, 7>(make_set<35, 70, 16, 16, 24, 2, 64>()),
+      with_row<35, 70, 16, 8, 32, 4, 4>(make_set<35, 70, 16, 16, 24, 2, 64>()),
+      with_row<35, 70, 16, 8, 32, 3, 6>(make_set<35, 70, 16, 16, 24, 2, 64>()),
+      with_row<35, 70, 16, 8, 32, 3, 0>(make_set<35, 70, 16, 16, 24, 2, 64>()),
+      with_row<35, 70, 16, 8, 64, 3, 2>(make_set<35, 70, 16, 16, 24, 2, 64>())};
 }
 
 }  // namespace cdg_gpu
