@@ -24,6 +24,7 @@ struct CurvedParams {
   const double* minv;      // [Kc][NP][NP]
   const double* frag_opc;  // B fragments of [D^T | -I_g^T]
   double* vol;             // [Kc*5][NP8] epilogue scratch when the tile's vol does not fit smem
+  double* q_out;           // [3][K*5][BP] aux gradient (k_aux_curved)
   int Kc;
 };
 
@@ -38,7 +39,7 @@ struct CurvedLayout {
   static constexpr size_t SMEM_BYTES = SMEM_NO_V + (GV ? 0 : sizeof(double) * (size_t)C::R * LDV);
 };
 
-template <class C, bool UPDATE>
+template <class C, bool UPDATE, bool VISC = false>
 __global__ void __launch_bounds__(kThreads, 1) k_rhs_curved(CurvedParams cp) {
   using L = CurvedLayout<C>;
   const RhsParams& p = cp.base;
@@ -106,9 +107,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_rhs_curved(CurvedParams cp) {
           const double pr = pressure(s, gamma);
           const double vx = s.mx / s.r, vy = s.my / s.r, vz = s.mz / s.r;
           const double ep = s.E + pr;
-          const double F[3][5] = {{s.mx, s.mx * vx + pr, s.my * vx, s.mz * vx, vx * ep},
-                                  {s.my, s.mx * vy, s.my * vy + pr, s.mz * vy, vy * ep},
-                                  {s.mz, s.mx * vz, s.my * vz, s.mz * vz + pr, vz * ep}};
+          double F[3][5] = {{s.mx, s.mx * vx + pr, s.my * vx, s.mz * vx, vx * ep},
+                            {s.my, s.mx * vy, s.my * vy + pr, s.mz * vy, vy * ep},
+                            {s.mz, s.mx * vz, s.my * vz, s.mz * vz + pr, vz * ep}};
+          if (VISC) {
+            // F_m <- F_m - sqrt(eps) I_cub q_m  (solver.cpp:398-406)
+            const double se = p.sqrt_eps[sId[e]];
+            if (se > 0.0) {
+              const size_t qstride = (size_t)p.K * 5 * C::BP;
+              const double* irow = p.icub + (size_t)q * C::NP;
+#pragma unroll
+              for (int m = 0; m < 3; ++m)
+#pragma unroll
+                for (int c = 0; c < 5; ++c) {
+                  const double* qrow = p.q + m * qstride + ((size_t)sId[e] * 5 + c) * C::BP;
+                  double qc = 0.0;
+                  for (int j = 0; j < C::NP; ++j) qc += __ldg(irow + j) * __ldg(qrow + j);
+                  F[m][c] -= se * qc;
+                }
+            }
+          }
           const double* met = cp.jwr + ((size_t)ce * C::NCUB + q) * 9;
 #pragma unroll
           for (int m = 0; m < 3; ++m) {
@@ -151,8 +169,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_rhs_curved(CurvedParams cp) {
         const double4 fn = cp.face[(size_t)ce * C::NF + fq];
         const int2 cw = sConn[e * 4 + f];
         State5 up;
+        int h = 0;
         if (cw.x >= 0) {
-          const int h = __ldg(p.code_map + (cw.y >> 8) * C::NG + gq);
+          h = __ldg(p.code_map + (cw.y >> 8) * C::NG + gq);
           const double* tp = p.traces + (size_t)cw.x * 5 * C::TB + (cw.y & 3) * C::NG + h;
           up = State5{tp[0], tp[C::TB], tp[2 * C::TB], tp[3 * C::TB], tp[4 * C::TB]};
         } else {
@@ -165,6 +184,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_rhs_curved(CurvedParams cp) {
           hllc_flux(um, up, fn.x, fn.y, fn.z, gamma, fs);
         else
           llf_flux(um, up, fn.x, fn.y, fn.z, gamma, fs);
+        if (VISC) {
+          // BR1 central viscous flux with per-side sqrt(eps) (solver.cpp:438-453)
+          const double se = p.sqrt_eps[eg];
+          const bool has_nb = cw.x >= 0;
+          const double snb = has_nb ? p.sqrt_eps[cw.x] : se;
+          const double nrm[3] = {fn.x, fn.y, fn.z};
+#pragma unroll
+          for (int c = 0; c < 5; ++c) {
+            double visc = 0.0;
+#pragma unroll
+            for (int m = 0; m < 3; ++m) {
+              const double* qt = p.qtr + m * p.qtr_stride;
+              const double qs = qt[((size_t)eg * 5 + c) * C::TB + fq];
+              const double qn = has_nb ? qt[((size_t)cw.x * 5 + c) * C::TB + (cw.y & 3) * C::NG + h] : qs;
+              visc += 0.5 * (se * qs + snb * qn) * nrm[m];
+            }
+            fs[c] -= visc;
+          }
+        }
 #pragma unroll
         for (int c = 0; c < 5; ++c) gout[c * C::LDG] = fn.w * fs[c];
       }
@@ -213,6 +251,154 @@ __global__ void __launch_bounds__(kThreads, 1) k_rhs_curved(CurvedParams cp) {
       }
     }
     __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Auxiliary gradient on curved elements (compute_aux_gradient, solver.cpp:
+// 264-312) with per-node metrics:
+//   q_m = M_e^-1 [ -se sum_k D_k^T (JW dr_k/dx_m U_cub)
+//                  + I_g^T ((sjac w) 1/2 (se U- + snb U+) n_m) ]
+// The shared operator is frag_opc = [D^T | -I_g^T]; the face term is fed
+// negated. Overwrites the affine kernel's q rows of the listed elements.
+// ---------------------------------------------------------------------------
+template <class C>
+__global__ void __launch_bounds__(kThreads, 1) k_aux_curved(CurvedParams cp) {
+  using L = CurvedLayout<C>;
+  const RhsParams& p = cp.base;
+  extern __shared__ __align__(16) double smem[];
+  double* sU = smem;
+  double* sC = sU + C::SMEM_U;
+  double* sG = sC + C::SMEM_C;
+  double* sV = sG + C::SMEM_G;
+  int2* sConn = reinterpret_cast<int2*>(sV + (L::GV ? 0 : (size_t)C::R * L::LDV));
+  int* sId = reinterpret_cast<int*>(sConn + C::E * 4);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const double2* fb1 = reinterpret_cast<const double2*>(p.frag_icub);
+  const double2* fbc = reinterpret_cast<const double2*>(cp.frag_opc);
+  const int t_begin = (warp * C::T2) / kWarps, t_end = ((warp + 1) * C::T2) / kWarps;
+  const int n_tiles = (cp.Kc + C::E - 1) / C::E;
+  const size_t qstride = (size_t)p.K * 5 * C::BP;
+
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int c0 = tile * C::E;
+    for (int idx = tid; idx < C::E; idx += kThreads) sId[idx] = c0 + idx < cp.Kc ? cp.ids[c0 + idx] : -1;
+    __syncthreads();
+    constexpr int V8 = C::KP / 8;
+    for (int idx = tid; idx < C::R * V8 * 2; idx += kThreads) {
+      const int hh = idx & 1, j = (idx >> 1) % V8, r = (idx >> 1) / V8;
+      const int e = sId[r / 5];
+      double2 x = make_double2(0.0, 0.0), y = make_double2(0.0, 0.0);
+      if (e >= 0) {
+        const double* src = p.u + ((size_t)e * 5 + r % 5) * C::BP + 8 * j + 2 * hh;
+        x = *reinterpret_cast<const double2*>(src);
+        y = *reinterpret_cast<const double2*>(src + 4);
+      }
+      double* o = sU + r * C::LDU + 8 * j + 4 * hh;
+      *reinterpret_cast<double2*>(o) = make_double2(x.x, y.x);
+      *reinterpret_cast<double2*>(o + 2) = make_double2(x.y, y.y);
+    }
+    for (int idx = tid; idx < C::E * 4; idx += kThreads) {
+      const int e = sId[idx / 4];
+      sConn[idx] = e >= 0 ? p.conn[(size_t)e * 4 + idx % 4] : make_int2(-1, pack_face(0, 0, 1, 0));
+    }
+    __syncthreads();
+    for (int m = 0; m < 3; ++m) {
+      double acc[C::MAXT2][4];
+#pragma unroll
+      for (int i = 0; i < C::MAXT2; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.0;
+      for (int ch = 0; ch < C::NCH; ++ch) {
+        const int q0 = ch * C::CH;
+        const int w = (C::NCUB8 - q0) < C::CH ? (C::NCUB8 - q0) : C::CH;
+        gemm1_chunk<C>(sU, sC, fb1, q0, w, warp, lane);
+        __syncthreads();
+        // G_k = -se (JW dr_k/dx_m) U_cub   (solver.cpp:283-289, operators.cpp:135-149)
+        for (int idx = tid; idx < C::R * w; idx += kThreads) {
+          const int r = idx / w, ql = idx % w, e = r / 5, q = q0 + ql;
+          const int ce = c0 + e;
+          double* o = sG + r * C::LDG;
+          if (q < C::NCUB && ce < cp.Kc) {
+            const double uc = sC[r * C::LDC + ql];
+            const double se = p.sqrt_eps[sId[e]];
+            const double* jw = cp.jwr + ((size_t)ce * C::NCUB + q) * 9;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) o[pcol(k * w + ql)] = -se * (__ldg(jw + k * 3 + m) * uc);
+          } else {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) o[pcol(k * w + ql)] = 0.0;
+          }
+        }
+        __syncthreads();
+        gemm2_partial<C>(acc, sG, fbc, (3 * q0) / 8, (3 * w) / 8, t_begin, t_end, lane);
+        __syncthreads();
+      }
+      for (int fc = 0; fc < C::NFCH; ++fc) {
+        const int f0 = fc * C::FCH;
+        const int wr = (C::NF - f0) < C::FCH ? (C::NF - f0) : C::FCH;
+        const int wp = round_up(wr, 8);
+        for (int idx = tid; idx < C::E * wp; idx += kThreads) {
+          const int e = idx / wp, fl = idx % wp, fq = f0 + fl;
+          const int ce = c0 + e, eg = sId[e];
+          double* gout = sG + (e * 5) * C::LDG + pcol(fl);
+          if (ce >= cp.Kc || fl >= wr) {
+            for (int c = 0; c < 5; ++c) gout[c * C::LDG] = 0.0;
+            continue;
+          }
+          const int f = fq / C::NG, gq = fq - f * C::NG;
+          const double* tm = p.traces + (size_t)eg * 5 * C::TB + fq;
+          const State5 um{tm[0], tm[C::TB], tm[2 * C::TB], tm[3 * C::TB], tm[4 * C::TB]};
+          const double4 fn = cp.face[(size_t)ce * C::NF + fq];
+          const int2 cw = sConn[e * 4 + f];
+          const double se = p.sqrt_eps[eg];
+          State5 up;
+          double snb;
+          if (cw.x >= 0) {
+            const int hn = __ldg(p.code_map + (cw.y >> 8) * C::NG + gq);
+            const double* tp = p.traces + (size_t)cw.x * 5 * C::TB + (cw.y & 3) * C::NG + hn;
+            up = State5{tp[0], tp[C::TB], tp[2 * C::TB], tp[3 * C::TB], tp[4 * C::TB]};
+            snb = p.sqrt_eps[cw.x];
+          } else {
+            up = boundary_state(um, fn.x, fn.y, fn.z, (cw.y >> 2) & 3, p.gas);
+            snb = se;
+          }
+          const double nm = m == 0 ? fn.x : (m == 1 ? fn.y : fn.z);
+          const double umv[5] = {um.r, um.mx, um.my, um.mz, um.E};
+          const double upv[5] = {up.r, up.mx, up.my, up.mz, up.E};
+          for (int c = 0; c < 5; ++c) gout[c * C::LDG] = -fn.w * (0.5 * (se * umv[c] + snb * upv[c]) * nm);
+        }
+        __syncthreads();
+        gemm2_partial<C>(acc, sG, fbc, (C::K2CUB + f0) / 8, wp / 8, t_begin, t_end, lane);
+        __syncthreads();
+      }
+      // q_m = M_e^-1 vol
+      double* vbase = L::GV ? cp.vol + (size_t)c0 * 5 * L::LDV : sV;
+#pragma unroll
+      for (int i = 0; i < C::MAXT2; ++i) {
+        const int t = t_begin + i;
+        if (t < t_end) {
+          const int nt = t / C::MT, mt = t % C::MT;
+          for (int hh = 0; hh < 2; ++hh) {
+            const int r = mt * 16 + g + 8 * hh;
+            if (L::GV && c0 + r / 5 >= cp.Kc) continue;
+            vbase[r * L::LDV + nt * 8 + 2 * tq] = acc[i][2 * hh];
+            vbase[r * L::LDV + nt * 8 + 2 * tq + 1] = acc[i][2 * hh + 1];
+          }
+        }
+      }
+      __syncthreads();
+      for (int idx = tid; idx < C::R * C::NP; idx += kThreads) {
+        const int r = idx / C::NP, i = idx - r * C::NP, e = r / 5;
+        const int ce = c0 + e;
+        if (ce >= cp.Kc) continue;
+        const double* mrow = cp.minv + ((size_t)ce * C::NP + i) * C::NP;
+        const double* v = vbase + r * L::LDV;
+        double qv = 0.0;
+        for (int j = 0; j < C::NP; ++j) qv += __ldg(mrow + j) * v[j];
+        cp.q_out[m * qstride + ((size_t)sId[e] * 5 + r % 5) * C::BP + i] = qv;
+      }
+      __syncthreads();
+    }
   }
 }
 

@@ -265,7 +265,8 @@ RhsParams rhs_params(cdg_gpu_level* lv, int stage) {
   return p;
 }
 
-void launch_curved(cdg_gpu_level* lv, bool update, int stage) {
+// mode 0: inviscid RHS(+update), 1: viscous RHS(+update), 2: aux gradient q
+void launch_curved(cdg_gpu_level* lv, bool update, int stage, int mode = 0) {
   if (!lv->n_curved) return;
   CurvedParams cp{};
   cp.base = rhs_params(lv, stage);
@@ -275,9 +276,12 @@ void launch_curved(cdg_gpu_level* lv, bool update, int stage) {
   cp.minv = lv->curved_minv;
   cp.frag_opc = lv->frag_opc;
   cp.vol = lv->curved_vol;
+  cp.q_out = lv->q;
   cp.Kc = lv->n_curved;
   const int tiles = (lv->n_curved + lv->ks->E - 1) / lv->ks->E;
-  auto fn = update ? lv->ks->curved_update : lv->ks->curved_only;
+  auto fn = mode == 2 ? lv->ks->aux_curved
+                      : mode == 1 ? (update ? lv->ks->curved_visc_update : lv->ks->curved_visc_only)
+                                  : (update ? lv->ks->curved_update : lv->ks->curved_only);
   fn<<<std::max(1, std::min(tiles, lv->n_sms)), kThreads, lv->ks->smem_curved, lv->stream>>>(cp);
   ++lv->launches;
 }
@@ -338,15 +342,13 @@ void launch_rhs(cdg_gpu_level* lv, bool update, bool viscous, int stage) {
                     : (update ? lv->ks->rhs_update : lv->ks->rhs_only);
   fn<<<lv->grid(tiles), lv->ks->nth, lv->ks->smem_rhs, lv->stream>>>(p);
   ++lv->launches;
-  launch_curved(lv, update, stage);
+  launch_curved(lv, update, stage, viscous ? 1 : 0);
 }
 
 // Viscosity phase: sensor -> eps, then (if any eps > 0) aux gradient q and its
 // traces (solver.cpp:239-321). Returns whether the viscous path is active.
 bool viscosity_phase(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg) {
   if (!cfg->visc_enabled) return false;
-  if (lv->n_curved)
-    throw Status(CDG_GPU_ERR_CONFIG, "artificial viscosity on curved elements is not supported by this build");
   if (cfg->eps0 < 0.0) throw Status(CDG_GPU_ERR_CONFIG, "viscosity_amount: eps0 must be >= 0");
   if (cfg->jacobian_weighted)
     throw Status(CDG_GPU_ERR_CONFIG, "jacobian_weighted indicator is not supported on the GPU path");
@@ -399,6 +401,7 @@ bool viscosity_phase(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg) {
   ap.gas = lv->gas;
   lv->ks->aux_q<<<lv->grid(lv->n_tiles()), kThreads, lv->ks->smem_aux, lv->stream>>>(ap);
   ++lv->launches;
+  launch_curved(lv, false, 0, 2);  // per-node-metric q of the curved elements
   // q traces: 3 x (K*5 rows)
   const size_t n = (size_t)lv->K * 5 * lv->bp;
   const size_t nt = (size_t)(lv->K + lv->n_halo) * 5 * lv->tb;
@@ -723,7 +726,8 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
       for (auto fn : {lv->ks->warp_update[0], lv->ks->warp_update[1], lv->ks->warp_only[0], lv->ks->warp_only[1]})
         CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lv->ks->smem_warp));
     if (lv->n_curved)
-      for (auto fn : {lv->ks->curved_update, lv->ks->curved_only})
+      for (auto fn : {lv->ks->curved_update, lv->ks->curved_only, lv->ks->curved_visc_update,
+                      lv->ks->curved_visc_only, lv->ks->aux_curved})
         CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lv->ks->smem_curved));
     CUDA_OK(cudaFuncSetAttribute(lv->ks->traces, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)lv->ks->smem_traces));

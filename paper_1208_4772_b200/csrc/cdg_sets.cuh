@@ -25,6 +25,9 @@ struct KernelSet {
   void (*visc_rhs_only)(RhsParams);
   void (*curved_update)(CurvedParams);
   void (*curved_only)(CurvedParams);
+  void (*curved_visc_update)(CurvedParams);
+  void (*curved_visc_only)(CurvedParams);
+  void (*aux_curved)(CurvedParams);
   size_t smem_curved;
   // warp-tile inviscid kernel (cdg_warp.cuh), p <= 3
   void (*warp_update[2])(WarpParams) = {nullptr, nullptr};  // [riemann]
@@ -90,6 +93,9 @@ KernelSet make_set() {
   k.visc_rhs_only = &k_rhs<C, false, true>;
   k.curved_update = &k_rhs_curved<C8, true>;
   k.curved_only = &k_rhs_curved<C8, false>;
+  k.curved_visc_update = &k_rhs_curved<C8, true, true>;
+  k.curved_visc_only = &k_rhs_curved<C8, false, true>;
+  k.aux_curved = &k_aux_curved<C8>;
   k.smem_curved = CurvedLayout<C8>::SMEM_BYTES;
   return k;
 }

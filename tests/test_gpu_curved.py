@@ -83,3 +83,35 @@ def test_curved_sphere_freestream_preservation(gpu_lib, refmod, p):
     lv2 = gpu.GpuLevel(mesh, p, bc={"sphere": 1, "farfield": 1}, freestream=fs, curved=(ids, nodes[ids]))
     r = lv2.compute_rhs(gpu.run_config("llf"), gpu.freestream_store(lv2, fs))
     assert np.max(np.abs(r)) < 1e-8, np.max(np.abs(r))
+
+
+# ---- artificial viscosity on curved elements (the NACA-type configuration:
+# curved wall elements + Persson-Peraire AV; BASELINE config 2 kernel proxy) --
+VISC_FORCED = dict(enabled=True, eps0=0.04, kappa=4.0, s0_offset=-100.0)
+VISC_RAMP = dict(enabled=True, eps0=0.3, kappa=4.0, s0_offset=0.0)
+
+
+@pytest.mark.parametrize("p", [2, 3, 4])
+@pytest.mark.parametrize("visc,riem", [(VISC_FORCED, "llf"), (VISC_RAMP, "hllc")])
+def test_curved_sphere_viscous_matches_reference(gpu_lib, refmod, p, visc, riem):
+    gpu, ref = gpu_lib, refmod
+    rm, rl, mesh, ids, nodes = sphere_case(ref, p)
+    fs = _fs(gpu)
+    lv = gpu.GpuLevel(mesh, p, bc={"sphere": 0, "farfield": 1}, freestream=fs, curved=(ids, nodes[ids]))
+    u = rl.random_admissible_store(11)
+    r_ref = rl.compute_rhs(u, ref.make_cfg(riem, viscosity=visc), fs)
+    eps_ref, q_ref = rl.last_viscosity()
+    r_gpu = lv.compute_rhs(gpu.run_config(riem, viscosity=visc), u)
+    eps = lv.viscosity()
+    assert np.allclose(eps, eps_ref, rtol=1e-12, atol=1e-15)
+    assert (eps > 0).any()
+    q = np.stack([lv.aux_gradient(m) for m in range(3)])
+    assert rel(q, q_ref) < 1e-10, rel(q, q_ref)
+    assert rel(r_gpu, r_ref) < 1e-10, rel(r_gpu, r_ref)
+    # two RK steps (sensor + aux gradient + viscous RHS in every stage)
+    cfg_r = ref.make_cfg(riem, viscosity=visc)
+    dt = 0.1 * rl.compute_timestep(u, ref.make_cfg(riem), eps_ref)
+    lv.set_state(u)
+    lv.rk_steps(gpu.run_config(riem, viscosity=visc), dt, 2)
+    u_ref, _ = rl.rk_steps(u, np.zeros_like(u), cfg_r, fs, dt, 2)
+    assert rel(lv.get_state()[0], u_ref) < 1e-12
