@@ -167,6 +167,34 @@ int cdg_gpu_timestep(cdg_gpu_level *lv, const cdg_gpu_run_config *cfg, int use_v
 int cdg_gpu_snapshot(cdg_gpu_level *lv);
 int cdg_gpu_residual(cdg_gpu_level *lv, int kind, double dt, double *out);
 
+/* ---- device-resident run_steady (solver.cpp:594-676) --------------------------
+ * The reference's per-level loop with the state on the device: RK steps run
+ * back to back (graph replays) and the host synchronises only at the check
+ * iterations, where it reads back one residual and one time step. */
+typedef struct cdg_gpu_steady_params {
+  long max_iterations;    /* RunConfig::max_iterations_per_level */
+  long fixed_iterations;  /* RunConfig::fixed_iterations[level], or <= 0 */
+  int check_interval;     /* RunConfig::check_interval */
+  int residual_kind;      /* RunConfig::residual_norm: 0 "inf", 1 "l2" */
+  double tolerance;       /* final_tolerance on the last level, else intermediate_tolerance */
+  double dt_override;     /* RunConfig::dt_override (> 0 replaces the CFL formula) */
+  int degree;             /* p of this level (divergence message) */
+} cdg_gpu_steady_params;
+
+/* u = freestream_store(level, freestream) (solver.cpp:559-568), res = 0. */
+int cdg_gpu_fill_freestream(cdg_gpu_level *lv);
+/* to.u = p_refine_embed(from.u) (solver.cpp:528-549) with the caller's
+ * embedding matrix embed[np_to][np_from] = V_to[:, :np_from] V_from^-1;
+ * to.res = 0. Both levels on the same device, same element count. */
+int cdg_gpu_p_refine_embed(cdg_gpu_level *to, const cdg_gpu_level *from, const double *embed);
+/* One level of run_steady (solver.cpp:622-668). rows receives
+ * (iteration, dt, residual) for every check iteration (at most max_rows);
+ * *converged = 1 when the level stopped on its tolerance. A residual above
+ * 1e6 x the first one returns 3 with the reference's "run_steady: divergence
+ * detected at p=P iteration I (residual R)" text. */
+int cdg_gpu_run_level(cdg_gpu_level *lv, const cdg_gpu_run_config *cfg, const cdg_gpu_steady_params *sp,
+                      double *rows, int max_rows, int *n_rows, int *converged, char *err, size_t errlen);
+
 /* ---- multi-GPU halo plumbing (one process per GPU) --------------------------
  * send_elem_face[i] = element*4+face of an owned element whose face trace
  * (5*N_g values) is packed into row i of the caller-owned DEVICE buffer

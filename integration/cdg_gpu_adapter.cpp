@@ -9,6 +9,9 @@
 //   cdg::current_viscosity     solver.hpp:100  -> cdg_gpu_viscosity
 //   cdg::aux_gradient          solver.hpp:103  -> cdg_gpu_aux_gradient
 //   cdg::rk_step               solver.hpp:107  -> cdg_gpu_rk_steps (1 step)
+//   cdg::run_steady            solver.hpp:128  -> cdg_gpu_fill_freestream / cdg_gpu_p_refine_embed /
+//                                                 cdg_gpu_run_level (device-resident levels; the host
+//                                                 syncs only at check iterations)
 //
 // Build (reference side): compile this file against proj/core/include, link
 // libcdg_gpu.so, and compile solver.cpp with the six names above renamed
@@ -16,6 +19,7 @@
 // test_solver_gpu does exactly this to run the reference's test_solver.cpp on
 // the GPU). Exceptions and messages are the reference's: status 3 ->
 // NumericsError, 2 -> ConfigError.
+#include <chrono>
 #include <cmath>
 #include <map>
 #include <memory>
@@ -224,6 +228,71 @@ void rk_step(const DgLevel& level, SolutionStore& u, SolutionStore& res, const R
   throw_status(cdg_gpu_rk_steps(ws.lv, &c, 1, dt, scheme.a.data(), scheme.b.data(), err, sizeof err), err);
   throw_status(cdg_gpu_get_state(ws.lv, u.raw().data(), res.raw().data()), "get_state failed");
   if (cfg.viscosity.enabled) throw_status(cdg_gpu_viscosity(ws.lv, ws.eps.data()), "viscosity failed");
+}
+
+// run_steady (solver.cpp:594-676) with every level device-resident. Host work
+// per level is the reference's: build the DgLevel (setup tables), then one
+// cdg_gpu_run_level call; rows reach on_row when the level finishes.
+SteadyResult run_steady(const CurvedMesh& cmesh, const BcMap& bc_map, const RunConfig& cfg,
+                        const ConservedState& freestream, const std::function<void(const ConvergenceRow&)>& on_row) {
+  if (cfg.p_schedule.empty()) throw ConfigError("run_steady: empty p-schedule");
+  for (size_t i = 1; i < cfg.p_schedule.size(); ++i)
+    if (cfg.p_schedule[i] <= cfg.p_schedule[i - 1])
+      throw ConfigError("run_steady: p-schedule must be strictly increasing");
+  if (cfg.residual_norm != "inf" && cfg.residual_norm != "l2")
+    throw ConfigError("run_steady: unknown residual norm '" + cfg.residual_norm + "'");
+  SteadyResult result;
+  const auto wall_start = std::chrono::steady_clock::now();
+  const cdg_gpu_run_config c = to_cfg(cfg);
+  std::unique_ptr<cdg_gpu_level, void (*)(cdg_gpu_level*)> prev(nullptr, cdg_gpu_level_destroy);
+  std::shared_ptr<const ReferenceElement> re_prev;
+  for (size_t li = 0; li < cfg.p_schedule.size(); ++li) {
+    const int p = cfg.p_schedule[li];
+    auto re = level_reference_element(cmesh, p, cfg);
+    DgLevel level(cmesh, re, bc_map, cfg.padded);
+    std::unique_ptr<cdg_gpu_level, void (*)(cdg_gpu_level*)> lv(create_level(level, freestream),
+                                                                cdg_gpu_level_destroy);
+    if (li == 0) {
+      throw_status(cdg_gpu_fill_freestream(lv.get()), "fill_freestream failed");
+    } else {
+      const Eigen::MatrixXd embed = re->vandermonde().leftCols(re_prev->n_basis()) * re_prev->vandermonde_inv();
+      const std::vector<double> e = row_major(embed);
+      throw_status(cdg_gpu_p_refine_embed(lv.get(), prev.get(), e.data()), "p_refine_embed failed");
+    }
+    prev.reset();
+    re_prev = re;
+    const bool last = li + 1 == cfg.p_schedule.size();
+    cdg_gpu_steady_params sp{};
+    sp.max_iterations = cfg.max_iterations_per_level;
+    sp.fixed_iterations = li < cfg.fixed_iterations.size() ? cfg.fixed_iterations[li] : -1;
+    sp.check_interval = cfg.check_interval;
+    sp.residual_kind = cfg.residual_norm == "l2" ? 1 : 0;
+    sp.tolerance = last ? cfg.final_tolerance : cfg.intermediate_tolerance;
+    sp.dt_override = cfg.dt_override;
+    sp.degree = p;
+    const int max_rows = static_cast<int>(cfg.max_iterations_per_level / std::max(1, cfg.check_interval)) + 2;
+    std::vector<double> rows(3 * (size_t)max_rows);
+    int n_rows = 0, converged = 0;
+    char err[512] = {0};
+    throw_status(cdg_gpu_run_level(lv.get(), &c, &sp, rows.data(), max_rows, &n_rows, &converged, err, sizeof err),
+                 err);
+    const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall_start).count();
+    for (int i = 0; i < n_rows && i < max_rows; ++i) {
+      ConvergenceRow row{p, static_cast<long>(rows[3 * i]), rows[3 * i + 1], rows[3 * i + 2], wall};
+      result.log.push_back(row);
+      if (on_row) on_row(row);
+    }
+    if (last) {
+      result.converged = converged != 0;
+      if (sp.fixed_iterations > 0 && !result.log.empty())
+        result.converged = result.log.back().residual < cfg.final_tolerance;
+      result.solution = level.make_store();
+      throw_status(cdg_gpu_get_state(lv.get(), result.solution.raw().data(), nullptr), "get_state failed");
+    }
+    result.final_degree = p;
+    prev = std::move(lv);
+  }
+  return result;
 }
 
 }  // namespace cdg

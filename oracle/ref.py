@@ -80,6 +80,10 @@ def lib():
         L.ref_refelem_sizes.argtypes = [C.c_int, C.c_int, C.c_int, _ip]
         L.ref_refelem_tables.argtypes = [C.c_int, C.c_int, C.c_int] + [_dp] * 12
         L.ref_num_threads.argtypes = [C.c_int]
+        L.ref_run_steady.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(RunCfg), _ip, C.c_int,
+                                     C.POINTER(C.c_long), C.c_int, C.c_double, C.c_double, C.c_int, C.c_int,
+                                     C.c_int, C.c_double, _dp, _dp, C.c_int, _ip, _ip, _ip, _dp, C.c_long,
+                                     C.c_char_p, C.c_size_t]
         _lib = L
     return _lib
 
@@ -150,6 +154,33 @@ class Mesh:
         if getattr(self, "h", None) and _lib is not None:
             _lib.ref_mesh_free(self.h)
             self.h = None
+
+
+def run_steady(mesh, cfg: RunCfg, freestream, p_schedule, fixed=(), final_tol=1e-9, inter_tol=1e-4,
+               max_iters=20000, check_interval=1000, residual="inf", dt_override=0.0, bc_wall=0, bc_far=1,
+               u_cap=None):
+    """The reference's run_steady (solver.cpp:594-676) on `mesh` (Mesh handle).
+    Returns (rows [n][5] = level, iteration, dt, residual, wall_s; converged;
+    final_degree; solution raw store)."""
+    ps = np.ascontiguousarray(p_schedule, np.int32)
+    fx = (C.c_long * max(1, len(fixed)))(*fixed)
+    rows = np.zeros((4096, 5))
+    n = np.zeros(1, np.int32)
+    conv = np.zeros(1, np.int32)
+    fdeg = np.zeros(1, np.int32)
+    ex = mesh.export()
+    K = len(ex["tets"])
+    pmax = int(max(p_schedule))
+    cap = u_cap or K * 5 * 176 * (pmax + 1)
+    u = np.zeros(cap)
+    fs = np.ascontiguousarray(freestream, np.float64)
+    err = C.create_string_buffer(512)
+    st = lib().ref_run_steady(mesh.h, bc_wall, bc_far, C.byref(cfg), _p(ps), len(ps), fx, len(fixed), final_tol,
+                              inter_tol, max_iters, check_interval, 1 if residual == "l2" else 0, dt_override,
+                              _p(fs), _p(rows), rows.shape[0], _p(n), _p(conv), _p(fdeg), _p(u), cap, err, 512)
+    if st:
+        raise RefError(st, err.value.decode())
+    return rows[: int(n[0])], bool(conv[0]), int(fdeg[0]), u
 
 
 class Level:

@@ -454,4 +454,50 @@ int ref_compute_timestep(void* h, const ref_run_cfg* c, const double* u_in, cons
   }
 }
 
+// run_steady (solver.cpp:594-676) on the mesh handle's CurvedMesh (the curved
+// sidecar when present, else the straight mesh at the last schedule degree,
+// as cmd_solve does, cli_ops.cpp:97-108). rows_out [max_rows][5] =
+// (level, iteration, dt, residual, wall_seconds); u_out receives the final
+// solution (capacity u_cap doubles).
+int ref_run_steady(void* mesh_h, int bc_wall, int bc_far, const ref_run_cfg* c, const int* p_schedule,
+                   int n_levels, const long* fixed, int n_fixed, double final_tol, double inter_tol,
+                   int max_iters, int check_interval, int residual_kind, double dt_override,
+                   const double* freestream, double* rows_out, int max_rows, int* n_rows, int* converged,
+                   int* final_degree, double* u_out, long u_cap, char* err, size_t errn) {
+  try {
+    auto* m = static_cast<RefMesh*>(mesh_h);
+    RunConfig cfg = to_cfg(c);
+    cfg.p_schedule.assign(p_schedule, p_schedule + n_levels);
+    cfg.fixed_iterations.assign(fixed, fixed + n_fixed);
+    cfg.final_tolerance = final_tol;
+    cfg.intermediate_tolerance = inter_tol;
+    cfg.max_iterations_per_level = max_iters;
+    cfg.check_interval = check_interval;
+    cfg.residual_norm = residual_kind == 1 ? "l2" : "inf";
+    cfg.dt_override = dt_override;
+    const CurvedMesh cmesh = m->curved ? *m->curved : CurvedMesh(m->mesh, cfg.p_schedule.back());
+    const BcMap bcs = {{"wall", static_cast<BcKind>(bc_wall)},
+                       {"sphere", static_cast<BcKind>(bc_wall)},
+                       {"farfield", static_cast<BcKind>(bc_far)}};
+    const SteadyResult r = run_steady(cmesh, bcs, cfg, to_state(freestream), nullptr);
+    *n_rows = static_cast<int>(r.log.size());
+    for (int i = 0; i < *n_rows && i < max_rows; ++i) {
+      rows_out[5 * i + 0] = r.log[i].level;
+      rows_out[5 * i + 1] = static_cast<double>(r.log[i].iteration);
+      rows_out[5 * i + 2] = r.log[i].dt;
+      rows_out[5 * i + 3] = r.log[i].residual;
+      rows_out[5 * i + 4] = r.log[i].wall_seconds;
+    }
+    *converged = r.converged ? 1 : 0;
+    *final_degree = r.final_degree;
+    const auto& raw = r.solution.raw();
+    if (static_cast<long>(raw.size()) > u_cap) throw ConfigError("ref_run_steady: u_out too small");
+    std::memcpy(u_out, raw.data(), raw.size() * sizeof(double));
+    return 0;
+  } catch (const std::exception& e) {
+    copy_err(e, err, errn);
+    return status_of(e);
+  }
+}
+
 }  // extern "C"

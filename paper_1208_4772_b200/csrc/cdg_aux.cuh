@@ -283,6 +283,33 @@ __global__ void k_halo_copy(double* traces, double* buf, const int* idx, int n, 
       *t = *s;
   }
 }
+
+// ---------------------------------------------------------------------------
+// p_refine_embed (solver.cpp:528-549): out(e, c) = E in(e, c), one warp per
+// (element, field) row, lanes over the target nodes.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_embed(const double* __restrict__ in, double* __restrict__ out,
+                                               const double* __restrict__ E, int rows, int np_in, int bp_in,
+                                               int np_out, int bp_out) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const double* src = in + (size_t)row * bp_in;
+  for (int i = lane; i < bp_out; i += 32) {
+    double s = 0.0;
+    if (i < np_out)
+      for (int j = 0; j < np_in; ++j) s += __ldg(E + (size_t)i * np_in + j) * __ldg(src + j);
+    out[(size_t)row * bp_out + i] = s;
+  }
+}
+
+// freestream_store (solver.cpp:559-568): u(e, c)[i] = u_inf[c], padding 0
+__global__ void __launch_bounds__(256) k_fill_freestream(double* u, GasParams gp, size_t rows, int np, int bp) {
+  const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= rows * bp) return;
+  const int i = (int)(idx % bp);
+  const int c = (int)((idx / bp) % 5);
+  u[idx] = i < np ? gp.fs[c] : 0.0;
+}
 #endif  // CDG_SET_TU
 
 }  // namespace cdg_gpu

@@ -1040,6 +1040,96 @@ int cdg_gpu_residual(cdg_gpu_level* lv, int kind, double dt, double* out) {
   });
 }
 
+// ---- device-resident run_steady -----------------------------------------------
+int cdg_gpu_fill_freestream(cdg_gpu_level* lv) {
+  return guarded(nullptr, 0, [&] {
+    CUDA_OK(cudaSetDevice(lv->device));
+    const size_t rows = (size_t)lv->K * 5, n = rows * lv->bp;
+    k_fill_freestream<<<(unsigned)((n + 255) / 256), 256, 0, lv->stream>>>(lv->u, lv->gas, rows, lv->np, lv->bp);
+    ++lv->launches;
+    CUDA_OK(cudaMemsetAsync(lv->res, 0, n * sizeof(double), lv->stream));
+    CUDA_OK(cudaGetLastError());
+    CUDA_OK(cudaStreamSynchronize(lv->stream));
+  });
+}
+
+int cdg_gpu_p_refine_embed(cdg_gpu_level* to, const cdg_gpu_level* from, const double* embed) {
+  return guarded(nullptr, 0, [&] {
+    if (to->K != from->K || to->device != from->device)
+      throw Status(CDG_GPU_ERR_CONFIG, "p_refine_embed: levels differ in element count or device");
+    if (to->degree < from->degree) throw Status(CDG_GPU_ERR_CONFIG, "p_refine_embed: target degree must not decrease");
+    CUDA_OK(cudaSetDevice(to->device));
+    // the source state must be complete before the target stream reads it
+    CUDA_OK(cudaStreamSynchronize(from->stream));
+    double* dE = dev_upload(std::vector<double>(embed, embed + (size_t)to->np * from->np));
+    const int rows = to->K * 5;
+    k_embed<<<(rows + 7) / 8, 256, 0, to->stream>>>(from->u, to->u, dE, rows, from->np, from->bp, to->np, to->bp);
+    ++to->launches;
+    CUDA_OK(cudaMemsetAsync(to->res, 0, (size_t)rows * to->bp * sizeof(double), to->stream));
+    CUDA_OK(cudaGetLastError());
+    CUDA_OK(cudaStreamSynchronize(to->stream));
+    cudaFree(dE);
+  });
+}
+
+int cdg_gpu_run_level(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, const cdg_gpu_steady_params* sp,
+                      double* rows, int max_rows, int* n_rows, int* converged, char* err, size_t errlen) {
+  // Carpenter-Kennedy LSRK4(5) coefficients (rk.hpp:15-24)
+  static const double A[5] = {0.0, -567301805773.0 / 1357537059087.0, -2404267990393.0 / 2016746695238.0,
+                              -3550918686646.0 / 2091501179385.0, -1275806237668.0 / 842570457699.0};
+  static const double B[5] = {1432997174477.0 / 9575080441755.0, 5161836677717.0 / 13612068292357.0,
+                              1720146321549.0 / 2090206949498.0, 3134564353537.0 / 4481467310338.0,
+                              2277821191437.0 / 14882151754819.0};
+  *n_rows = 0;
+  *converged = 0;
+  return guarded(err, errlen, [&] {
+    if (sp->check_interval <= 0) throw Status(CDG_GPU_ERR_CONFIG, "run_steady: check_interval must be positive");
+    auto ok = [&](int st) {
+      if (st != CDG_GPU_OK) throw Status(st, err && errlen ? std::string(err) : std::string("run_level failed"));
+    };
+    double dt = 0.0;
+    if (sp->dt_override > 0.0)
+      dt = sp->dt_override;
+    else
+      ok(cdg_gpu_timestep(lv, cfg, 0, &dt, err, errlen));
+    double initial = -1.0;
+    long iter = 0;
+    bool done = false;
+    while (!done && iter < sp->max_iterations) {
+      // next check iteration: iter % interval == 0, the last iteration, or the fixed count
+      long next = (iter / sp->check_interval + 1) * sp->check_interval;
+      next = std::min(next, sp->max_iterations);
+      if (sp->fixed_iterations > iter) next = std::min(next, sp->fixed_iterations);
+      if (next - iter - 1 > 0) ok(cdg_gpu_rk_steps(lv, cfg, (int)(next - iter - 1), dt, A, B, err, errlen));
+      ok(cdg_gpu_snapshot(lv));
+      ok(cdg_gpu_rk_steps(lv, cfg, 1, dt, A, B, err, errlen));
+      iter = next;
+      double r = 0.0;
+      ok(cdg_gpu_residual(lv, sp->residual_kind, dt, &r));
+      if (*n_rows < max_rows) {
+        rows[3 * *n_rows + 0] = (double)iter;
+        rows[3 * *n_rows + 1] = dt;
+        rows[3 * *n_rows + 2] = r;
+      }
+      ++*n_rows;
+      if (initial < 0.0) initial = std::max(r, 1e-300);
+      if (r > 1e6 * initial && r > 1e-12) {
+        char buf[256];
+        std::snprintf(buf, sizeof buf, "run_steady: divergence detected at p=%d iteration %ld (residual %f)",
+                      sp->degree, iter, r);
+        throw Status(CDG_GPU_ERR_NUMERICS, buf);
+      }
+      if (sp->fixed_iterations > 0) {
+        if (iter >= sp->fixed_iterations) done = true;
+      } else if (r < sp->tolerance) {
+        done = true;
+        *converged = 1;
+      }
+      if (!done && sp->dt_override <= 0.0) ok(cdg_gpu_timestep(lv, cfg, cfg->visc_enabled ? 1 : 0, &dt, err, errlen));
+    }
+  });
+}
+
 // ---- multi-GPU halo plumbing -------------------------------------------------
 int cdg_gpu_halo_setup(cdg_gpu_level* lv, int n_send, const int* send_ef, int n_recv, const int* recv_ef,
                        double* send_buf, double* recv_buf) {

@@ -60,6 +60,13 @@ def run_config(riemann="llf", gamma=1.4, viscosity=None, cfl=0.5) -> RunConfig:
                      v["s0_offset"], v["indicator_component"], int(v["jacobian_weighted"]), cfl)
 
 
+class SteadyParams(C.Structure):
+    """cdg_gpu_steady_params: the RunConfig fields run_steady reads per level."""
+    _fields_ = [("max_iterations", C.c_long), ("fixed_iterations", C.c_long), ("check_interval", C.c_int),
+                ("residual_kind", C.c_int), ("tolerance", C.c_double), ("dt_override", C.c_double),
+                ("degree", C.c_int)]
+
+
 class LevelDesc(C.Structure):
     _fields_ = [("degree", C.c_int), ("n_basis", C.c_int), ("n_cub", C.c_int), ("n_face_quad", C.c_int),
                 ("n_elements", C.c_int), ("n_halo", C.c_int), ("padded", C.c_int),
@@ -114,6 +121,10 @@ def lib():
         L.cdg_gpu_last_profile.argtypes = [vp, _dp]
         L.cdg_gpu_version.restype = C.c_char_p
         L.cdg_gpu_measure_fp64_peak.argtypes = [C.c_int, _dp]
+        L.cdg_gpu_fill_freestream.argtypes = [vp]
+        L.cdg_gpu_p_refine_embed.argtypes = [vp, vp, _dp]
+        L.cdg_gpu_run_level.argtypes = [vp, C.POINTER(RunConfig), C.POINTER(SteadyParams), _dp, C.c_int, _ip, _ip,
+                                        C.c_char_p, C.c_size_t]
         _lib = L
     return _lib
 
@@ -304,6 +315,73 @@ class GpuLevel:
 
     def stream(self) -> int:
         return int(lib().cdg_gpu_stream(self.h) or 0)
+
+    # -- device-resident run_steady (solver.cpp:594-676) -------------------------
+    def fill_freestream(self):
+        _raise(lib().cdg_gpu_fill_freestream(self.h), "fill_freestream failed")
+
+    def p_refine_embed(self, src: "GpuLevel"):
+        """self.u = p_refine_embed(src.u) (solver.cpp:528-549)."""
+        e = embed_matrix(src.re, self.re)
+        _raise(lib().cdg_gpu_p_refine_embed(self.h, src.h, _p(e)), "p_refine_embed failed")
+
+    def run_level(self, cfg: RunConfig, params: SteadyParams, max_rows: int = 100000):
+        rows = np.zeros((max_rows, 3))
+        n = np.zeros(1, np.int32)
+        conv = np.zeros(1, np.int32)
+        err = C.create_string_buffer(1024)
+        st = lib().cdg_gpu_run_level(self.h, C.byref(cfg), C.byref(params), _p(rows), max_rows, _p(n), _p(conv),
+                                     err, 1024)
+        _raise(st, err.value.decode())
+        return rows[: min(int(n[0]), max_rows)], bool(conv[0])
+
+
+def embed_matrix(re_from: R.ReferenceElement, re_to: R.ReferenceElement) -> np.ndarray:
+    """p_refine_embed's matrix V_to[:, :np_from] V_from^-1 (solver.cpp:536-537)."""
+    if re_to.degree < re_from.degree:
+        raise ConfigError("p_refine_embed: target degree must not decrease")
+    return np.ascontiguousarray(re_to.vandermonde[:, : re_from.n_basis] @ re_from.vandermonde_inv)
+
+
+def run_steady(make_level, p_schedule, cfg: RunConfig, final_tolerance=1e-9, intermediate_tolerance=1e-4,
+               max_iterations=20000, fixed_iterations=(), check_interval=1000, residual="inf", dt_override=0.0,
+               on_row=None):
+    """run_steady (solver.cpp:594-676) with every level device-resident.
+
+    make_level(p) -> GpuLevel builds the level of degree p (host setup, as the
+    reference's DgLevel). Returns (rows [(level, iteration, dt, residual,
+    wall_seconds)], converged, final_degree, final level)."""
+    import time
+    if not p_schedule:
+        raise ConfigError("run_steady: empty p-schedule")
+    if any(b <= a for a, b in zip(p_schedule, p_schedule[1:])):
+        raise ConfigError("run_steady: p-schedule must be strictly increasing")
+    t0 = time.perf_counter()
+    rows, converged, prev = [], False, None
+    for li, p in enumerate(p_schedule):
+        lv = make_level(p)
+        if prev is None:
+            lv.fill_freestream()
+        else:
+            lv.p_refine_embed(prev)
+            prev.close()
+        last = li + 1 == len(p_schedule)
+        fixed = fixed_iterations[li] if li < len(fixed_iterations) else -1
+        sp = SteadyParams(max_iterations, fixed, check_interval, 1 if residual == "l2" else 0,
+                          final_tolerance if last else intermediate_tolerance, dt_override, p)
+        lrows, conv = lv.run_level(cfg, sp)
+        wall = time.perf_counter() - t0
+        for it, dt, r in lrows:
+            row = (p, int(it), float(dt), float(r), wall)
+            rows.append(row)
+            if on_row:
+                on_row(row)
+        if last:
+            converged = conv
+            if fixed > 0 and rows:
+                converged = rows[-1][3] < final_tolerance
+        prev = lv
+    return rows, converged, p_schedule[-1], prev
 
 
 def measure_fp64_peak(device: int = 0):

@@ -149,7 +149,12 @@ class LevelArrays:
         else:
             kinds = np.zeros((K, 4), np.int32)
             for tag_id, tag in enumerate(mesh.tags):
-                kinds[mesh.boundary_tag[:K] == tag_id] = BC_KINDS[bc[tag]] if isinstance(bc[tag], str) else bc[tag]
+                sel = mesh.boundary_tag[:K] == tag_id
+                if tag not in bc:
+                    if sel.any():  # validate_boundary_tags (cli_ops.cpp:80-91)
+                        raise ValueError(f"boundary tag '{tag}' has no boundary condition")
+                    continue
+                kinds[sel] = BC_KINDS[bc[tag]] if isinstance(bc[tag], str) else bc[tag]
         self.bc = np.ascontiguousarray(np.where(self.neighbor < 0, kinds, 0), np.int32)
         self.freestream = np.zeros(5) if freestream is None else np.asarray(freestream, float)
         self.curved_ids = None
