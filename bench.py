@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--p", type=int, default=P_DEFAULT)
     ap.add_argument("--n", type=int, default=N_DEFAULT, help="cube cells per side (6 n^3 tets)")
     ap.add_argument("--riemann", default="llf")
+    ap.add_argument("--cfl", type=float, default=0.5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -209,7 +210,7 @@ def main():
     t_setup = time.perf_counter()
     part = partition.rank_part(args.n, world, rank)
     lv = gpu.GpuLevel(part.mesh, p, bc=0, freestream=fs, re=re, device=local_rank)
-    cfg = gpu.run_config(args.riemann, cfl=0.5)
+    cfg = gpu.run_config(args.riemann, cfl=args.cfl)
     K = lv.K
     # random admissible state generated on the device (bench.cpp:22-40 recipe)
     g = torch.Generator(device="cuda").manual_seed(42 + rank)

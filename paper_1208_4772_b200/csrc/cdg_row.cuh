@@ -31,12 +31,15 @@ namespace cdg_gpu {
 
 // MODE bits: 1 operator ring (bulk-copy staged B fragments; else __ldg from
 // L1/L2), 2 U fragments register-resident for the whole tile (else reloaded
-// per chunk, which frees ~40 registers), 4 res staged to smem for the epilogue.
+// per chunk, which frees ~40 registers), 4 res staged to smem for the epilogue,
+// 8 U rows staged once per tile in smem by cp.async (GEMM1 A fragments and the
+// epilogue's old u come from there; excludes 2).
 template <int NP_, int NCUB_, int NG_, int CH_ = 8, int FCH_ = 32, int MINB_ = 3, int MODE_ = 7>
 struct RCfg {
   static constexpr int NP = NP_, NCUB = NCUB_, NG = NG_, NF = 4 * NG_;
   static constexpr int E = 16, R = 80, NW = 5, NTH = 160, MINB = MINB_;
-  static constexpr bool OPRING = MODE_ & 1, UREG = MODE_ & 2, RESS = MODE_ & 4;
+  static constexpr bool OPRING = MODE_ & 1, RESS = MODE_ & 4, USMEM = MODE_ & 8;
+  static constexpr bool UREG = (MODE_ & 2) && !USMEM;
   static constexpr int BP = round_up(NP, 16), TB = round_up(NF, 16);
   static constexpr int KP = round_up(NP, 8), KS1 = KP / 8, NT2 = KS1;
   static constexpr int NCUB8 = round_up(NCUB, 8), NF8 = round_up(NF, 8);
@@ -48,7 +51,11 @@ struct RCfg {
   static constexpr int LDF = frag_ld8(FCH);           // face-flux chunk
   // volume phase: one U_cub chunk (rewritten only after the barrier that
   // follows the pointwise pass) + two flux chunks (double buffer)
-  static constexpr int VOL = R * LDC + 2 * R * LDG;
+  // (single buffers suffice: PW(i+1) writes the flux chunk only after the
+  // barrier that follows GEMM1(i+1), which every warp reaches after GEMM2(i))
+  static constexpr int VOL = R * LDC + R * LDG;
+  static constexpr int LDU = frag_ld8(KP);
+  static constexpr int UPANEL = USMEM ? R * LDU : 0;  // doubles
   static constexpr int RES = RESS ? NTH * 2 * NT2 * 2 : 0;  // doubles: each thread's epilogue res values
   static constexpr int FACE = R * LDF + RES;              // doubles, face phase (aliases VOL)
   static constexpr int WORK = VOL > FACE ? VOL : FACE;
@@ -61,7 +68,7 @@ struct RCfg {
   static constexpr int OPF = (FCH / 8) * NT2 * 64;
   static constexpr int OPB = !OPRING ? 0 : (OPV > OPF ? OPV : OPF);
   static constexpr int NCHT = NCH + NFCH;  // operator chunks per tile
-  static constexpr size_t SMEM_BYTES = sizeof(double) * ((size_t)WORK + 2 * OPB + E * 9 + E * 4 * 4) +
+  static constexpr size_t SMEM_BYTES = sizeof(double) * ((size_t)WORK + UPANEL + 2 * OPB + E * 9 + E * 4 * 4) +
                                        sizeof(int) * (E * 4 * 2) + 2 * sizeof(unsigned long long);
 };
 
@@ -127,7 +134,8 @@ template <class C, bool UPDATE, int RM>
 __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_row(RhsParams p) {
   extern __shared__ __align__(16) double smem[];
   double* sWork = smem;
-  double* sOp = sWork + C::WORK;                                  // [2][OPB] operator chunks
+  double* sUp = sWork + C::WORK;                                  // [R][LDU] U rows (USMEM)
+  double* sOp = sUp + C::UPANEL;                                  // [2][OPB] operator chunks
   double* sMet = sOp + 2 * C::OPB;                                // [E][9]
   double4* sFace = reinterpret_cast<double4*>(sMet + C::E * 9);    // [E][4]
   int2* sConn = reinterpret_cast<int2*>(sFace + C::E * 4);         // [E][4]
@@ -187,6 +195,19 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_row(RhsParams p) {
       }
     };
     if (C::UREG) load_u();
+    if (C::USMEM) {
+      constexpr int V = C::KP / 2;  // 16-byte pieces per row
+      for (int idx = tid; idx < C::R * V; idx += C::NTH) {
+        const int r = idx / V, j = idx - r * V;
+        const bool ok = row0 + r < n_rows;
+        double* dst = sUp + r * C::LDU + 2 * j;
+        if (ok)
+          cp_async16_sh(dst, p.u + (size_t)(row0 + r) * C::BP + 2 * j);
+        else
+          *reinterpret_cast<double2*>(dst) = make_double2(0.0, 0.0);
+      }
+      cp_async_wait0();
+    }
     for (int idx = tid; idx < C::E * 9; idx += C::NTH)
       sMet[idx] = e0 + idx / 9 < p.K ? __ldg(p.metric + (size_t)e0 * 9 + idx) : 0.0;
     for (int idx = tid; idx < C::E * 4; idx += C::NTH) {
@@ -217,7 +238,7 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_row(RhsParams p) {
       const int q0 = ch * C::CH;
       const int w = (C::NCUB8 - q0) < C::CH ? (C::NCUB8 - q0) : C::CH;  // multiple of 8
       double* sC = sWork;
-      double* sG = sWork + C::R * C::LDC + (ch & 1) * (C::R * C::LDG);
+      double* sG = sWork + C::R * C::LDC;
       const double2 *fb1, *fb2;  // [CH/8][KS1][32], [3CH/8][NT2][32]
       if (C::OPRING) {
         fb1 = reinterpret_cast<const double2*>(sOp + (n & 1) * C::OPB);
@@ -227,20 +248,28 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_row(RhsParams p) {
         fb1 = reinterpret_cast<const double2*>(p.frag_icub) + (size_t)(q0 / 8) * C::KS1 * 32;
         fb2 = reinterpret_cast<const double2*>(p.frag_op2) + (size_t)(3 * q0 / 8) * C::NT2 * 32;
       }
-      if (!C::UREG) load_u();
+      if (!C::UREG && !C::USMEM) load_u();
       // GEMM1: U_cub[rows, q0:q0+w] for this warp's 16 rows
       {
         double c1[C::CH / 8][4];
 #pragma unroll
         for (int j = 0; j < C::CH / 8; ++j) c1[j][0] = c1[j][1] = c1[j][2] = c1[j][3] = 0.0;
 #pragma unroll
-        for (int ks = 0; ks < C::KS1; ++ks)
+        for (int ks = 0; ks < C::KS1; ++ks) {
+          double a0, a1, a2, a3;
+          if (C::USMEM) {
+            const AFrag a = load_afrag(sUp, C::LDU, warp * 16, ks * 8, g, tq);
+            a0 = a.a0, a1 = a.a1, a2 = a.a2, a3 = a.a3;
+          } else {
+            a0 = uA[ks][0], a1 = uA[ks][1], a2 = uA[ks][2], a3 = uA[ks][3];
+          }
 #pragma unroll
           for (int j = 0; j < C::CH / 8; ++j)
             if (j * 8 < w) {
               const double2 b = C::OPRING ? fb1[(j * C::KS1 + ks) * 32 + lane] : __ldg(fb1 + (j * C::KS1 + ks) * 32 + lane);
-              dmma_k8(c1[j], uA[ks][0], uA[ks][1], uA[ks][2], uA[ks][3], b.x, b.y);
+              dmma_k8(c1[j], a0, a1, a2, a3, b.x, b.y);
             }
+        }
 #pragma unroll
         for (int j = 0; j < C::CH / 8; ++j)
           if (j * 8 < w) {
@@ -387,7 +416,7 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_row(RhsParams p) {
       if (fc + 1 < C::NFCH) __syncthreads();
     }
     if (UPDATE && C::RESS) cp_async_wait0();
-    if (UPDATE && !C::UREG) load_u();  // old u for the update
+    if (UPDATE && !C::UREG && !C::USMEM) load_u();  // old u for the update
 
     // ---- epilogue: rhs -> (res, u) update or rhs store ---------------------------
     double a_c = 0.0, b_c = 0.0, dt = 0.0;
@@ -413,7 +442,13 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_row(RhsParams p) {
           const double n0 = a_c * rs.x + dt * r0, n1 = a_c * rs.y + dt * r1;
           *reinterpret_cast<double2*>(p.res + rowoff + col) = make_double2(n0, n1);
           // old u: the A fragment of k-step j holds (row, 8j+2t) / (row, 8j+2t+1)
-          const double u0 = hh ? uA[j][1] : uA[j][0], u1 = hh ? uA[j][3] : uA[j][2];
+          double u0, u1;
+          if (C::USMEM) {
+            const double2 uo = *reinterpret_cast<const double2*>(sUp + (warp * 16 + g + 8 * hh) * C::LDU + col);
+            u0 = uo.x, u1 = uo.y;
+          } else {
+            u0 = hh ? uA[j][1] : uA[j][0], u1 = hh ? uA[j][3] : uA[j][2];
+          }
           *reinterpret_cast<double2*>(p.u + rowoff + col) = make_double2(u0 + b_c * n0, u1 + b_c * n1);
         } else {
           *reinterpret_cast<double2*>(p.rhs_out + rowoff + col) = make_double2(r0, r1);

@@ -10,12 +10,10 @@ std::vector<KernelSet> kernel_sets_p4() {
       with_row<35, 70, 16, 8, 32, 4, 0>(make_set<35, 70, 16, 16, 24, 2, 64>()),
       with_row<35, 70, 56, 8, 32, 4, 0>(make_set<35, 70, 56, 16, 24, 2>()),
       // P=4 straight tuning variants, selected with CDG_KCFG=<n> (bench sweeps)
-      make_set<35, 70, 16, 16, 24, 2, 64>(), make_set<35, 70, 16, 16, 8, 4, 24, 5>(),
-      with_row<35, 70, 16, 8, 32, 3, 7>(make_set<35, 70, 16, 16, 24, 2, 64>()),
-      with_row<35, 70, 16, 8, 32, 4, 4>(make_set<35, 70, 16, 16, 24, 2, 64>()),
-      with_row<35, 70, 16, 8, 32, 3, 6>(make_set<35, 70, 16, 16, 24, 2, 64>()),
-      with_row<35, 70, 16, 8, 32, 3, 0>(make_set<35, 70, 16, 16, 24, 2, 64>()),
-      with_row<35, 70, 16, 8, 64, 3, 2>(make_set<35, 70, 16, 16, 24, 2, 64>())};
+      make_set<35, 70, 16, 16, 24, 2, 64>(),
+      with_rowp<35, 70, 16, 4, false>(make_set<35, 70, 16, 16, 24, 2, 64>()),
+      with_rowp<35, 70, 16, 4, true>(make_set<35, 70, 16, 16, 24, 2, 64>()),
+      with_rowp<35, 70, 16, 3, true>(make_set<35, 70, 16, 16, 24, 2, 64>())};
 }
 
 }  // namespace cdg_gpu
