@@ -255,6 +255,9 @@ def main():
     ext = torch.cuda.ExternalStream(lv.stream())
 
     def step_multi():
+        # per stage: traces + pack (phase 0) | NCCL halo exchange on NCCL's stream,
+        # overlapped with the interior tiles' RHS + update (phase 2) | the halo
+        # tiles after the traces land (phase 3)  (the paper's overlap)
         with torch.cuda.stream(ext):
             for stage in range(5):
                 lv.stage_phase(cfg, stage, 0, dt)
@@ -262,9 +265,11 @@ def main():
                 for peer, sb, rb in bufs:
                     ops.append(dist.P2POp(dist.isend, sb, peer))
                     ops.append(dist.P2POp(dist.irecv, rb, peer))
-                for w in dist.batch_isend_irecv(ops):
+                works = dist.batch_isend_irecv(ops)
+                lv.stage_phase(cfg, stage, 2, dt)
+                for w in works:
                     w.wait()
-                lv.stage_phase(cfg, stage, 1, dt)
+                lv.stage_phase(cfg, stage, 3, dt)
 
     def run_steps(n):
         if world > 1:

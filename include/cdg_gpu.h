@@ -207,7 +207,10 @@ int cdg_gpu_halo_pack(cdg_gpu_level *lv);
 int cdg_gpu_halo_unpack(cdg_gpu_level *lv);
 /* Runs one RK stage in split form for overlap: trace kernel, then (caller
  * exchanges halos) then RHS+update. phase 0 = traces + pack, phase 1 =
- * unpack + RHS + update for stage `stage`. */
+ * unpack + RHS + update for stage `stage`. Overlapped form: phase 2 = RHS +
+ * update of the interior tiles (no ghost neighbour; launch it while the halo
+ * exchange is in flight), phase 3 = unpack + RHS + update of the halo tiles
+ * (after the exchange). 0,1 and 0,2,3 give bitwise identical states. */
 int cdg_gpu_rk_stage_phase(cdg_gpu_level *lv, const cdg_gpu_run_config *cfg, int stage, int phase,
                            double dt, const double a[5], const double b[5], char *err,
                            size_t errlen);

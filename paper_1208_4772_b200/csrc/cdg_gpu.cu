@@ -170,6 +170,9 @@ struct cdg_gpu_level {
   bool use_warp = false;
   double* rfrag2 = nullptr;  // row kernel (its I_cub fragments are wfrag1)
   bool use_row = false;
+  const int* cur_tiles = nullptr;  // tile list of the next RHS launch (null: all)
+  std::vector<char> ghost_adjacent;  // [K] element has a ghost (halo) neighbour
+  int cur_n_list = 0;
   // curved elements
   int n_curved = 0;
   int* curved_ids = nullptr;
@@ -194,6 +197,9 @@ struct cdg_gpu_level {
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
   // halo
   int n_send = 0, n_recv = 0;
+  // interior / halo tile lists (E = 16 element tiles) for comm-compute overlap
+  int *d_tiles_int = nullptr, *d_tiles_halo = nullptr;
+  int n_tiles_int = 0, n_tiles_halo = 0;
   int *d_send_idx = nullptr, *d_recv_idx = nullptr;
   double *send_buf = nullptr, *recv_buf = nullptr;
   double freestream[5] = {0, 0, 0, 0, 0};
@@ -238,6 +244,8 @@ void launch_traces(cdg_gpu_level* lv, const double* u, double* traces) {
 
 RhsParams rhs_params(cdg_gpu_level* lv, int stage) {
   RhsParams p{};
+  p.tiles = lv->cur_tiles;
+  p.n_list = lv->cur_n_list;
   p.u = lv->u;
   p.res = lv->res;
   p.rhs_out = lv->rhs;
@@ -305,7 +313,10 @@ void launch_rhs_warp(cdg_gpu_level* lv, bool update, int stage) {
   w.elem_offset = 0;
   w.gas = lv->gas;
   w.err = lv->d_err;
-  const int tiles = (lv->K + 15) / 16;
+  w.tiles = lv->cur_tiles;
+  w.n_list = lv->cur_n_list;
+  const int tiles = lv->cur_tiles ? lv->cur_n_list : (lv->K + 15) / 16;
+  if (tiles == 0) return;
   const int ctas = std::max(1, std::min((tiles + lv->ks->warp_warps - 1) / lv->ks->warp_warps,
                                         lv->n_sms * lv->ks->warp_minb));
   const int rm = lv->gas.riemann == 1 ? 1 : 0;
@@ -321,7 +332,8 @@ void launch_rhs_row(cdg_gpu_level* lv, bool update, int stage) {
   p.frag_op2 = lv->rfrag2;
   const int rm = lv->gas.riemann == 1 ? 1 : 0;
   auto fn = update ? lv->ks->row_update[rm] : lv->ks->row_only[rm];
-  const int tiles = (lv->K + 15) / 16;
+  const int tiles = lv->cur_tiles ? lv->cur_n_list : (lv->K + 15) / 16;
+  if (tiles == 0) return;
   fn<<<std::max(1, std::min(tiles, lv->n_sms * lv->ks->row_minb)), 160, lv->ks->smem_row, lv->stream>>>(p);
   ++lv->launches;
   launch_curved(lv, update, stage);
@@ -337,7 +349,8 @@ void launch_rhs(cdg_gpu_level* lv, bool update, bool viscous, int stage) {
     return;
   }
   RhsParams p = rhs_params(lv, stage);
-  const int tiles = lv->n_tiles();
+  const int tiles = lv->cur_tiles ? lv->cur_n_list : lv->n_tiles();
+  if (tiles == 0) return;
   auto fn = viscous ? (update ? lv->ks->visc_rhs_update : lv->ks->visc_rhs_only)
                     : (update ? lv->ks->rhs_update : lv->ks->rhs_only);
   fn<<<lv->grid(tiles), lv->ks->nth, lv->ks->smem_rhs, lv->stream>>>(p);
@@ -645,6 +658,12 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
       }
     }
     if (codes.empty()) codes.assign(ng, 0);
+    if (lv->n_halo > 0) {
+      lv->ghost_adjacent.assign(K, 0);
+      for (int e = 0; e < K; ++e)
+        for (int f = 0; f < 4; ++f)
+          if (d->neighbor[(size_t)e * 4 + f] >= K) lv->ghost_adjacent[e] = 1;
+    }
     if (d->n_curved > 0) {
       if (!d->curved_ids || !d->curved_jwr || !d->curved_face || !d->curved_minv)
         throw Status(CDG_GPU_ERR_CONFIG, "curved elements need curved_ids/jwr/face/minv");
@@ -752,7 +771,8 @@ void cdg_gpu_level_destroy(cdg_gpu_level* lv) {
                   (void*)lv->frag_ig, (void*)lv->frag_aux, (void*)lv->wfrag1, (void*)lv->wfrag2v, (void*)lv->wfrag2f, (void*)lv->rfrag2,
                   (void*)lv->curved_ids, (void*)lv->curved_jwr, (void*)lv->curved_minv, (void*)lv->frag_opc,
                   (void*)lv->curved_vol, (void*)lv->curved_face, (void*)lv->d_coef, (void*)lv->d_err,
-                  (void*)lv->d_scratch, (void*)lv->d_send_idx, (void*)lv->d_recv_idx})
+                  (void*)lv->d_scratch, (void*)lv->d_send_idx, (void*)lv->d_recv_idx,
+                  (void*)lv->d_tiles_int, (void*)lv->d_tiles_halo})
     if (p) cudaFree(p);
   if (lv->h_coef) cudaFreeHost(lv->h_coef);
   if (lv->h_err) cudaFreeHost(lv->h_err);
@@ -1148,6 +1168,23 @@ int cdg_gpu_halo_setup(cdg_gpu_level* lv, int n_send, const int* send_ef, int n_
     lv->d_recv_idx = n_recv ? dev_upload(std::vector<int>(recv_ef, recv_ef + n_recv)) : nullptr;
     lv->send_buf = send_buf;  // caller-owned (e.g. NCCL-registered torch tensors)
     lv->recv_buf = recv_buf;
+    // interior tiles (no element with a ghost neighbour) run while the halo
+    // traces are in flight; halo tiles after they land (rk_stage_phase 2 / 3)
+    const int E = lv->use_row ? 16 : lv->ks->E;
+    const int nt = (lv->K + E - 1) / E;
+    std::vector<int> ti, th;
+    for (int t = 0; t < nt; ++t) {
+      bool halo = false;
+      for (int e = t * E; e < std::min(lv->K, (t + 1) * E) && !halo; ++e)
+        halo = !lv->ghost_adjacent.empty() && lv->ghost_adjacent[e];
+      (halo ? th : ti).push_back(t);
+    }
+    if (lv->d_tiles_int) cudaFree(lv->d_tiles_int);
+    if (lv->d_tiles_halo) cudaFree(lv->d_tiles_halo);
+    lv->d_tiles_int = dev_upload(ti);
+    lv->d_tiles_halo = dev_upload(th);
+    lv->n_tiles_int = (int)ti.size();
+    lv->n_tiles_halo = (int)th.size();
   });
 }
 
@@ -1193,12 +1230,31 @@ int cdg_gpu_rk_stage_phase(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, int
       if (lv->n_send)
         k_halo_copy<<<(lv->n_send + 7) / 8, 256, 0, lv->stream>>>(lv->traces, lv->send_buf, lv->d_send_idx,
                                                                    lv->n_send, lv->ng, lv->tb, 0);
-    } else {
+    } else if (phase == 1) {
       if (lv->n_recv)
         k_halo_copy<<<(lv->n_recv + 7) / 8, 256, 0, lv->stream>>>(lv->traces, lv->recv_buf, lv->d_recv_idx,
                                                                    lv->n_recv, lv->ng, lv->tb, 1);
       launch_rhs(lv, true, false, stage);
       if (stage == 4) check_device_error(lv);
+    } else {
+      // 2: interior tiles (overlaps the halo exchange); 3: unpack + halo tiles
+      if (lv->n_curved) throw Status(CDG_GPU_ERR_CONFIG, "split interior/halo phases need an affine level");
+      if (phase == 3 && lv->n_recv)
+        k_halo_copy<<<(lv->n_recv + 7) / 8, 256, 0, lv->stream>>>(lv->traces, lv->recv_buf, lv->d_recv_idx,
+                                                                   lv->n_recv, lv->ng, lv->tb, 1);
+      if (!lv->d_tiles_int && !lv->d_tiles_halo) throw Status(CDG_GPU_ERR_CONFIG, "phases 2/3 need halo_setup");
+      lv->cur_tiles = phase == 2 ? lv->d_tiles_int : lv->d_tiles_halo;
+      lv->cur_n_list = phase == 2 ? lv->n_tiles_int : lv->n_tiles_halo;
+      if (!lv->cur_tiles) lv->cur_tiles = phase == 2 ? lv->d_tiles_halo : lv->d_tiles_int;  // empty list
+      try {
+        launch_rhs(lv, true, false, stage);
+      } catch (...) {
+        lv->cur_tiles = nullptr;
+        throw;
+      }
+      lv->cur_tiles = nullptr;
+      lv->cur_n_list = 0;
+      if (phase == 3 && stage == 4) check_device_error(lv);
     }
     CUDA_OK(cudaGetLastError());
   });

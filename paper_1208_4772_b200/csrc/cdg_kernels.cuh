@@ -392,7 +392,12 @@ struct RhsParams {
   const double* icub;         // [NCUB][NP] row-major (viscous volume term)
   size_t qtr_stride;          // elements per direction of qtr
   int prefetch;               // L2 prefetch mask: 1 res, 2 next-tile u, 4 own traces, 8 neighbour traces
+  const int* tiles;           // optional tile list (multi-GPU interior / halo split); null = all tiles
+  int n_list;                 // entries of `tiles`
 };
+
+// i-th tile of a launch: the tile list when given, else tile i
+__device__ __forceinline__ int tile_at(const RhsParams& p, int i) { return p.tiles ? __ldg(p.tiles + i) : i; }
 
 __device__ __forceinline__ void l2_prefetch(const void* ptr) { asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr)); }
 
@@ -548,7 +553,9 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs(RhsParams p) {
   const int t_begin = (warp * C::T2) / C::NW, t_end = ((warp + 1) * C::T2) / C::NW;
 
   __shared__ int s_stop;
-  for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+  const int n_iter = p.tiles ? p.n_list : p.n_tiles;
+  for (int it_t = blockIdx.x; it_t < n_iter; it_t += gridDim.x) {
+    const int tile = tile_at(p, it_t);
     // block-uniform early exit after a recorded error (no divergent barriers)
     if (tid == 0) s_stop = *(volatile int*)&p.err->flag;
     __syncthreads();

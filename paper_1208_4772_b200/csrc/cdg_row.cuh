@@ -148,7 +148,8 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_row(RhsParams p) {
   const int n_tiles = (p.K + C::E - 1) / C::E;
   __shared__ int s_stop;
   // operator chunk pipeline: chunk n of this CTA lives in buffer n & 1
-  const int my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int n_iter = p.tiles ? p.n_list : n_tiles;
+  const int my_tiles = blockIdx.x < n_iter ? (n_iter - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int n_chunks = my_tiles * C::NCHT;
   int n = 0;  // current chunk
   if (C::OPRING) {
@@ -161,7 +162,8 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_row(RhsParams p) {
     if (tid == 0 && n_chunks > 0) issue_op_chunk<C>(0, sOp, bars, p.frag_icub, p.frag_op2);
   }
 
-  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+  for (int it_t = blockIdx.x; it_t < n_iter; it_t += gridDim.x) {
+    const int tile = tile_at(p, it_t);
     // block-uniform early exit after a recorded error (no divergent barriers)
     if (tid == 0) s_stop = *(volatile int*)&p.err->flag;
     __syncthreads();

@@ -64,7 +64,9 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_rowp(RhsParams p) {
   const double2* fb2g = reinterpret_cast<const double2*>(p.frag_op2);   // [KS2][NT2][32]
   __shared__ int s_stop;
 
-  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+  const int n_iter = p.tiles ? p.n_list : n_tiles;
+  for (int it_t = blockIdx.x; it_t < n_iter; it_t += gridDim.x) {
+    const int tile = tile_at(p, it_t);
     if (tid == 0) s_stop = *(volatile int*)&p.err->flag;
     __syncthreads();
     if (s_stop) return;

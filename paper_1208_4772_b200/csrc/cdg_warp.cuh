@@ -82,6 +82,8 @@ struct WarpParams {
   int elem_offset;
   GasParams gas;
   DevError* err;
+  const int* tiles;  // optional 16-element tile list (multi-GPU interior / halo split)
+  int n_list;
 };
 
 template <class C, bool UPDATE, int RIEMANN>
@@ -95,7 +97,9 @@ __global__ void __launch_bounds__(32 * C::WARPS, C::MINB) k_rhs_warp(WarpParams 
   const int n_tiles = (p.K + C::EW - 1) / C::EW;
   const int warps_total = gridDim.x * C::WARPS;
 
-  for (int tile = blockIdx.x * C::WARPS + warp; tile < n_tiles; tile += warps_total) {
+  const int n_iter = p.tiles ? p.n_list : n_tiles;
+  for (int it_t = blockIdx.x * C::WARPS + warp; it_t < n_iter; it_t += warps_total) {
+    const int tile = p.tiles ? __ldg(p.tiles + it_t) : it_t;
     if (*(volatile int*)&p.err->flag) return;  // warp-uniform: no barrier to desynchronise
     const int e0 = tile * C::EW;
     // ---- stage U (rows (c, e), natural node order) + metrics ----------------
@@ -112,7 +116,7 @@ __global__ void __launch_bounds__(32 * C::WARPS, C::MINB) k_rhs_warp(WarpParams 
         sMet[idx] = (e0 + idx / 9 < p.K) ? __ldg(p.metric + (size_t)e0 * 9 + idx) : 0.0;
       // next tile of this warp -> L2 while this one computes
       const int nt_e0 = (tile + warps_total) * C::EW;
-      if (nt_e0 < p.K) {
+      if (!p.tiles && nt_e0 < p.K) {
         const char* base = reinterpret_cast<const char*>(p.u + (size_t)nt_e0 * 5 * C::BP);
         const int bytes = min(C::EW, p.K - nt_e0) * 5 * C::BP * 8;
         for (int off = lane * 128; off < bytes; off += 32 * 128) prefetch_l2(base + off);
