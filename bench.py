@@ -365,7 +365,8 @@ def main():
         peak = max(fp64_dmma, fp64_dfma, fp64_k8, fp64_k16)
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": traffic,
-                "kernel": f"k_rhs<P={p}> (fused volume+surface+lift+LSRK update, FP64 DMMA)",
+                "kernel": (f"k_rhs_row<P={p}> (fused volume+surface+lift+LSRK update, FP64 DMMA, one m-tile row per warp)"
+                           if p == 4 else f"RHS+update kernel <P={p}> (fused volume+surface+lift+LSRK update, FP64 DMMA)"),
                 "algorithmic_flops_per_launch": F_rhs * K,
                 "peak_source": "max of the FP64 DMMA (m16n8k4/k8/k16) and DFMA peaks measured live on this "
                                "GPU by cdg_gpu_measure_fp64_peak (the kernel uses DMMA m16n8k8); "

@@ -330,6 +330,10 @@ void launch_rhs_row(cdg_gpu_level* lv, bool update, int stage) {
   RhsParams p = rhs_params(lv, stage);
   p.frag_icub = lv->wfrag1;
   p.frag_op2 = lv->rfrag2;
+  // L2 prefetching measured neutral-to-negative for the row kernel (4 CTAs/SM
+  // already cover the latency; profiles/r1); it stays on for the CTA kernel
+  static const int pf_row = std::getenv("CDG_PREFETCH_ROW") ? std::atoi(std::getenv("CDG_PREFETCH_ROW")) : 0;
+  p.prefetch = pf_row;
   const int rm = lv->gas.riemann == 1 ? 1 : 0;
   auto fn = update ? lv->ks->row_update[rm] : lv->ks->row_only[rm];
   const int tiles = lv->cur_tiles ? lv->cur_n_list : (lv->K + 15) / 16;

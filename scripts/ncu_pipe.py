@@ -15,7 +15,8 @@ raw = list(csv.reader(open(sys.argv[2])))
 d = dict(zip(raw[0], raw[2]))
 dur = float(d["gpu__time_duration.sum"].replace(",", ""))  # ns or us per unit row
 unit = raw[1][raw[0].index("gpu__time_duration.sum")]
-dur_s = dur * {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3}.get(unit, 1e-9)
+dur_s = dur * {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "ns": 1e-9, "us": 1e-6, "ms": 1e-3,
+               "s": 1.0}.get(unit, 1e-9)
 clk = float(d.get("smsp__cycles_elapsed.avg.per_second", "0").replace(",", "") or 0)
 nsm = 148
 dmma = sum(v for k, v in cnt.items() if k.startswith("DMMA"))
