@@ -114,6 +114,13 @@ typedef struct cdg_gpu_level_desc {
   const double *curved_jwr;      /* [Kc][N_cub][9] cub_jac*W*cub_dr (m*3+d) */
   const double *curved_face;     /* [Kc][4N_g][4] face_normal xyz, face_sjac*w */
   const double *curved_minv;     /* [Kc][N_p][N_p] (I_cub^T diag(JW) I_cub)^-1 */
+
+  /* Physical-space (J-weighted) smoothness indicator, viscosity.cpp:28-45
+   * (ViscosityModel::jacobian_weighted). Both may be NULL when that option is
+   * never used: modal_cub defaults to I_cub * (V^-1)^-1 and curved_jac is
+   * then required only for curved levels. */
+  const double *modal_cub;       /* [N_cub][N_p] modal_basis_eval(p, cub_nodes) (refelem.hpp:21) */
+  const double *curved_jac;      /* [Kc][N_cub] cub_jac of the curved elements */
 } cdg_gpu_level_desc;
 
 typedef struct cdg_gpu_level cdg_gpu_level;

@@ -69,7 +69,7 @@ cdg_gpu_level* create_level(const DgLevel& level, const ConservedState& fs) {
   std::vector<int> nb(4 * (size_t)K), nbf(4 * (size_t)K), bc(4 * (size_t)K), nmap(4 * (size_t)K * ng);
   // curved (isoparametric) elements: per-node geometry + M_e^-1
   std::vector<int> cids;
-  std::vector<double> cjwr, cface, cminv;
+  std::vector<double> cjwr, cface, cminv, cjac;
   for (int e = 0; e < K; ++e) {
     const auto& g = level.geom(e);
     bool curved = false;
@@ -80,6 +80,7 @@ cdg_gpu_level* create_level(const DgLevel& level, const ConservedState& fs) {
     }
     if (curved) {
       cids.push_back(e);
+      for (int q = 0; q < ncub; ++q) cjac.push_back(g.cub_jac[q]);
       for (int q = 0; q < ncub; ++q)
         for (int k = 0; k < 9; ++k) cjwr.push_back(g.cub_jac[q] * re.cub_weights()[q] * g.cub_dr[q][k]);
       for (int q = 0; q < 4 * ng; ++q) {
@@ -149,6 +150,10 @@ cdg_gpu_level* create_level(const DgLevel& level, const ConservedState& fs) {
   d.curved_jwr = cjwr.data();
   d.curved_face = cface.data();
   d.curved_minv = cminv.data();
+  d.curved_jac = cjac.data();
+  // modal basis at the cubature nodes: the J-weighted indicator's V_cub (viscosity.cpp:35)
+  const std::vector<double> vcub = row_major(modal_basis_eval(re.degree(), re.cub_nodes()));
+  d.modal_cub = vcub.data();
   cdg_gpu_level* lv = nullptr;
   char err[512] = {0};
   throw_status(cdg_gpu_level_create(&d, 0, &lv, err, sizeof err), err);

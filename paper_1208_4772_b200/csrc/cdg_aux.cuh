@@ -19,7 +19,23 @@ struct SensorParams {
   unsigned long long* maxeps;  // bit pattern of max eps (non-negative doubles)
   int K, np, np_prev, bp, comp;
   double eps0, kappa, s0;
+  // J-weighted variant (viscosity.cpp:28-45)
+  const double* vcub;       // [ncub][np] modal basis at the cubature nodes
+  const double* wcub;       // [ncub]
+  const double* jac;        // [K] affine cub_jac
+  const int* curved_slot;   // [K] index into curved_jac or -1 (may be null)
+  const double* curved_jac; // [Kc][ncub]
+  int ncub;
 };
+
+// viscosity_amount (viscosity.cpp:48-56) of the indicator value sk_val
+__device__ __forceinline__ double viscosity_ramp(double sk_val, const SensorParams& p) {
+  if (!(sk_val > 0.0)) return 0.0;
+  const double sk = log10(sk_val);
+  if (sk < p.s0 - p.kappa) return 0.0;
+  if (sk > p.s0 + p.kappa) return p.eps0;
+  return 0.5 * p.eps0 * (1.0 + sin(M_PI * (sk - p.s0) / (2.0 * p.kappa)));
+}
 
 #ifndef CDG_SET_TU  // non-template kernels: defined once, in cdg_gpu.cu
 __global__ void __launch_bounds__(256) k_sensor(SensorParams p) {
@@ -42,17 +58,51 @@ __global__ void __launch_bounds__(256) k_sensor(SensorParams p) {
     top += __shfl_xor_sync(0xffffffffu, top, off);
   }
   if (lane == 0) {
-    const double sk_val = total <= 0.0 ? 0.0 : top / total;
-    double eps = 0.0;
-    if (sk_val > 0.0) {
-      const double sk = log10(sk_val);
-      if (sk < p.s0 - p.kappa)
-        eps = 0.0;
-      else if (sk > p.s0 + p.kappa)
-        eps = p.eps0;
-      else
-        eps = 0.5 * p.eps0 * (1.0 + sin(M_PI * (sk - p.s0) / (2.0 * p.kappa)));
+    const double eps = viscosity_ramp(total <= 0.0 ? 0.0 : top / total, p);
+    p.eps[e] = eps;
+    p.sqrt_eps[e] = sqrt(eps);
+    atomicMax(p.maxeps, (unsigned long long)__double_as_longlong(eps));
+  }
+}
+
+// Physical-space indicator (viscosity.cpp:28-45): modal = V^-1 u,
+// u_q = Vc modal, ut_q = Vc modal_trunc, S = sum JW (u-ut)^2 / sum JW u^2.
+// One warp per element; the modal vector goes through shared memory.
+__global__ void __launch_bounds__(256) k_sensor_jw(SensorParams p) {
+  __shared__ double s_modal[8][176];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int e = blockIdx.x * 8 + wib;
+  if (e >= p.K) return;
+  const double* f = p.u + ((size_t)e * 5 + p.comp) * p.bp;
+  for (int j = lane; j < p.np; j += 32) {
+    double m = 0.0;
+    const double* row = p.vinv + (size_t)j * p.np;
+    for (int i = 0; i < p.np; ++i) m += __ldg(row + i) * f[i];
+    s_modal[wib][j] = m;
+  }
+  __syncwarp();
+  const int slot = p.curved_slot ? p.curved_slot[e] : -1;
+  double num = 0.0, den = 0.0;
+  for (int q = lane; q < p.ncub; q += 32) {
+    const double* vr = p.vcub + (size_t)q * p.np;
+    double uq = 0.0, ut = 0.0;
+    for (int j = 0; j < p.np; ++j) {
+      const double v = __ldg(vr + j) * s_modal[wib][j];
+      uq += v;
+      if (j < p.np_prev) ut += v;
     }
+    const double jq = slot >= 0 ? p.curved_jac[(size_t)slot * p.ncub + q] : p.jac[e];
+    const double jw = p.wcub[q] * jq;
+    num += jw * (uq - ut) * (uq - ut);
+    den += jw * uq * uq;
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    num += __shfl_xor_sync(0xffffffffu, num, off);
+    den += __shfl_xor_sync(0xffffffffu, den, off);
+  }
+  if (lane == 0) {
+    const double eps = viscosity_ramp(den <= 0.0 ? 0.0 : num / den, p);
     p.eps[e] = eps;
     p.sqrt_eps[e] = sqrt(eps);
     atomicMax(p.maxeps, (unsigned long long)__double_as_longlong(eps));

@@ -103,6 +103,38 @@ std::vector<double> spd_inverse(const std::vector<double>& m, int n) {
   return inv;
 }
 
+// General dense inverse (Gauss-Jordan with partial pivoting), setup only.
+std::vector<double> dense_inverse(std::vector<double> a, int n) {
+  std::vector<double> inv((size_t)n * n, 0.0);
+  for (int i = 0; i < n; ++i) inv[(size_t)i * n + i] = 1.0;
+  for (int c = 0; c < n; ++c) {
+    int piv = c;
+    for (int r = c + 1; r < n; ++r)
+      if (std::fabs(a[(size_t)r * n + c]) > std::fabs(a[(size_t)piv * n + c])) piv = r;
+    if (a[(size_t)piv * n + c] == 0.0) throw Status(CDG_GPU_ERR_NUMERICS, "singular Vandermonde inverse");
+    if (piv != c)
+      for (int k = 0; k < n; ++k) {
+        std::swap(a[(size_t)c * n + k], a[(size_t)piv * n + k]);
+        std::swap(inv[(size_t)c * n + k], inv[(size_t)piv * n + k]);
+      }
+    const double d = 1.0 / a[(size_t)c * n + c];
+    for (int k = 0; k < n; ++k) {
+      a[(size_t)c * n + k] *= d;
+      inv[(size_t)c * n + k] *= d;
+    }
+    for (int r = 0; r < n; ++r)
+      if (r != c) {
+        const double m = a[(size_t)r * n + c];
+        if (m == 0.0) continue;
+        for (int k = 0; k < n; ++k) {
+          a[(size_t)r * n + k] -= m * a[(size_t)c * n + k];
+          inv[(size_t)r * n + k] -= m * inv[(size_t)c * n + k];
+        }
+      }
+  }
+  return inv;
+}
+
 // B-operand fragments for mma.m16n8k8 (.col): frag[nt][ks][lane] = the pair
 // (op[nt*8 + lane/4][ks*8 + lane%4], op[nt*8 + lane/4][ks*8 + lane%4 + 4]),
 // zero outside [rows x cols]: one coalesced 16-byte load per thread per step.
@@ -155,6 +187,9 @@ struct cdg_gpu_level {
   // viscous workspace
   double *q = nullptr, *qtr = nullptr, *eps = nullptr, *sqrt_eps = nullptr;
   double* d_vinv = nullptr;
+  // J-weighted indicator (viscosity.cpp:28-45)
+  double *d_vcub = nullptr, *d_wcub = nullptr, *d_jac = nullptr, *d_curved_jac = nullptr;
+  int* d_curved_slot = nullptr;
   double* d_icub = nullptr;  // row-major I_cub (viscous volume term)
   unsigned long long* d_maxeps = nullptr;
   bool last_viscous = false;
@@ -367,8 +402,10 @@ void launch_rhs(cdg_gpu_level* lv, bool update, bool viscous, int stage) {
 bool viscosity_phase(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg) {
   if (!cfg->visc_enabled) return false;
   if (cfg->eps0 < 0.0) throw Status(CDG_GPU_ERR_CONFIG, "viscosity_amount: eps0 must be >= 0");
-  if (cfg->jacobian_weighted)
-    throw Status(CDG_GPU_ERR_CONFIG, "jacobian_weighted indicator is not supported on the GPU path");
+  if (cfg->jacobian_weighted && lv->n_curved && !lv->d_curved_jac)
+    throw Status(CDG_GPU_ERR_CONFIG, "jacobian_weighted indicator on curved elements needs curved_jac");
+  if (cfg->jacobian_weighted && !lv->d_vcub)
+    throw Status(CDG_GPU_ERR_CONFIG, "jacobian_weighted indicator needs vandermonde_inv");
   if (!lv->q) {
     const size_t n = (size_t)lv->K * 5 * lv->bp;
     const size_t nt = (size_t)(lv->K + lv->n_halo) * 5 * lv->tb;
@@ -392,7 +429,17 @@ bool viscosity_phase(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg) {
   sp.eps0 = cfg->eps0;
   sp.kappa = cfg->kappa;
   sp.s0 = std::log10(1.0 / std::pow((double)lv->degree, 4)) + cfg->s0_offset;
-  k_sensor<<<(lv->K + 7) / 8, 256, 0, lv->stream>>>(sp);
+  if (cfg->jacobian_weighted) {
+    sp.vcub = lv->d_vcub;
+    sp.wcub = lv->d_wcub;
+    sp.jac = lv->d_jac;
+    sp.curved_slot = lv->d_curved_slot;
+    sp.curved_jac = lv->d_curved_jac;
+    sp.ncub = lv->ncub;
+    k_sensor_jw<<<(lv->K + 7) / 8, 256, 0, lv->stream>>>(sp);
+  } else {
+    k_sensor<<<(lv->K + 7) / 8, 256, 0, lv->stream>>>(sp);
+  }
   ++lv->launches;
   unsigned long long bits = 0;
   CUDA_OK(cudaMemcpyAsync(&bits, lv->d_maxeps, sizeof bits, cudaMemcpyDeviceToHost, lv->stream));
@@ -609,8 +656,27 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
       const char* nw = std::getenv("CDG_NOWARP");
       lv->use_warp = lv->ks->warp_update[0] && !(nw && std::atoi(nw));
     }
-    if (d->vandermonde_inv)
+    if (d->vandermonde_inv) {
       lv->d_vinv = dev_upload(std::vector<double>(d->vandermonde_inv, d->vandermonde_inv + (size_t)np * np));
+      // modal basis at the cubature nodes for the J-weighted indicator:
+      // the caller's modal_basis_eval table, else I_cub (V^-1)^-1
+      std::vector<double> vcub;
+      if (d->modal_cub) {
+        vcub.assign(d->modal_cub, d->modal_cub + (size_t)ncub * np);
+      } else {
+        const std::vector<double> v = dense_inverse(std::vector<double>(d->vandermonde_inv,
+                                                                        d->vandermonde_inv + (size_t)np * np), np);
+        vcub.assign((size_t)ncub * np, 0.0);
+        for (int q = 0; q < ncub; ++q)
+          for (int j = 0; j < np; ++j) {
+            double s = 0.0;
+            for (int i = 0; i < np; ++i) s += icub[(size_t)q * np + i] * v[(size_t)i * np + j];
+            vcub[(size_t)q * np + j] = s;
+          }
+      }
+      lv->d_vcub = dev_upload(vcub);
+      lv->d_wcub = dev_upload(std::vector<double>(d->cub_weights, d->cub_weights + ncub));
+    }
 
     // ---- per-element geometry + coupling -----------------------------------
     std::vector<double> met(d->metric, d->metric + (size_t)K * 9);
@@ -703,6 +769,18 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
       // epilogue scratch for configurations whose vol panel does not fit smem (p=8)
       CUDA_OK(cudaMalloc(&lv->curved_vol, sizeof(double) * (size_t)d->n_curved * 5 * (np8 + 1)));
     }
+    {
+      std::vector<double> jv(K);
+      for (int e = 0; e < K; ++e) jv[e] = is_curved[e] ? 1.0 : d->jac[e];
+      lv->d_jac = dev_upload(jv);
+      if (d->n_curved > 0) {
+        std::vector<int> slot(K, -1);
+        for (int i = 0; i < d->n_curved; ++i) slot[d->curved_ids[i]] = i;
+        lv->d_curved_slot = dev_upload(slot);
+        if (d->curved_jac)
+          lv->d_curved_jac = dev_upload(std::vector<double>(d->curved_jac, d->curved_jac + (size_t)d->n_curved * ncub));
+      }
+    }
     lv->metric = dev_upload(met);
     lv->face = dev_upload(face);
     lv->conn = dev_upload(conn);
@@ -769,7 +847,8 @@ void cdg_gpu_level_destroy(cdg_gpu_level* lv) {
   cudaSetDevice(lv->device);
   if (lv->graph) cudaGraphExecDestroy(lv->graph);
   for (void* p : {(void*)lv->u, (void*)lv->res, (void*)lv->rhs, (void*)lv->traces, (void*)lv->before,
-                  (void*)lv->q, (void*)lv->qtr, (void*)lv->eps, (void*)lv->sqrt_eps, (void*)lv->d_vinv,
+                  (void*)lv->q, (void*)lv->qtr, (void*)lv->eps, (void*)lv->sqrt_eps, (void*)lv->d_vinv, (void*)lv->d_vcub, (void*)lv->d_wcub, (void*)lv->d_jac,
+                  (void*)lv->d_curved_jac, (void*)lv->d_curved_slot,
                   (void*)lv->d_icub, (void*)lv->d_maxeps, (void*)lv->metric, (void*)lv->face, (void*)lv->conn,
                   (void*)lv->code_map, (void*)lv->h, (void*)lv->frag_icub, (void*)lv->frag_op2,
                   (void*)lv->frag_ig, (void*)lv->frag_aux, (void*)lv->wfrag1, (void*)lv->wfrag2v, (void*)lv->wfrag2f, (void*)lv->rfrag2,

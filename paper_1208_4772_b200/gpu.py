@@ -77,7 +77,7 @@ class LevelDesc(C.Structure):
                 ("face_code", _ip), ("code_node_map", _ip), ("n_codes", C.c_int),
                 ("freestream", C.c_double * 5),
                 ("n_curved", C.c_int), ("curved_ids", _ip), ("curved_jwr", _dp), ("curved_face", _dp),
-                ("curved_minv", _dp)]
+                ("curved_minv", _dp), ("modal_cub", _dp), ("curved_jac", _dp)]
 
 
 _lib = None
@@ -182,6 +182,8 @@ class GpuLevel:
             d.n_curved = len(a.curved_ids)
             d.curved_ids, d.curved_jwr = _p(a.curved_ids), _p(a.curved_jwr)
             d.curved_face, d.curved_minv = _p(a.curved_face), _p(a.curved_minv)
+            d.curved_jac = _p(a.curved_jac)
+        d.modal_cub = _p(t["modal_cub"])
         self._desc = d
         h = C.c_void_p()
         err = C.create_string_buffer(1024)

@@ -21,7 +21,7 @@ from __future__ import annotations
 import numpy as np
 
 from .mesh import PERMS, Mesh
-from .refelem import FACE_VERTS, TET_VERTS, ReferenceElement, pad16, tri_quadrature
+from .refelem import FACE_VERTS, TET_VERTS, ReferenceElement, modal_basis_eval, pad16, tri_quadrature
 
 BC_KINDS = {"slip_wall": 0, "wall": 0, "farfield": 1, "symmetry": 2}
 
@@ -90,7 +90,8 @@ def curved_geometry(nodes: np.ndarray, re: ReferenceElement):
     mass = np.einsum("qi,kq,qj->kij", re.interp_cub, jw, re.interp_cub)
     minv = np.linalg.inv(mass)
     h = 6.0 * jw.sum(axis=1) / area
-    return np.ascontiguousarray(jwr), np.ascontiguousarray(face), np.ascontiguousarray(minv), h
+    return np.ascontiguousarray(jwr), np.ascontiguousarray(face), np.ascontiguousarray(minv), h, \
+        np.ascontiguousarray(jac)
 
 
 def perm_node_maps(re: ReferenceElement) -> np.ndarray:
@@ -161,8 +162,10 @@ class LevelArrays:
         if curved is not None and len(curved[0]):
             ids = np.ascontiguousarray(curved[0], np.int32)
             self.curved_ids = ids
-            self.curved_jwr, self.curved_face, self.curved_minv, hc = curved_geometry(curved[1], re)
+            self.curved_jwr, self.curved_face, self.curved_minv, hc, self.curved_jac = curved_geometry(curved[1], re)
             self.h[ids] = hc
         self.tables = {k: np.ascontiguousarray(getattr(re, k)) for k in
                        ("interp_cub", "interp_face", "deriv_r", "deriv_s", "deriv_t", "cub_weights",
                         "face_weights", "vandermonde_inv")}
+        # modal basis at the cubature nodes (refelem.hpp:21), J-weighted indicator
+        self.tables["modal_cub"] = np.ascontiguousarray(modal_basis_eval(re.degree, re.cub_nodes))

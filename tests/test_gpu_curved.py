@@ -115,3 +115,23 @@ def test_curved_sphere_viscous_matches_reference(gpu_lib, refmod, p, visc, riem)
     lv.rk_steps(gpu.run_config(riem, viscosity=visc), dt, 2)
     u_ref, _ = rl.rk_steps(u, np.zeros_like(u), cfg_r, fs, dt, 2)
     assert rel(lv.get_state()[0], u_ref) < 1e-12
+
+
+@pytest.mark.parametrize("p", [2, 3])
+def test_curved_sphere_jacobian_weighted_indicator(gpu_lib, refmod, p):
+    """The physical-space (J-weighted) smoothness indicator (viscosity.cpp:28-45,
+    ViscosityModel::jacobian_weighted) with per-node Jacobians on the curved
+    elements, against the reference."""
+    gpu, ref = gpu_lib, refmod
+    rm, rl, mesh, ids, nodes = sphere_case(ref, p)
+    fs = _fs(gpu)
+    lv = gpu.GpuLevel(mesh, p, bc={"sphere": 0, "farfield": 1}, freestream=fs, curved=(ids, nodes[ids]))
+    visc = dict(VISC_RAMP, jacobian_weighted=True, s0_offset=1.0)
+    u = rl.random_admissible_store(13)
+    r_ref = rl.compute_rhs(u, ref.make_cfg("llf", viscosity=visc), fs)
+    eps_ref, _ = rl.last_viscosity(with_q=False)
+    r_gpu = lv.compute_rhs(gpu.run_config("llf", viscosity=visc), u)
+    eps = lv.viscosity()
+    assert (eps_ref > 0).any()
+    assert np.allclose(eps, eps_ref, rtol=1e-10, atol=1e-14)
+    assert rel(r_gpu, r_ref) < 1e-10
