@@ -9,11 +9,15 @@ std::vector<KernelSet> kernel_sets_p4() {
   return {
       with_row<35, 70, 16, 8, 32, 4, 0>(make_set<35, 70, 16, 16, 24, 2, 64>()),
       with_row<35, 70, 56, 8, 32, 4, 0>(make_set<35, 70, 56, 16, 24, 2>()),
-      // P=4 straight tuning variants, selected with CDG_KCFG=<n> (bench sweeps)
-      make_set<35, 70, 16, 16, 24, 2, 64>(),
-      with_rowp<35, 70, 16, 4, false>(make_set<35, 70, 16, 16, 24, 2, 64>()),
-      with_rowp<35, 70, 16, 4, true>(make_set<35, 70, 16, 16, 24, 2, 64>()),
-      with_rowp<35, 70, 16, 3, true>(make_set<35, 70, 16, 16, 24, 2, 64>())};
+      // P=4 straight tuning variants, selected with CDG_KCFG=<n> (bench sweeps;
+      // DESIGN.md §6 lists what each measured)
+      make_set<35, 70, 16, 16, 24, 2, 64>(),                                 // 1 CTA kernel, 8 warps
+      with_row<35, 70, 16, 16, 32, 4, 0>(make_set<35, 70, 16, 16, 24, 2, 64>()),  // 2 16-node chunks
+      with_row<35, 70, 16, 8, 32, 4, 1>(make_set<35, 70, 16, 16, 24, 2, 64>()),   // 3 operator ring
+      with_row<35, 70, 16, 8, 32, 4, 8>(make_set<35, 70, 16, 16, 24, 2, 64>()),   // 4 U staged in smem
+      with_row<35, 70, 16, 8, 32, 4, 4>(make_set<35, 70, 16, 16, 24, 2, 64>()),   // 5 res staged in smem
+      with_row<35, 70, 16, 8, 32, 3, 2>(make_set<35, 70, 16, 16, 24, 2, 64>()),   // 6 U in registers, 3 CTAs
+      with_rowp<35, 70, 16, 4, false>(make_set<35, 70, 16, 16, 24, 2, 64>())};    // 7 pipelined chunks
 }
 
 }  // namespace cdg_gpu
