@@ -371,9 +371,10 @@ void launch_rhs_row(cdg_gpu_level* lv, bool update, int stage) {
   p.prefetch = pf_row;
   const int rm = lv->gas.riemann == 1 ? 1 : 0;
   auto fn = update ? lv->ks->row_update[rm] : lv->ks->row_only[rm];
-  const int tiles = lv->cur_tiles ? lv->cur_n_list : (lv->K + 15) / 16;
+  const int E = lv->ks->row_e;
+  const int tiles = lv->cur_tiles ? lv->cur_n_list : (lv->K + E - 1) / E;
   if (tiles == 0) return;
-  fn<<<std::max(1, std::min(tiles, lv->n_sms * lv->ks->row_minb)), 160, lv->ks->smem_row, lv->stream>>>(p);
+  fn<<<std::max(1, std::min(tiles, lv->n_sms * lv->ks->row_minb)), lv->ks->row_nth, lv->ks->smem_row, lv->stream>>>(p);
   ++lv->launches;
   launch_curved(lv, update, stage);
 }
@@ -1253,7 +1254,7 @@ int cdg_gpu_halo_setup(cdg_gpu_level* lv, int n_send, const int* send_ef, int n_
     lv->recv_buf = recv_buf;
     // interior tiles (no element with a ghost neighbour) run while the halo
     // traces are in flight; halo tiles after they land (rk_stage_phase 2 / 3)
-    const int E = lv->use_row ? 16 : lv->ks->E;
+    const int E = lv->use_row ? lv->ks->row_e : lv->ks->E;
     const int nt = (lv->K + E - 1) / E;
     std::vector<int> ti, th;
     for (int t = 0; t < nt; ++t) {

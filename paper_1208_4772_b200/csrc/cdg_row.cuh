@@ -34,10 +34,11 @@ namespace cdg_gpu {
 // per chunk, which frees ~40 registers), 4 res staged to smem for the epilogue,
 // 8 U rows staged once per tile in smem by cp.async (GEMM1 A fragments and the
 // epilogue's old u come from there; excludes 2).
-template <int NP_, int NCUB_, int NG_, int CH_ = 8, int FCH_ = 32, int MINB_ = 3, int MODE_ = 7>
+template <int NP_, int NCUB_, int NG_, int CH_ = 8, int FCH_ = 32, int MINB_ = 3, int MODE_ = 7, int E_ = 16>
 struct RCfg {
   static constexpr int NP = NP_, NCUB = NCUB_, NG = NG_, NF = 4 * NG_;
-  static constexpr int E = 16, R = 80, NW = 5, NTH = 160, MINB = MINB_;
+  // E elements per tile (multiple of 16): 5E rows = 5E/16 m-tiles, one warp each
+  static constexpr int E = E_, R = 5 * E_, NW = R / 16, NTH = 32 * NW, MINB = MINB_;
   static constexpr bool OPRING = MODE_ & 1, RESS = MODE_ & 4, USMEM = MODE_ & 8;
   static constexpr bool UREG = (MODE_ & 2) && !USMEM;
   static constexpr int BP = round_up(NP, 16), TB = round_up(NF, 16);

@@ -39,12 +39,12 @@ struct KernelSet {
   void (*row_update[2])(RhsParams) = {nullptr, nullptr};  // [riemann]
   void (*row_only[2])(RhsParams) = {nullptr, nullptr};
   size_t smem_row = 0;
-  int row_minb = 0, row_ch = 0;
+  int row_minb = 0, row_ch = 0, row_e = 16, row_nth = 160;
 };
 
-template <int NP, int NCUB, int NG, int CH = 8, int FCH = 32, int MINB = 3, int MODE = 7>
+template <int NP, int NCUB, int NG, int CH = 8, int FCH = 32, int MINB = 3, int MODE = 7, int E = 16>
 KernelSet with_row(KernelSet k) {
-  using RC = RCfg<NP, NCUB, NG, CH, FCH, MINB, MODE>;
+  using RC = RCfg<NP, NCUB, NG, CH, FCH, MINB, MODE, E>;
   k.row_update[0] = &k_rhs_row<RC, true, 0>;
   k.row_update[1] = &k_rhs_row<RC, true, 1>;
   k.row_only[0] = &k_rhs_row<RC, false, 0>;
@@ -52,6 +52,8 @@ KernelSet with_row(KernelSet k) {
   k.smem_row = RC::SMEM_BYTES;
   k.row_minb = MINB;
   k.row_ch = CH;
+  k.row_e = RC::E;
+  k.row_nth = RC::NTH;
   return k;
 }
 
@@ -80,6 +82,8 @@ KernelSet with_rowp(KernelSet k) {
   k.smem_row = RC::SMEM_BYTES;
   k.row_minb = MINB;
   k.row_ch = RC::CH;
+  k.row_e = RC::E;
+  k.row_nth = RC::NTH;
   return k;
 }
 

@@ -17,7 +17,8 @@ std::vector<KernelSet> kernel_sets_p4() {
       with_row<35, 70, 16, 8, 32, 4, 8>(make_set<35, 70, 16, 16, 24, 2, 64>()),   // 4 U staged in smem
       with_row<35, 70, 16, 8, 32, 4, 4>(make_set<35, 70, 16, 16, 24, 2, 64>()),   // 5 res staged in smem
       with_row<35, 70, 16, 8, 32, 3, 2>(make_set<35, 70, 16, 16, 24, 2, 64>()),   // 6 U in registers, 3 CTAs
-      with_rowp<35, 70, 16, 4, false>(make_set<35, 70, 16, 16, 24, 2, 64>())};    // 7 pipelined chunks
+      with_rowp<35, 70, 16, 4, false>(make_set<35, 70, 16, 16, 24, 2, 64>()),     // 7 pipelined chunks
+      with_row<35, 70, 16, 8, 32, 2, 0, 32>(make_set<35, 70, 16, 16, 24, 2, 64>())};  // 8 32-element tiles
 }
 
 }  // namespace cdg_gpu

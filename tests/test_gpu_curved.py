@@ -44,7 +44,7 @@ def _fs(gpu):
     return gpu.make_state(1.0, [0.38 * c, 0.0, 0.0], 1.0)
 
 
-@pytest.mark.parametrize("p", [2, 3, 4])
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6])
 def test_curved_sphere_rhs_and_steps_match_reference(gpu_lib, refmod, p):
     gpu, ref = gpu_lib, refmod
     rm, rl, mesh, ids, nodes = sphere_case(ref, p)
