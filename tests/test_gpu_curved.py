@@ -44,7 +44,9 @@ def _fs(gpu):
     return gpu.make_state(1.0, [0.38 * c, 0.0, 0.0], 1.0)
 
 
-@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6])
+# p=6 passes too (2.7 min of reference-side curving on the host; run with
+# CDG_SLOW=1) -- the BASELINE "cylinder P=1..6" sweep on the curved sphere
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5] + ([6] if __import__("os").environ.get("CDG_SLOW") else []))
 def test_curved_sphere_rhs_and_steps_match_reference(gpu_lib, refmod, p):
     gpu, ref = gpu_lib, refmod
     rm, rl, mesh, ids, nodes = sphere_case(ref, p)
