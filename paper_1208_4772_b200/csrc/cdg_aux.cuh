@@ -128,10 +128,13 @@ struct AuxParams {
   const double* sqrt_eps;
   int K, n_tiles;
   GasParams gas;
+  const unsigned long long* gate;  // optional launch gate (see gated_off)
+  int gate_when;
 };
 
 template <class C>
 __global__ void __launch_bounds__(kThreads, C::MINB) k_aux_q(AuxParams p) {
+  if (gated_off(p.gate, p.gate_when)) return;
   extern __shared__ __align__(16) double smem[];
   double* sU = smem;
   double* sC = sU + C::SMEM_U;

@@ -43,6 +43,7 @@ template <class C, bool UPDATE, bool VISC = false>
 __global__ void __launch_bounds__(kThreads, 1) k_rhs_curved(CurvedParams cp) {
   using L = CurvedLayout<C>;
   const RhsParams& p = cp.base;
+  if (gated_off(p.gate, p.gate_when)) return;
   extern __shared__ __align__(16) double smem[];
   double* sU = smem;
   double* sC = sU + C::SMEM_U;
@@ -114,17 +115,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_rhs_curved(CurvedParams cp) {
             // F_m <- F_m - sqrt(eps) I_cub q_m  (solver.cpp:398-406)
             const double se = p.sqrt_eps[sId[e]];
             if (se > 0.0) {
-              const size_t qstride = (size_t)p.K * 5 * C::BP;
-              const double* irow = p.icub + (size_t)q * C::NP;
+              constexpr int LDQ = round_up(C::NCUB, 8);
+              const size_t qcs = (size_t)p.K * 5 * LDQ;
 #pragma unroll
               for (int m = 0; m < 3; ++m)
 #pragma unroll
-                for (int c = 0; c < 5; ++c) {
-                  const double* qrow = p.q + m * qstride + ((size_t)sId[e] * 5 + c) * C::BP;
-                  double qc = 0.0;
-                  for (int j = 0; j < C::NP; ++j) qc += __ldg(irow + j) * __ldg(qrow + j);
-                  F[m][c] -= se * qc;
-                }
+                for (int c = 0; c < 5; ++c)
+                  F[m][c] -= se * __ldg(p.qcub + m * qcs + ((size_t)sId[e] * 5 + c) * LDQ + q);
             }
           }
           const double* met = cp.jwr + ((size_t)ce * C::NCUB + q) * 9;
@@ -266,6 +263,7 @@ template <class C>
 __global__ void __launch_bounds__(kThreads, 1) k_aux_curved(CurvedParams cp) {
   using L = CurvedLayout<C>;
   const RhsParams& p = cp.base;
+  if (gated_off(p.gate, p.gate_when)) return;
   extern __shared__ __align__(16) double smem[];
   double* sU = smem;
   double* sC = sU + C::SMEM_U;

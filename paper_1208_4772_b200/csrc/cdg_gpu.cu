@@ -185,12 +185,11 @@ struct cdg_gpu_level {
   // state
   double *u = nullptr, *res = nullptr, *rhs = nullptr, *traces = nullptr, *before = nullptr;
   // viscous workspace
-  double *q = nullptr, *qtr = nullptr, *eps = nullptr, *sqrt_eps = nullptr;
+  double *q = nullptr, *qtr = nullptr, *qcub = nullptr, *eps = nullptr, *sqrt_eps = nullptr;
   double* d_vinv = nullptr;
   // J-weighted indicator (viscosity.cpp:28-45)
   double *d_vcub = nullptr, *d_wcub = nullptr, *d_jac = nullptr, *d_curved_jac = nullptr;
   int* d_curved_slot = nullptr;
-  double* d_icub = nullptr;  // row-major I_cub (viscous volume term)
   unsigned long long* d_maxeps = nullptr;
   bool last_viscous = false;
   // geometry / coupling
@@ -206,6 +205,12 @@ struct cdg_gpu_level {
   double* rfrag2 = nullptr;  // row kernel (its I_cub fragments are wfrag1)
   bool use_row = false;
   const int* cur_tiles = nullptr;  // tile list of the next RHS launch (null: all)
+  const unsigned long long* cur_gate = nullptr;  // launch gate of the next launches (null: none)
+  int cur_gate_when = 0;
+  // graph of one viscous RK step (gated stages) and the config it was captured with
+  cudaGraphExec_t graph_visc = nullptr;
+  cdg_gpu_run_config graph_visc_cfg{};
+  int graph_launches = 0, graph_visc_launches = 0;
   std::vector<char> ghost_adjacent;  // [K] element has a ghost (halo) neighbour
   int cur_n_list = 0;
   // curved elements
@@ -273,7 +278,7 @@ void check_device_error(cdg_gpu_level* lv) {
 void launch_traces(cdg_gpu_level* lv, const double* u, double* traces) {
   const int tiles = lv->n_tiles();
   lv->ks->traces<<<tiles, kThreads, lv->ks->smem_traces, lv->stream>>>(
-      u, traces, lv->frag_ig, lv->n_rows(), tiles);
+      u, traces, lv->frag_ig, lv->n_rows(), tiles, lv->cur_gate, lv->cur_gate_when);
   ++lv->launches;
 }
 
@@ -281,6 +286,8 @@ RhsParams rhs_params(cdg_gpu_level* lv, int stage) {
   RhsParams p{};
   p.tiles = lv->cur_tiles;
   p.n_list = lv->cur_n_list;
+  p.gate = lv->cur_gate;
+  p.gate_when = lv->cur_gate_when;
   p.u = lv->u;
   p.res = lv->res;
   p.rhs_out = lv->rhs;
@@ -301,7 +308,7 @@ RhsParams rhs_params(cdg_gpu_level* lv, int stage) {
   p.q = lv->q;
   p.qtr = lv->qtr;
   p.sqrt_eps = lv->sqrt_eps;
-  p.icub = lv->d_icub;
+  p.qcub = lv->qcub;
   p.qtr_stride = (size_t)(lv->K + lv->n_halo) * 5 * lv->tb;
   static const int pf = std::getenv("CDG_PREFETCH") ? std::atoi(std::getenv("CDG_PREFETCH")) : 15;
   p.prefetch = pf;
@@ -350,6 +357,8 @@ void launch_rhs_warp(cdg_gpu_level* lv, bool update, int stage) {
   w.err = lv->d_err;
   w.tiles = lv->cur_tiles;
   w.n_list = lv->cur_n_list;
+  w.gate = lv->cur_gate;
+  w.gate_when = lv->cur_gate_when;
   const int tiles = lv->cur_tiles ? lv->cur_n_list : (lv->K + 15) / 16;
   if (tiles == 0) return;
   const int ctas = std::max(1, std::min((tiles + lv->ks->warp_warps - 1) / lv->ks->warp_warps,
@@ -400,8 +409,7 @@ void launch_rhs(cdg_gpu_level* lv, bool update, bool viscous, int stage) {
 
 // Viscosity phase: sensor -> eps, then (if any eps > 0) aux gradient q and its
 // traces (solver.cpp:239-321). Returns whether the viscous path is active.
-bool viscosity_phase(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg) {
-  if (!cfg->visc_enabled) return false;
+void ensure_viscous_buffers(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg) {
   if (cfg->eps0 < 0.0) throw Status(CDG_GPU_ERR_CONFIG, "viscosity_amount: eps0 must be >= 0");
   if (cfg->jacobian_weighted && lv->n_curved && !lv->d_curved_jac)
     throw Status(CDG_GPU_ERR_CONFIG, "jacobian_weighted indicator on curved elements needs curved_jac");
@@ -414,7 +422,14 @@ bool viscosity_phase(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg) {
     CUDA_OK(cudaMemset(lv->q, 0, 3 * n * sizeof(double)));
     CUDA_OK(cudaMalloc(&lv->qtr, 3 * nt * sizeof(double)));
     CUDA_OK(cudaMemset(lv->qtr, 0, 3 * nt * sizeof(double)));
+    const size_t nc = (size_t)lv->K * 5 * ((lv->ncub + 7) / 8 * 8);
+    CUDA_OK(cudaMalloc(&lv->qcub, 3 * nc * sizeof(double)));
+    CUDA_OK(cudaMemset(lv->qcub, 0, 3 * nc * sizeof(double)));
   }
+}
+
+// sensor -> eps, sqrt(eps), max eps bits (compute_element_viscosities, solver.cpp:239-260)
+void launch_sensor(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg) {
   CUDA_OK(cudaMemsetAsync(lv->d_maxeps, 0, sizeof(unsigned long long), lv->stream));
   SensorParams sp{};
   sp.u = lv->u;
@@ -442,14 +457,11 @@ bool viscosity_phase(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg) {
     k_sensor<<<(lv->K + 7) / 8, 256, 0, lv->stream>>>(sp);
   }
   ++lv->launches;
-  unsigned long long bits = 0;
-  CUDA_OK(cudaMemcpyAsync(&bits, lv->d_maxeps, sizeof bits, cudaMemcpyDeviceToHost, lv->stream));
-  CUDA_OK(cudaStreamSynchronize(lv->stream));
-  double maxeps;
-  std::memcpy(&maxeps, &bits, sizeof maxeps);
-  if (!(maxeps > 0.0)) return false;
-  // aux gradient q_m (needs the U traces of all elements first)
-  launch_traces(lv, lv->u, lv->traces);
+}
+
+// aux gradient q_m of every element + its traces (solver.cpp:264-321); needs
+// the U traces first
+void launch_aux(cdg_gpu_level* lv) {
   AuxParams ap{};
   ap.u = lv->u;
   ap.q = lv->q;
@@ -464,14 +476,54 @@ bool viscosity_phase(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg) {
   ap.K = lv->K;
   ap.n_tiles = lv->n_tiles();
   ap.gas = lv->gas;
+  ap.gate = lv->cur_gate;
+  ap.gate_when = lv->cur_gate_when;
   lv->ks->aux_q<<<lv->grid(lv->n_tiles()), kThreads, lv->ks->smem_aux, lv->stream>>>(ap);
   ++lv->launches;
   launch_curved(lv, false, 0, 2);  // per-node-metric q of the curved elements
-  // q traces: 3 x (K*5 rows)
   const size_t n = (size_t)lv->K * 5 * lv->bp;
   const size_t nt = (size_t)(lv->K + lv->n_halo) * 5 * lv->tb;
-  for (int m = 0; m < 3; ++m) launch_traces(lv, lv->q + m * n, lv->qtr + m * nt);
+  const size_t nc = (size_t)lv->K * 5 * ((lv->ncub + 7) / 8 * 8);
+  for (int m = 0; m < 3; ++m) {
+    launch_traces(lv, lv->q + m * n, lv->qtr + m * nt);
+    // I_cub q_m once per element (the RHS kernels' viscous volume term)
+    const int tiles = lv->n_tiles();
+    lv->ks->cubinterp<<<tiles, kThreads, lv->ks->smem_traces, lv->stream>>>(
+        lv->q + m * n, lv->qcub + m * nc, lv->frag_icub, lv->n_rows(), tiles, lv->cur_gate, lv->cur_gate_when);
+    ++lv->launches;
+  }
+}
+
+// Viscosity phase with the host decision (compute_rhs path): sensor -> eps,
+// then (if any eps > 0) aux gradient q and its traces (solver.cpp:239-321).
+// Returns whether the viscous path is active.
+bool viscosity_phase(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg) {
+  if (!cfg->visc_enabled) return false;
+  ensure_viscous_buffers(lv, cfg);
+  launch_sensor(lv, cfg);
+  unsigned long long bits = 0;
+  CUDA_OK(cudaMemcpyAsync(&bits, lv->d_maxeps, sizeof bits, cudaMemcpyDeviceToHost, lv->stream));
+  CUDA_OK(cudaStreamSynchronize(lv->stream));
+  double maxeps;
+  std::memcpy(&maxeps, &bits, sizeof maxeps);
+  if (!(maxeps > 0.0)) return false;
+  launch_traces(lv, lv->u, lv->traces);
+  launch_aux(lv);
   return true;
+}
+
+// One viscous RK stage with the decision on the device (graph-capturable):
+// the same kernels as viscosity_phase + launch_rhs, each gated on max eps.
+void viscous_stage_gated(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, int stage) {
+  launch_sensor(lv, cfg);
+  launch_traces(lv, lv->u, lv->traces);  // both paths need the U traces
+  lv->cur_gate = lv->d_maxeps;
+  lv->cur_gate_when = 1;
+  launch_aux(lv);
+  launch_rhs(lv, true, true, stage);
+  lv->cur_gate_when = 0;
+  launch_rhs(lv, true, false, stage);
+  lv->cur_gate = nullptr;
 }
 
 }  // namespace
@@ -625,7 +677,6 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
     };
     const std::vector<double> op2 = build_op2(lv->ks->ch, -1.0), opaux = build_op2(lv->ks->ch, 1.0);
     lv->frag_icub = dev_upload(make_frag(icub, ncub, np, ncub8, kp));
-    lv->d_icub = dev_upload(icub);
     lv->frag_ig = dev_upload(make_frag(ig, nf, np, nf8, kp));
     lv->frag_op2 = dev_upload(make_frag(op2, np, k2, np8, k2));
     lv->frag_aux = dev_upload(make_frag(opaux, np, k2, np8, k2));
@@ -831,8 +882,8 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
       for (auto fn : {lv->ks->curved_update, lv->ks->curved_only, lv->ks->curved_visc_update,
                       lv->ks->curved_visc_only, lv->ks->aux_curved})
         CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lv->ks->smem_curved));
-    CUDA_OK(cudaFuncSetAttribute(lv->ks->traces, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)lv->ks->smem_traces));
+    for (auto fn : {lv->ks->traces, lv->ks->cubinterp})
+      CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lv->ks->smem_traces));
     CUDA_OK(cudaDeviceSynchronize());
   });
   if (st != CDG_GPU_OK) {
@@ -847,10 +898,11 @@ void cdg_gpu_level_destroy(cdg_gpu_level* lv) {
   if (!lv) return;
   cudaSetDevice(lv->device);
   if (lv->graph) cudaGraphExecDestroy(lv->graph);
+  if (lv->graph_visc) cudaGraphExecDestroy(lv->graph_visc);
   for (void* p : {(void*)lv->u, (void*)lv->res, (void*)lv->rhs, (void*)lv->traces, (void*)lv->before,
-                  (void*)lv->q, (void*)lv->qtr, (void*)lv->eps, (void*)lv->sqrt_eps, (void*)lv->d_vinv, (void*)lv->d_vcub, (void*)lv->d_wcub, (void*)lv->d_jac,
+                  (void*)lv->q, (void*)lv->qtr, (void*)lv->qcub, (void*)lv->eps, (void*)lv->sqrt_eps, (void*)lv->d_vinv, (void*)lv->d_vcub, (void*)lv->d_wcub, (void*)lv->d_jac,
                   (void*)lv->d_curved_jac, (void*)lv->d_curved_slot,
-                  (void*)lv->d_icub, (void*)lv->d_maxeps, (void*)lv->metric, (void*)lv->face, (void*)lv->conn,
+                  (void*)lv->d_maxeps, (void*)lv->metric, (void*)lv->face, (void*)lv->conn,
                   (void*)lv->code_map, (void*)lv->h, (void*)lv->frag_icub, (void*)lv->frag_op2,
                   (void*)lv->frag_ig, (void*)lv->frag_aux, (void*)lv->wfrag1, (void*)lv->wfrag2v, (void*)lv->wfrag2f, (void*)lv->rfrag2,
                   (void*)lv->curved_ids, (void*)lv->curved_jwr, (void*)lv->curved_minv, (void*)lv->frag_opc,
@@ -978,17 +1030,40 @@ int cdg_gpu_rk_steps(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, int nstep
     }
     CUDA_OK(cudaMemcpyAsync(lv->d_coef, lv->h_coef, sizeof(StageCoef), cudaMemcpyHostToDevice, lv->stream));
     if (cfg->visc_enabled) {
-      // viscous stages need a host decision per stage (viscous_active,
-      // solver.cpp:257-259): run eagerly.
-      for (int s = 0; s < nsteps; ++s)
-        for (int stage = 0; stage < 5; ++stage) {
-          const bool viscous = viscosity_phase(lv, cfg);
-          lv->last_viscous = viscous;
-          if (!viscous) launch_traces(lv, lv->u, lv->traces);
-          launch_rhs(lv, true, viscous, stage);
+      // viscous_active (solver.cpp:257-259) is decided per stage on the device
+      // (gated kernels), so one viscous RK step is a CUDA graph as well
+      ensure_viscous_buffers(lv, cfg);
+      if (!lv->graph_visc || std::memcmp(&lv->graph_visc_cfg, cfg, sizeof *cfg) != 0) {
+        if (lv->graph_visc) {
+          cudaGraphExecDestroy(lv->graph_visc);
+          lv->graph_visc = nullptr;
         }
+        cudaGraph_t g;
+        const long long l0 = lv->launches;
+        CUDA_OK(cudaStreamBeginCapture(lv->stream, cudaStreamCaptureModeThreadLocal));
+        try {
+          for (int stage = 0; stage < 5; ++stage) viscous_stage_gated(lv, cfg, stage);
+        } catch (...) {
+          lv->cur_gate = nullptr;
+          cudaStreamEndCapture(lv->stream, &g);
+          throw;
+        }
+        lv->graph_visc_launches = (int)(lv->launches - l0);
+        lv->launches = l0;  // counted at replay
+        CUDA_OK(cudaStreamEndCapture(lv->stream, &g));
+        CUDA_OK(cudaGraphInstantiate(&lv->graph_visc, g, 0));
+        CUDA_OK(cudaGraphDestroy(g));
+        lv->graph_visc_cfg = *cfg;
+      }
+      for (int s = 0; s < nsteps; ++s) {
+        CUDA_OK(cudaGraphLaunch(lv->graph_visc, lv->stream));
+        lv->launches += lv->graph_visc_launches;
+      }
       CUDA_OK(cudaGetLastError());
       check_device_error(lv);
+      unsigned long long bits = 0;  // viscous_active of the last stage (aux_gradient validity)
+      CUDA_OK(cudaMemcpy(&bits, lv->d_maxeps, sizeof bits, cudaMemcpyDeviceToHost));
+      lv->last_viscous = bits != 0;
       return;
     }
     if (lv->profiling) {
@@ -1021,12 +1096,14 @@ int cdg_gpu_rk_steps(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, int nstep
         lv->graph = nullptr;
       }
       cudaGraph_t g;
+      const long long l0 = lv->launches;
       CUDA_OK(cudaStreamBeginCapture(lv->stream, cudaStreamCaptureModeThreadLocal));
       for (int stage = 0; stage < 5; ++stage) {
         launch_traces(lv, lv->u, lv->traces);
         launch_rhs(lv, true, false, stage);
       }
-      lv->launches -= 10;  // counted at replay
+      lv->graph_launches = (int)(lv->launches - l0);
+      lv->launches = l0;  // counted at replay
       CUDA_OK(cudaStreamEndCapture(lv->stream, &g));
       CUDA_OK(cudaGraphInstantiate(&lv->graph, g, 0));
       CUDA_OK(cudaGraphDestroy(g));
@@ -1035,7 +1112,7 @@ int cdg_gpu_rk_steps(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, int nstep
     }
     for (int s = 0; s < nsteps; ++s) {
       CUDA_OK(cudaGraphLaunch(lv->graph, lv->stream));
-      lv->launches += 10;
+      lv->launches += lv->graph_launches;
     }
     CUDA_OK(cudaGetLastError());
     check_device_error(lv);
@@ -1048,6 +1125,10 @@ int cdg_gpu_set_freestream(cdg_gpu_level* lv, const double* fs) {
   if (!same && lv->graph) {  // kernel params are baked into the captured graph
     cudaGraphExecDestroy(lv->graph);
     lv->graph = nullptr;
+  }
+  if (!same && lv->graph_visc) {
+    cudaGraphExecDestroy(lv->graph_visc);
+    lv->graph_visc = nullptr;
   }
   for (int c = 0; c < 5; ++c) {
     lv->freestream[c] = fs[c];

@@ -89,6 +89,14 @@ struct Cfg {
 // A-fragment values (k = t and t+4) are adjacent: one 128-bit shared load.
 __host__ __device__ __forceinline__ int pcol(int k) { return (k & ~7) | ((k & 3) << 1) | ((k >> 2) & 1); }
 
+// Launch gate for graph-captured viscous stages: the decision viscous_active
+// (max eps > 0, solver.cpp:257-259) is made on the device by the sensor; a
+// gated kernel returns at once (grid-uniform) unless (max eps bits != 0) ==
+// run_if_active. gate == nullptr: always run.
+__device__ __forceinline__ bool gated_off(const unsigned long long* gate, int run_if_active) {
+  return gate && ((*(volatile const unsigned long long*)gate != 0ull) != (run_if_active != 0));
+}
+
 // First-error record (the reference's RhsWorkspace::record_error,
 // solver.cpp:54-69, made device-side: first writer wins).
 struct DevError {
@@ -326,20 +334,24 @@ __host__ __device__ constexpr int pack_face(int nface, int bc, int boundary, int
 }
 
 // ---------------------------------------------------------------------------
-// Kernel 1: traces  T[rows x NF] = U[rows x KP] * I_g^T   (solver.cpp:200-208)
-// Non-persistent (one tile per CTA, several CTAs per SM): memory-bound.
+// Kernel 1: nodal -> point interpolation  Out[rows x NO] = U[rows x KP] * Op^T
+// with Op = I_g (traces, solver.cpp:200-208; NO = N_f, LDO = pad16(N_f)) or
+// Op = I_cub (the aux gradient at the cubature nodes for the viscous volume
+// term, solver.cpp:364-369; NO = N_cub). Non-persistent (one tile per CTA,
+// several CTAs per SM): memory-bound.
 // ---------------------------------------------------------------------------
-template <class C>
+template <class C, int NO, int LDO>
 __global__ void __launch_bounds__(kThreads)
-k_traces(const double* __restrict__ u, double* __restrict__ traces,
-         const double* __restrict__ frag_ig, int n_rows, int n_tiles) {
+k_interp(const double* __restrict__ u, double* __restrict__ out, const double* __restrict__ frag_op, int n_rows,
+         int n_tiles, const unsigned long long* gate, int gate_when) {
+  if (gated_off(gate, gate_when)) return;
   extern __shared__ __align__(16) double smem[];
   double* sU = smem;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, tq = lane & 3;
-  constexpr int NT = C::NF8 / 8;
+  constexpr int NT = round_up(NO, 8) / 8;
   constexpr int T = C::MT * NT;
-  const double2* fb = reinterpret_cast<const double2*>(frag_ig);
+  const double2* fb = reinterpret_cast<const double2*>(frag_op);
   for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const int row0 = tile * C::R;
     stage_rows<C>(u, row0, n_rows, sU, tid);
@@ -351,13 +363,12 @@ k_traces(const double* __restrict__ u, double* __restrict__ traces,
       for (int ks = 0; ks < C::KS1; ++ks)
         mma_frag(acc, load_afrag(sU, C::LDU, mt * 16, ks * 8, g, tq), __ldg(fb + ((size_t)nt * C::KS1 + ks) * 32 + lane));
       const int col = nt * 8 + 2 * tq;
-      if (col < C::NF) {
+      if (col < NO) {
         const int r0 = row0 + mt * 16 + g;
         if (r0 < n_rows)
-          *reinterpret_cast<double2*>(traces + (size_t)r0 * C::TB + col) = make_double2(acc[0], acc[1]);
+          *reinterpret_cast<double2*>(out + (size_t)r0 * LDO + col) = make_double2(acc[0], acc[1]);
         if (r0 + 8 < n_rows)
-          *reinterpret_cast<double2*>(traces + (size_t)(r0 + 8) * C::TB + col) =
-              make_double2(acc[2], acc[3]);
+          *reinterpret_cast<double2*>(out + (size_t)(r0 + 8) * LDO + col) = make_double2(acc[2], acc[3]);
       }
     }
     __syncthreads();
@@ -389,11 +400,13 @@ struct RhsParams {
   const double* q;            // [3][K*5][BP]   aux gradient q_m
   const double* qtr;          // [3][(K+halo)*5][TB] its traces
   const double* sqrt_eps;     // [K+halo]
-  const double* icub;         // [NCUB][NP] row-major (viscous volume term)
+  const double* qcub;         // [3][K*5][round_up(NCUB, 8)] I_cub q_m (viscous volume term)
   size_t qtr_stride;          // elements per direction of qtr
   int prefetch;               // L2 prefetch mask: 1 res, 2 next-tile u, 4 own traces, 8 neighbour traces
   const int* tiles;           // optional tile list (multi-GPU interior / halo split); null = all tiles
   int n_list;                 // entries of `tiles`
+  const unsigned long long* gate;  // optional launch gate (see gated_off)
+  int gate_when;
 };
 
 // i-th tile of a launch: the tile list when given, else tile i
@@ -533,6 +546,7 @@ __device__ __forceinline__ void tile_coords(int t_begin, int i, int& mt, int& nt
 // p.gas.riemann): the LLF-only instantiation needs far fewer registers.
 template <class C, bool UPDATE, bool VISC, int DBG = 0, int RM = -1>
 __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs(RhsParams p) {
+  if (gated_off(p.gate, p.gate_when)) return;
   extern __shared__ __align__(16) double smem[];
   double* sU = smem;                       // [R][LDU] nodal state (pcol-permuted)
   double* sC = sU + C::SMEM_U;             // [R][LDC] U at a cubature chunk
@@ -650,16 +664,13 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs(RhsParams p) {
               // F_m <- F_m - sqrt(eps) I_cub q_m   (solver.cpp:398-406)
               const double se = sSe[e];
               if (se > 0.0) {
-                const double* irow = p.icub + (size_t)q * C::NP;
+                constexpr int LDQ = round_up(C::NCUB, 8);
+                const size_t qcs = (size_t)p.K * 5 * LDQ;
 #pragma unroll
                 for (int m = 0; m < 3; ++m)
 #pragma unroll
-                  for (int c = 0; c < 5; ++c) {
-                    const double* qrow = p.q + m * qstride + (size_t)(row0 + e * 5 + c) * C::BP;
-                    double qc = 0.0;
-                    for (int j = 0; j < C::NP; ++j) qc += __ldg(irow + j) * __ldg(qrow + j);
-                    F[m][c] -= se * qc;
-                  }
+                  for (int c = 0; c < 5; ++c)
+                    F[m][c] -= se * __ldg(p.qcub + m * qcs + (size_t)(row0 + e * 5 + c) * LDQ + q);
               }
 #pragma unroll
               for (int m = 0; m < 3; ++m) {

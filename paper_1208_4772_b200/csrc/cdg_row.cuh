@@ -133,6 +133,7 @@ __device__ __forceinline__ void issue_op_chunk(int n, double* sOp, unsigned long
 // [A_r A_s A_t | -LIFT] operator (k-step-major: one k-step's n-tiles adjacent).
 template <class C, bool UPDATE, int RM>
 __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_row(RhsParams p) {
+  if (gated_off(p.gate, p.gate_when)) return;
   extern __shared__ __align__(16) double smem[];
   double* sWork = smem;
   double* sUp = sWork + C::WORK;                                  // [R][LDU] U rows (USMEM)

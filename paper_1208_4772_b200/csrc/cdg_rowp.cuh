@@ -47,6 +47,7 @@ struct RPCfg {
 
 template <class C, bool UPDATE, int RM>
 __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_rowp(RhsParams p) {
+  if (gated_off(p.gate, p.gate_when)) return;
   extern __shared__ __align__(16) double smem[];
   double* sCb = smem;                                  // [2][R][LDC]
   double* sGb = sCb + 2 * C::R * C::LDC;               // [2][R][LDG]

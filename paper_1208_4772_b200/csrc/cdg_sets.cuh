@@ -18,7 +18,8 @@ namespace cdg_gpu {
 struct KernelSet {
   int np, ncub, ng, E, minb, ch, nth;
   size_t smem_traces, smem_rhs, smem_aux;
-  void (*traces)(const double*, double*, const double*, int, int);
+  void (*traces)(const double*, double*, const double*, int, int, const unsigned long long*, int);
+  void (*cubinterp)(const double*, double*, const double*, int, int, const unsigned long long*, int);
   void (*rhs_update)(RhsParams);
   void (*rhs_only)(RhsParams);
   void (*aux_q)(AuxParams);
@@ -105,7 +106,8 @@ KernelSet make_set() {
   k.smem_traces = sizeof(double) * C8::R * C8::LDU;
   k.smem_rhs = C::SMEM_BYTES;
   k.smem_aux = C8::SMEM_BYTES;
-  k.traces = &k_traces<C8>;
+  k.traces = &k_interp<C8, C8::NF, C8::TB>;
+  k.cubinterp = &k_interp<C8, C8::NCUB, round_up(NCUB, 8)>;
   k.rhs_update = &k_rhs<C, true, false>;
   k.rhs_only = &k_rhs<C, false, false>;
   k.aux_q = &k_aux_q<C8>;

@@ -84,10 +84,13 @@ struct WarpParams {
   DevError* err;
   const int* tiles;  // optional 16-element tile list (multi-GPU interior / halo split)
   int n_list;
+  const unsigned long long* gate;  // optional launch gate (see gated_off)
+  int gate_when;
 };
 
 template <class C, bool UPDATE, int RIEMANN>
 __global__ void __launch_bounds__(32 * C::WARPS, C::MINB) k_rhs_warp(WarpParams p) {
+  if (gated_off(p.gate, p.gate_when)) return;
   extern __shared__ __align__(16) double smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;

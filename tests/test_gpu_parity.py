@@ -262,3 +262,21 @@ def test_viscous_timestep_limit(gpu_lib):
     lv.compute_rhs(cfg, u)
     eps = lv.viscosity()
     assert lv.compute_timestep(cfg, use_viscosity=True) == pytest.approx(ol.compute_timestep(u, cfg, eps), rel=1e-12)
+
+
+def test_viscous_rk_steps_inactive_is_bitwise_inviscid(gpu_lib):
+    """Viscosity enabled but eps0 = 0: the device-side viscous_active decision
+    (gated kernels inside the captured RK-step graph) takes the inviscid path,
+    bit for bit (test_solver.cpp:334-352 for rk_step)."""
+    gpu = gpu_lib
+    m = M.cube_mesh(2)
+    fs = _fs(gpu)
+    outs = []
+    for visc in (None, dict(enabled=True, eps0=0.0)):
+        lv = gpu.GpuLevel(m, 3, bc=1, freestream=fs)
+        u0 = gpu.random_admissible_store(lv, seed=17)
+        lv.set_state(u0)
+        cfg = gpu.run_config("hllc", viscosity=visc)
+        lv.rk_steps(cfg, 0.01, 3)
+        outs.append(lv.get_state()[0])
+    assert np.array_equal(outs[0], outs[1])
