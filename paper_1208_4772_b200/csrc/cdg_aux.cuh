@@ -125,6 +125,7 @@ struct AuxParams {
   const int* code_map;
   const double* frag_icub;
   const double* frag_aux;
+  const double* frag_dtil;  // [3][NT2][KS1][32] B fragments of A_k I_cub (N_p x N_p)
   const double* sqrt_eps;
   int K, n_tiles;
   GasParams gas;
@@ -148,7 +149,6 @@ __global__ void __launch_bounds__(kThreads, C::MINB) k_aux_q(AuxParams p) {
   const int n_rows = p.K * 5;
   const size_t qstride = (size_t)p.K * 5 * C::BP;
   const int t_begin = (warp * C::T2) / kWarps, t_end = ((warp + 1) * C::T2) / kWarps;
-  const double2* fb1 = reinterpret_cast<const double2*>(p.frag_icub);
   const double2* fba = reinterpret_cast<const double2*>(p.frag_aux);
 
   for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
@@ -168,21 +168,29 @@ __global__ void __launch_bounds__(kThreads, C::MINB) k_aux_q(AuxParams p) {
       double acc[C::MAXT2][4];
 #pragma unroll
       for (int i = 0; i < C::MAXT2; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.0;
-      for (int ch = 0; ch < C::NCH; ++ch) {
-        const int q0 = ch * C::CH;
-        const int w = (C::NCUB8 - q0) < C::CH ? (C::NCUB8 - q0) : C::CH;
-        gemm1_chunk<C>(sU, sC, fb1, q0, w, warp, lane);
-        __syncthreads();
-        // G_k = -se * r_{k,m} * U_cub  for every field (solver.cpp:283-289)
-        for (int idx = tid; idx < C::R * w; idx += kThreads) {
-          const int r = idx / w, ql = idx % w, e = r / 5;
-          const double uc = (q0 + ql < C::NCUB) ? sC[r * C::LDC + ql] : 0.0;
-          const double se = sSe[e];
-#pragma unroll
-          for (int k = 0; k < 3; ++k) sG[r * C::LDG + pcol(k * w + ql)] = -se * (sMet[e * 9 + k * 3 + m] * uc);
+      // volume part: for an affine element the metric r_km is constant, so
+      //   -se sum_k A_k (r_km U_cub) = sum_k (A_k I_cub) (-se r_km U)
+      // (matrix associativity; A_k I_cub = M_ref^-1 D_k^T W I_cub precomputed,
+      // N_p x N_p): three N_p-deep contractions of row-scaled U instead of the
+      // cubature round trip (solver.cpp:283-289 with operators.cpp:135-149).
+      for (int k = 0; k < 3; ++k) {
+        for (int idx = tid; idx < C::R * C::KP; idx += kThreads) {
+          const int r = idx / C::KP, j = idx - r * C::KP, e = r / 5;
+          sG[r * C::LDG + j] = -sSe[e] * sMet[e * 9 + k * 3 + m] * sU[r * C::LDU + j];  // same pcol layout
         }
         __syncthreads();
-        gemm2_partial<C>(acc, sG, fba, (3 * q0) / 8, (3 * w) / 8, t_begin, t_end, lane);
+        const double2* fbd = reinterpret_cast<const double2*>(p.frag_dtil) + (size_t)k * C::NT2 * C::KS1 * 32;
+#pragma unroll
+        for (int i = 0; i < C::MAXT2; ++i) {
+          const int t = t_begin + i;
+          if (t < t_end) {
+            const int nt = t / C::MT, mt = t % C::MT;
+#pragma unroll
+            for (int ks = 0; ks < C::KS1; ++ks)
+              mma_frag(acc[i], load_afrag(sG, C::LDG, mt * 16, ks * 8, g, tq),
+                       __ldg(fbd + ((size_t)nt * C::KS1 + ks) * 32 + lane));
+          }
+        }
         __syncthreads();
       }
       for (int fc = 0; fc < C::NFCH; ++fc) {

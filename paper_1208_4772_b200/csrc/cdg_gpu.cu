@@ -199,7 +199,7 @@ struct cdg_gpu_level {
   int* code_map = nullptr;
   double* h = nullptr;
   // operators
-  double *frag_icub = nullptr, *frag_op2 = nullptr, *frag_ig = nullptr, *frag_aux = nullptr;
+  double *frag_icub = nullptr, *frag_op2 = nullptr, *frag_ig = nullptr, *frag_aux = nullptr, *frag_dtil = nullptr;
   double *wfrag1 = nullptr, *wfrag2v = nullptr, *wfrag2f = nullptr;  // warp-tile kernel
   bool use_warp = false;
   double* rfrag2 = nullptr;  // row kernel (its I_cub fragments are wfrag1)
@@ -472,6 +472,7 @@ void launch_aux(cdg_gpu_level* lv) {
   ap.code_map = lv->code_map;
   ap.frag_icub = lv->frag_icub;
   ap.frag_aux = lv->frag_aux;
+  ap.frag_dtil = lv->frag_dtil;
   ap.sqrt_eps = lv->sqrt_eps;
   ap.K = lv->K;
   ap.n_tiles = lv->n_tiles();
@@ -680,6 +681,21 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
     lv->frag_ig = dev_upload(make_frag(ig, nf, np, nf8, kp));
     lv->frag_op2 = dev_upload(make_frag(op2, np, k2, np8, k2));
     lv->frag_aux = dev_upload(make_frag(opaux, np, k2, np8, k2));
+    {  // A_k I_cub (N_p x N_p) for the affine aux-gradient volume term
+      std::vector<double> fd;
+      for (int m = 0; m < 3; ++m) {
+        std::vector<double> dt((size_t)np * np, 0.0);
+        for (int i = 0; i < np; ++i)
+          for (int j = 0; j < np; ++j) {
+            double s = 0.0;
+            for (int q = 0; q < ncub; ++q) s += amat[m][(size_t)i * ncub + q] * icub[(size_t)q * np + j];
+            dt[(size_t)i * np + j] = s;
+          }
+        const std::vector<double> f = make_frag(dt, np, np, np8, kp);
+        fd.insert(fd.end(), f.begin(), f.end());
+      }
+      lv->frag_dtil = dev_upload(fd);
+    }
     if (lv->ks->row_update[0]) {
       const std::vector<double> op2r = build_op2(lv->ks->row_ch, -1.0);
       std::vector<double> f2;
@@ -904,7 +920,7 @@ void cdg_gpu_level_destroy(cdg_gpu_level* lv) {
                   (void*)lv->d_curved_jac, (void*)lv->d_curved_slot,
                   (void*)lv->d_maxeps, (void*)lv->metric, (void*)lv->face, (void*)lv->conn,
                   (void*)lv->code_map, (void*)lv->h, (void*)lv->frag_icub, (void*)lv->frag_op2,
-                  (void*)lv->frag_ig, (void*)lv->frag_aux, (void*)lv->wfrag1, (void*)lv->wfrag2v, (void*)lv->wfrag2f, (void*)lv->rfrag2,
+                  (void*)lv->frag_ig, (void*)lv->frag_aux, (void*)lv->frag_dtil, (void*)lv->wfrag1, (void*)lv->wfrag2v, (void*)lv->wfrag2f, (void*)lv->rfrag2,
                   (void*)lv->curved_ids, (void*)lv->curved_jwr, (void*)lv->curved_minv, (void*)lv->frag_opc,
                   (void*)lv->curved_vol, (void*)lv->curved_face, (void*)lv->d_coef, (void*)lv->d_err,
                   (void*)lv->d_scratch, (void*)lv->d_send_idx, (void*)lv->d_recv_idx,
