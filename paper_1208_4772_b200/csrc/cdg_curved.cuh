@@ -230,21 +230,31 @@ __global__ void __launch_bounds__(kThreads, 1) k_rhs_curved(CurvedParams cp) {
       b_c = p.coef->b[p.stage];
       dt = p.coef->dt;
     }
-    for (int idx = tid; idx < C::R * C::NP; idx += kThreads) {
-      const int r = idx / C::NP, i = idx - r * C::NP, e = r / 5;
+    // thread <-> (element, output node i): one pass over row i of M_e^-1 serves
+    // all five fields
+    for (int idx = tid; idx < C::E * C::NP; idx += kThreads) {
+      const int e = idx / C::NP, i = idx - e * C::NP;
       const int ce = c0 + e;
       if (ce >= cp.Kc) continue;
       const double* mrow = cp.minv + ((size_t)ce * C::NP + i) * C::NP;
-      const double* v = vbase + r * L::LDV;
-      double rhs = 0.0;
-      for (int j = 0; j < C::NP; ++j) rhs += __ldg(mrow + j) * v[j];
-      const size_t gi = ((size_t)sId[e] * 5 + r % 5) * C::BP + i;
-      if (UPDATE) {
-        const double rn = a_c * p.res[gi] + dt * rhs;
-        p.res[gi] = rn;
-        p.u[gi] = sU[r * C::LDU + pcol(i)] + b_c * rn;
-      } else {
-        p.rhs_out[gi] = rhs;
+      const double* v = vbase + (e * 5) * L::LDV;
+      double rhs[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+      for (int j = 0; j < C::NP; ++j) {
+        const double mij = __ldg(mrow + j);
+#pragma unroll
+        for (int f = 0; f < 5; ++f) rhs[f] += mij * v[f * L::LDV + j];
+      }
+#pragma unroll
+      for (int f = 0; f < 5; ++f) {
+        const int r = e * 5 + f;
+        const size_t gi = ((size_t)sId[e] * 5 + f) * C::BP + i;
+        if (UPDATE) {
+          const double rn = a_c * p.res[gi] + dt * rhs[f];
+          p.res[gi] = rn;
+          p.u[gi] = sU[r * C::LDU + pcol(i)] + b_c * rn;
+        } else {
+          p.rhs_out[gi] = rhs[f];
+        }
       }
     }
     __syncthreads();
@@ -385,15 +395,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_aux_curved(CurvedParams cp) {
         }
       }
       __syncthreads();
-      for (int idx = tid; idx < C::R * C::NP; idx += kThreads) {
-        const int r = idx / C::NP, i = idx - r * C::NP, e = r / 5;
+      for (int idx = tid; idx < C::E * C::NP; idx += kThreads) {
+        const int e = idx / C::NP, i = idx - e * C::NP;
         const int ce = c0 + e;
         if (ce >= cp.Kc) continue;
         const double* mrow = cp.minv + ((size_t)ce * C::NP + i) * C::NP;
-        const double* v = vbase + r * L::LDV;
-        double qv = 0.0;
-        for (int j = 0; j < C::NP; ++j) qv += __ldg(mrow + j) * v[j];
-        cp.q_out[m * qstride + ((size_t)sId[e] * 5 + r % 5) * C::BP + i] = qv;
+        const double* v = vbase + (e * 5) * L::LDV;
+        double qv[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+        for (int j = 0; j < C::NP; ++j) {
+          const double mij = __ldg(mrow + j);
+#pragma unroll
+          for (int f = 0; f < 5; ++f) qv[f] += mij * v[f * L::LDV + j];
+        }
+#pragma unroll
+        for (int f = 0; f < 5; ++f) cp.q_out[m * qstride + ((size_t)sId[e] * 5 + f) * C::BP + i] = qv[f];
       }
       __syncthreads();
     }
