@@ -357,7 +357,12 @@ def main():
         launches_rhs = 5 * args.steps
         t_rhs = prof_rhs / launches_rhs * 1e-3
         t_tr = prof_tr / launches_rhs * 1e-3
-        achieved = F_rhs * K / t_rhs / 1e12
+        fused = lv.fused_traces()
+        # the fused kernel also produces the next stage's traces: its work is the
+        # whole stage model F (trace GEMM included); else F_rhs
+        F_k = F if fused else F_rhs
+        ex_k = ex_rhs + ex_tr if fused else ex_rhs
+        achieved = F_k * K / t_rhs / 1e12
         traffic = None
         ncu_file = ROOT / "profiles" / f"ncu_rhs_p{p}.json"
         if ncu_file.exists():
@@ -365,9 +370,11 @@ def main():
         peak = max(fp64_dmma, fp64_dfma, fp64_k8, fp64_k16)
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": traffic,
-                "kernel": (f"k_rhs_row<P={p}> (fused volume+surface+lift+LSRK update, FP64 DMMA, one m-tile row per warp)"
-                           if p == 4 else f"RHS+update kernel <P={p}> (fused volume+surface+lift+LSRK update, FP64 DMMA)"),
-                "algorithmic_flops_per_launch": F_rhs * K,
+                "kernel": (f"k_rhs_row<P={p}> (fused volume+surface+lift+LSRK update"
+                           + (" + next-stage traces" if fused else "") + ", FP64 DMMA, one m-tile row per warp)"
+                           if p in (4, 5) else f"RHS+update kernel <P={p}> (fused volume+surface+lift+LSRK update, FP64 DMMA)"),
+                "fused_traces": fused,
+                "algorithmic_flops_per_launch": F_k * K,
                 "peak_source": "max of the FP64 DMMA (m16n8k4/k8/k16) and DFMA peaks measured live on this "
                                "GPU by cdg_gpu_measure_fp64_peak (the kernel uses DMMA m16n8k8); "
                                "MEASURED_PEAKS.json has no fp64 entry",
@@ -376,7 +383,7 @@ def main():
                 "fp64_dmma_k16_tflops": fp64_k16,
                 "kernel_ms_avg": t_rhs * 1e3, "trace_kernel_ms_avg": t_tr * 1e3,
                 "rhs_share_of_stage": prof_rhs / (prof_rhs + prof_tr),
-                "executed_dmma_tflops": ex_rhs * K / t_rhs / 1e12,
+                "executed_dmma_tflops": ex_k * K / t_rhs / 1e12,
                 "hbm_achieved_gbs": B * K / t_rhs / 1e9, "hbm_peak_gbs": hbm_peak,
                 "hbm_frac": B * K / t_rhs / 1e9 / hbm_peak,
                 "stage_model_tflops": F * K / ((t_rhs + t_tr)) / 1e12}

@@ -222,6 +222,11 @@ int cdg_gpu_rk_stage_phase(cdg_gpu_level *lv, const cdg_gpu_run_config *cfg, int
                            double dt, const double a[5], const double b[5], char *err,
                            size_t errlen);
 
+/* 1 when cdg_gpu_rk_steps runs the fused-trace path (the RHS kernel's epilogue
+ * writes the next stage's face traces; one trace kernel seeds each call),
+ * else 0. Informational (bench roofline accounting). */
+int cdg_gpu_fused_traces(const cdg_gpu_level *lv);
+
 /* Replace the farfield ghost state (compute_rhs/rk_step take it per call,
  * solver.hpp:94-109). */
 int cdg_gpu_set_freestream(cdg_gpu_level *lv, const double *freestream5);

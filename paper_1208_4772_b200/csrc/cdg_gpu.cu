@@ -203,6 +203,13 @@ struct cdg_gpu_level {
   double *wfrag1 = nullptr, *wfrag2v = nullptr, *wfrag2f = nullptr;  // warp-tile kernel
   bool use_warp = false;
   double* rfrag2 = nullptr;  // row kernel (its I_cub fragments are wfrag1)
+  double* tbuf[2] = {nullptr, nullptr};  // trace double buffer of the fused-trace path
+  int tcur = 0;                          // tbuf[tcur] == traces (current)
+  double* cur_traces_out = nullptr;
+  cudaGraphExec_t gft[2] = {nullptr, nullptr};
+  int gft_riemann[2] = {-1, -1};
+  double gft_gamma[2] = {0.0, 0.0};
+  int gft_launches = 0;
   bool use_row = false;
   const int* cur_tiles = nullptr;  // tile list of the next RHS launch (null: all)
   const unsigned long long* cur_gate = nullptr;  // launch gate of the next launches (null: none)
@@ -288,6 +295,8 @@ RhsParams rhs_params(cdg_gpu_level* lv, int stage) {
   p.n_list = lv->cur_n_list;
   p.gate = lv->cur_gate;
   p.gate_when = lv->cur_gate_when;
+  p.traces_out = lv->cur_traces_out;
+  p.frag_ig_nat = lv->frag_ig;  // the trace kernel's fragments (bitwise-identical fused traces)
   p.u = lv->u;
   p.res = lv->res;
   p.rhs_out = lv->rhs;
@@ -546,6 +555,10 @@ int guarded(char* err, size_t errlen, const std::function<void()>& fn) {
 
 extern "C" {
 
+int cdg_gpu_fused_traces(const cdg_gpu_level* lv) {
+  return (lv->use_row && lv->ks->row_ft && lv->n_curved == 0) ? 1 : 0;
+}
+
 const char* cdg_gpu_version(void) { return "cdg_gpu 0.1 (sm_100a, fp64 DMMA)"; }
 
 // out[0] = DMMA m16n8k4, out[1] = DFMA, out[2] = DMMA m16n8k8, out[3] = DMMA m16n8k16 TFLOP/s
@@ -678,7 +691,12 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
     };
     const std::vector<double> op2 = build_op2(lv->ks->ch, -1.0), opaux = build_op2(lv->ks->ch, 1.0);
     lv->frag_icub = dev_upload(make_frag(icub, ncub, np, ncub8, kp));
-    lv->frag_ig = dev_upload(make_frag(ig, nf, np, nf8, kp));
+    {  // I_g B fragments in the natural pairing (k_interp<NAT> + fused traces)
+      std::vector<double> fi;
+      for (int n = 0; n < nf8 / 8; ++n)
+        for (int k = 0; k < kp / 8; ++k) frag_nat(fi, ig, nf, np, n, k);
+      lv->frag_ig = dev_upload(fi);
+    }
     lv->frag_op2 = dev_upload(make_frag(op2, np, k2, np8, k2));
     lv->frag_aux = dev_upload(make_frag(opaux, np, k2, np8, k2));
     {  // A_k I_cub (N_p x N_p) for the affine aux-gradient volume term
@@ -702,6 +720,7 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
       for (int k = 0; k < k2 / 8; ++k)
         for (int n = 0; n < np8 / 8; ++n) frag_nat(f2, op2r, np, k2, n, k);
       lv->rfrag2 = dev_upload(f2);
+
       const char* nr = std::getenv("CDG_NOROW");
       lv->use_row = !(nr && std::atoi(nr));
     }
@@ -915,12 +934,14 @@ void cdg_gpu_level_destroy(cdg_gpu_level* lv) {
   cudaSetDevice(lv->device);
   if (lv->graph) cudaGraphExecDestroy(lv->graph);
   if (lv->graph_visc) cudaGraphExecDestroy(lv->graph_visc);
-  for (void* p : {(void*)lv->u, (void*)lv->res, (void*)lv->rhs, (void*)lv->traces, (void*)lv->before,
+  for (auto ge : lv->gft)
+    if (ge) cudaGraphExecDestroy(ge);
+  for (void* p : {(void*)lv->u, (void*)lv->res, (void*)lv->rhs, (void*)(lv->tbuf[1] ? lv->tbuf[0] : lv->traces), (void*)lv->before,
                   (void*)lv->q, (void*)lv->qtr, (void*)lv->qcub, (void*)lv->eps, (void*)lv->sqrt_eps, (void*)lv->d_vinv, (void*)lv->d_vcub, (void*)lv->d_wcub, (void*)lv->d_jac,
                   (void*)lv->d_curved_jac, (void*)lv->d_curved_slot,
                   (void*)lv->d_maxeps, (void*)lv->metric, (void*)lv->face, (void*)lv->conn,
                   (void*)lv->code_map, (void*)lv->h, (void*)lv->frag_icub, (void*)lv->frag_op2,
-                  (void*)lv->frag_ig, (void*)lv->frag_aux, (void*)lv->frag_dtil, (void*)lv->wfrag1, (void*)lv->wfrag2v, (void*)lv->wfrag2f, (void*)lv->rfrag2,
+                  (void*)lv->frag_ig, (void*)lv->frag_aux, (void*)lv->frag_dtil, (void*)lv->wfrag1, (void*)lv->wfrag2v, (void*)lv->wfrag2f, (void*)lv->rfrag2, (void*)lv->tbuf[1],
                   (void*)lv->curved_ids, (void*)lv->curved_jwr, (void*)lv->curved_minv, (void*)lv->frag_opc,
                   (void*)lv->curved_vol, (void*)lv->curved_face, (void*)lv->d_coef, (void*)lv->d_err,
                   (void*)lv->d_scratch, (void*)lv->d_send_idx, (void*)lv->d_recv_idx,
@@ -1082,6 +1103,74 @@ int cdg_gpu_rk_steps(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, int nstep
       lv->last_viscous = bits != 0;
       return;
     }
+    if (lv->use_row && lv->ks->row_ft && lv->n_curved == 0) {
+      // fused traces: each RHS launch writes the next stage's traces into the
+      // other half of a double buffer; one trace kernel per call seeds it
+      if (!lv->tbuf[1]) {
+        const size_t ntr = (size_t)(lv->K + lv->n_halo) * 5 * lv->tb;
+        CUDA_OK(cudaMalloc(&lv->tbuf[1], ntr * sizeof(double)));
+        CUDA_OK(cudaMemset(lv->tbuf[1], 0, ntr * sizeof(double)));
+        lv->tbuf[0] = lv->traces;
+        lv->tcur = 0;
+      }
+      auto stage_launch = [&](int b, int stage) {  // reads tbuf[(b+s)%2], writes the other
+        lv->traces = lv->tbuf[(b + stage) & 1];
+        lv->cur_traces_out = lv->tbuf[(b + stage + 1) & 1];
+        launch_rhs(lv, true, false, stage);
+        lv->cur_traces_out = nullptr;
+        lv->traces = lv->tbuf[lv->tcur];
+      };
+      float t_tr = 0.f, t_rhs = 0.f;
+      if (lv->profiling) CUDA_OK(cudaEventRecord(lv->ev[0], lv->stream));
+      launch_traces(lv, lv->u, lv->traces);
+      if (lv->profiling) {
+        CUDA_OK(cudaEventRecord(lv->ev[1], lv->stream));
+        CUDA_OK(cudaEventSynchronize(lv->ev[1]));
+        CUDA_OK(cudaEventElapsedTime(&t_tr, lv->ev[0], lv->ev[1]));
+        for (int s = 0; s < nsteps; ++s) {
+          for (int stage = 0; stage < 5; ++stage) {
+            CUDA_OK(cudaEventRecord(lv->ev[1], lv->stream));
+            stage_launch(lv->tcur, stage);
+            CUDA_OK(cudaEventRecord(lv->ev[2], lv->stream));
+            CUDA_OK(cudaEventSynchronize(lv->ev[2]));
+            float y;
+            CUDA_OK(cudaEventElapsedTime(&y, lv->ev[1], lv->ev[2]));
+            t_rhs += y;
+          }
+          lv->tcur ^= 1;
+          lv->traces = lv->tbuf[lv->tcur];
+        }
+        lv->prof[0] = t_tr;
+        lv->prof[1] = t_rhs;
+        lv->prof[2] = 5.0 * nsteps + 1;
+      } else {
+        for (int s = 0; s < nsteps; ++s) {
+          const int b = lv->tcur;
+          if (!lv->gft[b] || lv->gft_riemann[b] != cfg->riemann || lv->gft_gamma[b] != cfg->gamma) {
+            if (lv->gft[b]) cudaGraphExecDestroy(lv->gft[b]);
+            lv->gft[b] = nullptr;
+            cudaGraph_t g;
+            const long long l0 = lv->launches;
+            CUDA_OK(cudaStreamBeginCapture(lv->stream, cudaStreamCaptureModeThreadLocal));
+            for (int stage = 0; stage < 5; ++stage) stage_launch(b, stage);
+            lv->gft_launches = (int)(lv->launches - l0);
+            lv->launches = l0;
+            CUDA_OK(cudaStreamEndCapture(lv->stream, &g));
+            CUDA_OK(cudaGraphInstantiate(&lv->gft[b], g, 0));
+            CUDA_OK(cudaGraphDestroy(g));
+            lv->gft_riemann[b] = cfg->riemann;
+            lv->gft_gamma[b] = cfg->gamma;
+          }
+          CUDA_OK(cudaGraphLaunch(lv->gft[b], lv->stream));
+          lv->launches += lv->gft_launches;
+          lv->tcur ^= 1;
+          lv->traces = lv->tbuf[lv->tcur];
+        }
+      }
+      CUDA_OK(cudaGetLastError());
+      check_device_error(lv);
+      return;
+    }
     if (lv->profiling) {
       float t_tr = 0.f, t_rhs = 0.f;
       for (int s = 0; s < nsteps; ++s)
@@ -1146,6 +1235,11 @@ int cdg_gpu_set_freestream(cdg_gpu_level* lv, const double* fs) {
     cudaGraphExecDestroy(lv->graph_visc);
     lv->graph_visc = nullptr;
   }
+  for (auto& ge : lv->gft)
+    if (!same && ge) {
+      cudaGraphExecDestroy(ge);
+      ge = nullptr;
+    }
   for (int c = 0; c < 5; ++c) {
     lv->freestream[c] = fs[c];
     lv->gas.fs[c] = fs[c];

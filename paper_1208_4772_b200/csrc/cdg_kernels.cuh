@@ -340,7 +340,10 @@ __host__ __device__ constexpr int pack_face(int nface, int bc, int boundary, int
 // term, solver.cpp:364-369; NO = N_cub). Non-persistent (one tile per CTA,
 // several CTAs per SM): memory-bound.
 // ---------------------------------------------------------------------------
-template <class C, int NO, int LDO>
+// NAT: the U panel is staged in natural node order and frag_op uses the natural
+// pairing (k = t <-> node 8ks+2t, k = t+4 <-> 8ks+2t+1; cdg_warp.cuh), which is
+// the pairing the row kernel's fused traces use -- both then agree bit for bit.
+template <class C, int NO, int LDO, bool NAT = false>
 __global__ void __launch_bounds__(kThreads)
 k_interp(const double* __restrict__ u, double* __restrict__ out, const double* __restrict__ frag_op, int n_rows,
          int n_tiles, const unsigned long long* gate, int gate_when) {
@@ -354,7 +357,17 @@ k_interp(const double* __restrict__ u, double* __restrict__ out, const double* _
   const double2* fb = reinterpret_cast<const double2*>(frag_op);
   for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const int row0 = tile * C::R;
-    stage_rows<C>(u, row0, n_rows, sU, tid);
+    if (NAT) {
+      constexpr int V = C::KP / 2;
+      for (int idx = tid; idx < C::R * V; idx += kThreads) {
+        const int r = idx / V, j = idx - r * V;
+        double2 x = make_double2(0.0, 0.0);
+        if (row0 + r < n_rows) x = *reinterpret_cast<const double2*>(u + (size_t)(row0 + r) * C::BP + 2 * j);
+        *reinterpret_cast<double2*>(sU + r * C::LDU + 2 * j) = x;
+      }
+    } else {
+      stage_rows<C>(u, row0, n_rows, sU, tid);
+    }
     __syncthreads();
     for (int t = warp; t < T; t += kWarps) {
       const int mt = t / NT, nt = t % NT;
@@ -407,6 +420,8 @@ struct RhsParams {
   int n_list;                 // entries of `tiles`
   const unsigned long long* gate;  // optional launch gate (see gated_off)
   int gate_when;
+  double* traces_out;         // fused traces of u_new (k_rhs_row MODE 32)
+  const double* frag_ig_nat;  // I_g B fragments, natural pairing
 };
 
 // i-th tile of a launch: the tile list when given, else tile i

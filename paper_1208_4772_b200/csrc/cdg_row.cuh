@@ -41,6 +41,9 @@ struct RCfg {
   static constexpr int E = E_, R = 5 * E_, NW = R / 16, NTH = 32 * NW, MINB = MINB_;
   static constexpr bool OPRING = MODE_ & 1, RESS = MODE_ & 4, USMEM = MODE_ & 8;
   static constexpr bool UREG = (MODE_ & 2) && !USMEM;
+  // 32: fused traces -- the epilogue also writes I_g u_new (the next stage's
+  // face traces) to p.traces_out, which replaces the separate trace kernel
+  static constexpr bool FT = MODE_ & 32;
   static constexpr int BP = round_up(NP, 16), TB = round_up(NF, 16);
   static constexpr int KP = round_up(NP, 8), KS1 = KP / 8, NT2 = KS1;
   static constexpr int NCUB8 = round_up(NCUB, 8), NF8 = round_up(NF, 8);
@@ -453,9 +456,54 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_row(RhsParams p) {
           } else {
             u0 = hh ? uA[j][1] : uA[j][0], u1 = hh ? uA[j][3] : uA[j][2];
           }
-          *reinterpret_cast<double2*>(p.u + rowoff + col) = make_double2(u0 + b_c * n0, u1 + b_c * n1);
+          const double w0 = u0 + b_c * n0, w1 = u1 + b_c * n1;
+          *reinterpret_cast<double2*>(p.u + rowoff + col) = make_double2(w0, w1);
+          if (C::FT) {  // keep u_new in the accumulator (= A fragment) layout
+            acc[j][2 * hh] = w0;
+            acc[j][2 * hh + 1] = w1;
+          }
         } else {
           *reinterpret_cast<double2*>(p.rhs_out + rowoff + col) = make_double2(r0, r1);
+        }
+      }
+    }
+    if (UPDATE && C::FT && p.traces_out) {
+      // next stage's traces  T = u_new I_g^T  (solver.cpp:200-208) from the
+      // registers: accumulator fragment of n-tile j == A fragment of k-step j
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int grow = hh ? r_hi : r_lo;
+        if (grow >= n_rows || (hh ? cur_hi : cur_lo))
+#pragma unroll
+          for (int j = 0; j < C::NT2; ++j) acc[j][2 * hh] = acc[j][2 * hh + 1] = 0.0;
+      }
+      constexpr int NFT = C::NF8 / 8;
+      // natural pairing (accumulator fragment of n-tile j == A fragment of
+      // k-step j), the pairing of the trace kernel too (k_interp<NAT>): fused
+      // and separate traces agree bit for bit
+      const double2* fbi = reinterpret_cast<const double2*>(p.frag_ig_nat);  // [NFT][KS1][32]
+      AFrag fa[C::KS1];
+#pragma unroll
+      for (int ks = 0; ks < C::KS1; ++ks) fa[ks] = AFrag{acc[ks][0], acc[ks][2], acc[ks][1], acc[ks][3]};
+#pragma unroll 1
+      for (int nt0 = 0; nt0 < NFT; nt0 += 4) {
+        double tacc[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) tacc[i][0] = tacc[i][1] = tacc[i][2] = tacc[i][3] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < C::KS1; ++ks)
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (nt0 + i < NFT) mma_frag(tacc[i], fa[ks], __ldg(fbi + ((size_t)(nt0 + i) * C::KS1 + ks) * 32 + lane));
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int col = (nt0 + i) * 8 + 2 * tq;
+          if (nt0 + i < NFT && col < C::NF) {
+            if (r_lo < n_rows)
+              *reinterpret_cast<double2*>(p.traces_out + (size_t)r_lo * C::TB + col) = make_double2(tacc[i][0], tacc[i][1]);
+            if (r_hi < n_rows)
+              *reinterpret_cast<double2*>(p.traces_out + (size_t)r_hi * C::TB + col) = make_double2(tacc[i][2], tacc[i][3]);
+          }
         }
       }
     }

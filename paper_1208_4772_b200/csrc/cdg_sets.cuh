@@ -41,6 +41,7 @@ struct KernelSet {
   void (*row_only[2])(RhsParams) = {nullptr, nullptr};
   size_t smem_row = 0;
   int row_minb = 0, row_ch = 0, row_e = 16, row_nth = 160;
+  bool row_ft = false;  // row kernel writes the next stage's traces (MODE 32)
 };
 
 template <int NP, int NCUB, int NG, int CH = 8, int FCH = 32, int MINB = 3, int MODE = 7, int E = 16>
@@ -55,6 +56,7 @@ KernelSet with_row(KernelSet k) {
   k.row_ch = CH;
   k.row_e = RC::E;
   k.row_nth = RC::NTH;
+  k.row_ft = RC::FT;
   return k;
 }
 
@@ -106,7 +108,7 @@ KernelSet make_set() {
   k.smem_traces = sizeof(double) * C8::R * C8::LDU;
   k.smem_rhs = C::SMEM_BYTES;
   k.smem_aux = C8::SMEM_BYTES;
-  k.traces = &k_interp<C8, C8::NF, C8::TB>;
+  k.traces = &k_interp<C8, C8::NF, C8::TB, true>;
   k.cubinterp = &k_interp<C8, C8::NCUB, round_up(NCUB, 8)>;
   k.rhs_update = &k_rhs<C, true, false>;
   k.rhs_only = &k_rhs<C, false, false>;

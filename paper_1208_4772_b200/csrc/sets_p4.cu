@@ -7,7 +7,8 @@ namespace cdg_gpu {
 
 std::vector<KernelSet> kernel_sets_p4() {
   return {
-      with_row<35, 70, 16, 8, 32, 4, 0>(make_set<35, 70, 16, 16, 24, 2, 64>()),
+      // default: row kernel with fused traces (the next stage's traces from its epilogue)
+      with_row<35, 70, 16, 8, 32, 4, 32>(make_set<35, 70, 16, 16, 24, 2, 64>()),
       with_row<35, 70, 56, 8, 32, 4, 0>(make_set<35, 70, 56, 16, 24, 2>()),
       // P=4 straight tuning variants, selected with CDG_KCFG=<n> (bench sweeps;
       // DESIGN.md §6 lists what each measured)
@@ -18,7 +19,8 @@ std::vector<KernelSet> kernel_sets_p4() {
       with_row<35, 70, 16, 8, 32, 4, 4>(make_set<35, 70, 16, 16, 24, 2, 64>()),   // 5 res staged in smem
       with_row<35, 70, 16, 8, 32, 3, 2>(make_set<35, 70, 16, 16, 24, 2, 64>()),   // 6 U in registers, 3 CTAs
       with_rowp<35, 70, 16, 4, false>(make_set<35, 70, 16, 16, 24, 2, 64>()),     // 7 pipelined chunks
-      with_row<35, 70, 16, 8, 32, 2, 0, 32>(make_set<35, 70, 16, 16, 24, 2, 64>())};  // 8 32-element tiles
+      with_row<35, 70, 16, 8, 32, 2, 0, 32>(make_set<35, 70, 16, 16, 24, 2, 64>()),  // 8 32-element tiles
+      with_row<35, 70, 16, 8, 32, 4, 0>(make_set<35, 70, 16, 16, 24, 2, 64>())};      // 9 separate trace kernel
 }
 
 }  // namespace cdg_gpu

@@ -122,6 +122,7 @@ def lib():
         L.cdg_gpu_version.restype = C.c_char_p
         L.cdg_gpu_measure_fp64_peak.argtypes = [C.c_int, _dp]
         L.cdg_gpu_fill_freestream.argtypes = [vp]
+        L.cdg_gpu_fused_traces.argtypes = [vp]
         L.cdg_gpu_p_refine_embed.argtypes = [vp, vp, _dp]
         L.cdg_gpu_run_level.argtypes = [vp, C.POINTER(RunConfig), C.POINTER(SteadyParams), _dp, C.c_int, _ip, _ip,
                                         C.c_char_p, C.c_size_t]
@@ -288,6 +289,9 @@ class GpuLevel:
         out = np.zeros(1)
         _raise(lib().cdg_gpu_residual(self.h, 1 if kind == "l2" else 0, dt, _p(out)), "residual failed")
         return float(out[0])
+
+    def fused_traces(self) -> bool:
+        return bool(lib().cdg_gpu_fused_traces(self.h))
 
     def launch_count(self) -> int:
         return int(lib().cdg_gpu_launch_count(self.h))
