@@ -205,6 +205,7 @@ struct cdg_gpu_level {
   double* rfrag2 = nullptr;  // row kernel (its I_cub fragments are wfrag1)
   double* tbuf[2] = {nullptr, nullptr};  // trace double buffer of the fused-trace path
   int tcur = 0;                          // tbuf[tcur] == traces (current)
+  bool traces_valid = false;             // traces == I_g u for the current u (owned rows)
   double* cur_traces_out = nullptr;
   cudaGraphExec_t gft[2] = {nullptr, nullptr};
   int gft_riemann[2] = {-1, -1};
@@ -263,6 +264,7 @@ void check_device_error(cdg_gpu_level* lv) {
                           lv->stream));
   CUDA_OK(cudaStreamSynchronize(lv->stream));
   if (lv->h_err->flag) {
+    lv->traces_valid = false;  // an aborted fused stage leaves partial traces
     const DevError e = *lv->h_err;
     CUDA_OK(cudaMemsetAsync(lv->d_err, 0, sizeof(DevError), lv->stream));
     CUDA_OK(cudaStreamSynchronize(lv->stream));
@@ -287,6 +289,24 @@ void launch_traces(cdg_gpu_level* lv, const double* u, double* traces) {
   lv->ks->traces<<<tiles, kThreads, lv->ks->smem_traces, lv->stream>>>(
       u, traces, lv->frag_ig, lv->n_rows(), tiles, lv->cur_gate, lv->cur_gate_when);
   ++lv->launches;
+}
+
+bool fused_traces(const cdg_gpu_level* lv) { return lv->use_row && lv->ks->row_ft && lv->n_curved == 0; }
+
+void ensure_tbuf(cdg_gpu_level* lv) {
+  if (lv->tbuf[1]) return;
+  const size_t ntr = (size_t)(lv->K + lv->n_halo) * 5 * lv->tb;
+  CUDA_OK(cudaMalloc(&lv->tbuf[1], ntr * sizeof(double)));
+  CUDA_OK(cudaMemset(lv->tbuf[1], 0, ntr * sizeof(double)));
+  lv->tbuf[0] = lv->traces;
+  lv->tcur = 0;
+}
+
+// the traces of the current u, unless they are already there
+void seed_traces(cdg_gpu_level* lv) {
+  if (lv->traces_valid) return;
+  launch_traces(lv, lv->u, lv->traces);
+  lv->traces_valid = true;
 }
 
 RhsParams rhs_params(cdg_gpu_level* lv, int stage) {
@@ -980,6 +1000,7 @@ static void copy_rows(cdg_gpu_level* lv, double* dst, int dst_block, const doubl
 }
 
 int cdg_gpu_set_state(cdg_gpu_level* lv, const double* u, const double* res) {
+  lv->traces_valid = false;
   return guarded(nullptr, 0, [&] {
     CUDA_OK(cudaSetDevice(lv->device));
     copy_rows(lv, lv->u, lv->bp, u, lv->caller_block, lv->np, lv->n_rows(), cudaMemcpyHostToDevice);
@@ -992,6 +1013,7 @@ int cdg_gpu_set_state(cdg_gpu_level* lv, const double* u, const double* res) {
 }
 
 int cdg_gpu_set_state_device(cdg_gpu_level* lv, const double* u, const double* res) {
+  lv->traces_valid = false;
   return guarded(nullptr, 0, [&] {
     CUDA_OK(cudaSetDevice(lv->device));
     copy_rows(lv, lv->u, lv->bp, u, lv->caller_block, lv->np, lv->n_rows(), cudaMemcpyDeviceToDevice);
@@ -1070,6 +1092,7 @@ int cdg_gpu_rk_steps(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, int nstep
       // viscous_active (solver.cpp:257-259) is decided per stage on the device
       // (gated kernels), so one viscous RK step is a CUDA graph as well
       ensure_viscous_buffers(lv, cfg);
+      lv->traces_valid = false;
       if (!lv->graph_visc || std::memcmp(&lv->graph_visc_cfg, cfg, sizeof *cfg) != 0) {
         if (lv->graph_visc) {
           cudaGraphExecDestroy(lv->graph_visc);
@@ -1103,16 +1126,11 @@ int cdg_gpu_rk_steps(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, int nstep
       lv->last_viscous = bits != 0;
       return;
     }
-    if (lv->use_row && lv->ks->row_ft && lv->n_curved == 0) {
+    if (fused_traces(lv)) {
       // fused traces: each RHS launch writes the next stage's traces into the
-      // other half of a double buffer; one trace kernel per call seeds it
-      if (!lv->tbuf[1]) {
-        const size_t ntr = (size_t)(lv->K + lv->n_halo) * 5 * lv->tb;
-        CUDA_OK(cudaMalloc(&lv->tbuf[1], ntr * sizeof(double)));
-        CUDA_OK(cudaMemset(lv->tbuf[1], 0, ntr * sizeof(double)));
-        lv->tbuf[0] = lv->traces;
-        lv->tcur = 0;
-      }
+      // other half of a double buffer; a trace kernel seeds it only when the
+      // state changed since the last fused stage
+      ensure_tbuf(lv);
       auto stage_launch = [&](int b, int stage) {  // reads tbuf[(b+s)%2], writes the other
         lv->traces = lv->tbuf[(b + stage) & 1];
         lv->cur_traces_out = lv->tbuf[(b + stage + 1) & 1];
@@ -1122,7 +1140,7 @@ int cdg_gpu_rk_steps(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, int nstep
       };
       float t_tr = 0.f, t_rhs = 0.f;
       if (lv->profiling) CUDA_OK(cudaEventRecord(lv->ev[0], lv->stream));
-      launch_traces(lv, lv->u, lv->traces);
+      seed_traces(lv);
       if (lv->profiling) {
         CUDA_OK(cudaEventRecord(lv->ev[1], lv->stream));
         CUDA_OK(cudaEventSynchronize(lv->ev[1]));
@@ -1167,10 +1185,12 @@ int cdg_gpu_rk_steps(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, int nstep
           lv->traces = lv->tbuf[lv->tcur];
         }
       }
+      lv->traces_valid = true;
       CUDA_OK(cudaGetLastError());
       check_device_error(lv);
       return;
     }
+    lv->traces_valid = false;  // the unfused paths leave the previous stage's traces
     if (lv->profiling) {
       float t_tr = 0.f, t_rhs = 0.f;
       for (int s = 0; s < nsteps; ++s)
@@ -1337,6 +1357,7 @@ int cdg_gpu_residual(cdg_gpu_level* lv, int kind, double dt, double* out) {
 
 // ---- device-resident run_steady -----------------------------------------------
 int cdg_gpu_fill_freestream(cdg_gpu_level* lv) {
+  lv->traces_valid = false;
   return guarded(nullptr, 0, [&] {
     CUDA_OK(cudaSetDevice(lv->device));
     const size_t rows = (size_t)lv->K * 5, n = rows * lv->bp;
@@ -1349,6 +1370,7 @@ int cdg_gpu_fill_freestream(cdg_gpu_level* lv) {
 }
 
 int cdg_gpu_p_refine_embed(cdg_gpu_level* to, const cdg_gpu_level* from, const double* embed) {
+  to->traces_valid = false;
   return guarded(nullptr, 0, [&] {
     if (to->K != from->K || to->device != from->device)
       throw Status(CDG_GPU_ERR_CONFIG, "p_refine_embed: levels differ in element count or device");
@@ -1491,6 +1513,34 @@ int cdg_gpu_rk_stage_phase(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, int
       throw Status(CDG_GPU_ERR_CONFIG, "split-phase stages support the inviscid path only");
     lv->gas.gamma = cfg->gamma;
     lv->gas.riemann = cfg->riemann;
+    const bool ft = fused_traces(lv);
+    if (ft) ensure_tbuf(lv);
+    // fused traces: the RHS of stage s writes the traces of stage s+1 into the
+    // other buffer (owned rows); the ghost rows arrive by the halo exchange
+    auto rhs = [&](const int* tiles, int n_list) {
+      lv->cur_tiles = tiles;
+      lv->cur_n_list = n_list;
+      if (ft) lv->cur_traces_out = lv->tbuf[lv->tcur ^ 1];
+      try {
+        launch_rhs(lv, true, false, stage);
+      } catch (...) {
+        lv->cur_tiles = nullptr;
+        lv->cur_traces_out = nullptr;
+        throw;
+      }
+      lv->cur_tiles = nullptr;
+      lv->cur_n_list = 0;
+      lv->cur_traces_out = nullptr;
+    };
+    auto swap = [&] {
+      if (ft) {
+        lv->tcur ^= 1;
+        lv->traces = lv->tbuf[lv->tcur];
+        lv->traces_valid = true;
+      } else {
+        lv->traces_valid = false;
+      }
+    };
     if (phase == 0) {
       if (stage == 0) {
         lv->h_coef->dt = dt;
@@ -1501,7 +1551,10 @@ int cdg_gpu_rk_stage_phase(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, int
         CUDA_OK(cudaMemcpyAsync(lv->d_coef, lv->h_coef, sizeof(StageCoef), cudaMemcpyHostToDevice,
                                 lv->stream));
       }
-      launch_traces(lv, lv->u, lv->traces);
+      if (ft)
+        seed_traces(lv);
+      else
+        launch_traces(lv, lv->u, lv->traces);
       if (lv->n_send)
         k_halo_copy<<<(lv->n_send + 7) / 8, 256, 0, lv->stream>>>(lv->traces, lv->send_buf, lv->d_send_idx,
                                                                    lv->n_send, lv->ng, lv->tb, 0);
@@ -1509,7 +1562,8 @@ int cdg_gpu_rk_stage_phase(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, int
       if (lv->n_recv)
         k_halo_copy<<<(lv->n_recv + 7) / 8, 256, 0, lv->stream>>>(lv->traces, lv->recv_buf, lv->d_recv_idx,
                                                                    lv->n_recv, lv->ng, lv->tb, 1);
-      launch_rhs(lv, true, false, stage);
+      rhs(nullptr, 0);
+      swap();
       if (stage == 4) check_device_error(lv);
     } else {
       // 2: interior tiles (overlaps the halo exchange); 3: unpack + halo tiles
@@ -1518,18 +1572,14 @@ int cdg_gpu_rk_stage_phase(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, int
         k_halo_copy<<<(lv->n_recv + 7) / 8, 256, 0, lv->stream>>>(lv->traces, lv->recv_buf, lv->d_recv_idx,
                                                                    lv->n_recv, lv->ng, lv->tb, 1);
       if (!lv->d_tiles_int && !lv->d_tiles_halo) throw Status(CDG_GPU_ERR_CONFIG, "phases 2/3 need halo_setup");
-      lv->cur_tiles = phase == 2 ? lv->d_tiles_int : lv->d_tiles_halo;
-      lv->cur_n_list = phase == 2 ? lv->n_tiles_int : lv->n_tiles_halo;
-      if (!lv->cur_tiles) lv->cur_tiles = phase == 2 ? lv->d_tiles_halo : lv->d_tiles_int;  // empty list
-      try {
-        launch_rhs(lv, true, false, stage);
-      } catch (...) {
-        lv->cur_tiles = nullptr;
-        throw;
+      const int* tl = phase == 2 ? lv->d_tiles_int : lv->d_tiles_halo;
+      const int nl = phase == 2 ? lv->n_tiles_int : lv->n_tiles_halo;
+      if (!tl) tl = phase == 2 ? lv->d_tiles_halo : lv->d_tiles_int;  // empty list
+      rhs(tl, nl);
+      if (phase == 3) {
+        swap();
+        if (stage == 4) check_device_error(lv);
       }
-      lv->cur_tiles = nullptr;
-      lv->cur_n_list = 0;
-      if (phase == 3 && stage == 4) check_device_error(lv);
     }
     CUDA_OK(cudaGetLastError());
   });
