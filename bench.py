@@ -198,11 +198,21 @@ def main():
     import torch
     from paper_1208_4772_b200 import gpu, partition, refelem as R
 
+    # CDG_BENCH_DIST=gloo (+ CDG_BENCH_ONE_GPU=1): functional check of the
+    # multi-rank path on a 1-GPU box (halo buffers staged through the host);
+    # never used for measurements
+    backend = os.environ.get("CDG_BENCH_DIST", "nccl")
+    if os.environ.get("CDG_BENCH_ONE_GPU"):
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
+    red_dev = "cuda" if backend == "nccl" else "cpu"
 
     p = args.p
     re = R.get_reference_element(p)
@@ -232,7 +242,7 @@ def main():
     torch.cuda.empty_cache()
     dt = lv.compute_timestep(cfg)
     if dist is not None:
-        t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        t = torch.tensor([dt], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MIN)
         dt = float(t.item())
     setup_s = time.perf_counter() - t_setup
@@ -261,6 +271,20 @@ def main():
         with torch.cuda.stream(ext):
             for stage in range(5):
                 lv.stage_phase(cfg, stage, 0, dt)
+                if backend != "nccl":  # host-staged functional path (gloo)
+                    ext.synchronize()
+                    hs = [(peer, sb.cpu(), torch.empty_like(rb, device="cpu"), rb) for peer, sb, rb in bufs]
+                    works = []
+                    for peer, hsb, hrb, _ in hs:
+                        works.append(dist.isend(hsb, peer))
+                        works.append(dist.irecv(hrb, peer))
+                    lv.stage_phase(cfg, stage, 2, dt)
+                    for w in works:
+                        w.wait()
+                    for _, _, hrb, rb in hs:
+                        rb.copy_(hrb)
+                    lv.stage_phase(cfg, stage, 3, dt)
+                    continue
                 ops = []
                 for peer, sb, rb in bufs:
                     ops.append(dist.P2POp(dist.isend, sb, peer))
@@ -307,7 +331,7 @@ def main():
     launches = lv.launch_count() - launches0
     ms_total = ev0.elapsed_time(ev1)
     if dist is not None:
-        t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+        t = torch.tensor([ms_total], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     K_global = 6 * args.n ** 3
@@ -317,6 +341,28 @@ def main():
 
     # ---- end-to-end through the public API with host buffers -----------------
     e2e = None
+    if not args.no_e2e and world > 1:
+        # per step and rank: snapshot + one halo-exchanging RK step + the
+        # residual's inf-norm partials D2H, all-reduced (MAX) over ranks; wall
+        # clock, max over ranks
+        steps = max(3, args.steps // 2)
+        step_multi()
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            lv.snapshot()
+            step_multi()
+            r = torch.tensor([lv.residual(dt, "inf")], dtype=torch.float64, device=red_dev)
+            dist.all_reduce(r, op=dist.ReduceOp.MAX)
+        t_e2e = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=red_dev)
+        dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
+        t_e2e = float(t_e2e.item())
+        assert math.isfinite(float(r.item()))
+        e2e = {"value": dofs_per_step * steps / t_e2e, "unit": "DOF-updates/s",
+               "h2d_bytes_per_step": world * 8 * 11, "d2h_bytes_per_step": world * 8 * 592,
+               "what": "per step on every rank: snapshot + 5 x stage_phase 0/2/3 with the halo exchange + "
+                       "cdg_gpu_residual (inf-norm partials D2H) + all-reduce MAX; wall clock, max over ranks"}
     if not args.no_e2e and world == 1:
         # per step: H2D of dt/RK coefficients (pinned), RK step, D2H residual
         steps = max(3, args.steps // 2)
@@ -399,7 +445,9 @@ def main():
                        "elements": K_global, "p": p, "riemann": args.riemann, "dof": K_global * npb * 5,
                        "partition": f"{world} z-slab(s)", "l2": "working set ~%.0f GB >> 126 MB L2 (no flush needed)"
                        % (K_global * (3 * 5 * lv.device_block + 5 * lv.trace_block) * 8 / 1e9),
-                       "setup_s": round(setup_s, 1)},
+                       "setup_s": round(setup_s, 1),
+                       **({"dist_backend": backend + " (host-staged halos; functional check, not a measurement)"}
+                          if world > 1 and backend != "nccl" else {})},
             "gpu_launches": launches, "clocks": clocks}
     if e2e:
         line["e2e"] = e2e
