@@ -21,7 +21,7 @@ struct CurvedParams {
   const int* ids;          // [Kc] element ids
   const double* jwr;       // [Kc][NCUB][9]  J W dr_m/dx_d  (m*3+d)
   const double4* face;     // [Kc][NF]       (nx, ny, nz, sjac*w)
-  const double* minv;      // [Kc][NP][NP]
+  const double* minv;      // [Kc][NP][NP], transposed: (M_e^-1)[i][j] at [c][j][i]
   const double* frag_opc;  // B fragments of [D^T | -I_g^T]
   double* vol;             // [Kc*5][NP8] epilogue scratch when the tile's vol does not fit smem
   double* q_out;           // [3][K*5][BP] aux gradient (k_aux_curved)
@@ -236,11 +236,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_rhs_curved(CurvedParams cp) {
       const int e = idx / C::NP, i = idx - e * C::NP;
       const int ce = c0 + e;
       if (ce >= cp.Kc) continue;
-      const double* mrow = cp.minv + ((size_t)ce * C::NP + i) * C::NP;
+      const double* mcol = cp.minv + (size_t)ce * C::NP * C::NP + i;  // (M_e^-1)[i][j] at j*NP + i
       const double* v = vbase + (e * 5) * L::LDV;
       double rhs[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
       for (int j = 0; j < C::NP; ++j) {
-        const double mij = __ldg(mrow + j);
+        const double mij = __ldg(mcol + (size_t)j * C::NP);
 #pragma unroll
         for (int f = 0; f < 5; ++f) rhs[f] += mij * v[f * L::LDV + j];
       }
@@ -399,11 +399,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_aux_curved(CurvedParams cp) {
         const int e = idx / C::NP, i = idx - e * C::NP;
         const int ce = c0 + e;
         if (ce >= cp.Kc) continue;
-        const double* mrow = cp.minv + ((size_t)ce * C::NP + i) * C::NP;
+        const double* mcol = cp.minv + (size_t)ce * C::NP * C::NP + i;
         const double* v = vbase + (e * 5) * L::LDV;
         double qv[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
         for (int j = 0; j < C::NP; ++j) {
-          const double mij = __ldg(mrow + j);
+          const double mij = __ldg(mcol + (size_t)j * C::NP);
 #pragma unroll
           for (int f = 0; f < 5; ++f) qv[f] += mij * v[f * L::LDV + j];
         }

@@ -225,6 +225,10 @@ struct cdg_gpu_level {
   int n_curved = 0;
   int* curved_ids = nullptr;
   double *curved_jwr = nullptr, *curved_minv = nullptr, *frag_opc = nullptr, *curved_vol = nullptr;
+  double* rfrag_opc = nullptr;  // [D^T | -I_g^T] for k_rhs_rowc (natural pairing)
+  bool use_rowc = false;
+  int* d_affine_tiles = nullptr;  // 16-element tiles holding an affine element (curved levels)
+  int n_affine_tiles = 0;
   double4* curved_face = nullptr;
   // control
   StageCoef* d_coef = nullptr;
@@ -309,10 +313,20 @@ void seed_traces(cdg_gpu_level* lv) {
   lv->traces_valid = true;
 }
 
+// tile list of the next affine-kernel launch: the phase list (multi-GPU), else
+// on a curved level the tiles that hold an affine element, else all (null)
+const int* affine_tiles(const cdg_gpu_level* lv, int* n_list) {
+  if (lv->cur_tiles) {
+    *n_list = lv->cur_n_list;
+    return lv->cur_tiles;
+  }
+  *n_list = lv->n_affine_tiles;
+  return lv->d_affine_tiles;
+}
+
 RhsParams rhs_params(cdg_gpu_level* lv, int stage) {
   RhsParams p{};
-  p.tiles = lv->cur_tiles;
-  p.n_list = lv->cur_n_list;
+  p.tiles = affine_tiles(lv, &p.n_list);
   p.gate = lv->cur_gate;
   p.gate_when = lv->cur_gate_when;
   p.traces_out = lv->cur_traces_out;
@@ -357,6 +371,17 @@ void launch_curved(cdg_gpu_level* lv, bool update, int stage, int mode = 0) {
   cp.vol = lv->curved_vol;
   cp.q_out = lv->q;
   cp.Kc = lv->n_curved;
+  if (mode == 0 && lv->use_rowc) {  // row-per-warp curved kernel (cdg_rowc.cuh)
+    cp.base.frag_icub = lv->wfrag1;
+    cp.frag_opc = lv->rfrag_opc;
+    const int rm = lv->gas.riemann == 1 ? 1 : 0;
+    auto fr = update ? lv->ks->rowc_update[rm] : lv->ks->rowc_only[rm];
+    const int tiles = (lv->n_curved + lv->ks->rowc_e - 1) / lv->ks->rowc_e;
+    fr<<<std::max(1, std::min(tiles, lv->n_sms * lv->ks->rowc_minb)), lv->ks->rowc_nth, lv->ks->smem_rowc,
+         lv->stream>>>(cp);
+    ++lv->launches;
+    return;
+  }
   const int tiles = (lv->n_curved + lv->ks->E - 1) / lv->ks->E;
   auto fn = mode == 2 ? lv->ks->aux_curved
                       : mode == 1 ? (update ? lv->ks->curved_visc_update : lv->ks->curved_visc_only)
@@ -384,12 +409,14 @@ void launch_rhs_warp(cdg_gpu_level* lv, bool update, int stage) {
   w.elem_offset = 0;
   w.gas = lv->gas;
   w.err = lv->d_err;
-  w.tiles = lv->cur_tiles;
-  w.n_list = lv->cur_n_list;
+  w.tiles = affine_tiles(lv, &w.n_list);
   w.gate = lv->cur_gate;
   w.gate_when = lv->cur_gate_when;
-  const int tiles = lv->cur_tiles ? lv->cur_n_list : (lv->K + 15) / 16;
-  if (tiles == 0) return;
+  const int tiles = w.tiles ? w.n_list : (lv->K + 15) / 16;
+  if (tiles == 0) {
+    launch_curved(lv, update, stage);
+    return;
+  }
   const int ctas = std::max(1, std::min((tiles + lv->ks->warp_warps - 1) / lv->ks->warp_warps,
                                         lv->n_sms * lv->ks->warp_minb));
   const int rm = lv->gas.riemann == 1 ? 1 : 0;
@@ -410,8 +437,11 @@ void launch_rhs_row(cdg_gpu_level* lv, bool update, int stage) {
   const int rm = lv->gas.riemann == 1 ? 1 : 0;
   auto fn = update ? lv->ks->row_update[rm] : lv->ks->row_only[rm];
   const int E = lv->ks->row_e;
-  const int tiles = lv->cur_tiles ? lv->cur_n_list : (lv->K + E - 1) / E;
-  if (tiles == 0) return;
+  const int tiles = p.tiles ? p.n_list : (lv->K + E - 1) / E;
+  if (tiles == 0) {
+    launch_curved(lv, update, stage);
+    return;
+  }
   fn<<<std::max(1, std::min(tiles, lv->n_sms * lv->ks->row_minb)), lv->ks->row_nth, lv->ks->smem_row, lv->stream>>>(p);
   ++lv->launches;
   launch_curved(lv, update, stage);
@@ -427,8 +457,11 @@ void launch_rhs(cdg_gpu_level* lv, bool update, bool viscous, int stage) {
     return;
   }
   RhsParams p = rhs_params(lv, stage);
-  const int tiles = lv->cur_tiles ? lv->cur_n_list : lv->n_tiles();
-  if (tiles == 0) return;
+  const int tiles = p.tiles ? p.n_list : lv->n_tiles();
+  if (tiles == 0) {
+    launch_curved(lv, update, stage, viscous ? 1 : 0);
+    return;
+  }
   auto fn = viscous ? (update ? lv->ks->visc_rhs_update : lv->ks->visc_rhs_only)
                     : (update ? lv->ks->rhs_update : lv->ks->rhs_only);
   fn<<<lv->grid(tiles), lv->ks->nth, lv->ks->smem_rhs, lv->stream>>>(p);
@@ -857,7 +890,15 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
         cf[i] = make_double4(d->curved_face[4 * i], d->curved_face[4 * i + 1], d->curved_face[4 * i + 2],
                              d->curved_face[4 * i + 3]);
       lv->curved_face = dev_upload(cf);
-      lv->curved_minv = dev_upload(std::vector<double>(d->curved_minv, d->curved_minv + (size_t)d->n_curved * np * np));
+      {  // M_e^-1 transposed per element: the epilogue threads (consecutive
+         // output nodes i) then read consecutive addresses
+        std::vector<double> mt((size_t)d->n_curved * np * np);
+        for (int c = 0; c < d->n_curved; ++c)
+          for (int i = 0; i < np; ++i)
+            for (int j = 0; j < np; ++j)
+              mt[((size_t)c * np + j) * np + i] = d->curved_minv[((size_t)c * np + i) * np + j];
+        lv->curved_minv = dev_upload(mt);
+      }
       // [D_r^T D_s^T D_t^T | -I_g^T] in the chunked K layout of op2
       std::vector<double> opc((size_t)np * k2, 0.0);
       const int CHc = lv->ks->ch;
@@ -873,6 +914,42 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
       for (int i = 0; i < np; ++i)
         for (int fq = 0; fq < nf; ++fq) opc[(size_t)i * k2 + k2cub + fq] = -ig[(size_t)fq * np + i];
       lv->frag_opc = dev_upload(make_frag(opc, np, k2, np8, k2));
+      if (lv->ks->rowc_update[0]) {  // the same operator for k_rhs_rowc: its chunking, natural pairing
+        std::vector<double> opr((size_t)np * k2, 0.0);
+        const int CHr = lv->ks->rowc_ch;
+        for (int q0 = 0; q0 < ncub8; q0 += CHr) {
+          const int w = std::min(CHr, ncub8 - q0);
+          for (int m = 0; m < 3; ++m)
+            for (int ql = 0; ql < w; ++ql) {
+              const int q = q0 + ql;
+              if (q >= ncub) continue;
+              for (int i = 0; i < np; ++i) opr[(size_t)i * k2 + 3 * q0 + m * w + ql] = dm[m][(size_t)q * np + i];
+            }
+        }
+        for (int i = 0; i < np; ++i)
+          for (int fq = 0; fq < nf; ++fq) opr[(size_t)i * k2 + k2cub + fq] = -ig[(size_t)fq * np + i];
+        std::vector<double> f2;
+        for (int k = 0; k < k2 / 8; ++k)
+          for (int n = 0; n < np8 / 8; ++n) frag_nat(f2, opr, np, k2, n, k);
+        lv->rfrag_opc = dev_upload(f2);
+        if (lv->ks->warp_update[0] || lv->ks->row_update[0]) {
+          const char* nr = std::getenv("CDG_NOROWC");
+          lv->use_rowc = !(nr && std::atoi(nr));
+        }
+      }
+      // tiles of 16 elements with at least one affine element: the affine
+      // kernels skip the all-curved tiles
+      {
+        std::vector<int> at;
+        for (int t = 0; t * 16 < K; ++t) {
+          bool any = false;
+          for (int e = t * 16; e < std::min(K, t * 16 + 16); ++e) any = any || !is_curved[e];
+          if (any) at.push_back(t);
+        }
+        lv->n_affine_tiles = (int)at.size();
+        if (at.empty()) at.push_back(0);
+        lv->d_affine_tiles = dev_upload(at);
+      }
       // epilogue scratch for configurations whose vol panel does not fit smem (p=8)
       CUDA_OK(cudaMalloc(&lv->curved_vol, sizeof(double) * (size_t)d->n_curved * 5 * (np8 + 1)));
     }
@@ -963,7 +1040,7 @@ void cdg_gpu_level_destroy(cdg_gpu_level* lv) {
                   (void*)lv->code_map, (void*)lv->h, (void*)lv->frag_icub, (void*)lv->frag_op2,
                   (void*)lv->frag_ig, (void*)lv->frag_aux, (void*)lv->frag_dtil, (void*)lv->wfrag1, (void*)lv->wfrag2v, (void*)lv->wfrag2f, (void*)lv->rfrag2, (void*)lv->tbuf[1],
                   (void*)lv->curved_ids, (void*)lv->curved_jwr, (void*)lv->curved_minv, (void*)lv->frag_opc,
-                  (void*)lv->curved_vol, (void*)lv->curved_face, (void*)lv->d_coef, (void*)lv->d_err,
+                  (void*)lv->rfrag_opc, (void*)lv->d_affine_tiles, (void*)lv->curved_vol, (void*)lv->curved_face, (void*)lv->d_coef, (void*)lv->d_err,
                   (void*)lv->d_scratch, (void*)lv->d_send_idx, (void*)lv->d_recv_idx,
                   (void*)lv->d_tiles_int, (void*)lv->d_tiles_halo})
     if (p) cudaFree(p);

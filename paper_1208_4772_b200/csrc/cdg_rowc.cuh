@@ -1,0 +1,258 @@
+// cdg_rowc.cuh -- inviscid RHS + LSRK kernel for CURVED (isoparametric)
+// elements on the row-per-warp layout of k_rhs_row (cdg_row.cuh).
+//
+// Math as k_rhs_curved (cdg_curved.cuh; reference operators.cpp:32-167,
+// solver.cpp:362-464):
+//   vol = sum_m D_m^T (JW r_m . F) - I_g^T ((sjac w) F*),   rhs = M_e^-1 vol
+// Mapping as k_rhs_row: a CTA is 5E/16 warps on a tile of E curved elements
+// (consecutive entries of the curved list), warp w owns rows [16w, 16w+16)
+// of the (element, field) rows in both contractions, so each A fragment is
+// reused across all N_p/8 n-tiles and the B fragments of the shared
+// [D^T | -I_g^T] operator come from L1/L2 in the natural pairing. What is
+// per element here and shared there:
+//   * pointwise flux: the contravariant metric J W dr_m/dx_d is read per
+//     cubature node (9 doubles) instead of once per element;
+//   * face flux: (n, sjac w) per face node instead of per face;
+//   * epilogue: vol goes through shared memory and M_e^-1 (dense, per
+//     element, stored transposed so that the threads of a warp -- consecutive
+//     output nodes i -- read consecutive addresses) is applied as a SIMT GEMV,
+//     one thread per (element, node) for all five fields (on B200 the DFMA
+//     pipe matches the DMMA pipe per flop; the GEMV is ~5% of the work).
+#pragma once
+
+#include "cdg_curved.cuh"
+#include "cdg_row.cuh"
+
+namespace cdg_gpu {
+
+template <class C>
+struct RowCurvedLayout {
+  static constexpr int LDV = C::KP + 1;  // vol panel [R][LDV] (aliases the work area)
+  static constexpr int WORK = C::WORK > C::R * LDV ? C::WORK : C::R * LDV;
+  static constexpr size_t SMEM_BYTES = sizeof(double) * WORK + sizeof(int) * (C::E + C::E * 4 * 2);
+};
+
+template <class C, bool UPDATE, int RM>
+__global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_rowc(CurvedParams cp) {
+  using L = RowCurvedLayout<C>;
+  const RhsParams& p = cp.base;
+  if (gated_off(p.gate, p.gate_when)) return;
+  extern __shared__ __align__(16) double smem[];
+  double* sWork = smem;
+  int2* sConn = reinterpret_cast<int2*>(sWork + L::WORK);  // [E][4]
+  int* sId = reinterpret_cast<int*>(sConn + C::E * 4);     // [E] element ids of the tile
+  __shared__ int s_stop;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const double gamma = p.gas.gamma;
+  const int n_tiles = (cp.Kc + C::E - 1) / C::E;
+  const double2* fb1all = reinterpret_cast<const double2*>(p.frag_icub);
+  const double2* fb2all = reinterpret_cast<const double2*>(cp.frag_opc);
+  const int lr_lo = warp * 16 + g, lr_hi = lr_lo + 8;  // this thread's two tile rows
+
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int c0 = tile * C::E;  // index into the curved list
+    if (tid == 0) s_stop = *(volatile int*)&p.err->flag;
+    for (int idx = tid; idx < C::E; idx += C::NTH) sId[idx] = c0 + idx < cp.Kc ? __ldg(cp.ids + c0 + idx) : -1;
+    __syncthreads();
+    if (s_stop) return;  // block-uniform
+    for (int idx = tid; idx < C::E * 4; idx += C::NTH) {
+      const int e = sId[idx / 4];
+      sConn[idx] = e >= 0 ? p.conn[(size_t)e * 4 + idx % 4] : make_int2(-1, pack_face(0, 0, 1, 0));
+    }
+    const int el_lo = sId[lr_lo / 5], el_hi = sId[lr_hi / 5];
+    const bool ok_lo = el_lo >= 0, ok_hi = el_hi >= 0;
+    const double* u_lo = p.u + (ok_lo ? (size_t)el_lo * 5 + lr_lo % 5 : 0) * C::BP + 2 * tq;
+    const double* u_hi = p.u + (ok_hi ? (size_t)el_hi * 5 + lr_hi % 5 : 0) * C::BP + 2 * tq;
+
+    double acc[C::NT2][4];
+#pragma unroll
+    for (int i = 0; i < C::NT2; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.0;
+
+    // ---- volume: chunks of CH cubature nodes --------------------------------
+#pragma unroll 1
+    for (int ch = 0; ch < C::NCH; ++ch) {
+      const int q0 = ch * C::CH;
+      const int w = (C::NCUB8 - q0) < C::CH ? (C::NCUB8 - q0) : C::CH;
+      double* sC = sWork;
+      double* sG = sWork + C::R * C::LDC;
+      const double2* fb1 = fb1all + (size_t)(q0 / 8) * C::KS1 * 32;
+      const double2* fb2 = fb2all + (size_t)(3 * q0 / 8) * C::NT2 * 32;
+      {  // GEMM1: U_cub[rows, q0:q0+w], U rows as A fragments straight from HBM/L2
+        double c1[C::CH / 8][4];
+#pragma unroll
+        for (int j = 0; j < C::CH / 8; ++j) c1[j][0] = c1[j][1] = c1[j][2] = c1[j][3] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < C::KS1; ++ks) {
+          double2 x = make_double2(0.0, 0.0), y = make_double2(0.0, 0.0);
+          if (ok_lo) x = *reinterpret_cast<const double2*>(u_lo + ks * 8);
+          if (ok_hi) y = *reinterpret_cast<const double2*>(u_hi + ks * 8);
+#pragma unroll
+          for (int j = 0; j < C::CH / 8; ++j)
+            if (j * 8 < w) {
+              const double2 b = __ldg(fb1 + (j * C::KS1 + ks) * 32 + lane);
+              dmma_k8(c1[j], x.x, y.x, x.y, y.y, b.x, b.y);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < C::CH / 8; ++j)
+          if (j * 8 < w) {
+            double* o = sC + lr_lo * C::LDC + j * 8 + 2 * tq;
+            *reinterpret_cast<double2*>(o) = make_double2(c1[j][0], c1[j][1]);
+            *reinterpret_cast<double2*>(o + 8 * C::LDC) = make_double2(c1[j][2], c1[j][3]);
+          }
+      }
+      __syncthreads();
+      // pointwise Euler flux -> G_m = sum_d (J W dr_m/dx_d) F_d per cubature node
+#pragma unroll 1
+      for (int it = 0; it < C::IT_P; ++it) {
+        const int idx = tid + it * C::NTH;
+        if (idx < C::E * w) {
+          const int e = idx / w, ql = idx - e * w, q = q0 + ql;
+          const double* uc = sC + (e * 5) * C::LDC + ql;
+          double* gout = sG + (e * 5) * C::LDG + ql;
+          const int ce = c0 + e;
+          if (q < C::NCUB && ce < cp.Kc) {
+            const State5 s{uc[0], uc[C::LDC], uc[2 * C::LDC], uc[3 * C::LDC], uc[4 * C::LDC]};
+            if (!admissible(s, gamma)) record_error(p.err, 1, p.elem_offset + sId[e], q, 0, s.r);
+            const double ir = 1.0 / s.r;
+            const double pr = (gamma - 1.0) * (s.E - 0.5 * ir * (s.mx * s.mx + s.my * s.my + s.mz * s.mz));
+            const double vx = s.mx * ir, vy = s.my * ir, vz = s.mz * ir;
+            const double ep = s.E + pr;
+            const double* met = cp.jwr + ((size_t)ce * C::NCUB + q) * 9;
+#pragma unroll
+            for (int m = 0; m < 3; ++m) {
+              const double r0 = __ldg(met + m * 3), r1 = __ldg(met + m * 3 + 1), r2 = __ldg(met + m * 3 + 2);
+              const double um = r0 * vx + r1 * vy + r2 * vz;
+              double* o = gout + m * w;
+              o[0] = s.r * um;
+              o[C::LDG] = s.mx * um + pr * r0;
+              o[2 * C::LDG] = s.my * um + pr * r1;
+              o[3 * C::LDG] = s.mz * um + pr * r2;
+              o[4 * C::LDG] = ep * um;
+            }
+          } else {
+#pragma unroll
+            for (int m = 0; m < 3; ++m)
+#pragma unroll
+              for (int c = 0; c < 5; ++c) gout[m * w + c * C::LDG] = 0.0;
+          }
+        }
+      }
+      __syncthreads();
+      {  // GEMM2 (volume part): acc += G[rows, 3w] [D^T chunk]
+        const int nks = (3 * w) / 8;
+#pragma unroll 1
+        for (int ks = 0; ks < nks; ++ks) {
+          const AFrag a = load_afrag(sG, C::LDG, warp * 16, ks * 8, g, tq);
+#pragma unroll
+          for (int nt = 0; nt < C::NT2; ++nt) mma_frag(acc[nt], a, __ldg(fb2 + (ks * C::NT2 + nt) * 32 + lane));
+        }
+      }
+    }
+    __syncthreads();  // the face phase reuses the volume buffers
+
+    // ---- surface: chunks of FCH face nodes -----------------------------------
+    double* sF = sWork;
+#pragma unroll 1
+    for (int fc = 0; fc < C::NFCH; ++fc) {
+      const int f0 = fc * C::FCH;
+      const int wr = (C::NF - f0) < C::FCH ? (C::NF - f0) : C::FCH;
+      const int wp = round_up(wr, 8);
+#pragma unroll 1
+      for (int it = 0; it < C::IT_F; ++it) {
+        const int idx = tid + it * C::NTH;
+        if (idx >= C::E * wp) continue;
+        const int e = idx / wp, fl = idx - e * wp, fq = f0 + fl;
+        double* gout = sF + (e * 5) * C::LDF + fl;
+        const int ce = c0 + e, eg = sId[e];
+        if (ce >= cp.Kc || fl >= wr) {
+#pragma unroll
+          for (int c = 0; c < 5; ++c) gout[c * C::LDF] = 0.0;
+          continue;
+        }
+        const int f = fq / C::NG, gq = fq - f * C::NG;
+        const double* tm = p.traces + (size_t)eg * 5 * C::TB + fq;
+        const State5 um{tm[0], tm[C::TB], tm[2 * C::TB], tm[3 * C::TB], tm[4 * C::TB]};
+        const double4 fn = cp.face[(size_t)ce * C::NF + fq];
+        const int2 cw = sConn[e * 4 + f];
+        State5 up;
+        if (cw.x >= 0) {
+          const int h = __ldg(p.code_map + (cw.y >> 8) * C::NG + gq);
+          const double* tp = p.traces + (size_t)cw.x * 5 * C::TB + (cw.y & 3) * C::NG + h;
+          up = State5{tp[0], tp[C::TB], tp[2 * C::TB], tp[3 * C::TB], tp[4 * C::TB]};
+        } else {
+          up = boundary_state(um, fn.x, fn.y, fn.z, (cw.y >> 2) & 3, p.gas);
+        }
+        if (!admissible(um, gamma) || !admissible(up, gamma)) record_error(p.err, 2, p.elem_offset + eg, f, gq, um.r);
+        double fs[5];
+        if (RM == 1)
+          hllc_flux(um, up, fn.x, fn.y, fn.z, gamma, fs);
+        else
+          llf_flux_fast(um, up, fn.x, fn.y, fn.z, gamma, fs);
+#pragma unroll
+        for (int c = 0; c < 5; ++c) gout[c * C::LDF] = fn.w * fs[c];
+      }
+      __syncthreads();
+      {
+        const double2* fb2 = fb2all + (size_t)((C::K2CUB + f0) / 8) * C::NT2 * 32;
+        const int nks = wp / 8;
+#pragma unroll 1
+        for (int ks = 0; ks < nks; ++ks) {
+          const AFrag a = load_afrag(sF, C::LDF, warp * 16, ks * 8, g, tq);
+#pragma unroll
+          for (int nt = 0; nt < C::NT2; ++nt) mma_frag(acc[nt], a, __ldg(fb2 + (ks * C::NT2 + nt) * 32 + lane));
+        }
+      }
+      __syncthreads();  // sF is rewritten by the next chunk / the vol panel
+    }
+
+    // ---- epilogue: vol -> smem, rhs = M_e^-1 vol, update --------------------
+    double* sV = sWork;
+#pragma unroll
+    for (int nt = 0; nt < C::NT2; ++nt) {
+      const int col = nt * 8 + 2 * tq;
+      sV[lr_lo * L::LDV + col] = acc[nt][0];
+      sV[lr_lo * L::LDV + col + 1] = acc[nt][1];
+      sV[lr_hi * L::LDV + col] = acc[nt][2];
+      sV[lr_hi * L::LDV + col + 1] = acc[nt][3];
+    }
+    __syncthreads();
+    double a_c = 0.0, b_c = 0.0, dt = 0.0;
+    if (UPDATE) {
+      a_c = p.coef->a[p.stage];
+      b_c = p.coef->b[p.stage];
+      dt = p.coef->dt;
+    }
+    for (int idx = tid; idx < C::E * C::NP; idx += C::NTH) {
+      const int e = idx / C::NP, i = idx - e * C::NP;
+      const int ce = c0 + e;
+      if (ce >= cp.Kc) continue;
+      const double* mcol = cp.minv + (size_t)ce * C::NP * C::NP + i;  // (M_e^-1)[i][j] at j*NP + i
+      const double* v = sV + (e * 5) * L::LDV;
+      double rhs[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll 7
+      for (int j = 0; j < C::NP; ++j) {
+        const double mij = __ldg(mcol + (size_t)j * C::NP);
+#pragma unroll
+        for (int f = 0; f < 5; ++f) rhs[f] += mij * v[f * L::LDV + j];
+      }
+      const int eg = sId[e];
+#pragma unroll
+      for (int f = 0; f < 5; ++f) {
+        const size_t gi = ((size_t)eg * 5 + f) * C::BP + i;
+        if (UPDATE) {
+          const double rn = a_c * p.res[gi] + dt * rhs[f];
+          p.res[gi] = rn;
+          p.u[gi] = p.u[gi] + b_c * rn;
+        } else {
+          p.rhs_out[gi] = rhs[f];
+        }
+      }
+    }
+    __syncthreads();  // sId / sConn / sWork are restaged next tile
+  }
+}
+
+}  // namespace cdg_gpu

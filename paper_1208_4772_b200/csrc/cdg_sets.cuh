@@ -10,6 +10,7 @@
 #include "cdg_curved.cuh"
 #include "cdg_kernels.cuh"
 #include "cdg_row.cuh"
+#include "cdg_rowc.cuh"
 #include "cdg_rowp.cuh"
 #include "cdg_warp.cuh"
 
@@ -42,7 +43,27 @@ struct KernelSet {
   size_t smem_row = 0;
   int row_minb = 0, row_ch = 0, row_e = 16, row_nth = 160;
   bool row_ft = false;  // row kernel writes the next stage's traces (MODE 32)
+  // row-per-warp inviscid kernel for curved elements (cdg_rowc.cuh)
+  void (*rowc_update[2])(CurvedParams) = {nullptr, nullptr};  // [riemann]
+  void (*rowc_only[2])(CurvedParams) = {nullptr, nullptr};
+  size_t smem_rowc = 0;
+  int rowc_minb = 0, rowc_ch = 0, rowc_e = 16, rowc_nth = 160;
 };
+
+template <int NP, int NCUB, int NG, int CH = 8, int FCH = 32, int MINB = 3, int E = 16>
+KernelSet with_rowc(KernelSet k) {
+  using RC = RCfg<NP, NCUB, NG, CH, FCH, MINB, 0, E>;
+  k.rowc_update[0] = &k_rhs_rowc<RC, true, 0>;
+  k.rowc_update[1] = &k_rhs_rowc<RC, true, 1>;
+  k.rowc_only[0] = &k_rhs_rowc<RC, false, 0>;
+  k.rowc_only[1] = &k_rhs_rowc<RC, false, 1>;
+  k.smem_rowc = RowCurvedLayout<RC>::SMEM_BYTES;
+  k.rowc_minb = MINB;
+  k.rowc_ch = CH;
+  k.rowc_e = RC::E;
+  k.rowc_nth = RC::NTH;
+  return k;
+}
 
 template <int NP, int NCUB, int NG, int CH = 8, int FCH = 32, int MINB = 3, int MODE = 7, int E = 16>
 KernelSet with_row(KernelSet k) {

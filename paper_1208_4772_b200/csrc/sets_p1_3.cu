@@ -8,10 +8,10 @@ namespace cdg_gpu {
 std::vector<KernelSet> kernel_sets_p1_3() {
   return {
       // straight-sided strengths (2p+1 / 2p): refelem.cpp:311-317
-      with_warp<4, 5, 3>(make_set<4, 5, 3, 16, 8, 2>()), with_warp<10, 15, 6>(make_set<10, 15, 6, 16, 16, 2>()),
+      with_rowc<4, 5, 3, 8, 32, 4>(with_warp<4, 5, 3>(make_set<4, 5, 3, 16, 8, 2>())), with_rowc<10, 15, 6, 8, 32, 4>(with_warp<10, 15, 6>(make_set<10, 15, 6, 16, 16, 2>())),
       with_warp<20, 35, 12>(make_set<20, 35, 12, 16, 16, 2>()),
       // curved-mesh strengths (3p-3 / 3p-2): refelem.hpp:118-119
-      with_warp<20, 35, 16>(make_set<20, 35, 16, 16, 16, 2>())};
+      with_rowc<20, 35, 16, 8, 32, 4>(with_warp<20, 35, 16>(make_set<20, 35, 16, 16, 16, 2>()))};
 }
 
 }  // namespace cdg_gpu

@@ -9,7 +9,7 @@ std::vector<KernelSet> kernel_sets_p4() {
   return {
       // default: row kernel with fused traces (the next stage's traces from its epilogue)
       with_row<35, 70, 16, 8, 32, 4, 32>(make_set<35, 70, 16, 16, 24, 2, 64>()),
-      with_row<35, 70, 56, 8, 32, 4, 0>(make_set<35, 70, 56, 16, 24, 2>()),
+      with_rowc<35, 70, 56, 8, 32, 4>(with_row<35, 70, 56, 8, 32, 4, 0>(make_set<35, 70, 56, 16, 24, 2>())),
       // P=4 straight tuning variants, selected with CDG_KCFG=<n> (bench sweeps;
       // DESIGN.md §6 lists what each measured)
       make_set<35, 70, 16, 16, 24, 2, 64>(),                                 // 1 CTA kernel, 8 warps
