@@ -374,6 +374,8 @@ void launch_curved(cdg_gpu_level* lv, bool update, int stage, int mode = 0) {
   if (mode == 0 && lv->use_rowc) {  // row-per-warp curved kernel (cdg_rowc.cuh)
     cp.base.frag_icub = lv->wfrag1;
     cp.frag_opc = lv->rfrag_opc;
+    static const int pf_rowc = std::getenv("CDG_PREFETCH_ROWC") ? std::atoi(std::getenv("CDG_PREFETCH_ROWC")) : 0;
+    cp.base.prefetch = pf_rowc;
     const int rm = lv->gas.riemann == 1 ? 1 : 0;
     auto fr = update ? lv->ks->rowc_update[rm] : lv->ks->rowc_only[rm];
     const int tiles = (lv->n_curved + lv->ks->rowc_e - 1) / lv->ks->rowc_e;

@@ -61,6 +61,11 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_rowc(CurvedParams cp) {
       const int e = sId[idx / 4];
       sConn[idx] = e >= 0 ? p.conn[(size_t)e * 4 + idx % 4] : make_int2(-1, pack_face(0, 0, 1, 0));
     }
+    const int ne = min(C::E, cp.Kc - c0);  // curved elements in this tile
+    // L2 prefetch (p.prefetch bits): 1 the tile's per-node metrics, 4 its
+    // per-face-node geometry -- both contiguous in the curved list order
+    if (p.prefetch & 1) l2_prefetch_range(cp.jwr + (size_t)c0 * C::NCUB * 9, (size_t)ne * C::NCUB * 9 * 8, tid, C::NTH);
+    if (p.prefetch & 4) l2_prefetch_range(cp.face + (size_t)c0 * C::NF, (size_t)ne * C::NF * 32, tid, C::NTH);
     const int el_lo = sId[lr_lo / 5], el_hi = sId[lr_hi / 5];
     const bool ok_lo = el_lo >= 0, ok_hi = el_hi >= 0;
     const double* u_lo = p.u + (ok_lo ? (size_t)el_lo * 5 + lr_lo % 5 : 0) * C::BP + 2 * tq;
@@ -154,6 +159,8 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_rowc(CurvedParams cp) {
     __syncthreads();  // the face phase reuses the volume buffers
 
     // ---- surface: chunks of FCH face nodes -----------------------------------
+    // prefetch bit 2: the tile's M_e^-1 (read by the epilogue) into L2
+    if (p.prefetch & 2) l2_prefetch_range(cp.minv + (size_t)c0 * C::NP * C::NP, (size_t)ne * C::NP * C::NP * 8, tid, C::NTH);
     double* sF = sWork;
 #pragma unroll 1
     for (int fc = 0; fc < C::NFCH; ++fc) {
@@ -225,27 +232,54 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_rowc(CurvedParams cp) {
       b_c = p.coef->b[p.stage];
       dt = p.coef->dt;
     }
+    // one thread per (element, node i): rhs_f(i) = sum_j (M_e^-1)[i][j] vol_f(j)
+    // for the five fields. The column stream of M_e^-1 is software-pipelined
+    // in groups of MG (the next group's loads are in flight while the current
+    // one is consumed); res and u are loaded up front, before the sums.
+    constexpr int MG = 7, NGR = ceil_div(C::NP, MG);
     for (int idx = tid; idx < C::E * C::NP; idx += C::NTH) {
       const int e = idx / C::NP, i = idx - e * C::NP;
       const int ce = c0 + e;
       if (ce >= cp.Kc) continue;
       const double* mcol = cp.minv + (size_t)ce * C::NP * C::NP + i;  // (M_e^-1)[i][j] at j*NP + i
       const double* v = sV + (e * 5) * L::LDV;
-      double rhs[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-#pragma unroll 7
-      for (int j = 0; j < C::NP; ++j) {
-        const double mij = __ldg(mcol + (size_t)j * C::NP);
+      const size_t g0 = ((size_t)sId[e] * 5) * C::BP + i;
+      double m[MG];
 #pragma unroll
-        for (int f = 0; f < 5; ++f) rhs[f] += mij * v[f * L::LDV + j];
+      for (int k = 0; k < MG; ++k) m[k] = k < C::NP ? __ldg(mcol + (size_t)k * C::NP) : 0.0;
+      double ro[5], uo[5];
+      if (UPDATE) {
+#pragma unroll
+        for (int f = 0; f < 5; ++f) {
+          ro[f] = p.res[g0 + (size_t)f * C::BP];
+          uo[f] = p.u[g0 + (size_t)f * C::BP];
+        }
       }
-      const int eg = sId[e];
+      double rhs[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll 1
+      for (int gr = 0; gr < NGR; ++gr) {
+        const int j0 = gr * MG;
+        double mn[MG];
+#pragma unroll
+        for (int k = 0; k < MG; ++k) {
+          const int j = j0 + MG + k;
+          mn[k] = j < C::NP ? __ldg(mcol + (size_t)j * C::NP) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < MG; ++k)
+          if (j0 + k < C::NP)
+#pragma unroll
+            for (int f = 0; f < 5; ++f) rhs[f] += m[k] * v[f * L::LDV + j0 + k];
+#pragma unroll
+        for (int k = 0; k < MG; ++k) m[k] = mn[k];
+      }
 #pragma unroll
       for (int f = 0; f < 5; ++f) {
-        const size_t gi = ((size_t)eg * 5 + f) * C::BP + i;
+        const size_t gi = g0 + (size_t)f * C::BP;
         if (UPDATE) {
-          const double rn = a_c * p.res[gi] + dt * rhs[f];
+          const double rn = a_c * ro[f] + dt * rhs[f];
           p.res[gi] = rn;
-          p.u[gi] = p.u[gi] + b_c * rn;
+          p.u[gi] = uo[f] + b_c * rn;
         } else {
           p.rhs_out[gi] = rhs[f];
         }
