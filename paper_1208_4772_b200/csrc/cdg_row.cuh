@@ -37,6 +37,7 @@ namespace cdg_gpu {
 template <int NP_, int NCUB_, int NG_, int CH_ = 8, int FCH_ = 32, int MINB_ = 3, int MODE_ = 7, int E_ = 16>
 struct RCfg {
   static constexpr int NP = NP_, NCUB = NCUB_, NG = NG_, NF = 4 * NG_;
+  static constexpr int MODE = MODE_;
   // E elements per tile (multiple of 16): 5E rows = 5E/16 m-tiles, one warp each
   static constexpr int E = E_, R = 5 * E_, NW = R / 16, NTH = 32 * NW, MINB = MINB_;
   static constexpr bool OPRING = MODE_ & 1, RESS = MODE_ & 4, USMEM = MODE_ & 8;

@@ -50,9 +50,9 @@ struct KernelSet {
   int rowc_minb = 0, rowc_ch = 0, rowc_e = 16, rowc_nth = 160;
 };
 
-template <int NP, int NCUB, int NG, int CH = 8, int FCH = 32, int MINB = 3, int E = 16>
+template <int NP, int NCUB, int NG, int CH = 8, int FCH = 32, int MINB = 3, int MODE = 0, int E = 16>
 KernelSet with_rowc(KernelSet k) {
-  using RC = RCfg<NP, NCUB, NG, CH, FCH, MINB, 0, E>;
+  using RC = RCfg<NP, NCUB, NG, CH, FCH, MINB, MODE, E>;
   k.rowc_update[0] = &k_rhs_rowc<RC, true, 0>;
   k.rowc_update[1] = &k_rhs_rowc<RC, true, 1>;
   k.rowc_only[0] = &k_rhs_rowc<RC, false, 0>;

@@ -46,9 +46,13 @@ def _fs(gpu):
 
 # p=6 passes too (2.7 min of reference-side curving on the host; run with
 # CDG_SLOW=1) -- the BASELINE "cylinder P=1..6" sweep on the curved sphere
+@pytest.mark.parametrize("kernel", ["row", "cta"])
 @pytest.mark.parametrize("p", [1, 2, 3, 4, 5] + ([6] if __import__("os").environ.get("CDG_SLOW") else []))
-def test_curved_sphere_rhs_and_steps_match_reference(gpu_lib, refmod, p):
+def test_curved_sphere_rhs_and_steps_match_reference(gpu_lib, refmod, p, kernel, monkeypatch):
+    """kernel: the row-per-warp curved kernel (k_rhs_rowc, default for p <= 5)
+    or the CTA kernel (k_rhs_curved; CDG_NOROWC=1, the p >= 6 path)."""
     gpu, ref = gpu_lib, refmod
+    monkeypatch.setenv("CDG_NOROWC", "1" if kernel == "cta" else "0")
     rm, rl, mesh, ids, nodes = sphere_case(ref, p)
     assert len(ids) > 0 and rl.n_cub > 0
     fs = _fs(gpu)
@@ -137,3 +141,72 @@ def test_curved_sphere_jacobian_weighted_indicator(gpu_lib, refmod, p):
     assert (eps_ref > 0).any()
     assert np.allclose(eps, eps_ref, rtol=1e-10, atol=1e-14)
     assert rel(r_gpu, r_ref) < 1e-10
+
+
+# ---- the curved kernels at GPU-filling sizes: make_cube_mesh(n) with the
+# collocation nodes moved by a smooth global map (scripts/bench_curved.py) ---
+def _mapped_cube(gpu, R, n, p, amp, frac=1.0, kernel="row", monkeypatch=None):
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench_curved", "scripts/bench_curved.py")
+    bcm = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bcm)
+    mesh = M.cube_mesh(n)
+    re = R.level_reference_element(p, True)
+    X = bcm.curved_nodes(mesh, re, amp)
+    ids = np.arange(int(round(frac * mesh.n_owned)))
+    if monkeypatch is not None:
+        monkeypatch.setenv("CDG_NOROWC", "1" if kernel == "cta" else "0")
+    fs = gpu.make_state(1.0, [0.4, 0.05, -0.1], 1.0)
+    return gpu.GpuLevel(mesh, p, bc=0, freestream=fs, curved=(ids, X[ids])), mesh, fs
+
+
+def _smooth_state(lv, seed):
+    rng = np.random.default_rng(seed)
+    K, npb = lv.K, lv.n_basis
+    u = np.zeros((K, 5, lv.block))
+    j = lambda: (rng.random((K, npb)) - 0.5) * 0.1
+    rho, vx, vy, vz, pr = 1.0 + j(), 0.3 + j(), j(), j(), 1.0 + j()
+    u[:, 0, :npb], u[:, 1, :npb], u[:, 2, :npb], u[:, 3, :npb] = rho, rho * vx, rho * vy, rho * vz
+    u[:, 4, :npb] = pr / 0.4 + 0.5 * rho * (vx * vx + vy * vy + vz * vz)
+    return u.reshape(-1)
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 5])
+def test_curved_path_on_straight_elements_equals_affine_path(gpu_lib, p):
+    """With the map switched off (amp 0) every element goes through the curved
+    kernels (per-node metrics, per-face-node normals, per-element M_e^-1) and
+    must reproduce the affine kernels (constant metrics, M^-1 folded into the
+    shared operators) on the same straight mesh and quadrature."""
+    gpu = gpu_lib
+    from paper_1208_4772_b200 import refelem as R
+    lvc, mesh, fs = _mapped_cube(gpu, R, 5, p, 0.0)
+    lva = gpu.GpuLevel(mesh, p, bc=0, freestream=fs, curved_quadrature=True)
+    u = _smooth_state(lva, 3)
+    for riem in ("llf", "hllc"):
+        cfg = gpu.run_config(riem)
+        ra, rc = lva.compute_rhs(cfg, u), lvc.compute_rhs(cfg, u)
+        assert rel(rc, ra) < 1e-11, (riem, rel(rc, ra))
+    lva.close()
+    lvc.close()
+
+
+@pytest.mark.parametrize("frac", [1.0, 0.3])
+def test_curved_row_kernel_matches_cta_kernel_mapped_cube(gpu_lib, frac, monkeypatch):
+    """k_rhs_rowc vs k_rhs_curved on 6,000 curved (or 30% curved + affine)
+    elements, RHS and three RK steps (the affine kernels skip the all-curved
+    tiles, the mixed tiles keep their affine rows)."""
+    gpu = gpu_lib
+    from paper_1208_4772_b200 import refelem as R
+    out = {}
+    for kernel in ("row", "cta"):
+        lv, mesh, fs = _mapped_cube(gpu, R, 10, 4, 0.02, frac, kernel, monkeypatch)
+        u = _smooth_state(lv, 5)
+        cfg = gpu.run_config("llf")
+        r = lv.compute_rhs(cfg, u)
+        lv.set_state(u)
+        dt = 0.3 * lv.compute_timestep(cfg)
+        lv.rk_steps(cfg, dt, 3)
+        out[kernel] = (r, lv.get_state()[0])
+        lv.close()
+    assert rel(out["row"][0], out["cta"][0]) < 1e-11
+    assert rel(out["row"][1], out["cta"][1]) < 1e-12
