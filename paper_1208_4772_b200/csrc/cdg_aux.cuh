@@ -131,6 +131,8 @@ struct AuxParams {
   GasParams gas;
   const unsigned long long* gate;  // optional launch gate (see gated_off)
   int gate_when;
+  const int* tiles;  // optional tile list (curved levels: tiles holding an affine element)
+  int n_list;
 };
 
 template <class C>
@@ -151,7 +153,9 @@ __global__ void __launch_bounds__(kThreads, C::MINB) k_aux_q(AuxParams p) {
   const int t_begin = (warp * C::T2) / kWarps, t_end = ((warp + 1) * C::T2) / kWarps;
   const double2* fba = reinterpret_cast<const double2*>(p.frag_aux);
 
-  for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+  const int n_iter = p.tiles ? p.n_list : p.n_tiles;
+  for (int it_t = blockIdx.x; it_t < n_iter; it_t += gridDim.x) {
+    const int tile = p.tiles ? __ldg(p.tiles + it_t) : it_t;
     const int e0 = tile * C::E, row0 = e0 * 5;
     stage_rows<C>(p.u, row0, n_rows, sU, tid);
     for (int idx = tid; idx < C::E * 9; idx += kThreads)

@@ -371,13 +371,13 @@ void launch_curved(cdg_gpu_level* lv, bool update, int stage, int mode = 0) {
   cp.vol = lv->curved_vol;
   cp.q_out = lv->q;
   cp.Kc = lv->n_curved;
-  if (mode == 0 && lv->use_rowc) {  // row-per-warp curved kernel (cdg_rowc.cuh)
+  if (lv->use_rowc) {  // row-per-warp curved kernels (cdg_rowc.cuh)
     cp.base.frag_icub = lv->wfrag1;
     cp.frag_opc = lv->rfrag_opc;
-    static const int pf_rowc = std::getenv("CDG_PREFETCH_ROWC") ? std::atoi(std::getenv("CDG_PREFETCH_ROWC")) : 0;
-    cp.base.prefetch = pf_rowc;
     const int rm = lv->gas.riemann == 1 ? 1 : 0;
-    auto fr = update ? lv->ks->rowc_update[rm] : lv->ks->rowc_only[rm];
+    auto fr = mode == 2   ? lv->ks->rowc_aux
+              : mode == 1 ? (update ? lv->ks->rowc_visc_update[rm] : lv->ks->rowc_visc_only[rm])
+                          : (update ? lv->ks->rowc_update[rm] : lv->ks->rowc_only[rm]);
     const int tiles = (lv->n_curved + lv->ks->rowc_e - 1) / lv->ks->rowc_e;
     fr<<<std::max(1, std::min(tiles, lv->n_sms * lv->ks->rowc_minb)), lv->ks->rowc_nth, lv->ks->smem_rowc,
          lv->stream>>>(cp);
@@ -543,8 +543,13 @@ void launch_aux(cdg_gpu_level* lv) {
   ap.gas = lv->gas;
   ap.gate = lv->cur_gate;
   ap.gate_when = lv->cur_gate_when;
-  lv->ks->aux_q<<<lv->grid(lv->n_tiles()), kThreads, lv->ks->smem_aux, lv->stream>>>(ap);
-  ++lv->launches;
+  ap.tiles = lv->d_affine_tiles;  // curved levels: skip the all-curved tiles
+  ap.n_list = lv->n_affine_tiles;
+  const int aux_tiles = ap.tiles ? ap.n_list : lv->n_tiles();
+  if (aux_tiles > 0) {
+    lv->ks->aux_q<<<lv->grid(aux_tiles), kThreads, lv->ks->smem_aux, lv->stream>>>(ap);
+    ++lv->launches;
+  }
   launch_curved(lv, false, 0, 2);  // per-node-metric q of the curved elements
   const size_t n = (size_t)lv->K * 5 * lv->bp;
   const size_t nt = (size_t)(lv->K + lv->n_halo) * 5 * lv->tb;

@@ -46,6 +46,9 @@ struct KernelSet {
   // row-per-warp inviscid kernel for curved elements (cdg_rowc.cuh)
   void (*rowc_update[2])(CurvedParams) = {nullptr, nullptr};  // [riemann]
   void (*rowc_only[2])(CurvedParams) = {nullptr, nullptr};
+  void (*rowc_visc_update[2])(CurvedParams) = {nullptr, nullptr};
+  void (*rowc_visc_only[2])(CurvedParams) = {nullptr, nullptr};
+  void (*rowc_aux)(CurvedParams) = nullptr;
   size_t smem_rowc = 0;
   int rowc_minb = 0, rowc_ch = 0, rowc_e = 16, rowc_nth = 160;
 };
@@ -57,6 +60,11 @@ KernelSet with_rowc(KernelSet k) {
   k.rowc_update[1] = &k_rhs_rowc<RC, true, 1>;
   k.rowc_only[0] = &k_rhs_rowc<RC, false, 0>;
   k.rowc_only[1] = &k_rhs_rowc<RC, false, 1>;
+  k.rowc_visc_update[0] = &k_rhs_rowc<RC, true, 0, 1>;
+  k.rowc_visc_update[1] = &k_rhs_rowc<RC, true, 1, 1>;
+  k.rowc_visc_only[0] = &k_rhs_rowc<RC, false, 0, 1>;
+  k.rowc_visc_only[1] = &k_rhs_rowc<RC, false, 1, 1>;
+  k.rowc_aux = &k_rhs_rowc<RC, false, 0, 2>;
   k.smem_rowc = RowCurvedLayout<RC>::SMEM_BYTES;
   k.rowc_minb = MINB;
   k.rowc_ch = CH;

@@ -97,10 +97,12 @@ VISC_FORCED = dict(enabled=True, eps0=0.04, kappa=4.0, s0_offset=-100.0)
 VISC_RAMP = dict(enabled=True, eps0=0.3, kappa=4.0, s0_offset=0.0)
 
 
+@pytest.mark.parametrize("kernel", ["row", "cta"])
 @pytest.mark.parametrize("p", [2, 3, 4])
 @pytest.mark.parametrize("visc,riem", [(VISC_FORCED, "llf"), (VISC_RAMP, "hllc")])
-def test_curved_sphere_viscous_matches_reference(gpu_lib, refmod, p, visc, riem):
+def test_curved_sphere_viscous_matches_reference(gpu_lib, refmod, p, visc, riem, kernel, monkeypatch):
     gpu, ref = gpu_lib, refmod
+    monkeypatch.setenv("CDG_NOROWC", "1" if kernel == "cta" else "0")
     rm, rl, mesh, ids, nodes = sphere_case(ref, p)
     fs = _fs(gpu)
     lv = gpu.GpuLevel(mesh, p, bc={"sphere": 0, "farfield": 1}, freestream=fs, curved=(ids, nodes[ids]))
