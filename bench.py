@@ -40,11 +40,14 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--p", type=int, default=P_DEFAULT)
-    ap.add_argument("--n", type=int, default=N_DEFAULT, help="cube cells per side (6 n^3 tets)")
+    ap.add_argument("--n", "--cube-n", dest="n", type=int, default=N_DEFAULT,
+                    help="cube cells per side (6 n^3 tets); --cube-n under torchrun")
     ap.add_argument("--riemann", default="llf")
     ap.add_argument("--cfl", type=float, default=0.5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--partition", default="slab", choices=["slab", "rcb"],
+                    help="N>1: z-slabs of the cube mesh, or recursive coordinate bisection (general meshes)")
     return ap.parse_args()
 
 
@@ -218,7 +221,13 @@ def main():
     re = R.get_reference_element(p)
     fs = freestream_state()
     t_setup = time.perf_counter()
-    part = partition.rank_part(args.n, world, rank)
+    if args.partition == "rcb" and world > 1:
+        from paper_1208_4772_b200 import mesh as M
+        g_mesh = M.cube_mesh(args.n)
+        part = partition.mesh_part(g_mesh, partition.rcb_owner(g_mesh, world), rank)
+        del g_mesh
+    else:
+        part = partition.rank_part(args.n, world, rank)
     lv = gpu.GpuLevel(part.mesh, p, bc=0, freestream=fs, re=re, device=local_rank)
     cfg = gpu.run_config(args.riemann, cfl=args.cfl)
     K = lv.K
@@ -443,7 +452,7 @@ def main():
                                    f"(N_p={npb}, N_cub={re.n_cub}, N_f={4 * re.n_face_quad}), {args.riemann.upper()}, "
                                    f"slip walls, random admissible state (bench.cpp:22-40)",
                        "elements": K_global, "p": p, "riemann": args.riemann, "dof": K_global * npb * 5,
-                       "partition": f"{world} z-slab(s)", "l2": "working set ~%.0f GB >> 126 MB L2 (no flush needed)"
+                       "partition": f"{world} z-slab(s)" if args.partition == "slab" or world == 1 else f"{world} RCB parts", "l2": "working set ~%.0f GB >> 126 MB L2 (no flush needed)"
                        % (K_global * (3 * 5 * lv.device_block + 5 * lv.trace_block) * 8 / 1e9),
                        "setup_s": round(setup_s, 1),
                        **({"dist_backend": backend + " (host-staged halos; functional check, not a measurement)"}

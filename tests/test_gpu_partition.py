@@ -1,4 +1,4 @@
-"""Multi-rank code path on ONE GPU: the z-slab partition with the per-stage
+"""Multi-rank code path on ONE GPU: the z-slab (and the general RCB) partition with the per-stage
 halo exchange (cdg_gpu_rk_stage_phase + halo buffers), ranks emulated by
 several levels on cuda:0 and the NCCL send/recv replaced by device copies.
 Per-element arithmetic is partition independent, so the result must be
@@ -11,8 +11,10 @@ from paper_1208_4772_b200 import mesh as M, partition as P
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("R,p,overlap", [(2, 3, False), (3, 4, False), (2, 3, True), (3, 4, True), (4, 2, True)])
-def test_partitioned_rk_steps_bitwise_equal(gpu_lib, R, p, overlap):
+@pytest.mark.parametrize("R,p,overlap,kind", [(2, 3, False, "slab"), (3, 4, False, "slab"), (2, 3, True, "slab"),
+                                               (3, 4, True, "slab"), (4, 2, True, "slab"), (3, 4, True, "rcb"),
+                                               (5, 3, True, "rcb"), (4, 4, False, "rcb")])
+def test_partitioned_rk_steps_bitwise_equal(gpu_lib, R, p, overlap, kind):
     """overlap=True: interior tiles (phase 2) run before the halo traces land,
     halo tiles (phase 3) after -- the comm/compute overlap of the multi-GPU
     stage; still bitwise identical."""
@@ -31,13 +33,17 @@ def test_partitioned_rk_steps_bitwise_equal(gpu_lib, R, p, overlap):
     u_ref = lv.get_state()[0].reshape(lv.K, 5, lv.block)
     u0 = u0.reshape(lv.K, 5, lv.block)
     # R "ranks" on the same device
-    parts = [P.rank_part(n, R, r) for r in range(R)]
+    if kind == "slab":
+        parts = [P.rank_part(n, R, r) for r in range(R)]
+    else:  # general-mesh partition: recursive coordinate bisection
+        owner = P.rcb_owner(g, R)
+        parts = [P.mesh_part(g, owner, r) for r in range(R)]
+    owned = [np.arange(*pt.elem_range) if pt.owned is None else pt.owned for pt in parts]
     levels, bufs = [], []
     per = 5 * lv.n_face_quad
-    for pt in parts:
+    for pt, own in zip(parts, owned):
         L = gpu.GpuLevel(pt.mesh, p, bc=1, freestream=fs)
-        lo, hi = pt.elem_range
-        L.set_state(np.ascontiguousarray(u0[lo:hi]).reshape(-1))
+        L.set_state(np.ascontiguousarray(u0[own]).reshape(-1))
         send_all = np.concatenate([pe.send_elem_face for pe in pt.peers])
         recv_all = np.concatenate([pe.recv_elem_face for pe in pt.peers])
         sb = torch.zeros(len(send_all) * per, dtype=torch.float64, device="cuda")
@@ -71,5 +77,7 @@ def test_partitioned_rk_steps_bitwise_equal(gpu_lib, R, p, overlap):
             for L in levels:
                 L.stage_phase(cfg, stage, 3 if overlap else 1, dt)
             torch.cuda.synchronize()
-    out = np.concatenate([L.get_state()[0].reshape(L.K, 5, L.block) for L in levels])
+    out = np.empty_like(u_ref)
+    for L, own in zip(levels, owned):
+        out[own] = L.get_state()[0].reshape(L.K, 5, L.block)
     assert np.array_equal(out, u_ref)
