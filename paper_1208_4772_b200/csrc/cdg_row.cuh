@@ -33,7 +33,9 @@ namespace cdg_gpu {
 // L1/L2), 2 U fragments register-resident for the whole tile (else reloaded
 // per chunk, which frees ~40 registers), 4 res staged to smem for the epilogue,
 // 8 U rows staged once per tile in smem by cp.async (GEMM1 A fragments and the
-// epilogue's old u come from there; excludes 2).
+// epilogue's old u come from there; excludes 2), 32 fused traces, 64 / 128
+// volume / face GEMM k-steps unrolled (the next k-step's A fragment and B
+// fragments in flight during the current one's MMAs).
 template <int NP_, int NCUB_, int NG_, int CH_ = 8, int FCH_ = 32, int MINB_ = 3, int MODE_ = 7, int E_ = 16>
 struct RCfg {
   static constexpr int NP = NP_, NCUB = NCUB_, NG = NG_, NF = 4 * NG_;
@@ -51,7 +53,10 @@ struct RCfg {
   static constexpr int CH = CH_, NCH = ceil_div(NCUB8, CH);
   static constexpr int FCH = FCH_, NFCH = ceil_div(NF, FCH);
   static constexpr int K2CUB = 3 * NCUB8, K2 = K2CUB + NF8, KS2 = K2 / 8;
-  static constexpr int LDC = CH + 4;                  // U_cub chunk (pointwise reads columns)
+  // U_cub chunk: LDC = 8 (mod 16) doubles makes both the GEMM1 stores (rows g,
+  // g+1 of a quarter-warp 64 B apart) and the pointwise column reads (elements
+  // e, e+1 of a half-warp 5*LDC doubles = 64 B (mod 128) apart) bank-conflict free
+  static constexpr int LDC = frag_ld8(CH);
   static constexpr int LDG = frag_ld8(3 * CH);        // flux chunk, conflict-free 128-bit A loads
   static constexpr int LDF = frag_ld8(FCH);           // face-flux chunk
   // volume phase: one U_cub chunk (rewritten only after the barrier that
@@ -333,12 +338,23 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_row(RhsParams p) {
       // GEMM2 (volume part of K): acc += G[rows, 3w] * Op2[:, 3 q0 : 3 q0 + 3w]^T
       {
         const int nks = (3 * w) / 8;
-#pragma unroll 1
-        for (int ks = 0; ks < nks; ++ks) {
+        auto kstep = [&](int ks) {
           const AFrag a = load_afrag(sG, C::LDG, warp * 16, ks * 8, g, tq);
 #pragma unroll
           for (int nt = 0; nt < C::NT2; ++nt)
             mma_frag(acc[nt], a, C::OPRING ? fb2[(ks * C::NT2 + nt) * 32 + lane] : __ldg(fb2 + (ks * C::NT2 + nt) * 32 + lane));
+        };
+        if constexpr (C::MODE & 64) {  // unrolled k-steps (A fragments of the next k-step in flight)
+          if (w == C::CH) {
+#pragma unroll
+            for (int ks = 0; ks < 3 * C::CH / 8; ++ks) kstep(ks);
+          } else {
+#pragma unroll 1
+            for (int ks = 0; ks < nks; ++ks) kstep(ks);
+          }
+        } else {
+#pragma unroll 1
+          for (int ks = 0; ks < nks; ++ks) kstep(ks);
         }
       }
       ++n;
@@ -412,12 +428,23 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_row(RhsParams p) {
           fb2 = reinterpret_cast<const double2*>(p.frag_op2) + (size_t)((C::K2CUB + f0) / 8) * C::NT2 * 32;
         }
         const int nks = wp / 8;
-#pragma unroll 1
-        for (int ks = 0; ks < nks; ++ks) {
+        auto kstep = [&](int ks) {
           const AFrag a = load_afrag(sF, C::LDF, warp * 16, ks * 8, g, tq);
 #pragma unroll
           for (int nt = 0; nt < C::NT2; ++nt)
             mma_frag(acc[nt], a, C::OPRING ? fb2[(ks * C::NT2 + nt) * 32 + lane] : __ldg(fb2 + (ks * C::NT2 + nt) * 32 + lane));
+        };
+        if constexpr (C::MODE & 128) {
+          if (wp == C::FCH) {
+#pragma unroll
+            for (int ks = 0; ks < C::FCH / 8; ++ks) kstep(ks);
+          } else {
+#pragma unroll 1
+            for (int ks = 0; ks < nks; ++ks) kstep(ks);
+          }
+        } else {
+#pragma unroll 1
+          for (int ks = 0; ks < nks; ++ks) kstep(ks);
         }
       }
       ++n;

@@ -173,13 +173,18 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_rowc(CurvedParams cp) {
           }
         }
         __syncthreads();
-        {  // GEMM2 (volume part): acc += G[rows, 3w] [D^T chunk]
-          const int nks = (3 * w) / 8;
-#pragma unroll 1
-          for (int ks = 0; ks < nks; ++ks) {
+        {  // GEMM2 (volume part): acc += G[rows, 3w] [D^T chunk]; full chunks unrolled
+          auto kstep = [&](int ks) {
             const AFrag a = load_afrag(sG, C::LDG, warp * 16, ks * 8, g, tq);
 #pragma unroll
             for (int nt = 0; nt < C::NT2; ++nt) mma_frag(acc[nt], a, __ldg(fb2 + (ks * C::NT2 + nt) * 32 + lane));
+          };
+          if (w == C::CH) {
+#pragma unroll
+            for (int ks = 0; ks < 3 * C::CH / 8; ++ks) kstep(ks);
+          } else {
+#pragma unroll 1
+            for (int ks = 0; ks < (3 * w) / 8; ++ks) kstep(ks);
           }
         }
       }
@@ -261,12 +266,17 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_rowc(CurvedParams cp) {
         __syncthreads();
         {
           const double2* fb2 = fb2all + (size_t)((C::K2CUB + f0) / 8) * C::NT2 * 32;
-          const int nks = wp / 8;
-#pragma unroll 1
-          for (int ks = 0; ks < nks; ++ks) {
+          auto kstep = [&](int ks) {
             const AFrag a = load_afrag(sF, C::LDF, warp * 16, ks * 8, g, tq);
 #pragma unroll
             for (int nt = 0; nt < C::NT2; ++nt) mma_frag(acc[nt], a, __ldg(fb2 + (ks * C::NT2 + nt) * 32 + lane));
+          };
+          if (wp == C::FCH) {
+#pragma unroll
+            for (int ks = 0; ks < C::FCH / 8; ++ks) kstep(ks);
+          } else {
+#pragma unroll 1
+            for (int ks = 0; ks < wp / 8; ++ks) kstep(ks);
           }
         }
         __syncthreads();  // sF is rewritten by the next chunk / the vol panel

@@ -9,11 +9,12 @@ std::vector<KernelSet> kernel_sets_p5_6() {
   return {
       // p=5: row-per-warp kernel (11.2 ms vs 11.9 for the CTA kernel at 511k
       // tets); p=6: CTA kernel with 8-node chunks (27.8 vs 34.8 ms)
-      with_row<56, 126, 56, 8, 32, 3, 0>(make_set<56, 126, 56, 16, 16, 2>()),
+      with_row<56, 126, 56, 8, 32, 3, 192>(make_set<56, 126, 56, 16, 16, 2>()),
       make_set<84, 210, 84, 16, 8, 2, 16>(),
       with_rowc<56, 210, 84, 8, 32, 3>(make_set<56, 210, 84, 16, 16, 2>()), make_set<84, 330, 165, 16>(),
       // tuning variants (CDG_KCFG)
-      make_set<56, 126, 56, 16, 16, 2>(), make_set<84, 210, 84, 16>()};
+      make_set<56, 126, 56, 16, 16, 2>(), make_set<84, 210, 84, 16>(),
+      with_row<56, 126, 56, 8, 32, 3, 0>(make_set<56, 126, 56, 16, 16, 2>())};  // p=5 k-steps not unrolled (CDG_KCFG=2)
 }
 
 }  // namespace cdg_gpu
