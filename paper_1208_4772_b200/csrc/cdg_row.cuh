@@ -380,17 +380,16 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_row(RhsParams p) {
       const int f0 = fc * C::FCH;
       const int wr = (C::NF - f0) < C::FCH ? (C::NF - f0) : C::FCH;
       const int wp = round_up(wr, 8);
-#pragma unroll 1
-      for (int it = 0; it < C::IT_F; ++it) {
+      auto face_item = [&](int it) {
         const int idx = tid + it * C::NTH;
-        if (idx >= C::E * wp) continue;
+        if (idx >= C::E * wp) return;
         const int e = idx / wp, fl = idx - e * wp, fq = f0 + fl;
         double* gout = sF + (e * 5) * C::LDF + fl;
         const int eg = e0 + e;
         if (eg >= p.K || fl >= wr) {
 #pragma unroll
           for (int c = 0; c < 5; ++c) gout[c * C::LDF] = 0.0;
-          continue;
+          return;
         }
         const int f = fq / C::NG, gq = fq - f * C::NG;
         const double* tm = p.traces + (size_t)eg * 5 * C::TB + fq;
@@ -413,7 +412,9 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_row(RhsParams p) {
           llf_flux_fast(um, up, fn.x, fn.y, fn.z, gamma, fs);
 #pragma unroll
         for (int c = 0; c < 5; ++c) gout[c * C::LDF] = fn.w * fs[c];
-      }
+      };
+#pragma unroll 1
+      for (int it = 0; it < C::IT_F; ++it) face_item(it);
       __syncthreads();
       if (C::OPRING && tid == 0 && n + 1 < n_chunks) {  // every warp is past the GEMM of chunk n-1
         fence_proxy_async();
@@ -462,18 +463,36 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_row(RhsParams p) {
     }
     const bool cur_lo = (sConn[((warp * 16 + g) / 5) * 4].y & kCurvedBit) != 0;
     const bool cur_hi = (sConn[((warp * 16 + g + 8) / 5) * 4].y & kCurvedBit) != 0;
+    // old res values are loaded before any store of the row (the compiler
+    // cannot move loads of p.res above stores to p.u / p.res, so loads
+    // interleaved with the stores would serialise NT2 memory round trips);
+    // MODE 256: both rows' values up front
+    constexpr bool RES2 = C::MODE & 256;
+    double2 rsv[RES2 ? 2 : 1][C::NT2];
+    auto load_res = [&](int hh, double2* dst) {
+      const int grow = hh ? r_hi : r_lo;
+      if (grow >= n_rows || (hh ? cur_hi : cur_lo)) return;
+#pragma unroll
+      for (int j = 0; j < C::NT2; ++j)
+        dst[j] = *reinterpret_cast<const double2*>(p.res + (size_t)grow * C::BP + j * 8 + 2 * tq);
+    };
+    if (UPDATE && !C::RESS && RES2) {
+      load_res(0, rsv[0]);
+      load_res(1, rsv[RES2 ? 1 : 0]);
+    }
 #pragma unroll
     for (int hh = 0; hh < 2; ++hh) {
       const int grow = hh ? r_hi : r_lo;
       if (grow >= n_rows || (hh ? cur_hi : cur_lo)) continue;  // curved rows: k_rhs_curved
       const size_t rowoff = (size_t)grow * C::BP;
+      if (UPDATE && !C::RESS && !RES2) load_res(hh, rsv[0]);
 #pragma unroll
       for (int j = 0; j < C::NT2; ++j) {
         const int col = j * 8 + 2 * tq;  // < KP <= BP; padded columns carry exact zeros
         const double r0 = acc[j][2 * hh], r1 = acc[j][2 * hh + 1];
         if (UPDATE) {
           const double2 rs = C::RESS ? *reinterpret_cast<const double2*>(sRes + (hh * C::NT2 + j) * 2)
-                                     : *reinterpret_cast<const double2*>(p.res + rowoff + col);
+                                     : rsv[RES2 ? hh : 0][j];
           const double n0 = a_c * rs.x + dt * r0, n1 = a_c * rs.y + dt * r1;
           *reinterpret_cast<double2*>(p.res + rowoff + col) = make_double2(n0, n1);
           // old u: the A fragment of k-step j holds (row, 8j+2t) / (row, 8j+2t+1)

@@ -26,7 +26,9 @@ std::vector<KernelSet> kernel_sets_p4() {
       with_row<35, 70, 16, 8, 32, 4, 96>(make_set<35, 70, 16, 16, 24, 2, 64>()),      // 11 volume k-steps unrolled
       with_row<35, 70, 16, 8, 32, 4, 160>(make_set<35, 70, 16, 16, 24, 2, 64>()),     // 12 face k-steps unrolled
       with_row<35, 70, 16, 8, 32, 3, 224>(make_set<35, 70, 16, 16, 24, 2, 64>()),     // 13 unrolled, 3 CTAs/SM
-      with_row<35, 70, 16, 8, 64, 4, 224>(make_set<35, 70, 16, 16, 24, 2, 64>())};    // 14 unrolled, 64-node face chunks
+      with_row<35, 70, 16, 8, 64, 4, 224>(make_set<35, 70, 16, 16, 24, 2, 64>()),     // 14 unrolled, 64-node face chunks
+      with_row<35, 70, 16, 8, 32, 4, 480>(make_set<35, 70, 16, 16, 24, 2, 64>()),     // 15 both rows' res loaded up front
+      with_row<35, 70, 16, 8, 32, 4, 228>(make_set<35, 70, 16, 16, 24, 2, 64>())};    // 16 res staged in smem (cp.async)
 }
 
 }  // namespace cdg_gpu
