@@ -797,6 +797,28 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs(RhsParams p) {
       b_c = p.coef->b[p.stage];
       dt = p.coef->dt;
     }
+    // all old res pairs of this thread are loaded before its first store (the
+    // compiler cannot move loads of p.res above stores to p.u / p.res; loads
+    // interleaved with the stores would serialise the memory round trips)
+    double2 rsv[C::MAXT2][2];
+    if (UPDATE) {
+#pragma unroll
+      for (int i = 0; i < C::MAXT2; ++i) {
+        rsv[i][0] = rsv[i][1] = make_double2(0.0, 0.0);
+        if (C::WROW || t_begin + i < t_end) {
+          int mt, nt;
+          tile_coords<C>(t_begin, i, mt, nt);
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int r = mt * 16 + g + 8 * hh;
+            const int grow = row0 + r;
+            const int col = nt * 8 + 2 * tq;
+            if (grow >= n_rows || col + 1 >= C::NP) continue;
+            rsv[i][hh] = *reinterpret_cast<const double2*>(p.res + (size_t)grow * C::BP + col);
+          }
+        }
+      }
+    }
 #pragma unroll
     for (int i = 0; i < C::MAXT2; ++i) {
       if (C::WROW || t_begin + i < t_end) {
@@ -813,7 +835,7 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs(RhsParams p) {
           const double r0 = acc[i][2 * hh], r1 = acc[i][2 * hh + 1];
           if (col + 1 < C::NP) {
             if (UPDATE) {
-              const double2 rs = *reinterpret_cast<const double2*>(p.res + gi);
+              const double2 rs = rsv[i][hh];
               const double n0 = a_c * rs.x + dt * r0, n1 = a_c * rs.y + dt * r1;
               *reinterpret_cast<double2*>(p.res + gi) = make_double2(n0, n1);
               *reinterpret_cast<double2*>(p.u + gi) =

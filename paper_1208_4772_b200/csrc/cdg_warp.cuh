@@ -270,6 +270,15 @@ __global__ void __launch_bounds__(32 * C::WARPS, C::MINB) k_rhs_warp(WarpParams 
       const int e = g + 8 * hh, eg = e0 + e;
       if (eg >= p.K) continue;
       if (__ldg(reinterpret_cast<const int*>(p.conn + (size_t)eg * 4) + 1) & kCurvedBit) continue;  // k_rhs_curved
+      // the element's old res values are loaded before any of its stores (loads
+      // of p.res cannot be moved above stores to p.u / p.res by the compiler)
+      double2 rsv[5][C::NT];
+      if (UPDATE)
+#pragma unroll
+        for (int c = 0; c < 5; ++c)
+#pragma unroll
+          for (int n = 0; n < C::NT; ++n)
+            rsv[c][n] = *reinterpret_cast<const double2*>(p.res + ((size_t)eg * 5 + c) * C::BP + n * 8 + 2 * t);
 #pragma unroll
       for (int c = 0; c < 5; ++c) {
         const size_t rowoff = ((size_t)eg * 5 + c) * C::BP;
@@ -278,7 +287,7 @@ __global__ void __launch_bounds__(32 * C::WARPS, C::MINB) k_rhs_warp(WarpParams 
           const int col = n * 8 + 2 * t;  // < NT*8 <= BP; padded columns carry exact zeros
           const double r0 = acc[c][n][2 * hh], r1 = acc[c][n][2 * hh + 1];
           if (UPDATE) {
-            const double2 rs = *reinterpret_cast<const double2*>(p.res + rowoff + col);
+            const double2 rs = rsv[c][n];
             const double n0 = a_c * rs.x + dt * r0, n1 = a_c * rs.y + dt * r1;
             *reinterpret_cast<double2*>(p.res + rowoff + col) = make_double2(n0, n1);
             const double2 uo = *reinterpret_cast<const double2*>(sU + (c * C::EW + e) * C::LDU + col);
