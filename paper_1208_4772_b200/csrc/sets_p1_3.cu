@@ -8,15 +8,19 @@ namespace cdg_gpu {
 std::vector<KernelSet> kernel_sets_p1_3() {
   return {
       // straight-sided strengths (2p+1 / 2p): refelem.cpp:311-317
-      // p=1: 4 CTAs (16 warps) per SM at 128 registers: 0.40 vs 0.52 ms at 2 CTAs/SM
-      with_rowc<4, 5, 3, 8, 32, 4>(with_warp<4, 5, 3, 4, 4>(make_set<4, 5, 3, 16, 8, 2>())), with_rowc<10, 15, 6, 8, 32, 4>(with_warp<10, 15, 6>(make_set<10, 15, 6, 16, 16, 2>())),
-      with_warp<20, 35, 12>(make_set<20, 35, 12, 16, 16, 2>()),
+      // p=1: warp-tile kernel, 4 CTAs (16 warps) per SM at 128 registers (0.40 ms
+      // vs 0.52 at 2 CTAs/SM and 0.50 for the row kernel, make_cube_mesh(44))
+      with_rowc<4, 5, 3, 8, 32, 4>(with_warp<4, 5, 3, 4, 4>(make_set<4, 5, 3, 16, 8, 2>())),
+      // p=2, 3: row-per-warp kernel with fused traces and unrolled k-steps
+      // (3.14e10 / 2.69e10 DOF-updates/s vs 2.41e10 / 2.27e10 for the warp-tile
+      // kernel + trace kernel)
+      with_rowc<10, 15, 6, 8, 32, 4>(with_row<10, 15, 6, 8, 32, 4, 224>(make_set<10, 15, 6, 16, 16, 2>())),
+      with_row<20, 35, 12, 8, 32, 4, 224>(make_set<20, 35, 12, 16, 16, 2>()),
       // curved-mesh strengths (3p-3 / 3p-2): refelem.hpp:118-119
-      with_rowc<20, 35, 16, 8, 32, 4>(with_warp<20, 35, 16>(make_set<20, 35, 16, 16, 16, 2>())),
-      // tuning variants (CDG_KCFG=1): p=1 at 2 CTAs/SM; p=2, 3 at 3 CTAs/SM
-      // (168 registers: spills, 1.14 / 2.68 ms vs 0.88 / 1.94)
-      with_warp<4, 5, 3, 4, 2>(make_set<4, 5, 3, 16, 8, 2>()), with_warp<10, 15, 6, 4, 3>(make_set<10, 15, 6, 16, 16, 2>()),
-      with_warp<20, 35, 12, 4, 3>(make_set<20, 35, 12, 16, 16, 2>())};
+      with_rowc<20, 35, 16, 8, 32, 4>(with_row<20, 35, 16, 8, 32, 4, 192>(make_set<20, 35, 16, 16, 16, 2>())),
+      // tuning variants (CDG_KCFG=1): the warp-tile kernel (p=1 at 2 CTAs/SM)
+      with_warp<4, 5, 3, 4, 2>(make_set<4, 5, 3, 16, 8, 2>()), with_warp<10, 15, 6>(make_set<10, 15, 6, 16, 16, 2>()),
+      with_warp<20, 35, 12>(make_set<20, 35, 12, 16, 16, 2>()), with_warp<20, 35, 16>(make_set<20, 35, 16, 16, 16, 2>())};
 }
 
 }  // namespace cdg_gpu
