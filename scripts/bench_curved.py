@@ -101,6 +101,9 @@ def main():
            "rhs_model_flop_per_elem": F_rhs, "rhs_tflops": ach, "fp64_peak_tflops": peak, "frac": ach / peak,
            "model_bytes_per_elem": B + geo * Kc / K,
            "hbm_gbs": (B + geo * Kc / K) * K / (t_rhs_s + t_tr_s) / 1e9}
+    if t_rhs == 0:  # viscous steps run as one CUDA graph: no per-kernel split
+        for k in ("rhs_kernel_ms", "trace_kernel_ms", "rhs_tflops", "frac", "hbm_gbs"):
+            out[k] = None
     print(json.dumps(out), flush=True)
     lv.close()
 
