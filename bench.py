@@ -31,6 +31,22 @@ sys.path.insert(0, str(ROOT))
 
 P_DEFAULT = 4
 N_DEFAULT = 88
+# BASELINE.json's metric (the reference is 3D: "curved-tri" reads as curved tets)
+METRIC = "DOF-updates/sec (RK-stage RHS+update), curved-tri Euler P=4, 1/2/4/8 B200"
+
+
+def workload_config(args, world: int) -> dict:
+    """The `config` of both arms' JSON lines (no device needed)."""
+    from paper_1208_4772_b200 import refelem as R
+    re = R.get_reference_element(args.p)
+    K = 6 * args.n ** 3
+    npb, nf = re.n_basis, 4 * re.n_face_quad
+    bp, tb = (npb + 15) // 16 * 16, (nf + 15) // 16 * 16
+    return {"workload": f"make_cube_mesh({args.n}) = {K} straight tets, P={args.p} (N_p={npb}, N_cub={re.n_cub}, "
+                        f"N_f={nf}), {args.riemann.upper()}, slip walls, random admissible state (bench.cpp:22-40)",
+            "elements": K, "p": args.p, "riemann": args.riemann, "dof": K * npb * 5,
+            "partition": f"{world} z-slab(s)" if args.partition == "slab" or world == 1 else f"{world} RCB parts",
+            "l2": "working set ~%.0f GB >> 126 MB L2 (no flush needed)" % (K * (3 * 5 * bp + 5 * tb) * 8 / 1e9)}
 
 
 def parse():
@@ -179,11 +195,10 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     cb = cpu_baseline(args.p, args.riemann, seconds_budget=max(10.0, 4.0 * args.steps))
-    line = {"impl": "reference", "metric": "DOF-updates/sec (RK-stage RHS+update)", "value": cb["value"],
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"],
             "unit": "DOF-updates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": f"make_cube_mesh P={args.p} (bounded CPU sample)",
-                                            "p": args.p, "riemann": args.riemann},
+            "data": "synthetic", "config": workload_config(args, world),
             "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": "DOF-updates/s",
                                         "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -444,20 +459,14 @@ def main():
                 "stage_model_tflops": F * K / ((t_rhs + t_tr)) / 1e12}
 
     clocks = clk.summary()
-    line = {"metric": "DOF-updates/sec (RK-stage RHS+update), Euler P=4, 1/2/4/8 B200",
+    line = {"metric": METRIC,
             "value": value, "unit": "DOF-updates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"make_cube_mesh({args.n}) = {K_global} straight tets, P={p} "
-                                   f"(N_p={npb}, N_cub={re.n_cub}, N_f={4 * re.n_face_quad}), {args.riemann.upper()}, "
-                                   f"slip walls, random admissible state (bench.cpp:22-40)",
-                       "elements": K_global, "p": p, "riemann": args.riemann, "dof": K_global * npb * 5,
-                       "partition": f"{world} z-slab(s)" if args.partition == "slab" or world == 1 else f"{world} RCB parts", "l2": "working set ~%.0f GB >> 126 MB L2 (no flush needed)"
-                       % (K_global * (3 * 5 * lv.device_block + 5 * lv.trace_block) * 8 / 1e9),
-                       "setup_s": round(setup_s, 1),
+            "config": {**workload_config(args, world),
                        **({"dist_backend": backend + " (host-staged halos; functional check, not a measurement)"}
                           if world > 1 and backend != "nccl" else {})},
-            "gpu_launches": launches, "clocks": clocks}
+            "setup_s": round(setup_s, 1), "gpu_launches": launches, "clocks": clocks}
     if e2e:
         line["e2e"] = e2e
     if roof:
