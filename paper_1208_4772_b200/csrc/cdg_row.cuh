@@ -35,7 +35,8 @@ namespace cdg_gpu {
 // 8 U rows staged once per tile in smem by cp.async (GEMM1 A fragments and the
 // epilogue's old u come from there; excludes 2), 32 fused traces, 64 / 128
 // volume / face GEMM k-steps unrolled (the next k-step's A fragment and B
-// fragments in flight during the current one's MMAs).
+// fragments in flight during the current one's MMAs), 256 both rows' old res
+// loaded up front, 1024 the fused-trace n-tile groups unrolled.
 template <int NP_, int NCUB_, int NG_, int CH_ = 8, int FCH_ = 32, int MINB_ = 3, int MODE_ = 7, int E_ = 16>
 struct RCfg {
   static constexpr int NP = NP_, NCUB = NCUB_, NG = NG_, NF = 4 * NG_;
@@ -532,8 +533,7 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_row(RhsParams p) {
       AFrag fa[C::KS1];
 #pragma unroll
       for (int ks = 0; ks < C::KS1; ++ks) fa[ks] = AFrag{acc[ks][0], acc[ks][2], acc[ks][1], acc[ks][3]};
-#pragma unroll 1
-      for (int nt0 = 0; nt0 < NFT; nt0 += 4) {
+      auto ft_group = [&](int nt0) {
         double tacc[4][4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) tacc[i][0] = tacc[i][1] = tacc[i][2] = tacc[i][3] = 0.0;
@@ -552,6 +552,13 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_row(RhsParams p) {
               *reinterpret_cast<double2*>(p.traces_out + (size_t)r_hi * C::TB + col) = make_double2(tacc[i][2], tacc[i][3]);
           }
         }
+      };
+      if constexpr (C::MODE & 1024) {  // both 4-n-tile groups unrolled
+#pragma unroll
+        for (int nt0 = 0; nt0 < NFT; nt0 += 4) ft_group(nt0);
+      } else {
+#pragma unroll 1
+        for (int nt0 = 0; nt0 < NFT; nt0 += 4) ft_group(nt0);
       }
     }
     __syncthreads();  // sConn / sWork are restaged next tile

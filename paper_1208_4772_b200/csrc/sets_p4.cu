@@ -8,8 +8,8 @@ namespace cdg_gpu {
 std::vector<KernelSet> kernel_sets_p4() {
   return {
       // default: row kernel with fused traces (the next stage's traces from its
-      // epilogue) and unrolled GEMM k-steps
-      with_row<35, 70, 16, 8, 32, 4, 224>(make_set<35, 70, 16, 16, 24, 2, 64>()),
+      // epilogue), unrolled GEMM k-steps and fused-trace n-tile groups
+      with_row<35, 70, 16, 8, 32, 4, 1248>(make_set<35, 70, 16, 16, 24, 2, 64>()),
       with_rowc<35, 70, 56, 8, 32, 4>(with_row<35, 70, 56, 8, 32, 4, 192>(make_set<35, 70, 56, 16, 24, 2>())),
       // P=4 straight tuning variants, selected with CDG_KCFG=<n> (bench sweeps;
       // DESIGN.md §6 lists what each measured)
@@ -28,7 +28,8 @@ std::vector<KernelSet> kernel_sets_p4() {
       with_row<35, 70, 16, 8, 32, 3, 224>(make_set<35, 70, 16, 16, 24, 2, 64>()),     // 13 unrolled, 3 CTAs/SM
       with_row<35, 70, 16, 8, 64, 4, 224>(make_set<35, 70, 16, 16, 24, 2, 64>()),     // 14 unrolled, 64-node face chunks
       with_row<35, 70, 16, 8, 32, 4, 480>(make_set<35, 70, 16, 16, 24, 2, 64>()),     // 15 both rows' res loaded up front
-      with_row<35, 70, 16, 8, 32, 4, 228>(make_set<35, 70, 16, 16, 24, 2, 64>())};    // 16 res staged in smem (cp.async)
+      with_row<35, 70, 16, 8, 32, 4, 228>(make_set<35, 70, 16, 16, 24, 2, 64>()),     // 16 res staged in smem (cp.async)
+      with_row<35, 70, 16, 8, 32, 4, 224>(make_set<35, 70, 16, 16, 24, 2, 64>())};    // 17 fused-trace groups not unrolled
 }
 
 }  // namespace cdg_gpu
