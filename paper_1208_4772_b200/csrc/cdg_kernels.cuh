@@ -314,6 +314,69 @@ __device__ __forceinline__ void hllc_flux(const State5& um, const State5& up, do
   for (int c = 0; c < 5; ++c) out[c] = f[c] + s_k * (star[c] - uu[c]);
 }
 
+// hllc_flux with one reciprocal per side and one for the Roe average (the
+// reference divides at every use, euler.cpp:70-138; rounding differs at the
+// 1e-16 level, the branch structure and the LLF fallback are the same)
+__device__ __forceinline__ void hllc_flux_fast(const State5& um, const State5& up, double nx, double ny,
+                                               double nz, double g, double (&out)[5]) {
+  const double il = 1.0 / um.r, ir = 1.0 / up.r;
+  const double pl = (g - 1.0) * (um.E - 0.5 * il * (um.mx * um.mx + um.my * um.my + um.mz * um.mz));
+  const double pr = (g - 1.0) * (up.E - 0.5 * ir * (up.mx * up.mx + up.my * up.my + up.mz * up.mz));
+  const double vlx = um.mx * il, vly = um.my * il, vlz = um.mz * il;
+  const double vrx = up.mx * ir, vry = up.my * ir, vrz = up.mz * ir;
+  const double unl = vlx * nx + vly * ny + vlz * nz;
+  const double unr = vrx * nx + vry * ny + vrz * nz;
+  const double cl = sqrt(g * pl * il), cr = sqrt(g * pr * ir);
+  const double sl_ = sqrt(um.r), sr_ = sqrt(up.r);
+  const double iden = 1.0 / (sl_ + sr_);
+  const double vx = (sl_ * vlx + sr_ * vrx) * iden, vy = (sl_ * vly + sr_ * vry) * iden,
+               vz = (sl_ * vlz + sr_ * vrz) * iden;
+  const double hl = (um.E + pl) * il, hr = (up.E + pr) * ir;
+  const double h_roe = (sl_ * hl + sr_ * hr) * iden;
+  const double c2_roe = (g - 1.0) * (h_roe - 0.5 * (vx * vx + vy * vy + vz * vz));
+  const double un_roe = vx * nx + vy * ny + vz * nz;
+  double s_left, s_right;
+  if (c2_roe <= 0.0) {
+    s_left = fmin(unl - cl, unr - cr);
+    s_right = fmax(unl + cl, unr + cr);
+  } else {
+    const double c_roe = sqrt(c2_roe);
+    s_left = fmin(unl - cl, un_roe - c_roe);
+    s_right = fmax(unr + cr, un_roe + c_roe);
+  }
+  if (!(s_left < s_right)) {
+    llf_flux_fast(um, up, nx, ny, nz, g, out);
+    return;
+  }
+  const double s_star = (pr - pl + um.r * unl * (s_left - unl) - up.r * unr * (s_right - unr)) /
+                        (um.r * (s_left - unl) - up.r * (s_right - unr));
+  if (!isfinite(s_star)) {
+    llf_flux_fast(um, up, nx, ny, nz, g, out);
+    return;
+  }
+  const bool left = 0.0 <= s_star;
+  const bool sup_l = 0.0 <= s_left, sup_r = 0.0 >= s_right;  // supersonic: plain one-sided flux
+  const bool use_l = sup_l || (!sup_r && left);
+  const State5& u = use_l ? um : up;
+  const double iu = use_l ? il : ir;
+  const double un_k = use_l ? unl : unr, p_k = use_l ? pl : pr;
+  double f[5] = {u.r * un_k, u.mx * un_k + p_k * nx, u.my * un_k + p_k * ny, u.mz * un_k + p_k * nz,
+                 un_k * (u.E + p_k)};
+  if (!(sup_l || sup_r)) {
+    const double s_k = left ? s_left : s_right;
+    const double dk = s_k - un_k;
+    const double factor = u.r * dk / (s_k - s_star);
+    const double ds = s_star - un_k;
+    const double star[5] = {factor, factor * (u.mx * iu + ds * nx), factor * (u.my * iu + ds * ny),
+                            factor * (u.mz * iu + ds * nz), factor * (u.E * iu + ds * (s_star + p_k * iu / dk))};
+    const double uu[5] = {u.r, u.mx, u.my, u.mz, u.E};
+#pragma unroll
+    for (int c = 0; c < 5; ++c) f[c] += s_k * (star[c] - uu[c]);
+  }
+#pragma unroll
+  for (int c = 0; c < 5; ++c) out[c] = f[c];
+}
+
 // boundary_state (euler.cpp:147-161)
 __device__ __forceinline__ State5 boundary_state(const State5& in, double nx, double ny, double nz,
                                                  int kind, const GasParams& gp) {
