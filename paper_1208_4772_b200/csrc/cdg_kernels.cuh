@@ -817,7 +817,7 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs(RhsParams p) {
           record_error(p.err, 2, p.elem_offset + eg, f, gq, um.r);
         double fs[5];
         if (RM == 1 || (RM == -1 && p.gas.riemann == 1))
-          hllc_flux(um, up, fn.x, fn.y, fn.z, gamma, fs);
+          hllc_flux_fast(um, up, fn.x, fn.y, fn.z, gamma, fs);
         else
           llf_flux_fast(um, up, fn.x, fn.y, fn.z, gamma, fs);
         if (VISC) {
