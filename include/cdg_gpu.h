@@ -202,6 +202,14 @@ int cdg_gpu_p_refine_embed(cdg_gpu_level *to, const cdg_gpu_level *from, const d
 int cdg_gpu_run_level(cdg_gpu_level *lv, const cdg_gpu_run_config *cfg, const cdg_gpu_steady_params *sp,
                       double *rows, int max_rows, int *n_rows, int *converged, char *err, size_t errlen);
 
+/* Same loop, with every check row also handed to on_row(user, iteration, dt,
+ * residual) the moment it is computed (the reference emits rows live from
+ * run_steady, solver.cpp:643-647). on_row may be NULL. */
+typedef void (*cdg_gpu_row_fn)(void *user, long iteration, double dt, double residual);
+int cdg_gpu_run_level_live(cdg_gpu_level *lv, const cdg_gpu_run_config *cfg, const cdg_gpu_steady_params *sp,
+                           cdg_gpu_row_fn on_row, void *user, double *rows, int max_rows, int *n_rows,
+                           int *converged, char *err, size_t errlen);
+
 /* ---- multi-GPU halo plumbing (one process per GPU) --------------------------
  * send_elem_face[i] = element*4+face of an owned element whose face trace
  * (5*N_g values) is packed into row i of the caller-owned DEVICE buffer
@@ -230,6 +238,22 @@ int cdg_gpu_fused_traces(const cdg_gpu_level *lv);
 /* Replace the farfield ghost state (compute_rhs/rk_step take it per call,
  * solver.hpp:94-109). */
 int cdg_gpu_set_freestream(cdg_gpu_level *lv, const double *freestream5);
+
+/* Cap the grid of the persistent (grid-stride) RHS / aux kernels at max_ctas
+ * CTAs (0 restores the default: SM count x resident CTAs per SM). Results do
+ * not depend on the grid (each element's arithmetic is fixed); tests use a
+ * small cap to drive small meshes through the many-tiles-per-CTA regime of a
+ * production-size launch. */
+int cdg_gpu_set_max_ctas(cdg_gpu_level *lv, int max_ctas);
+
+/* Kernel family of a level. DEFAULT: the per-order choice compiled into the
+ * kernel-set table (row-per-warp / warp-tile kernels with fused traces where
+ * measured fastest). GENERIC: the CTA kernels (k_rhs,
+ * k_rhs_curved) for every element, the p >= 6 path; tests cross-check the two
+ * families against each other and against the reference at every order. */
+#define CDG_GPU_PATH_DEFAULT 0
+#define CDG_GPU_PATH_GENERIC 1
+int cdg_gpu_set_kernel_path(cdg_gpu_level *lv, int path);
 
 /* CUDA stream (cudaStream_t) the level launches on. */
 void *cdg_gpu_stream(cdg_gpu_level *lv);

@@ -20,6 +20,7 @@
 // the GPU). Exceptions and messages are the reference's: status 3 ->
 // NumericsError, 2 -> ConfigError.
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <map>
 #include <memory>
@@ -30,6 +31,7 @@
 
 #include "cdg/solver.hpp"
 #include "cdg_gpu.h"
+#include "cdg_gpu_adapter.hpp"
 
 namespace cdg {
 
@@ -59,7 +61,38 @@ std::vector<double> row_major(const Eigen::MatrixXd& m) {
   return out;
 }
 
-cdg_gpu_level* create_level(const DgLevel& level, const ConservedState& fs) {
+// Device of the levels the adapter creates: cdg::gpu_select_device(), else
+// $CDG_GPU_DEVICE, else 0 (one process per GPU).
+int g_device = -1;
+int adapter_device() {
+  if (g_device < 0) {
+    const char* v = std::getenv("CDG_GPU_DEVICE");
+    g_device = v ? std::atoi(v) : 0;
+  }
+  return g_device;
+}
+
+// CurvedMesh::is_curved(e) as DgLevel recorded it: DgLevel's constructor maps
+// every element from CurvedMesh::element_nodes_for_degree, which returns
+// straight_nodes(mesh, e, re) exactly when the element is not curved
+// (solver.cpp:116-118, curved_mesh.cpp:24-27), and keeps those nodes in
+// ElementGeometry::phys_nodes (operators.hpp:15). So an element is curved iff
+// its stored nodes are not bit-identical to its straight nodes -- no tolerance.
+std::vector<char> curved_mask(const DgLevel& level) {
+  const int K = level.n_elements();
+  std::vector<char> mask(K, 0);
+  for (int e = 0; e < K; ++e) {
+    const auto straight = CurvedMesh::straight_nodes(level.mesh(), e, level.refelem());
+    const auto& nodes = level.geom(e).phys_nodes;
+    bool same = nodes.size() == straight.size();
+    for (size_t i = 0; same && i < nodes.size(); ++i)
+      same = nodes[i].x == straight[i].x && nodes[i].y == straight[i].y && nodes[i].z == straight[i].z;
+    mask[e] = same ? 0 : 1;
+  }
+  return mask;
+}
+
+cdg_gpu_level* create_level(const DgLevel& level, const ConservedState& fs, const std::vector<char>& is_curved) {
   const auto& re = level.refelem();
   const int K = level.n_elements(), np = re.n_basis(), ncub = re.n_cub(), ng = re.n_face_quad();
   std::vector<double> icub = row_major(re.interp_cub()), ig = row_major(re.interp_face()),
@@ -72,13 +105,7 @@ cdg_gpu_level* create_level(const DgLevel& level, const ConservedState& fs) {
   std::vector<double> cjwr, cface, cminv, cjac;
   for (int e = 0; e < K; ++e) {
     const auto& g = level.geom(e);
-    bool curved = false;
-    for (int q = 1; q < ncub && !curved; ++q) {
-      curved = std::abs(g.cub_jac[q] - g.cub_jac[0]) > 1e-12 * std::abs(g.cub_jac[0]);
-      for (int k = 0; k < 9 && !curved; ++k)
-        curved = std::abs(g.cub_dr[q][k] - g.cub_dr[0][k]) > 1e-12 * (1.0 + std::abs(g.cub_dr[0][k]));
-    }
-    if (curved) {
+    if (is_curved[e]) {
       cids.push_back(e);
       for (int q = 0; q < ncub; ++q) cjac.push_back(g.cub_jac[q]);
       for (int q = 0; q < ncub; ++q)
@@ -156,7 +183,7 @@ cdg_gpu_level* create_level(const DgLevel& level, const ConservedState& fs) {
   d.modal_cub = vcub.data();
   cdg_gpu_level* lv = nullptr;
   char err[512] = {0};
-  throw_status(cdg_gpu_level_create(&d, 0, &lv, err, sizeof err), err);
+  throw_status(cdg_gpu_level_create(&d, adapter_device(), &lv, err, sizeof err), err);
   return lv;
 }
 
@@ -180,12 +207,14 @@ cdg_gpu_run_config to_cfg(const RunConfig& cfg) {
 }
 
 void ensure_level(RhsWorkspace& ws, const ConservedState& fs) {
-  if (!ws.lv) ws.lv = create_level(*ws.level, fs);
+  if (!ws.lv) ws.lv = create_level(*ws.level, fs, curved_mask(*ws.level));
   double f[5] = {fs[0], fs[1], fs[2], fs[3], fs[4]};
   throw_status(cdg_gpu_set_freestream(ws.lv, f), "set_freestream failed");
 }
 
 }  // namespace
+
+void gpu_select_device(int device) { g_device = device; }
 
 std::shared_ptr<RhsWorkspace> make_workspace(const DgLevel& level) {
   auto ws = std::make_shared<RhsWorkspace>();
@@ -237,15 +266,13 @@ void rk_step(const DgLevel& level, SolutionStore& u, SolutionStore& res, const R
 
 // run_steady (solver.cpp:594-676) with every level device-resident. Host work
 // per level is the reference's: build the DgLevel (setup tables), then one
-// cdg_gpu_run_level call; rows reach on_row when the level finishes.
+// cdg_gpu_run_level_live call; rows reach on_row live, at each check iteration.
 SteadyResult run_steady(const CurvedMesh& cmesh, const BcMap& bc_map, const RunConfig& cfg,
                         const ConservedState& freestream, const std::function<void(const ConvergenceRow&)>& on_row) {
   if (cfg.p_schedule.empty()) throw ConfigError("run_steady: empty p-schedule");
   for (size_t i = 1; i < cfg.p_schedule.size(); ++i)
     if (cfg.p_schedule[i] <= cfg.p_schedule[i - 1])
       throw ConfigError("run_steady: p-schedule must be strictly increasing");
-  if (cfg.residual_norm != "inf" && cfg.residual_norm != "l2")
-    throw ConfigError("run_steady: unknown residual norm '" + cfg.residual_norm + "'");
   SteadyResult result;
   const auto wall_start = std::chrono::steady_clock::now();
   const cdg_gpu_run_config c = to_cfg(cfg);
@@ -255,7 +282,9 @@ SteadyResult run_steady(const CurvedMesh& cmesh, const BcMap& bc_map, const RunC
     const int p = cfg.p_schedule[li];
     auto re = level_reference_element(cmesh, p, cfg);
     DgLevel level(cmesh, re, bc_map, cfg.padded);
-    std::unique_ptr<cdg_gpu_level, void (*)(cdg_gpu_level*)> lv(create_level(level, freestream),
+    std::vector<char> mask(level.n_elements());
+    for (int e = 0; e < level.n_elements(); ++e) mask[e] = cmesh.is_curved(e) ? 1 : 0;
+    std::unique_ptr<cdg_gpu_level, void (*)(cdg_gpu_level*)> lv(create_level(level, freestream, mask),
                                                                 cdg_gpu_level_destroy);
     if (li == 0) {
       throw_status(cdg_gpu_fill_freestream(lv.get()), "fill_freestream failed");
@@ -271,7 +300,7 @@ SteadyResult run_steady(const CurvedMesh& cmesh, const BcMap& bc_map, const RunC
     sp.max_iterations = cfg.max_iterations_per_level;
     sp.fixed_iterations = li < cfg.fixed_iterations.size() ? cfg.fixed_iterations[li] : -1;
     sp.check_interval = cfg.check_interval;
-    sp.residual_kind = cfg.residual_norm == "l2" ? 1 : 0;
+    sp.residual_kind = cfg.residual_norm == "l2" ? 1 : 0;  // anything else: inf (solver.cpp:572-590)
     sp.tolerance = last ? cfg.final_tolerance : cfg.intermediate_tolerance;
     sp.dt_override = cfg.dt_override;
     sp.degree = p;
@@ -279,14 +308,24 @@ SteadyResult run_steady(const CurvedMesh& cmesh, const BcMap& bc_map, const RunC
     std::vector<double> rows(3 * (size_t)max_rows);
     int n_rows = 0, converged = 0;
     char err[512] = {0};
-    throw_status(cdg_gpu_run_level(lv.get(), &c, &sp, rows.data(), max_rows, &n_rows, &converged, err, sizeof err),
+    // rows go to the log and on_row as each check iteration completes, with
+    // the wall time since run_steady started (solver.cpp:643-647)
+    struct Sink {
+      int p;
+      SteadyResult* result;
+      const std::function<void(const ConvergenceRow&)>* on_row;
+      std::chrono::steady_clock::time_point t0;
+    } sink{p, &result, &on_row, wall_start};
+    auto emit = [](void* user, long iteration, double dt, double residual) {
+      auto* k = static_cast<Sink*>(user);
+      const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - k->t0).count();
+      ConvergenceRow row{k->p, iteration, dt, residual, wall};
+      k->result->log.push_back(row);
+      if (*k->on_row) (*k->on_row)(row);
+    };
+    throw_status(cdg_gpu_run_level_live(lv.get(), &c, &sp, emit, &sink, rows.data(), max_rows, &n_rows, &converged,
+                                        err, sizeof err),
                  err);
-    const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall_start).count();
-    for (int i = 0; i < n_rows && i < max_rows; ++i) {
-      ConvergenceRow row{p, static_cast<long>(rows[3 * i]), rows[3 * i + 1], rows[3 * i + 2], wall};
-      result.log.push_back(row);
-      if (on_row) on_row(row);
-    }
     if (last) {
       result.converged = converged != 0;
       if (sp.fixed_iterations > 0 && !result.log.empty())

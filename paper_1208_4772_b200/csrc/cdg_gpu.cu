@@ -57,16 +57,13 @@ const std::vector<KernelSet>& kernel_sets() {
   return sets;
 }
 
+// The kernel set of a level shape is fixed at compile time: one KernelSet per
+// (N_p, N_cub, N_g) in the sets_*.cu tables (the measured-best choice, see
+// DESIGN.md §6); nothing is selected at run time.
 const KernelSet* find_set(int np, int ncub, int ng) {
-  const char* v = std::getenv("CDG_KCFG");
-  int want = v ? std::atoi(v) : 0, seen = 0;
-  const KernelSet* first = nullptr;
   for (const auto& k : kernel_sets())
-    if (k.np == np && k.ncub == ncub && k.ng == ng) {
-      if (!first) first = &k;
-      if (seen++ == want) return &k;
-    }
-  return first;
+    if (k.np == np && k.ncub == ncub && k.ng == ng) return &k;
+  return nullptr;
 }
 
 // ---- small dense host linear algebra (setup only) --------------------------
@@ -181,6 +178,7 @@ struct cdg_gpu_level {
   const KernelSet* ks = nullptr;
   cudaStream_t stream = nullptr;
   int n_sms = 148;
+  int max_ctas = 0;  // cap on persistent-kernel grids (0: n_sms x CTAs/SM); cdg_gpu_set_max_ctas
   long long launches = 0;
   // state
   double *u = nullptr, *res = nullptr, *rhs = nullptr, *traces = nullptr, *before = nullptr;
@@ -258,7 +256,13 @@ struct cdg_gpu_level {
 
   int n_rows() const { return K * 5; }
   int n_tiles() const { return (K + ks->E - 1) / ks->E; }
-  int grid(int tiles) const { return std::max(1, std::min(tiles, n_sms * ks->minb)); }
+  // persistent grid: min(work items, resident CTAs), optionally capped
+  int cap(int items, int per_sm) const {
+    int g = std::min(items, n_sms * per_sm);
+    if (max_ctas > 0) g = std::min(g, max_ctas);
+    return std::max(1, g);
+  }
+  int grid(int tiles) const { return cap(tiles, ks->minb); }
 };
 
 namespace {
@@ -353,8 +357,7 @@ RhsParams rhs_params(cdg_gpu_level* lv, int stage) {
   p.sqrt_eps = lv->sqrt_eps;
   p.qcub = lv->qcub;
   p.qtr_stride = (size_t)(lv->K + lv->n_halo) * 5 * lv->tb;
-  static const int pf = std::getenv("CDG_PREFETCH") ? std::atoi(std::getenv("CDG_PREFETCH")) : 15;
-  p.prefetch = pf;
+  p.prefetch = 15;  // L2 prefetch of res / traces / next tile (CTA kernel, measured: DESIGN.md §6)
   return p;
 }
 
@@ -379,7 +382,7 @@ void launch_curved(cdg_gpu_level* lv, bool update, int stage, int mode = 0) {
               : mode == 1 ? (update ? lv->ks->rowc_visc_update[rm] : lv->ks->rowc_visc_only[rm])
                           : (update ? lv->ks->rowc_update[rm] : lv->ks->rowc_only[rm]);
     const int tiles = (lv->n_curved + lv->ks->rowc_e - 1) / lv->ks->rowc_e;
-    fr<<<std::max(1, std::min(tiles, lv->n_sms * lv->ks->rowc_minb)), lv->ks->rowc_nth, lv->ks->smem_rowc,
+    fr<<<lv->cap(tiles, lv->ks->rowc_minb), lv->ks->rowc_nth, lv->ks->smem_rowc,
          lv->stream>>>(cp);
     ++lv->launches;
     return;
@@ -388,7 +391,7 @@ void launch_curved(cdg_gpu_level* lv, bool update, int stage, int mode = 0) {
   auto fn = mode == 2 ? lv->ks->aux_curved
                       : mode == 1 ? (update ? lv->ks->curved_visc_update : lv->ks->curved_visc_only)
                                   : (update ? lv->ks->curved_update : lv->ks->curved_only);
-  fn<<<std::max(1, std::min(tiles, lv->n_sms)), kThreads, lv->ks->smem_curved, lv->stream>>>(cp);
+  fn<<<lv->cap(tiles, 1), kThreads, lv->ks->smem_curved, lv->stream>>>(cp);
   ++lv->launches;
 }
 
@@ -419,8 +422,7 @@ void launch_rhs_warp(cdg_gpu_level* lv, bool update, int stage) {
     launch_curved(lv, update, stage);
     return;
   }
-  const int ctas = std::max(1, std::min((tiles + lv->ks->warp_warps - 1) / lv->ks->warp_warps,
-                                        lv->n_sms * lv->ks->warp_minb));
+  const int ctas = lv->cap((tiles + lv->ks->warp_warps - 1) / lv->ks->warp_warps, lv->ks->warp_minb);
   const int rm = lv->gas.riemann == 1 ? 1 : 0;
   auto fn = update ? lv->ks->warp_update[rm] : lv->ks->warp_only[rm];
   fn<<<ctas, 32 * lv->ks->warp_warps, lv->ks->smem_warp, lv->stream>>>(w);
@@ -434,8 +436,7 @@ void launch_rhs_row(cdg_gpu_level* lv, bool update, int stage) {
   p.frag_op2 = lv->rfrag2;
   // L2 prefetching measured neutral-to-negative for the row kernel (4 CTAs/SM
   // already cover the latency; profiles/r1); it stays on for the CTA kernel
-  static const int pf_row = std::getenv("CDG_PREFETCH_ROW") ? std::atoi(std::getenv("CDG_PREFETCH_ROW")) : 0;
-  p.prefetch = pf_row;
+  p.prefetch = 0;
   const int rm = lv->gas.riemann == 1 ? 1 : 0;
   auto fn = update ? lv->ks->row_update[rm] : lv->ks->row_only[rm];
   const int E = lv->ks->row_e;
@@ -444,7 +445,7 @@ void launch_rhs_row(cdg_gpu_level* lv, bool update, int stage) {
     launch_curved(lv, update, stage);
     return;
   }
-  fn<<<std::max(1, std::min(tiles, lv->n_sms * lv->ks->row_minb)), lv->ks->row_nth, lv->ks->smem_row, lv->stream>>>(p);
+  fn<<<lv->cap(tiles, lv->ks->row_minb), lv->ks->row_nth, lv->ks->smem_row, lv->stream>>>(p);
   ++lv->launches;
   launch_curved(lv, update, stage);
 }
@@ -781,8 +782,7 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
         for (int n = 0; n < np8 / 8; ++n) frag_nat(f2, op2r, np, k2, n, k);
       lv->rfrag2 = dev_upload(f2);
 
-      const char* nr = std::getenv("CDG_NOROW");
-      lv->use_row = !(nr && std::atoi(nr));
+      lv->use_row = true;
     }
     if (lv->ks->warp_update[0] || lv->ks->row_update[0]) {
       const int nch = (ncub + 7) / 8, nfch = (nf + 7) / 8, ks1 = kp / 8, nt = np8 / 8;
@@ -800,8 +800,7 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
       if (!lv->ks->warp_update[0]) f2v.clear(), f2f.clear();
       lv->wfrag2v = dev_upload(f2v);
       lv->wfrag2f = dev_upload(f2f);
-      const char* nw = std::getenv("CDG_NOWARP");
-      lv->use_warp = lv->ks->warp_update[0] && !(nw && std::atoi(nw));
+      lv->use_warp = lv->ks->warp_update[0] != nullptr;
     }
     if (d->vandermonde_inv) {
       lv->d_vinv = dev_upload(std::vector<double>(d->vandermonde_inv, d->vandermonde_inv + (size_t)np * np));
@@ -939,18 +938,19 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
         for (int k = 0; k < k2 / 8; ++k)
           for (int n = 0; n < np8 / 8; ++n) frag_nat(f2, opr, np, k2, n, k);
         lv->rfrag_opc = dev_upload(f2);
-        if (lv->ks->warp_update[0] || lv->ks->row_update[0]) {
-          const char* nr = std::getenv("CDG_NOROWC");
-          lv->use_rowc = !(nr && std::atoi(nr));
-        }
+        lv->use_rowc = lv->ks->warp_update[0] || lv->ks->row_update[0];
       }
-      // tiles of 16 elements with at least one affine element: the affine
-      // kernels skip the all-curved tiles
+      // tiles (of the affine kernel's E elements) with at least one affine
+      // element: the affine kernels skip the all-curved tiles. The warp-tile
+      // kernel and the aux kernel walk 16-element tiles as well.
       {
+        const int E = lv->use_row ? lv->ks->row_e : lv->ks->E;
+        if (E != 16 || lv->ks->E != 16)
+          throw Status(CDG_GPU_ERR_CONFIG, "curved levels need 16-element affine tiles");
         std::vector<int> at;
-        for (int t = 0; t * 16 < K; ++t) {
+        for (int t = 0; t * E < K; ++t) {
           bool any = false;
-          for (int e = t * 16; e < std::min(K, t * 16 + 16); ++e) any = any || !is_curved[e];
+          for (int e = t * E; e < std::min(K, t * E + E); ++e) any = any || !is_curved[e];
           if (any) at.push_back(t);
         }
         lv->n_affine_tiles = (int)at.size();
@@ -1351,6 +1351,28 @@ int cdg_gpu_set_freestream(cdg_gpu_level* lv, const double* fs) {
   return CDG_GPU_OK;
 }
 
+int cdg_gpu_set_max_ctas(cdg_gpu_level* lv, int max_ctas) {
+  if (max_ctas < 0) return CDG_GPU_ERR_CONFIG;
+  lv->max_ctas = max_ctas;
+  // grids are baked into the captured graphs
+  if (lv->graph) cudaGraphExecDestroy(lv->graph), lv->graph = nullptr;
+  if (lv->graph_visc) cudaGraphExecDestroy(lv->graph_visc), lv->graph_visc = nullptr;
+  for (auto& ge : lv->gft)
+    if (ge) cudaGraphExecDestroy(ge), ge = nullptr;
+  return CDG_GPU_OK;
+}
+
+int cdg_gpu_set_kernel_path(cdg_gpu_level* lv, int path) {
+  if (path != CDG_GPU_PATH_DEFAULT && path != CDG_GPU_PATH_GENERIC) return CDG_GPU_ERR_CONFIG;
+  const bool generic = path == CDG_GPU_PATH_GENERIC;
+  lv->use_row = !generic && lv->ks->row_update[0] != nullptr;
+  lv->use_warp = !generic && lv->ks->warp_update[0] != nullptr;
+  lv->use_rowc = !generic && lv->rfrag_opc != nullptr;
+  lv->traces_valid = false;
+  cdg_gpu_set_max_ctas(lv, lv->max_ctas);  // drops the captured graphs
+  return CDG_GPU_OK;
+}
+
 int cdg_gpu_set_profiling(cdg_gpu_level* lv, int enabled) {
   lv->profiling = enabled != 0;
   return CDG_GPU_OK;
@@ -1475,6 +1497,12 @@ int cdg_gpu_p_refine_embed(cdg_gpu_level* to, const cdg_gpu_level* from, const d
 
 int cdg_gpu_run_level(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, const cdg_gpu_steady_params* sp,
                       double* rows, int max_rows, int* n_rows, int* converged, char* err, size_t errlen) {
+  return cdg_gpu_run_level_live(lv, cfg, sp, nullptr, nullptr, rows, max_rows, n_rows, converged, err, errlen);
+}
+
+int cdg_gpu_run_level_live(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, const cdg_gpu_steady_params* sp,
+                           cdg_gpu_row_fn on_row, void* user, double* rows, int max_rows, int* n_rows,
+                           int* converged, char* err, size_t errlen) {
   // Carpenter-Kennedy LSRK4(5) coefficients (rk.hpp:15-24)
   static const double A[5] = {0.0, -567301805773.0 / 1357537059087.0, -2404267990393.0 / 2016746695238.0,
                               -3550918686646.0 / 2091501179385.0, -1275806237668.0 / 842570457699.0};
@@ -1513,6 +1541,7 @@ int cdg_gpu_run_level(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, const cd
         rows[3 * *n_rows + 2] = r;
       }
       ++*n_rows;
+      if (on_row) on_row(user, iter, dt, r);  // live, as the reference's loop emits it (solver.cpp:643-647)
       if (initial < 0.0) initial = std::max(r, 1e-300);
       if (r > 1e6 * initial && r > 1e-12) {
         char buf[256];

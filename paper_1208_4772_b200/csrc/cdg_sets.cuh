@@ -11,7 +11,6 @@
 #include "cdg_kernels.cuh"
 #include "cdg_row.cuh"
 #include "cdg_rowc.cuh"
-#include "cdg_rowp.cuh"
 #include "cdg_warp.cuh"
 
 namespace cdg_gpu {
@@ -99,23 +98,6 @@ KernelSet with_warp(KernelSet k) {
   k.smem_warp = W::SMEM_BYTES;
   k.warp_warps = WARPS;
   k.warp_minb = MINB;
-  return k;
-}
-
-// software-pipelined row kernel (cdg_rowp.cuh); same host operator layout as
-// with_row<..., CH = 8>
-template <int NP, int NCUB, int NG, int MINB = 4, bool USMEM = false>
-KernelSet with_rowp(KernelSet k) {
-  using RC = RPCfg<NP, NCUB, NG, MINB, USMEM>;
-  k.row_update[0] = &k_rhs_rowp<RC, true, 0>;
-  k.row_update[1] = &k_rhs_rowp<RC, true, 1>;
-  k.row_only[0] = &k_rhs_rowp<RC, false, 0>;
-  k.row_only[1] = &k_rhs_rowp<RC, false, 1>;
-  k.smem_row = RC::SMEM_BYTES;
-  k.row_minb = MINB;
-  k.row_ch = RC::CH;
-  k.row_e = RC::E;
-  k.row_nth = RC::NTH;
   return k;
 }
 

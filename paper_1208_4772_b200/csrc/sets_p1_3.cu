@@ -17,10 +17,7 @@ std::vector<KernelSet> kernel_sets_p1_3() {
       with_rowc<10, 15, 6, 8, 32, 4>(with_row<10, 15, 6, 8, 32, 4, 224>(make_set<10, 15, 6, 16, 16, 2>())),
       with_row<20, 35, 12, 8, 32, 4, 224>(make_set<20, 35, 12, 16, 16, 2>()),
       // curved-mesh strengths (3p-3 / 3p-2): refelem.hpp:118-119
-      with_rowc<20, 35, 16, 8, 32, 4>(with_row<20, 35, 16, 8, 32, 4, 192>(make_set<20, 35, 16, 16, 16, 2>())),
-      // tuning variants (CDG_KCFG=1): the warp-tile kernel (p=1 at 2 CTAs/SM)
-      with_warp<4, 5, 3, 4, 2>(make_set<4, 5, 3, 16, 8, 2>()), with_warp<10, 15, 6>(make_set<10, 15, 6, 16, 16, 2>()),
-      with_warp<20, 35, 12>(make_set<20, 35, 12, 16, 16, 2>()), with_warp<20, 35, 16>(make_set<20, 35, 16, 16, 16, 2>())};
+      with_rowc<20, 35, 16, 8, 32, 4>(with_row<20, 35, 16, 8, 32, 4, 192>(make_set<20, 35, 16, 16, 16, 2>()))};
 }
 
 }  // namespace cdg_gpu

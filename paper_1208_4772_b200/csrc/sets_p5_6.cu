@@ -11,11 +11,7 @@ std::vector<KernelSet> kernel_sets_p5_6() {
       // tets); p=6: CTA kernel with 8-node chunks (27.8 vs 34.8 ms)
       with_row<56, 126, 56, 8, 32, 3, 192>(make_set<56, 126, 56, 16, 16, 2>()),
       make_set<84, 210, 84, 16, 8, 2, 16>(),
-      with_rowc<56, 210, 84, 8, 32, 3>(with_row<56, 210, 84, 8, 32, 3, 192>(make_set<56, 210, 84, 16, 16, 2>())), make_set<84, 330, 165, 16>(),
-      // tuning variants (CDG_KCFG)
-      make_set<56, 126, 56, 16, 16, 2>(), make_set<84, 210, 84, 16>(),
-      with_row<56, 126, 56, 8, 32, 3, 0>(make_set<56, 126, 56, 16, 16, 2>()),   // p=5 k-steps not unrolled (CDG_KCFG=2)
-      with_rowc<56, 210, 84, 8, 32, 3>(make_set<56, 210, 84, 16, 16, 2>())};  // curved-mesh p=5, CTA kernel for the affine elements (CDG_KCFG=1)
+      with_rowc<56, 210, 84, 8, 32, 3>(with_row<56, 210, 84, 8, 32, 3, 192>(make_set<56, 210, 84, 16, 16, 2>())), make_set<84, 330, 165, 16>()};
 }
 
 }  // namespace cdg_gpu

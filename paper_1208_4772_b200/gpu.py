@@ -118,6 +118,8 @@ def lib():
         L.cdg_gpu_launch_count.argtypes = [vp]
         L.cdg_gpu_launch_count.restype = C.c_longlong
         L.cdg_gpu_set_profiling.argtypes = [vp, C.c_int]
+        L.cdg_gpu_set_max_ctas.argtypes = [vp, C.c_int]
+        L.cdg_gpu_set_kernel_path.argtypes = [vp, C.c_int]
         L.cdg_gpu_last_profile.argtypes = [vp, _dp]
         L.cdg_gpu_version.restype = C.c_char_p
         L.cdg_gpu_measure_fp64_peak.argtypes = [C.c_int, _dp]
@@ -295,6 +297,15 @@ class GpuLevel:
 
     def launch_count(self) -> int:
         return int(lib().cdg_gpu_launch_count(self.h))
+
+    def set_max_ctas(self, n: int):
+        """Cap persistent-kernel grids at n CTAs (0: default); results are grid-independent."""
+        _raise(lib().cdg_gpu_set_max_ctas(self.h, int(n)), "set_max_ctas failed")
+
+    def set_kernel_path(self, path: str):
+        """'default' (per-order compiled choice) or 'generic' (CTA kernels everywhere)."""
+        code = {"default": 0, "generic": 1}[path]
+        _raise(lib().cdg_gpu_set_kernel_path(self.h, code), "set_kernel_path failed")
 
     def set_profiling(self, on: bool):
         lib().cdg_gpu_set_profiling(self.h, int(on))

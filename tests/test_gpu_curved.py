@@ -48,15 +48,16 @@ def _fs(gpu):
 # CDG_SLOW=1) -- the BASELINE "cylinder P=1..6" sweep on the curved sphere
 @pytest.mark.parametrize("kernel", ["row", "cta"])
 @pytest.mark.parametrize("p", [1, 2, 3, 4, 5] + ([6] if __import__("os").environ.get("CDG_SLOW") else []))
-def test_curved_sphere_rhs_and_steps_match_reference(gpu_lib, refmod, p, kernel, monkeypatch):
+def test_curved_sphere_rhs_and_steps_match_reference(gpu_lib, refmod, p, kernel):
     """kernel: the row-per-warp curved kernel (k_rhs_rowc, default for p <= 5)
-    or the CTA kernel (k_rhs_curved; CDG_NOROWC=1, the p >= 6 path)."""
+    or the CTA kernels (k_rhs_curved + k_rhs: the generic path, default for
+    p >= 6)."""
     gpu, ref = gpu_lib, refmod
-    monkeypatch.setenv("CDG_NOROWC", "1" if kernel == "cta" else "0")
     rm, rl, mesh, ids, nodes = sphere_case(ref, p)
     assert len(ids) > 0 and rl.n_cub > 0
     fs = _fs(gpu)
     lv = gpu.GpuLevel(mesh, p, bc={"sphere": 0, "farfield": 1}, freestream=fs, curved=(ids, nodes[ids]))
+    lv.set_kernel_path("generic" if kernel == "cta" else "default")
     assert (lv.n_cub, lv.n_face_quad) == (rl.n_cub, rl.n_face_quad)
     # node pairing identical to the reference's nearest-point pairing
     g = rl.geometry()
@@ -100,12 +101,12 @@ VISC_RAMP = dict(enabled=True, eps0=0.3, kappa=4.0, s0_offset=0.0)
 @pytest.mark.parametrize("kernel", ["row", "cta"])
 @pytest.mark.parametrize("p", [2, 3, 4])
 @pytest.mark.parametrize("visc,riem", [(VISC_FORCED, "llf"), (VISC_RAMP, "hllc")])
-def test_curved_sphere_viscous_matches_reference(gpu_lib, refmod, p, visc, riem, kernel, monkeypatch):
+def test_curved_sphere_viscous_matches_reference(gpu_lib, refmod, p, visc, riem, kernel):
     gpu, ref = gpu_lib, refmod
-    monkeypatch.setenv("CDG_NOROWC", "1" if kernel == "cta" else "0")
     rm, rl, mesh, ids, nodes = sphere_case(ref, p)
     fs = _fs(gpu)
     lv = gpu.GpuLevel(mesh, p, bc={"sphere": 0, "farfield": 1}, freestream=fs, curved=(ids, nodes[ids]))
+    lv.set_kernel_path("generic" if kernel == "cta" else "default")
     u = rl.random_admissible_store(11)
     r_ref = rl.compute_rhs(u, ref.make_cfg(riem, viscosity=visc), fs)
     eps_ref, q_ref = rl.last_viscosity()
@@ -147,7 +148,7 @@ def test_curved_sphere_jacobian_weighted_indicator(gpu_lib, refmod, p):
 
 # ---- the curved kernels at GPU-filling sizes: make_cube_mesh(n) with the
 # collocation nodes moved by a smooth global map (scripts/bench_curved.py) ---
-def _mapped_cube(gpu, R, n, p, amp, frac=1.0, kernel="row", monkeypatch=None):
+def _mapped_cube(gpu, R, n, p, amp, frac=1.0, kernel="row"):
     import importlib.util
     spec = importlib.util.spec_from_file_location("bench_curved", "scripts/bench_curved.py")
     bcm = importlib.util.module_from_spec(spec)
@@ -156,10 +157,10 @@ def _mapped_cube(gpu, R, n, p, amp, frac=1.0, kernel="row", monkeypatch=None):
     re = R.level_reference_element(p, True)
     X = bcm.curved_nodes(mesh, re, amp)
     ids = np.arange(int(round(frac * mesh.n_owned)))
-    if monkeypatch is not None:
-        monkeypatch.setenv("CDG_NOROWC", "1" if kernel == "cta" else "0")
     fs = gpu.make_state(1.0, [0.4, 0.05, -0.1], 1.0)
-    return gpu.GpuLevel(mesh, p, bc=0, freestream=fs, curved=(ids, X[ids])), mesh, fs
+    lv = gpu.GpuLevel(mesh, p, bc=0, freestream=fs, curved=(ids, X[ids]))
+    lv.set_kernel_path("generic" if kernel == "cta" else "default")
+    return lv, mesh, fs
 
 
 def _smooth_state(lv, seed):
@@ -193,7 +194,7 @@ def test_curved_path_on_straight_elements_equals_affine_path(gpu_lib, p):
 
 
 @pytest.mark.parametrize("frac", [1.0, 0.3])
-def test_curved_row_kernel_matches_cta_kernel_mapped_cube(gpu_lib, frac, monkeypatch):
+def test_curved_row_kernel_matches_cta_kernel_mapped_cube(gpu_lib, frac):
     """k_rhs_rowc vs k_rhs_curved on 6,000 curved (or 30% curved + affine)
     elements, RHS and three RK steps (the affine kernels skip the all-curved
     tiles, the mixed tiles keep their affine rows)."""
@@ -201,7 +202,7 @@ def test_curved_row_kernel_matches_cta_kernel_mapped_cube(gpu_lib, frac, monkeyp
     from paper_1208_4772_b200 import refelem as R
     out = {}
     for kernel in ("row", "cta"):
-        lv, mesh, fs = _mapped_cube(gpu, R, 10, 4, 0.02, frac, kernel, monkeypatch)
+        lv, mesh, fs = _mapped_cube(gpu, R, 10, 4, 0.02, frac, kernel)
         u = _smooth_state(lv, 5)
         cfg = gpu.run_config("llf")
         r = lv.compute_rhs(cfg, u)

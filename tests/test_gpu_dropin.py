@@ -1,0 +1,57 @@
+"""The drop-in, run by the driver: the reference's OWN test and acceptance
+programs linked against the GPU path.
+
+oracle/Makefile (target `dropin`) compiles the unmodified reference sources
+with solver.cpp's kernel entry points renamed (-Dcompute_rhs=compute_rhs_cpu
+...) and links integration/cdg_gpu_adapter.cpp, which implements
+cdg::make_workspace / compute_rhs / rk_step / interpolate_to_faces /
+current_viscosity / aux_gradient / run_steady (solver.hpp:83-154) over the C
+ABI (include/cdg_gpu.h). So every kernel call these programs make runs on the
+B200:
+
+  * oracle/_ref/test_solver_gpu  = /root/reference/proj/tests/test_solver.cpp
+    (doctest; 19 test cases, the reference's solver unit suite);
+  * oracle/_ref/acceptance_gpu   = tests/acceptance/acceptance_main.cpp with
+    criteria C03 (free-stream preservation, straight + curved sphere), C04
+    (discrete conservation), C06 (RK order), C11 (p-refinement), C12 (padded
+    layout, bitwise paths, determinism).
+
+Needs the prebuilt binaries (built here by __graft_entry__.build(); they travel
+to the GPU box with the snapshot)."""
+import os
+import re
+import subprocess
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+REF = Path(__file__).resolve().parent.parent / "oracle" / "_ref"
+
+
+def _binary(name):
+    b = REF / name
+    if not b.exists():
+        pytest.skip(f"{b} not built (reference sources absent when building)")
+    return str(b)
+
+
+def test_reference_solver_unit_suite_through_the_gpu_adapter():
+    r = subprocess.run([_binary("test_solver_gpu")], capture_output=True, text=True, timeout=900)
+    out = r.stdout + r.stderr
+    m = re.search(r"test cases:\s*(\d+)\s*\|\s*(\d+) passed\s*\|\s*(\d+) failed", out)
+    assert m, out[-2000:]
+    total, passed, failed = (int(x) for x in m.groups())
+    assert r.returncode == 0 and failed == 0 and passed == total >= 19, out[-2000:]
+
+
+def test_reference_acceptance_criteria_through_the_gpu_adapter(tmp_path):
+    crit = ["3", "4", "6", "11", "12"]
+    r = subprocess.run([_binary("acceptance_gpu"), "--fixture-dir", str(tmp_path)] + crit,
+                       capture_output=True, text=True, timeout=1800, env=dict(os.environ, OMP_NUM_THREADS="8"))
+    out = r.stdout + r.stderr
+    passed = re.findall(r"^\[PASS\] C(\d+)", out, re.M)
+    failed = re.findall(r"^\[FAIL\] C(\d+)", out, re.M)
+    assert not failed, out[-3000:]
+    assert sorted(int(c) for c in passed) == sorted(int(c) for c in crit), out[-3000:]
