@@ -63,6 +63,39 @@ def build_gpu(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+def build_variant(tag: str, defines, units=("sets_p4",), verbose: bool = False) -> Path:
+    """Tuning experiments only (not the product): recompile the kernel-set TUs
+    `units` with extra -D`defines` into build/<tag>/ and link
+    variants/libcdg_gpu_<tag>.so with the product objects of every other TU.
+    scripts/tune_p4.py times such libraries side by side (gpu.use_library)."""
+    build_gpu()
+    headers = sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "cdg_gpu.h"]
+    objdir = PKG / "build" / tag
+    objdir.mkdir(parents=True, exist_ok=True)
+    out = PKG / "variants" / f"libcdg_gpu_{tag}.so"
+    out.parent.mkdir(exist_ok=True)
+    comp = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+            "-Xcompiler", "-fPIC", "-ccbin", "/usr/bin/g++", "-I", str(ROOT / "include")]
+    comp += [f"-D{d}" for d in defines]
+    objs = []
+    for cu in sorted(CSRC.glob("*.cu")):
+        if cu.stem in units:
+            obj = objdir / (cu.stem + ".o")
+            if _stale(obj, [cu] + headers) or not (objdir / "defines").exists() or \
+                    (objdir / "defines").read_text() != " ".join(defines):
+                cmd = comp + ["-c", "-o", str(obj), str(cu)]
+                if verbose:
+                    print(" ".join(cmd), flush=True)
+                subprocess.run(cmd, check=True)
+            objs.append(obj)
+        else:
+            objs.append(PKG / "build" / (cu.stem + ".o"))
+    (objdir / "defines").write_text(" ".join(defines))
+    subprocess.run([_nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-ccbin", "/usr/bin/g++",
+                    "-o", str(out), *map(str, objs)], check=True)
+    return out
+
+
 def build_oracle(verbose: bool = False) -> None:
     """oracle/: the C restatement always; oracle/_ref when /root/reference exists."""
     env = dict(os.environ)

@@ -83,6 +83,15 @@ class LevelDesc(C.Structure):
 _lib = None
 
 
+def use_library(path) -> None:
+    """Load a different build of the C ABI (tuning experiments: build.build_variant).
+    Must be called before the first call into the library."""
+    global LIB_PATH
+    if _lib is not None:
+        raise RuntimeError("library already loaded")
+    LIB_PATH = Path(path).resolve()
+
+
 def lib():
     """Load libcdg_gpu.so (fails loudly: no fallback path exists)."""
     global _lib
