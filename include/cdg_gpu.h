@@ -230,6 +230,51 @@ int cdg_gpu_rk_stage_phase(cdg_gpu_level *lv, const cdg_gpu_run_config *cfg, int
                            double dt, const double a[5], const double b[5], char *err,
                            size_t errlen);
 
+/* ---- multi-rank driver (one shard per rank) -----------------------------------
+ * The reference runs one process over the whole mesh (rk_step / compute_rhs /
+ * compute_timestep / residual_norm / run_steady, solver.cpp:239-676); these
+ * entry points run the same loop over R shards -- cdg_gpu_level's with ghost
+ * elements K..K+n_halo-1 -- with one halo exchange of face traces per RK stage
+ * (inviscid) or per viscous phase (U traces + sqrt(eps), then the q_m traces),
+ * the interior tiles overlapping the transfer, and all-rank MIN / MAX / SUM
+ * reductions for the time step, the viscous gate and the residual. Results
+ * are bitwise identical to the single-level run (l2 residual: to rounding).
+ *
+ * cdg_gpu_halo_define: the shard's halo rows, peer by peer: rows
+ * [sum(send_count[<i]), +send_count[i]) of send_elem_face go to rank
+ * peer_rank[i], likewise recv. Both sides list a shared face in the same
+ * (canonical) order. The library owns the transfer buffers. */
+typedef struct cdg_gpu_comm cdg_gpu_comm;
+int cdg_gpu_halo_define(cdg_gpu_level *lv, int n_peers, const int *peer_rank, const int *send_count,
+                        const int *recv_count, const int *send_elem_face, const int *recv_elem_face);
+/* NCCL transport, one process per GPU: rank 0 calls cdg_gpu_comm_unique_id and
+ * the caller broadcasts the 128 bytes (MPI, torch.distributed, a file); every
+ * rank then creates its communicator over its shard. libnccl.so.2 is loaded at
+ * run time (status 2 when absent). */
+int cdg_gpu_comm_unique_id(unsigned char id[128], char *err, size_t errlen);
+int cdg_gpu_comm_create_nccl(cdg_gpu_level *shard, const unsigned char id[128], int rank, int nranks,
+                             cdg_gpu_comm **out, char *err, size_t errlen);
+/* In-process transport: one host thread drives all nranks shards (levels[r]
+ * is rank r; on one GPU or several, peer copies over NVLink). */
+int cdg_gpu_comm_create_local(int nranks, cdg_gpu_level *const *levels, cdg_gpu_comm **out, char *err,
+                              size_t errlen);
+void cdg_gpu_comm_destroy(cdg_gpu_comm *comm);
+/* rk_steps over every shard of the communicator (viscous or not). */
+int cdg_gpu_comm_rk_steps(cdg_gpu_comm *comm, const cdg_gpu_run_config *cfg, int nsteps, double dt,
+                          const double a[5], const double b[5], char *err, size_t errlen);
+/* global compute_timestep (MIN over ranks), snapshot, residual_norm (inf: MAX,
+ * l2: SUM of squares), fill_freestream, one run_steady level. */
+int cdg_gpu_comm_timestep(cdg_gpu_comm *comm, const cdg_gpu_run_config *cfg, int use_viscosity, double *dt_out,
+                          char *err, size_t errlen);
+int cdg_gpu_comm_snapshot(cdg_gpu_comm *comm);
+int cdg_gpu_comm_residual(cdg_gpu_comm *comm, int kind, double dt, double *out);
+int cdg_gpu_comm_fill_freestream(cdg_gpu_comm *comm);
+int cdg_gpu_comm_run_level(cdg_gpu_comm *comm, const cdg_gpu_run_config *cfg, const cdg_gpu_steady_params *sp,
+                           cdg_gpu_row_fn on_row, void *user, double *rows, int max_rows, int *n_rows,
+                           int *converged, char *err, size_t errlen);
+/* halo exchanges issued so far (evidence counter) */
+int cdg_gpu_comm_exchange_count(const cdg_gpu_comm *comm);
+
 /* 1 when cdg_gpu_rk_steps runs the fused-trace path (the RHS kernel's epilogue
  * writes the next stage's face traces; one trace kernel seeds each call),
  * else 0. Informational (bench roofline accounting). */

@@ -349,6 +349,55 @@ __global__ void k_halo_copy(double* traces, double* buf, const int* idx, int n, 
   }
 }
 
+// Halo payload rows of the multi-rank driver: row i of buf (width W doubles)
+// holds, for the face (elem, face) = idx[i] >> 2, idx[i] & 3, the 5 N_g face
+// values of each of `nplanes` trace-layout arrays (plane p at buf[i W + p 5 N_g])
+// and, when eps is given, eps[elem] after them. dir 0 packs (arrays -> buf),
+// 1 unpacks (buf -> the ghost rows). One warp per row.
+struct HaloXfer {
+  double* plane[3];
+  int nplanes;
+  double* eps;
+  double* buf;
+  const int* idx;
+  int n, ng, tb, W, dir;
+};
+
+__global__ void __launch_bounds__(256) k_halo_xfer(HaloXfer x) {
+  const int item = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (item >= x.n) return;
+  const int ef = __ldg(x.idx + item), elem = ef >> 2, face = ef & 3;
+  double* row = x.buf + (size_t)item * x.W;
+  for (int pl = 0; pl < x.nplanes; ++pl)
+    for (int k = lane; k < 5 * x.ng; k += 32) {
+      const int c = k / x.ng, gq = k - c * x.ng;
+      double* t = x.plane[pl] + ((size_t)elem * 5 + c) * x.tb + face * x.ng + gq;
+      double* s = row + pl * 5 * x.ng + k;
+      if (x.dir == 0)
+        *s = *t;
+      else
+        *t = *s;
+    }
+  if (x.eps && lane == 0) {
+    double* s = row + x.nplanes * 5 * x.ng;
+    if (x.dir == 0)
+      *s = x.eps[elem];
+    else
+      x.eps[elem] = *s;
+  }
+}
+
+// max over the ranks' local max-eps words (u64 bit patterns of non-negative
+// doubles order like the values): the viscous gate of an in-process
+// multi-rank group (peer pointers; NVLink loads across devices)
+__global__ void k_gate_max(const unsigned long long* const* src, int n, unsigned long long* dst) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    unsigned long long m = 0;
+    for (int i = 0; i < n; ++i) m = max(m, *(volatile const unsigned long long*)src[i]);
+    *dst = m;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // p_refine_embed (solver.cpp:528-549): out(e, c) = E in(e, c), one warp per
 // (element, field) row, lanes over the target nodes.

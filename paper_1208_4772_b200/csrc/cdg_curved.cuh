@@ -26,6 +26,8 @@ struct CurvedParams {
   double* vol;             // [Kc*5][NP8] epilogue scratch when the tile's vol does not fit smem
   double* q_out;           // [3][K*5][BP] aux gradient (k_aux_curved)
   int Kc;
+  const int* ctiles;       // optional list of curved tiles (E consecutive list entries each); null = all
+  int n_clist;
 };
 
 template <class C>
@@ -60,7 +62,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_rhs_curved(CurvedParams cp) {
   const int t_begin = (warp * C::T2) / kWarps, t_end = ((warp + 1) * C::T2) / kWarps;
   const int n_tiles = (cp.Kc + C::E - 1) / C::E;
 
-  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+  const int n_iter = cp.ctiles ? cp.n_clist : n_tiles;  // optional curved-tile list (multi-GPU split)
+  for (int it_t = blockIdx.x; it_t < n_iter; it_t += gridDim.x) {
+    const int tile = cp.ctiles ? __ldg(cp.ctiles + it_t) : it_t;
     if (tid == 0) s_stop = *(volatile int*)&p.err->flag;
     __syncthreads();
     if (s_stop) return;
@@ -289,7 +293,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_aux_curved(CurvedParams cp) {
   const int n_tiles = (cp.Kc + C::E - 1) / C::E;
   const size_t qstride = (size_t)p.K * 5 * C::BP;
 
-  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+  const int n_iter = cp.ctiles ? cp.n_clist : n_tiles;  // optional curved-tile list (multi-GPU split)
+  for (int it_t = blockIdx.x; it_t < n_iter; it_t += gridDim.x) {
+    const int tile = cp.ctiles ? __ldg(cp.ctiles + it_t) : it_t;
     const int c0 = tile * C::E;
     for (int idx = tid; idx < C::E; idx += kThreads) sId[idx] = c0 + idx < cp.Kc ? cp.ids[c0 + idx] : -1;
     __syncthreads();

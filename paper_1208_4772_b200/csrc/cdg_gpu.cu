@@ -252,6 +252,28 @@ struct cdg_gpu_level {
   int n_tiles_int = 0, n_tiles_halo = 0;
   int *d_send_idx = nullptr, *d_recv_idx = nullptr;
   double *send_buf = nullptr, *recv_buf = nullptr;
+  // library-owned halo rows of the multi-rank driver (cdg_gpu_halo_define):
+  // per peer, rows [off, off + n) of the send / receive lists; send rows
+  // double-buffered by exchange parity (cdg_comm.cuh)
+  struct Peer {
+    int rank, send_off, send_n, recv_off, recv_n;
+  };
+  std::vector<Peer> peers;
+  double* hsend[2] = {nullptr, nullptr};
+  double* hrecv = nullptr;
+  bool halo_defined = false;
+  // curved-list tiles split the same way (curved levels; k_rhs_rowc / k_rhs_curved)
+  int *d_ctiles_int = nullptr, *d_ctiles_halo = nullptr;
+  int n_ctiles_int = 0, n_ctiles_halo = 0;
+  const int* cur_ctiles = nullptr;  // curved-tile list of the next curved launch (null: all)
+  int cur_n_clist = 0;
+  std::vector<int> curved_ids_h;    // host copy of the curved list
+  // halo payload: row width (doubles) of send/recv rows; 5 N_g (traces only)
+  // unless a multi-rank driver (cdg_gpu_comm) owns the buffers
+  int halo_w = 0;
+  // launch gate of the viscous kernels: null = the local max eps (d_maxeps);
+  // a multi-rank driver points it at the all-rank max
+  unsigned long long* gate_buf = nullptr;
   double freestream[5] = {0, 0, 0, 0, 0};
 
   int n_rows() const { return K * 5; }
@@ -366,6 +388,9 @@ void launch_curved(cdg_gpu_level* lv, bool update, int stage, int mode = 0) {
   if (!lv->n_curved) return;
   CurvedParams cp{};
   cp.base = rhs_params(lv, stage);
+  cp.ctiles = lv->cur_ctiles;
+  cp.n_clist = lv->cur_n_clist;
+  if (cp.ctiles && cp.n_clist == 0) return;  // empty phase list
   cp.ids = lv->curved_ids;
   cp.jwr = lv->curved_jwr;
   cp.face = lv->curved_face;
@@ -381,13 +406,13 @@ void launch_curved(cdg_gpu_level* lv, bool update, int stage, int mode = 0) {
     auto fr = mode == 2   ? lv->ks->rowc_aux
               : mode == 1 ? (update ? lv->ks->rowc_visc_update[rm] : lv->ks->rowc_visc_only[rm])
                           : (update ? lv->ks->rowc_update[rm] : lv->ks->rowc_only[rm]);
-    const int tiles = (lv->n_curved + lv->ks->rowc_e - 1) / lv->ks->rowc_e;
+    const int tiles = cp.ctiles ? cp.n_clist : (lv->n_curved + lv->ks->rowc_e - 1) / lv->ks->rowc_e;
     fr<<<lv->cap(tiles, lv->ks->rowc_minb), lv->ks->rowc_nth, lv->ks->smem_rowc,
          lv->stream>>>(cp);
     ++lv->launches;
     return;
   }
-  const int tiles = (lv->n_curved + lv->ks->E - 1) / lv->ks->E;
+  const int tiles = cp.ctiles ? cp.n_clist : (lv->n_curved + lv->ks->E - 1) / lv->ks->E;
   auto fn = mode == 2 ? lv->ks->aux_curved
                       : mode == 1 ? (update ? lv->ks->curved_visc_update : lv->ks->curved_visc_only)
                                   : (update ? lv->ks->curved_update : lv->ks->curved_only);
@@ -588,7 +613,7 @@ bool viscosity_phase(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg) {
 void viscous_stage_gated(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, int stage) {
   launch_sensor(lv, cfg);
   launch_traces(lv, lv->u, lv->traces);  // both paths need the U traces
-  lv->cur_gate = lv->d_maxeps;
+  lv->cur_gate = lv->gate_buf ? lv->gate_buf : lv->d_maxeps;
   lv->cur_gate_when = 1;
   launch_aux(lv);
   launch_rhs(lv, true, true, stage);
@@ -597,6 +622,46 @@ void viscous_stage_gated(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, int s
   lv->cur_gate = nullptr;
 }
 
+}  // namespace
+
+namespace {
+// Interior / halo tile lists of the overlapped multi-GPU stage: a tile is a
+// halo tile when one of the elements it updates has a ghost (halo) neighbour.
+// Affine tiles (the affine kernel's E) that hold only curved elements are in
+// neither list; curved tiles (E consecutive curved-list entries) are split
+// the same way.
+void build_phase_lists(cdg_gpu_level* lv) {
+  const int K = lv->K;
+  std::vector<char> curved(K, 0);
+  for (int e : lv->curved_ids_h) curved[e] = 1;
+  auto ghost = [&](int e) { return !lv->ghost_adjacent.empty() && lv->ghost_adjacent[e]; };
+  const int E = lv->use_row ? lv->ks->row_e : lv->ks->E;
+  std::vector<int> ti, th;
+  for (int t = 0; t * E < K; ++t) {
+    bool any = false, halo = false;
+    for (int e = t * E; e < std::min(K, (t + 1) * E); ++e)
+      if (!curved[e]) any = true, halo = halo || ghost(e);
+    if (any) (halo ? th : ti).push_back(t);
+  }
+  for (int* p : {lv->d_tiles_int, lv->d_tiles_halo, lv->d_ctiles_int, lv->d_ctiles_halo})
+    if (p) cudaFree(p);
+  lv->d_tiles_int = dev_upload(ti.empty() ? std::vector<int>{0} : ti);
+  lv->d_tiles_halo = dev_upload(th.empty() ? std::vector<int>{0} : th);
+  lv->n_tiles_int = (int)ti.size();
+  lv->n_tiles_halo = (int)th.size();
+  std::vector<int> ci, chh;
+  const int Ec = lv->use_rowc ? lv->ks->rowc_e : lv->ks->E;
+  const int nc = (int)lv->curved_ids_h.size();
+  for (int t = 0; t * Ec < nc; ++t) {
+    bool halo = false;
+    for (int i = t * Ec; i < std::min(nc, (t + 1) * Ec); ++i) halo = halo || ghost(lv->curved_ids_h[i]);
+    (halo ? chh : ci).push_back(t);
+  }
+  lv->d_ctiles_int = dev_upload(ci.empty() ? std::vector<int>{0} : ci);
+  lv->d_ctiles_halo = dev_upload(chh.empty() ? std::vector<int>{0} : chh);
+  lv->n_ctiles_int = (int)ci.size();
+  lv->n_ctiles_halo = (int)chh.size();
+}
 }  // namespace
 
 namespace {
@@ -611,6 +676,70 @@ int guarded(char* err, size_t errlen, const std::function<void()>& fn) {
     set_err(err, errlen, e.what());
     return CDG_GPU_ERR_OTHER;
   }
+}
+}  // namespace
+
+namespace {
+// run_steady's per-level loop (solver.cpp:622-668) over a set of operations:
+// one level (cdg_gpu_run_level_live) or every shard of a multi-rank driver
+// (cdg_gpu_comm_run_level, global dt MIN / residual reductions).
+struct SteadyOps {
+  std::function<void(int, double, const double*, const double*)> rk_steps;
+  std::function<void()> snapshot;
+  std::function<double(int, double)> residual;
+  std::function<double(int)> timestep;
+};
+
+int run_level_loop(const SteadyOps& ops, const cdg_gpu_run_config* cfg, const cdg_gpu_steady_params* sp,
+                   cdg_gpu_row_fn on_row, void* user, double* rows, int max_rows, int* n_rows, int* converged,
+                   char* err, size_t errlen) {
+  // Carpenter-Kennedy LSRK4(5) coefficients (rk.hpp:15-24)
+  static const double A[5] = {0.0, -567301805773.0 / 1357537059087.0, -2404267990393.0 / 2016746695238.0,
+                              -3550918686646.0 / 2091501179385.0, -1275806237668.0 / 842570457699.0};
+  static const double B[5] = {1432997174477.0 / 9575080441755.0, 5161836677717.0 / 13612068292357.0,
+                              1720146321549.0 / 2090206949498.0, 3134564353537.0 / 4481467310338.0,
+                              2277821191437.0 / 14882151754819.0};
+  *n_rows = 0;
+  *converged = 0;
+  return guarded(err, errlen, [&] {
+    if (sp->check_interval <= 0) throw Status(CDG_GPU_ERR_CONFIG, "run_steady: check_interval must be positive");
+    double dt = sp->dt_override > 0.0 ? sp->dt_override : ops.timestep(0);
+    double initial = -1.0;
+    long iter = 0;
+    bool done = false;
+    while (!done && iter < sp->max_iterations) {
+      // next check iteration: iter % interval == 0, the last iteration, or the fixed count
+      long next = (iter / sp->check_interval + 1) * sp->check_interval;
+      next = std::min(next, sp->max_iterations);
+      if (sp->fixed_iterations > iter) next = std::min(next, sp->fixed_iterations);
+      if (next - iter - 1 > 0) ops.rk_steps((int)(next - iter - 1), dt, A, B);
+      ops.snapshot();
+      ops.rk_steps(1, dt, A, B);
+      iter = next;
+      const double r = ops.residual(sp->residual_kind, dt);
+      if (*n_rows < max_rows) {
+        rows[3 * *n_rows + 0] = (double)iter;
+        rows[3 * *n_rows + 1] = dt;
+        rows[3 * *n_rows + 2] = r;
+      }
+      ++*n_rows;
+      if (on_row) on_row(user, iter, dt, r);  // live, as the reference's loop emits it (solver.cpp:643-647)
+      if (initial < 0.0) initial = std::max(r, 1e-300);
+      if (r > 1e6 * initial && r > 1e-12) {
+        char buf[256];
+        std::snprintf(buf, sizeof buf, "run_steady: divergence detected at p=%d iteration %ld (residual %f)",
+                      sp->degree, iter, r);
+        throw Status(CDG_GPU_ERR_NUMERICS, buf);
+      }
+      if (sp->fixed_iterations > 0) {
+        if (iter >= sp->fixed_iterations) done = true;
+      } else if (r < sp->tolerance) {
+        done = true;
+        *converged = 1;
+      }
+      if (!done && sp->dt_override <= 0.0) dt = ops.timestep(cfg->visc_enabled ? 1 : 0);
+    }
+  });
 }
 }  // namespace
 
@@ -890,6 +1019,7 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
       }
       lv->n_curved = d->n_curved;
       lv->curved_ids = dev_upload(std::vector<int>(d->curved_ids, d->curved_ids + d->n_curved));
+      lv->curved_ids_h.assign(d->curved_ids, d->curved_ids + d->n_curved);
       lv->curved_jwr = dev_upload(std::vector<double>(d->curved_jwr, d->curved_jwr + (size_t)d->n_curved * ncub * 9));
       std::vector<double4> cf((size_t)d->n_curved * nf);
       for (size_t i = 0; i < cf.size(); ++i)
@@ -1049,7 +1179,10 @@ void cdg_gpu_level_destroy(cdg_gpu_level* lv) {
                   (void*)lv->curved_ids, (void*)lv->curved_jwr, (void*)lv->curved_minv, (void*)lv->frag_opc,
                   (void*)lv->rfrag_opc, (void*)lv->d_affine_tiles, (void*)lv->curved_vol, (void*)lv->curved_face, (void*)lv->d_coef, (void*)lv->d_err,
                   (void*)lv->d_scratch, (void*)lv->d_send_idx, (void*)lv->d_recv_idx,
-                  (void*)lv->d_tiles_int, (void*)lv->d_tiles_halo})
+                  (void*)lv->d_tiles_int, (void*)lv->d_tiles_halo,
+                  (void*)lv->d_ctiles_int, (void*)lv->d_ctiles_halo})
+    if (p) cudaFree(p);
+  for (double* p : {lv->hsend[0], lv->hsend[1], lv->hrecv})
     if (p) cudaFree(p);
   if (lv->h_coef) cudaFreeHost(lv->h_coef);
   if (lv->h_err) cudaFreeHost(lv->h_err);
@@ -1369,6 +1502,7 @@ int cdg_gpu_set_kernel_path(cdg_gpu_level* lv, int path) {
   lv->use_warp = !generic && lv->ks->warp_update[0] != nullptr;
   lv->use_rowc = !generic && lv->rfrag_opc != nullptr;
   lv->traces_valid = false;
+  if (lv->d_tiles_int || lv->d_tiles_halo) build_phase_lists(lv);  // tile sizes may differ per family
   cdg_gpu_set_max_ctas(lv, lv->max_ctas);  // drops the captured graphs
   return CDG_GPU_OK;
 }
@@ -1503,117 +1637,194 @@ int cdg_gpu_run_level(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, const cd
 int cdg_gpu_run_level_live(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, const cdg_gpu_steady_params* sp,
                            cdg_gpu_row_fn on_row, void* user, double* rows, int max_rows, int* n_rows,
                            int* converged, char* err, size_t errlen) {
-  // Carpenter-Kennedy LSRK4(5) coefficients (rk.hpp:15-24)
-  static const double A[5] = {0.0, -567301805773.0 / 1357537059087.0, -2404267990393.0 / 2016746695238.0,
-                              -3550918686646.0 / 2091501179385.0, -1275806237668.0 / 842570457699.0};
-  static const double B[5] = {1432997174477.0 / 9575080441755.0, 5161836677717.0 / 13612068292357.0,
-                              1720146321549.0 / 2090206949498.0, 3134564353537.0 / 4481467310338.0,
-                              2277821191437.0 / 14882151754819.0};
-  *n_rows = 0;
-  *converged = 0;
-  return guarded(err, errlen, [&] {
-    if (sp->check_interval <= 0) throw Status(CDG_GPU_ERR_CONFIG, "run_steady: check_interval must be positive");
-    auto ok = [&](int st) {
-      if (st != CDG_GPU_OK) throw Status(st, err && errlen ? std::string(err) : std::string("run_level failed"));
-    };
+  auto ok = [&](int st) {
+    if (st != CDG_GPU_OK) throw Status(st, err && errlen ? std::string(err) : std::string("run_level failed"));
+  };
+  SteadyOps ops;
+  ops.rk_steps = [&](int n, double dt, const double* A, const double* B) {
+    ok(cdg_gpu_rk_steps(lv, cfg, n, dt, A, B, err, errlen));
+  };
+  ops.snapshot = [&] { ok(cdg_gpu_snapshot(lv)); };
+  ops.residual = [&](int kind, double dt) {
+    double r = 0.0;
+    ok(cdg_gpu_residual(lv, kind, dt, &r));
+    return r;
+  };
+  ops.timestep = [&](int use_visc) {
     double dt = 0.0;
-    if (sp->dt_override > 0.0)
-      dt = sp->dt_override;
-    else
-      ok(cdg_gpu_timestep(lv, cfg, 0, &dt, err, errlen));
-    double initial = -1.0;
-    long iter = 0;
-    bool done = false;
-    while (!done && iter < sp->max_iterations) {
-      // next check iteration: iter % interval == 0, the last iteration, or the fixed count
-      long next = (iter / sp->check_interval + 1) * sp->check_interval;
-      next = std::min(next, sp->max_iterations);
-      if (sp->fixed_iterations > iter) next = std::min(next, sp->fixed_iterations);
-      if (next - iter - 1 > 0) ok(cdg_gpu_rk_steps(lv, cfg, (int)(next - iter - 1), dt, A, B, err, errlen));
-      ok(cdg_gpu_snapshot(lv));
-      ok(cdg_gpu_rk_steps(lv, cfg, 1, dt, A, B, err, errlen));
-      iter = next;
-      double r = 0.0;
-      ok(cdg_gpu_residual(lv, sp->residual_kind, dt, &r));
-      if (*n_rows < max_rows) {
-        rows[3 * *n_rows + 0] = (double)iter;
-        rows[3 * *n_rows + 1] = dt;
-        rows[3 * *n_rows + 2] = r;
-      }
-      ++*n_rows;
-      if (on_row) on_row(user, iter, dt, r);  // live, as the reference's loop emits it (solver.cpp:643-647)
-      if (initial < 0.0) initial = std::max(r, 1e-300);
-      if (r > 1e6 * initial && r > 1e-12) {
-        char buf[256];
-        std::snprintf(buf, sizeof buf, "run_steady: divergence detected at p=%d iteration %ld (residual %f)",
-                      sp->degree, iter, r);
-        throw Status(CDG_GPU_ERR_NUMERICS, buf);
-      }
-      if (sp->fixed_iterations > 0) {
-        if (iter >= sp->fixed_iterations) done = true;
-      } else if (r < sp->tolerance) {
-        done = true;
-        *converged = 1;
-      }
-      if (!done && sp->dt_override <= 0.0) ok(cdg_gpu_timestep(lv, cfg, cfg->visc_enabled ? 1 : 0, &dt, err, errlen));
-    }
-  });
+    ok(cdg_gpu_timestep(lv, cfg, use_visc, &dt, err, errlen));
+    return dt;
+  };
+  return run_level_loop(ops, cfg, sp, on_row, user, rows, max_rows, n_rows, converged, err, errlen);
 }
 
 // ---- multi-GPU halo plumbing -------------------------------------------------
+}  // extern "C"
+
+namespace {
+
+void drop_halo(cdg_gpu_level* lv) {
+  for (double*& p : {std::ref(lv->hsend[0]), std::ref(lv->hsend[1]), std::ref(lv->hrecv)})
+    if (p) cudaFree(p), p = nullptr;
+  lv->peers.clear();
+  lv->halo_defined = false;
+}
+
+// upload a (possibly empty) index list; never null, so an empty list stays a list
+int* upload_list(const std::vector<int>& v) {
+  return dev_upload(v.empty() ? std::vector<int>{0} : v);
+}
+
+void set_halo_lists(cdg_gpu_level* lv, int n_send, const int* send_ef, int n_recv, const int* recv_ef) {
+  for (int i = 0; i < n_send; ++i)
+    if ((send_ef[i] >> 2) < 0 || (send_ef[i] >> 2) >= lv->K)
+      throw Status(CDG_GPU_ERR_CONFIG, "halo: send rows must be owned elements");
+  for (int i = 0; i < n_recv; ++i)
+    if ((recv_ef[i] >> 2) < lv->K || (recv_ef[i] >> 2) >= lv->K + lv->n_halo)
+      throw Status(CDG_GPU_ERR_CONFIG, "halo_setup: receive rows must be ghost elements");
+  lv->n_send = n_send;
+  lv->n_recv = n_recv;
+  if (lv->d_send_idx) cudaFree(lv->d_send_idx);
+  if (lv->d_recv_idx) cudaFree(lv->d_recv_idx);
+  lv->d_send_idx = upload_list(std::vector<int>(send_ef, send_ef + n_send));
+  lv->d_recv_idx = upload_list(std::vector<int>(recv_ef, recv_ef + n_recv));
+}
+
+// what: 0 U traces, 1 U traces + sqrt(eps) of the element, 2 the three q_m traces
+int halo_width(const cdg_gpu_level* lv, int what) { return what == 2 ? 15 * lv->ng : 5 * lv->ng + (what == 1); }
+
+// pack (dir 0: owned faces -> buf) / unpack (dir 1: buf -> ghost faces)
+void halo_move(cdg_gpu_level* lv, int dir, int what, double* buf) {
+  const int n = dir == 0 ? lv->n_send : lv->n_recv;
+  if (!n) return;
+  HaloXfer x{};
+  if (what == 2) {
+    const size_t qs = (size_t)(lv->K + lv->n_halo) * 5 * lv->tb;
+    x.nplanes = 3;
+    for (int m = 0; m < 3; ++m) x.plane[m] = lv->qtr + m * qs;
+  } else {
+    x.nplanes = 1;
+    x.plane[0] = lv->traces;
+    x.eps = what == 1 ? lv->sqrt_eps : nullptr;
+  }
+  x.buf = buf;
+  x.idx = dir == 0 ? lv->d_send_idx : lv->d_recv_idx;
+  x.n = n;
+  x.ng = lv->ng;
+  x.tb = lv->tb;
+  x.W = halo_width(lv, what);
+  x.dir = dir;
+  k_halo_xfer<<<(n + 7) / 8, 256, 0, lv->stream>>>(x);
+  ++lv->launches;
+}
+
+void upload_coef(cdg_gpu_level* lv, double dt, const double* a, const double* b) {
+  lv->h_coef->dt = dt;
+  for (int i = 0; i < 5; ++i) {
+    lv->h_coef->a[i] = a[i];
+    lv->h_coef->b[i] = b[i];
+  }
+  CUDA_OK(cudaMemcpyAsync(lv->d_coef, lv->h_coef, sizeof(StageCoef), cudaMemcpyHostToDevice, lv->stream));
+}
+
+// One inviscid RK stage in split form (no host synchronisation):
+//  0: (stage 0: RK coefficients) traces of u (seeded, or already written by
+//     the previous fused stage) + pack the halo rows;
+//  1: unpack + RHS/update of every tile;
+//  2: RHS/update of the interior tiles (overlaps the exchange);
+//  3: unpack + RHS/update of the halo tiles.
+void stage_phase(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, int stage, int phase, double dt,
+                 const double* a, const double* b) {
+  if (cfg->riemann != 0 && cfg->riemann != 1) throw Status(CDG_GPU_ERR_CONFIG, "unknown Riemann solver (llf|hllc)");
+  lv->gas.gamma = cfg->gamma;
+  lv->gas.riemann = cfg->riemann;
+  const bool ft = fused_traces(lv);
+  if (ft) ensure_tbuf(lv);
+  // fused traces: the RHS of stage s writes the traces of stage s+1 into the
+  // other buffer (owned rows); the ghost rows arrive by the halo exchange
+  auto rhs = [&](const int* tiles, int n_list, const int* ctiles, int n_clist) {
+    lv->cur_tiles = tiles;
+    lv->cur_n_list = n_list;
+    lv->cur_ctiles = ctiles;
+    lv->cur_n_clist = n_clist;
+    if (ft) lv->cur_traces_out = lv->tbuf[lv->tcur ^ 1];
+    auto reset = [&] {
+      lv->cur_tiles = nullptr;
+      lv->cur_n_list = 0;
+      lv->cur_ctiles = nullptr;
+      lv->cur_n_clist = 0;
+      lv->cur_traces_out = nullptr;
+    };
+    try {
+      launch_rhs(lv, true, false, stage);
+    } catch (...) {
+      reset();
+      throw;
+    }
+    reset();
+  };
+  auto swap = [&] {
+    if (ft) {
+      lv->tcur ^= 1;
+      lv->traces = lv->tbuf[lv->tcur];
+      lv->traces_valid = true;
+    } else {
+      lv->traces_valid = false;
+    }
+  };
+  if (phase == 0) {
+    if (stage == 0) upload_coef(lv, dt, a, b);
+    if (ft)
+      seed_traces(lv);
+    else
+      launch_traces(lv, lv->u, lv->traces);
+    halo_move(lv, 0, 0, lv->send_buf);
+  } else if (phase == 1) {
+    halo_move(lv, 1, 0, lv->recv_buf);
+    rhs(nullptr, 0, nullptr, 0);
+    swap();
+  } else if (phase == 2 || phase == 3) {
+    if (!lv->d_tiles_int) throw Status(CDG_GPU_ERR_CONFIG, "phases 2/3 need halo_setup");
+    if (phase == 3) halo_move(lv, 1, 0, lv->recv_buf);
+    if (phase == 2)
+      rhs(lv->d_tiles_int, lv->n_tiles_int, lv->d_ctiles_int, lv->n_ctiles_int);
+    else
+      rhs(lv->d_tiles_halo, lv->n_tiles_halo, lv->d_ctiles_halo, lv->n_ctiles_halo);
+    if (phase == 3) swap();
+  } else {
+    throw Status(CDG_GPU_ERR_CONFIG, "rk_stage_phase: phase must be 0..3");
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
 int cdg_gpu_halo_setup(cdg_gpu_level* lv, int n_send, const int* send_ef, int n_recv, const int* recv_ef,
                        double* send_buf, double* recv_buf) {
   return guarded(nullptr, 0, [&] {
     CUDA_OK(cudaSetDevice(lv->device));
     if ((n_send && !send_buf) || (n_recv && !recv_buf))
       throw Status(CDG_GPU_ERR_CONFIG, "halo_setup: device buffers required");
-    for (int i = 0; i < n_recv; ++i)
-      if ((recv_ef[i] >> 2) < lv->K || (recv_ef[i] >> 2) >= lv->K + lv->n_halo)
-        throw Status(CDG_GPU_ERR_CONFIG, "halo_setup: receive rows must be ghost elements");
-    lv->n_send = n_send;
-    lv->n_recv = n_recv;
-    if (lv->d_send_idx) cudaFree(lv->d_send_idx);
-    if (lv->d_recv_idx) cudaFree(lv->d_recv_idx);
-    lv->d_send_idx = n_send ? dev_upload(std::vector<int>(send_ef, send_ef + n_send)) : nullptr;
-    lv->d_recv_idx = n_recv ? dev_upload(std::vector<int>(recv_ef, recv_ef + n_recv)) : nullptr;
+    set_halo_lists(lv, n_send, send_ef, n_recv, recv_ef);
     lv->send_buf = send_buf;  // caller-owned (e.g. NCCL-registered torch tensors)
     lv->recv_buf = recv_buf;
     // interior tiles (no element with a ghost neighbour) run while the halo
     // traces are in flight; halo tiles after they land (rk_stage_phase 2 / 3)
-    const int E = lv->use_row ? lv->ks->row_e : lv->ks->E;
-    const int nt = (lv->K + E - 1) / E;
-    std::vector<int> ti, th;
-    for (int t = 0; t < nt; ++t) {
-      bool halo = false;
-      for (int e = t * E; e < std::min(lv->K, (t + 1) * E) && !halo; ++e)
-        halo = !lv->ghost_adjacent.empty() && lv->ghost_adjacent[e];
-      (halo ? th : ti).push_back(t);
-    }
-    if (lv->d_tiles_int) cudaFree(lv->d_tiles_int);
-    if (lv->d_tiles_halo) cudaFree(lv->d_tiles_halo);
-    lv->d_tiles_int = dev_upload(ti);
-    lv->d_tiles_halo = dev_upload(th);
-    lv->n_tiles_int = (int)ti.size();
-    lv->n_tiles_halo = (int)th.size();
+    build_phase_lists(lv);
   });
 }
 
 int cdg_gpu_halo_pack(cdg_gpu_level* lv) {
   return guarded(nullptr, 0, [&] {
-    if (!lv->n_send) return;
-    k_halo_copy<<<(lv->n_send + 7) / 8, 256, 0, lv->stream>>>(lv->traces, lv->send_buf, lv->d_send_idx,
-                                                               lv->n_send, lv->ng, lv->tb, 0);
-    ++lv->launches;
+    halo_move(lv, 0, 0, lv->send_buf);
     CUDA_OK(cudaGetLastError());
   });
 }
 
 int cdg_gpu_halo_unpack(cdg_gpu_level* lv) {
   return guarded(nullptr, 0, [&] {
-    if (!lv->n_recv) return;
-    k_halo_copy<<<(lv->n_recv + 7) / 8, 256, 0, lv->stream>>>(lv->traces, lv->recv_buf, lv->d_recv_idx,
-                                                               lv->n_recv, lv->ng, lv->tb, 1);
-    ++lv->launches;
+    halo_move(lv, 1, 0, lv->recv_buf);
     CUDA_OK(cudaGetLastError());
   });
 }
@@ -1623,79 +1834,14 @@ int cdg_gpu_rk_stage_phase(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, int
   return guarded(err, errlen, [&] {
     CUDA_OK(cudaSetDevice(lv->device));
     if (cfg->visc_enabled)
-      throw Status(CDG_GPU_ERR_CONFIG, "split-phase stages support the inviscid path only");
-    lv->gas.gamma = cfg->gamma;
-    lv->gas.riemann = cfg->riemann;
-    const bool ft = fused_traces(lv);
-    if (ft) ensure_tbuf(lv);
-    // fused traces: the RHS of stage s writes the traces of stage s+1 into the
-    // other buffer (owned rows); the ghost rows arrive by the halo exchange
-    auto rhs = [&](const int* tiles, int n_list) {
-      lv->cur_tiles = tiles;
-      lv->cur_n_list = n_list;
-      if (ft) lv->cur_traces_out = lv->tbuf[lv->tcur ^ 1];
-      try {
-        launch_rhs(lv, true, false, stage);
-      } catch (...) {
-        lv->cur_tiles = nullptr;
-        lv->cur_traces_out = nullptr;
-        throw;
-      }
-      lv->cur_tiles = nullptr;
-      lv->cur_n_list = 0;
-      lv->cur_traces_out = nullptr;
-    };
-    auto swap = [&] {
-      if (ft) {
-        lv->tcur ^= 1;
-        lv->traces = lv->tbuf[lv->tcur];
-        lv->traces_valid = true;
-      } else {
-        lv->traces_valid = false;
-      }
-    };
-    if (phase == 0) {
-      if (stage == 0) {
-        lv->h_coef->dt = dt;
-        for (int i = 0; i < 5; ++i) {
-          lv->h_coef->a[i] = a[i];
-          lv->h_coef->b[i] = b[i];
-        }
-        CUDA_OK(cudaMemcpyAsync(lv->d_coef, lv->h_coef, sizeof(StageCoef), cudaMemcpyHostToDevice,
-                                lv->stream));
-      }
-      if (ft)
-        seed_traces(lv);
-      else
-        launch_traces(lv, lv->u, lv->traces);
-      if (lv->n_send)
-        k_halo_copy<<<(lv->n_send + 7) / 8, 256, 0, lv->stream>>>(lv->traces, lv->send_buf, lv->d_send_idx,
-                                                                   lv->n_send, lv->ng, lv->tb, 0);
-    } else if (phase == 1) {
-      if (lv->n_recv)
-        k_halo_copy<<<(lv->n_recv + 7) / 8, 256, 0, lv->stream>>>(lv->traces, lv->recv_buf, lv->d_recv_idx,
-                                                                   lv->n_recv, lv->ng, lv->tb, 1);
-      rhs(nullptr, 0);
-      swap();
-      if (stage == 4) check_device_error(lv);
-    } else {
-      // 2: interior tiles (overlaps the halo exchange); 3: unpack + halo tiles
-      if (lv->n_curved) throw Status(CDG_GPU_ERR_CONFIG, "split interior/halo phases need an affine level");
-      if (phase == 3 && lv->n_recv)
-        k_halo_copy<<<(lv->n_recv + 7) / 8, 256, 0, lv->stream>>>(lv->traces, lv->recv_buf, lv->d_recv_idx,
-                                                                   lv->n_recv, lv->ng, lv->tb, 1);
-      if (!lv->d_tiles_int && !lv->d_tiles_halo) throw Status(CDG_GPU_ERR_CONFIG, "phases 2/3 need halo_setup");
-      const int* tl = phase == 2 ? lv->d_tiles_int : lv->d_tiles_halo;
-      const int nl = phase == 2 ? lv->n_tiles_int : lv->n_tiles_halo;
-      if (!tl) tl = phase == 2 ? lv->d_tiles_halo : lv->d_tiles_int;  // empty list
-      rhs(tl, nl);
-      if (phase == 3) {
-        swap();
-        if (stage == 4) check_device_error(lv);
-      }
-    }
+      throw Status(CDG_GPU_ERR_CONFIG,
+                   "split-phase stages support the inviscid path only (viscous multi-rank steps: cdg_gpu_comm_rk_steps)");
+    stage_phase(lv, cfg, stage, phase, dt, a, b);
+    if (stage == 4 && (phase == 1 || phase == 3)) check_device_error(lv);
     CUDA_OK(cudaGetLastError());
   });
 }
 
 }  // extern "C"
+
+#include "cdg_comm.cuh"

@@ -63,7 +63,9 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_rowc(CurvedParams cp) {
   const size_t qcs = (size_t)p.K * 5 * LDQ;                // qcub direction stride
   const size_t qstride = (size_t)p.K * 5 * C::BP;          // q_out direction stride
 
-  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+  const int n_iter = cp.ctiles ? cp.n_clist : n_tiles;  // optional curved-tile list (multi-GPU split)
+  for (int it_t = blockIdx.x; it_t < n_iter; it_t += gridDim.x) {
+    const int tile = cp.ctiles ? __ldg(cp.ctiles + it_t) : it_t;
     const int c0 = tile * C::E;  // index into the curved list
     if (tid == 0) s_stop = *(volatile int*)&p.err->flag;
     for (int idx = tid; idx < C::E; idx += C::NTH) sId[idx] = c0 + idx < cp.Kc ? __ldg(cp.ids + c0 + idx) : -1;

@@ -137,6 +137,21 @@ def lib():
         L.cdg_gpu_p_refine_embed.argtypes = [vp, vp, _dp]
         L.cdg_gpu_run_level.argtypes = [vp, C.POINTER(RunConfig), C.POINTER(SteadyParams), _dp, C.c_int, _ip, _ip,
                                         C.c_char_p, C.c_size_t]
+        L.cdg_gpu_halo_define.argtypes = [vp, C.c_int, _ip, _ip, _ip, _ip, _ip]
+        L.cdg_gpu_comm_unique_id.argtypes = [C.c_char_p, C.c_char_p, C.c_size_t]
+        L.cdg_gpu_comm_create_nccl.argtypes = [vp, C.c_char_p, C.c_int, C.c_int, C.POINTER(vp), C.c_char_p,
+                                               C.c_size_t]
+        L.cdg_gpu_comm_create_local.argtypes = [C.c_int, C.POINTER(vp), C.POINTER(vp), C.c_char_p, C.c_size_t]
+        L.cdg_gpu_comm_destroy.argtypes = [vp]
+        L.cdg_gpu_comm_rk_steps.argtypes = [vp, C.POINTER(RunConfig), C.c_int, C.c_double, _dp, _dp, C.c_char_p,
+                                            C.c_size_t]
+        L.cdg_gpu_comm_timestep.argtypes = [vp, C.POINTER(RunConfig), C.c_int, _dp, C.c_char_p, C.c_size_t]
+        L.cdg_gpu_comm_snapshot.argtypes = [vp]
+        L.cdg_gpu_comm_residual.argtypes = [vp, C.c_int, C.c_double, _dp]
+        L.cdg_gpu_comm_fill_freestream.argtypes = [vp]
+        L.cdg_gpu_comm_run_level.argtypes = [vp, C.POINTER(RunConfig), C.POINTER(SteadyParams), C.c_void_p,
+                                             C.c_void_p, _dp, C.c_int, _ip, _ip, C.c_char_p, C.c_size_t]
+        L.cdg_gpu_comm_exchange_count.argtypes = [vp]
         _lib = L
     return _lib
 
@@ -332,6 +347,17 @@ class GpuLevel:
         _raise(lib().cdg_gpu_halo_setup(self.h, len(s), _p(s), len(r), _p(r), send_ptr, recv_ptr),
                "halo_setup failed")
 
+    def halo_define(self, peers):
+        """Register this shard's halo rows peer by peer (partition.HaloPeer list);
+        the library owns the transfer buffers (multi-rank driver, GpuComm)."""
+        ranks = np.array([pe.rank for pe in peers], np.int32)
+        sc = np.array([len(pe.send_elem_face) for pe in peers], np.int32)
+        rc = np.array([len(pe.recv_elem_face) for pe in peers], np.int32)
+        s = np.ascontiguousarray(np.concatenate([pe.send_elem_face for pe in peers] or [np.zeros(0)]), np.int32)
+        r = np.ascontiguousarray(np.concatenate([pe.recv_elem_face for pe in peers] or [np.zeros(0)]), np.int32)
+        _raise(lib().cdg_gpu_halo_define(self.h, len(peers), _p(ranks), _p(sc), _p(rc), _p(s), _p(r)),
+               "halo_define failed")
+
     def stage_phase(self, cfg: RunConfig, stage: int, phase: int, dt: float, a=LSRK_A, b=LSRK_B):
         a = np.ascontiguousarray(a, np.float64)
         b = np.ascontiguousarray(b, np.float64)
@@ -360,6 +386,92 @@ class GpuLevel:
                                      err, 1024)
         _raise(st, err.value.decode())
         return rows[: min(int(n[0]), max_rows)], bool(conv[0])
+
+
+class GpuComm:
+    """Multi-rank driver over shards (GpuLevel with ghost elements + halo_define):
+    rk_steps / timestep / residual / run_level over every rank (cdg_gpu_comm_*).
+
+    GpuComm.local(levels): one process drives every shard (one GPU or several,
+    peer copies over NVLink); GpuComm.nccl(level, uid, rank, nranks): one
+    process per GPU, NCCL inside the library (uid from unique_id() on rank 0,
+    broadcast by the caller)."""
+
+    def __init__(self, h, levels):
+        self.h = h
+        self.levels = levels  # keep the shards alive
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        err = C.create_string_buffer(1024)
+        _raise(lib().cdg_gpu_comm_unique_id(buf, err, 1024), err.value.decode())
+        return buf.raw
+
+    @classmethod
+    def local(cls, levels):
+        arr = (C.c_void_p * len(levels))(*[lv.h.value for lv in levels])
+        h = C.c_void_p()
+        err = C.create_string_buffer(1024)
+        _raise(lib().cdg_gpu_comm_create_local(len(levels), arr, C.byref(h), err, 1024), err.value.decode())
+        return cls(h, list(levels))
+
+    @classmethod
+    def nccl(cls, level, uid: bytes, rank: int, nranks: int):
+        h = C.c_void_p()
+        err = C.create_string_buffer(1024)
+        _raise(lib().cdg_gpu_comm_create_nccl(level.h, uid, rank, nranks, C.byref(h), err, 1024),
+               err.value.decode())
+        return cls(h, [level])
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().cdg_gpu_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def rk_steps(self, cfg: RunConfig, dt: float, nsteps: int = 1, a=LSRK_A, b=LSRK_B):
+        a = np.ascontiguousarray(a, np.float64)
+        b = np.ascontiguousarray(b, np.float64)
+        err = C.create_string_buffer(1024)
+        _raise(lib().cdg_gpu_comm_rk_steps(self.h, C.byref(cfg), nsteps, dt, _p(a), _p(b), err, 1024),
+               err.value.decode())
+
+    def compute_timestep(self, cfg: RunConfig, use_viscosity: bool = False) -> float:
+        dt = np.zeros(1)
+        err = C.create_string_buffer(1024)
+        _raise(lib().cdg_gpu_comm_timestep(self.h, C.byref(cfg), int(use_viscosity), _p(dt), err, 1024),
+               err.value.decode())
+        return float(dt[0])
+
+    def snapshot(self):
+        _raise(lib().cdg_gpu_comm_snapshot(self.h), "snapshot failed")
+
+    def residual(self, dt: float, kind: str = "inf") -> float:
+        out = np.zeros(1)
+        _raise(lib().cdg_gpu_comm_residual(self.h, 1 if kind == "l2" else 0, dt, _p(out)), "residual failed")
+        return float(out[0])
+
+    def fill_freestream(self):
+        _raise(lib().cdg_gpu_comm_fill_freestream(self.h), "fill_freestream failed")
+
+    def run_level(self, cfg: RunConfig, params: SteadyParams, max_rows: int = 100000):
+        rows = np.zeros((max_rows, 3))
+        n = np.zeros(1, np.int32)
+        conv = np.zeros(1, np.int32)
+        err = C.create_string_buffer(1024)
+        st = lib().cdg_gpu_comm_run_level(self.h, C.byref(cfg), C.byref(params), None, None, _p(rows), max_rows,
+                                          _p(n), _p(conv), err, 1024)
+        _raise(st, err.value.decode())
+        return rows[: min(int(n[0]), max_rows)], bool(conv[0])
+
+    def exchange_count(self) -> int:
+        return int(lib().cdg_gpu_comm_exchange_count(self.h))
 
 
 def embed_matrix(re_from: R.ReferenceElement, re_to: R.ReferenceElement) -> np.ndarray:

@@ -191,3 +191,22 @@ def slab_ranges(n: int, nranks: int):
     meshgen.cpp:53-66, so slabs are contiguous element ranges)."""
     bounds = [round(r * n / nranks) for r in range(nranks + 1)]
     return [(bounds[r], bounds[r + 1]) for r in range(nranks)]
+
+
+def warped_nodes(mesh: Mesh, re, amp: float = 0.02, ids=None) -> np.ndarray:
+    """Physical collocation nodes [len(ids), N_p, 3] of the owned elements `ids`
+    (default: all) under the smooth global map x -> x + amp sin(2 pi y) sin(2 pi z)
+    e_x + (cyclic): continuous across faces, so the face pairing is unchanged.
+    The synthetic curved (isoparametric) workload of the bench and of the
+    partitioned curved tests (every element it lists is a CurvedMesh element,
+    curved_mesh.hpp:14-51)."""
+    ids = np.arange(mesh.n_owned) if ids is None else np.asarray(ids)
+    lam = (re.colloc_nodes + 1.0) / 2.0
+    bary = np.concatenate([1.0 - lam.sum(axis=1, keepdims=True), lam], axis=1)  # [N_p, 4]
+    X = np.einsum("jv,kvd->kjd", bary, mesh.vertices[mesh.tets[ids]])
+    x, y, z = X[..., 0].copy(), X[..., 1].copy(), X[..., 2].copy()
+    t = 2.0 * np.pi
+    X[..., 0] = x + amp * np.sin(t * y) * np.sin(t * z)
+    X[..., 1] = y + amp * np.sin(t * z) * np.sin(t * x)
+    X[..., 2] = z + amp * np.sin(t * x) * np.sin(t * y)
+    return X
