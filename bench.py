@@ -3,13 +3,20 @@
 Workload (BASELINE.json configs[4], the single-GPU-fitting headline config):
 make_cube_mesh(88) = 4,088,832 straight tets, P=4 (N_p=35, N_cub=70, N_f=64),
 LLF, slip walls, random admissible state (bench.cpp:22-40 recipe), FP64.
-One "step" = one LSRK4 step = 5 x (traces kernel + fused RHS/update kernel).
-DOF-updates/s = K * N_p * 5 fields * 5 stages * steps / time.
+One "step" = one LSRK4 step = 5 fused RHS/update launches (each writes the
+next stage's face traces). DOF-updates/s = K * N_p * 5 fields * 5 stages *
+steps / time. The headline `value` is the graph-replayed production loop
+(no per-kernel events); a second, profiled pass gives the kernel times of the
+roofline. The `curved` object is the same metric on the curved
+(isoparametric) path: make_cube_mesh(32) with every element curved by a
+smooth map (196,608 curved tets, raised quadrature), LLF and HLLC, with its
+own roofline.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-N>1 (torchrun, one process per GPU, NCCL): strong scaling over z-slab
-partitions of the same mesh with a per-stage halo exchange of face traces.
+N>1 (torchrun, one process per GPU): strong scaling over z-slab partitions of
+the same mesh, driven by the library's multi-rank driver (cdg_gpu_comm, NCCL
+inside the library; the unique id travels over torch.distributed).
 """
 from __future__ import annotations
 
@@ -64,6 +71,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--partition", default="slab", choices=["slab", "rcb"],
                     help="N>1: z-slabs of the cube mesh, or recursive coordinate bisection (general meshes)")
+    ap.add_argument("--curved-n", type=int, default=32,
+                    help="cube cells per side of the curved block (6 n^3 curved tets; 0 = skip)")
+    ap.add_argument("--cpu-n", type=int, default=CPU_N_DEFAULT,
+                    help="cube cells per side of the reference CPU sample (6 n^3 tets)")
     return ap.parse_args()
 
 
@@ -139,34 +150,48 @@ class ClockSampler:
                 "reasons": reasons, "power_w_max": max(power) if power else None, "samples": len(self.samples)}
 
 
-def cpu_baseline(p, riemann, seconds_budget=25.0):
-    """The reference's own rk_step (oracle/_ref, all host threads) on a bounded
-    sample of the same workload; falls back to the C restatement (1 thread)."""
+CPU_N_DEFAULT = 30  # make_cube_mesh(30) = 162,000 tets: the largest cube sample whose reference DgLevel
+                    # (~140 KB/element at P=4) fits comfortably in the GPU box's host RAM
+
+
+def cpu_baseline(p, riemann, n_cpu=CPU_N_DEFAULT, steps=5, warmup=1, seconds_budget=60.0):
+    """The reference's own rk_step (oracle/_ref built in place from the
+    unmodified sources; the -O3 -march=native build of BASELINE.md §3 when this
+    CPU runs it) on all host threads, on make_cube_mesh(n_cpu) -- a bounded
+    sample of the same workload. Only the rk_step loop is timed (the store
+    copies in and out of the reference's SolutionStore are outside the timer).
+    Falls back to the C restatement (1 thread) without oracle/_ref."""
     try:
         from oracle import ref
-        if ref.available():
+        perf = ref.use_perf_build()
+        if ref.available() or perf:
             nthreads = ref.num_threads(os.cpu_count() or 1)
-            n_cpu = 14
+            t0 = time.perf_counter()
             mesh = ref.Mesh("cube", n_cpu)
             lv = ref.Level(mesh, p, bc_wall=0, bc_far=1)
+            setup = time.perf_counter() - t0
             cfg = ref.make_cfg(riemann)
             fs = freestream_state()
             u = lv.random_admissible_store(42)
             res = np.zeros_like(u)
             dt = 0.5 * lv.compute_timestep(u, cfg)
-            u, res = lv.rk_steps(u, res, cfg, fs, dt, 1)  # warm-up
+            if warmup:
+                u, res, _ = lv.rk_steps_timed(u, res, cfg, fs, dt, warmup)
             times = []
-            t_total = 0.0
-            while len(times) < 5 and t_total < seconds_budget:
-                t0 = time.perf_counter()
-                u, res = lv.rk_steps(u, res, cfg, fs, dt, 1)
-                times.append(time.perf_counter() - t0)
-                t_total += times[-1]
+            while len(times) < steps and sum(times) < seconds_budget:
+                u, res, secs = lv.rk_steps_timed(u, res, cfg, fs, dt, 1)
+                times.append(float(secs[0]))
             med = statistics.median(times)
             dofs = lv.K * lv.n_basis * 5 * 5
+            build = ("-O3 -march=native build (BASELINE.md §3 flags)" if perf else
+                     "-O3 -march=x86-64-v3 -ffp-contract=off build (bitwise-pinned oracle build)")
             return {"value": dofs / med, "unit": "DOF-updates/s", "cores": nthreads, "kind": "reference",
-                    "sample": f"make_cube_mesh({n_cpu}) = {lv.K} tets, P={p}, {len(times)} timed rk_step "
-                              f"(median {med:.3f} s), oracle/_ref (reference sources built in place)"}
+                    "cpu": ref.cpu_model(),
+                    "sample": f"make_cube_mesh({n_cpu}) = {lv.K} tets, P={p}, {riemann.upper()}, "
+                              f"{len(times)} timed rk_step after {warmup} warm-up (median {med:.3f} s; only the "
+                              f"step loop timed, level setup {setup:.1f} s outside), oracle/_ref: the reference "
+                              f"sources built in place, {build}, OpenMP {nthreads} threads",
+                    "steps_timed": len(times), "median_step_s": med}
     except Exception as e:  # pragma: no cover - diagnostic path
         err = repr(e)
     else:
@@ -177,9 +202,8 @@ def cpu_baseline(p, riemann, seconds_budget=25.0):
     re = R.get_reference_element(p)
     ol = port.OracleLevel(m, re, bc=0, freestream=freestream_state())
     cfg = gpu.run_config(riemann)
-    u = np.zeros(ol.store_size)
-    # same recipe via the product helper on a shape-compatible object
-    class _L:
+
+    class _L:  # same recipe via the product helper on a shape-compatible object
         K, n_basis, block = ol.K, re.n_basis, ol.block
     u = gpu.random_admissible_store(_L, seed=42)
     dt = 0.5 * ol.compute_timestep(u, cfg)
@@ -191,10 +215,12 @@ def cpu_baseline(p, riemann, seconds_budget=25.0):
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference's CPU rk_step on this box's host cores."""
+    """--impl reference: the reference's CPU rk_step on this box's host cores,
+    W warm-up + K timed steps of the bounded sample (at most ~2 min timed)."""
     if rank != 0:
         return
-    cb = cpu_baseline(args.p, args.riemann, seconds_budget=max(10.0, 4.0 * args.steps))
+    cb = cpu_baseline(args.p, args.riemann, n_cpu=args.cpu_n, steps=args.steps, warmup=args.warmup,
+                      seconds_budget=120.0)
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"],
             "unit": "DOF-updates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
@@ -202,6 +228,98 @@ def run_reference(args, rank, world):
             "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": "DOF-updates/s",
                                         "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def synthetic_state(lv, seed):
+    """bench.cpp:22-40's random admissible state, generated on the device."""
+    import torch
+    K, npb = lv.K, lv.n_basis
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    u = torch.zeros((K, 5, lv.block), dtype=torch.float64, device="cuda")
+    j = lambda: (torch.rand((K, npb), generator=g, dtype=torch.float64, device="cuda") - 0.5) * 0.1
+    rho = 1.0 + j()
+    vx, vy, vz = 0.3 + j(), j(), j()
+    pr = 1.0 + j()
+    u[:, 0, :npb] = rho
+    u[:, 1, :npb] = rho * vx
+    u[:, 2, :npb] = rho * vy
+    u[:, 3, :npb] = rho * vz
+    u[:, 4, :npb] = pr / 0.4 + 0.5 * rho * (vx * vx + vy * vy + vz * vz)
+    del rho, vx, vy, vz, pr
+    torch.cuda.synchronize()  # the level copies on its own (non-blocking) stream
+    lv.set_state_device(u.data_ptr(), None)
+    del u
+    torch.cuda.empty_cache()
+
+
+def time_steps(lv, run, steps):
+    """device time (CUDA events on the level's stream) of run(steps)."""
+    import torch
+    ext = torch.cuda.ExternalStream(lv.stream())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(ext)
+    run(steps)
+    e1.record(ext)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1)
+
+
+def profile_steps(lv, cfg, dt, steps):
+    """Per-kernel device times of `steps` RK steps (events around every launch
+    on the level's stream; not the production mode, hence a separate pass)."""
+    lv.set_profiling(True)
+    lv.rk_steps(cfg, dt, steps)
+    lv.set_profiling(False)
+    t_tr, t_rhs, _ = lv.last_profile()
+    return float(t_tr), float(t_rhs)
+
+
+def curved_block(args, peak, hbm_peak):
+    """The curved (isoparametric) path at a GPU-filling size: make_cube_mesh(n)
+    with every element's collocation nodes moved by a smooth global map
+    (mesh.warped_nodes), curved-mesh quadrature (P=4: N_cub 70, N_g 56), per-node
+    metrics, M_e^-1 epilogue -- LLF and HLLC, graph-replayed steps, plus a
+    profiled pass for the RHS kernel's roofline (F_rhs per curved element,
+    SURVEY §8d with the curved quadrature)."""
+    from paper_1208_4772_b200 import gpu, mesh as M, refelem as R
+    t0 = time.perf_counter()
+    p = args.p
+    re = R.level_reference_element(p, True)
+    mesh = M.cube_mesh(args.curved_n)
+    X = M.warped_nodes(mesh, re)
+    lv = gpu.GpuLevel(mesh, p, bc=0, freestream=freestream_state(), curved=(np.arange(mesh.n_owned), X), re=re)
+    del X
+    setup = time.perf_counter() - t0
+    synthetic_state(lv, 7)
+    K, npb, nf = lv.K, lv.n_basis, 4 * re.n_face_quad
+    F, F_rhs, B = model_flops_bytes(npb, re.n_cub, nf)
+    geo = 8 * (9 * re.n_cub + 4 * nf + npb * npb)  # per-node metric, per-face-node (n, sjac w), M_e^-1
+    out = {"workload": f"make_cube_mesh({args.curved_n}) = {K} tets, ALL curved (smooth isoparametric map, "
+                       f"amp 0.02), P={p} curved quadrature (N_cub={re.n_cub}, N_f={nf}), slip walls, random "
+                       f"admissible state", "elements": K, "curved_elements": K, "setup_s": round(setup, 1)}
+    for riemann in ("llf", "hllc"):
+        cfg = gpu.run_config(riemann, cfl=args.cfl)
+        dt = 0.5 * lv.compute_timestep(cfg)
+        steps = max(3, args.steps // 2)
+        lv.rk_steps(cfg, dt, 3)  # warm-up (graph capture)
+        ms = time_steps(lv, lambda n: lv.rk_steps(cfg, dt, n), steps)
+        t_tr, t_rhs = profile_steps(lv, cfg, dt, 2)
+        t_rhs_s, t_tr_s = t_rhs / 10 * 1e-3, t_tr / 10 * 1e-3
+        ach = F_rhs * K / t_rhs_s / 1e12
+        r = {"value": K * npb * 25 * steps / (ms * 1e-3), "unit": "DOF-updates/s", "ms_per_step": ms / steps,
+             "steps": steps, "rhs_kernel_ms": t_rhs_s * 1e3, "trace_kernel_ms": t_tr_s * 1e3,
+             "roofline": {"bound": "tensor", "kernel": "k_rhs_rowc<P=4> (curved: per-node metrics, fused "
+                          "volume+surface+lift, M_e^-1 epilogue + LSRK update)", "achieved": ach, "peak": peak,
+                          "unit": "TFLOP/s", "frac": ach / peak, "algorithmic_flops_per_elem": F_rhs,
+                          "model_bytes_per_elem": B + geo,
+                          "hbm_achieved_gbs": (B + geo) * K / t_rhs_s / 1e9, "hbm_peak_gbs": hbm_peak,
+                          "stage_frac": F * K / (t_rhs_s + t_tr_s) / 1e12 / peak}}
+        out[riemann] = r
+    out["value"] = out["llf"]["value"]
+    out["unit"] = "DOF-updates/s"
+    lv.close()
+    return out
 
 
 def main():
@@ -216,21 +334,11 @@ def main():
     import torch
     from paper_1208_4772_b200 import gpu, partition, refelem as R
 
-    # CDG_BENCH_DIST=gloo (+ CDG_BENCH_ONE_GPU=1): functional check of the
-    # multi-rank path on a 1-GPU box (halo buffers staged through the host);
-    # never used for measurements
-    backend = os.environ.get("CDG_BENCH_DIST", "nccl")
-    if os.environ.get("CDG_BENCH_ONE_GPU"):
-        local_rank = 0
     torch.cuda.set_device(local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-        else:
-            dist.init_process_group(backend)
-    red_dev = "cuda" if backend == "nccl" else "cpu"
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
     p = args.p
     re = R.get_reference_element(p)
@@ -246,83 +354,24 @@ def main():
     lv = gpu.GpuLevel(part.mesh, p, bc=0, freestream=fs, re=re, device=local_rank)
     cfg = gpu.run_config(args.riemann, cfl=args.cfl)
     K = lv.K
-    # random admissible state generated on the device (bench.cpp:22-40 recipe)
-    g = torch.Generator(device="cuda").manual_seed(42 + rank)
-    u = torch.zeros((K, 5, lv.block), dtype=torch.float64, device="cuda")
     npb = lv.n_basis
-    j = lambda: (torch.rand((K, npb), generator=g, dtype=torch.float64, device="cuda") - 0.5) * 0.1
-    rho = 1.0 + j()
-    vx, vy, vz = 0.3 + j(), j(), j()
-    pr = 1.0 + j()
-    u[:, 0, :npb] = rho
-    u[:, 1, :npb] = rho * vx
-    u[:, 2, :npb] = rho * vy
-    u[:, 3, :npb] = rho * vz
-    u[:, 4, :npb] = pr / 0.4 + 0.5 * rho * (vx * vx + vy * vy + vz * vz)
-    del rho, vx, vy, vz, pr
-    torch.cuda.synchronize()  # the level copies on its own (non-blocking) stream
-    lv.set_state_device(u.data_ptr(), None)
-    del u
-    torch.cuda.empty_cache()
-    dt = lv.compute_timestep(cfg)
-    if dist is not None:
-        t = torch.tensor([dt], dtype=torch.float64, device=red_dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MIN)
-        dt = float(t.item())
+    synthetic_state(lv, 42 + rank)
+    comm = None
+    if world > 1:
+        # the library's multi-rank driver: halo rows per peer, NCCL inside the
+        # library; rank 0's unique id is broadcast over torch.distributed
+        lv.halo_define(part.peers)
+        uid = [gpu.GpuComm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = gpu.GpuComm.nccl(lv, uid[0], rank, world)
+        dt = comm.compute_timestep(cfg)
+    else:
+        dt = lv.compute_timestep(cfg)
     setup_s = time.perf_counter() - t_setup
 
-    # ---- halo plumbing (N>1) ------------------------------------------------
-    bufs = []
-    if world > 1:
-        per = 5 * lv.n_face_quad
-        send_all = np.concatenate([pe.send_elem_face for pe in part.peers])
-        recv_all = np.concatenate([pe.recv_elem_face for pe in part.peers])
-        sbuf = torch.empty(len(send_all) * per, dtype=torch.float64, device="cuda")
-        rbuf = torch.empty(len(recv_all) * per, dtype=torch.float64, device="cuda")
-        lv.halo_setup(send_all, recv_all, sbuf.data_ptr(), rbuf.data_ptr())
-        off_s = off_r = 0
-        for pe in part.peers:
-            ns, nr = len(pe.send_elem_face) * per, len(pe.recv_elem_face) * per
-            bufs.append((pe.rank, sbuf[off_s:off_s + ns], rbuf[off_r:off_r + nr]))
-            off_s += ns
-            off_r += nr
-    ext = torch.cuda.ExternalStream(lv.stream())
-
-    def step_multi():
-        # per stage: traces + pack (phase 0) | NCCL halo exchange on NCCL's stream,
-        # overlapped with the interior tiles' RHS + update (phase 2) | the halo
-        # tiles after the traces land (phase 3)  (the paper's overlap)
-        with torch.cuda.stream(ext):
-            for stage in range(5):
-                lv.stage_phase(cfg, stage, 0, dt)
-                if backend != "nccl":  # host-staged functional path (gloo)
-                    ext.synchronize()
-                    hs = [(peer, sb.cpu(), torch.empty_like(rb, device="cpu"), rb) for peer, sb, rb in bufs]
-                    works = []
-                    for peer, hsb, hrb, _ in hs:
-                        works.append(dist.isend(hsb, peer))
-                        works.append(dist.irecv(hrb, peer))
-                    lv.stage_phase(cfg, stage, 2, dt)
-                    for w in works:
-                        w.wait()
-                    for _, _, hrb, rb in hs:
-                        rb.copy_(hrb)
-                    lv.stage_phase(cfg, stage, 3, dt)
-                    continue
-                ops = []
-                for peer, sb, rb in bufs:
-                    ops.append(dist.P2POp(dist.isend, sb, peer))
-                    ops.append(dist.P2POp(dist.irecv, rb, peer))
-                works = dist.batch_isend_irecv(ops)
-                lv.stage_phase(cfg, stage, 2, dt)
-                for w in works:
-                    w.wait()
-                lv.stage_phase(cfg, stage, 3, dt)
-
     def run_steps(n):
-        if world > 1:
-            for _ in range(n):
-                step_multi()
+        if comm is not None:
+            comm.rk_steps(cfg, dt, n)
         else:
             lv.rk_steps(cfg, dt, n)
 
@@ -330,24 +379,18 @@ def main():
     run_steps(args.warmup)
     torch.cuda.synchronize()
 
-    # ---- timed region (device events on the level's stream, max over ranks) --
+    # ---- timed region: the production loop (graph replays on one GPU),
+    # device events on the level's stream, max over ranks ----------------------
+    ext = torch.cuda.ExternalStream(lv.stream())
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     launches0 = lv.launch_count()
-    prof_tr = prof_rhs = 0.0
     with ClockSampler(local_rank) as clk:
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
         ev0.record(ext)
-        if world > 1:
-            run_steps(args.steps)
-        else:
-            lv.set_profiling(True)       # per-kernel CUDA events on the launching stream
-            lv.rk_steps(cfg, dt, args.steps)
-            lv.set_profiling(False)
-            prof = lv.last_profile()
-            prof_tr, prof_rhs = float(prof[0]), float(prof[1])
+        run_steps(args.steps)
         ev1.record(ext)
         torch.cuda.synchronize()
         if dist is not None:
@@ -355,7 +398,7 @@ def main():
     launches = lv.launch_count() - launches0
     ms_total = ev0.elapsed_time(ev1)
     if dist is not None:
-        t = torch.tensor([ms_total], dtype=torch.float64, device=red_dev)
+        t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     K_global = 6 * args.n ** 3
@@ -365,66 +408,65 @@ def main():
 
     # ---- end-to-end through the public API with host buffers -----------------
     e2e = None
-    if not args.no_e2e and world > 1:
-        # per step and rank: snapshot + one halo-exchanging RK step + the
-        # residual's inf-norm partials D2H, all-reduced (MAX) over ranks; wall
-        # clock, max over ranks
+    if not args.no_e2e:
+        # per step: snapshot + one RK step (dt/a/b H2D) + the residual's
+        # inf-norm partials D2H (multi-rank: reduced over ranks inside the
+        # library); wall clock, max over ranks -- run_steady's check loop
         steps = max(3, args.steps // 2)
-        step_multi()
+        run_steps(1)
         torch.cuda.synchronize()
-        dist.barrier()
+        if dist is not None:
+            dist.barrier()
         t0 = time.perf_counter()
         for _ in range(steps):
-            lv.snapshot()
-            step_multi()
-            r = torch.tensor([lv.residual(dt, "inf")], dtype=torch.float64, device=red_dev)
-            dist.all_reduce(r, op=dist.ReduceOp.MAX)
-        t_e2e = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=red_dev)
-        dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
-        t_e2e = float(t_e2e.item())
-        assert math.isfinite(float(r.item()))
-        e2e = {"value": dofs_per_step * steps / t_e2e, "unit": "DOF-updates/s",
-               "h2d_bytes_per_step": world * 8 * 11, "d2h_bytes_per_step": world * 8 * 592,
-               "what": "per step on every rank: snapshot + 5 x stage_phase 0/2/3 with the halo exchange + "
-                       "cdg_gpu_residual (inf-norm partials D2H) + all-reduce MAX; wall clock, max over ranks"}
-    if not args.no_e2e and world == 1:
-        # per step: H2D of dt/RK coefficients (pinned), RK step, D2H residual
-        steps = max(3, args.steps // 2)
-        lv.rk_steps(cfg, dt, 1)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(steps):
-            lv.snapshot()
-            lv.rk_steps(cfg, dt, 1)
-            r = lv.residual(dt, "inf")
+            if comm is not None:
+                comm.snapshot()
+                comm.rk_steps(cfg, dt, 1)
+                r = comm.residual(dt, "inf")
+            else:
+                lv.snapshot()
+                lv.rk_steps(cfg, dt, 1)
+                r = lv.residual(dt, "inf")
         t_e2e = time.perf_counter() - t0
+        if dist is not None:
+            t = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            t_e2e = float(t.item())
         assert math.isfinite(r)
         e2e = {"value": dofs_per_step * steps / t_e2e, "unit": "DOF-updates/s",
-               "h2d_bytes_per_step": 8 * 11, "d2h_bytes_per_step": 8 * 592,
+               "h2d_bytes_per_step": world * 8 * 11, "d2h_bytes_per_step": world * 8 * 592,
                "what": "per step: snapshot + cdg_gpu_rk_steps(1) (dt/a/b H2D) + cdg_gpu_residual (inf-norm "
-                       "partials D2H), wall clock, the run_steady check loop (solver.cpp:637-668)"}
-        # reference rk_step adapter semantics: full state host->device->host every step
-        u_host, res_host = lv.get_state()
-        t0 = time.perf_counter()
-        rt_steps = 2
-        for _ in range(rt_steps):
-            lv.set_state(u_host, res_host)
-            lv.rk_steps(cfg, dt, 1)
+                       "partials D2H), wall clock, the run_steady check loop (solver.cpp:637-668)"
+                       + ("; N>1: cdg_gpu_comm_* (halo exchange per stage, residual MAX over ranks)"
+                          if world > 1 else "")}
+        if world == 1:
+            # reference rk_step adapter semantics: full state host->device->host every step
             u_host, res_host = lv.get_state()
-        t_rt = time.perf_counter() - t0
-        e2e["roundtrip"] = {"value": dofs_per_step * rt_steps / t_rt, "unit": "DOF-updates/s",
-                            "h2d_bytes_per_step": 2 * u_host.nbytes, "d2h_bytes_per_step": 2 * u_host.nbytes,
-                            "what": "rk_step adapter: u,res H2D + 1 step + u,res D2H (pageable numpy)"}
+            t0 = time.perf_counter()
+            rt_steps = 2
+            for _ in range(rt_steps):
+                lv.set_state(u_host, res_host)
+                lv.rk_steps(cfg, dt, 1)
+                u_host, res_host = lv.get_state()
+            t_rt = time.perf_counter() - t0
+            e2e["roundtrip"] = {"value": dofs_per_step * rt_steps / t_rt, "unit": "DOF-updates/s",
+                                "h2d_bytes_per_step": 2 * u_host.nbytes, "d2h_bytes_per_step": 2 * u_host.nbytes,
+                                "what": "rk_step adapter: u,res H2D + 1 step + u,res D2H (pageable numpy)"}
+            del u_host, res_host
 
-    # ---- roofline -----------------------------------------------------------
+    # ---- roofline (one GPU): a separate profiled pass for the kernel times ----
     F, F_rhs, B = model_flops_bytes(npb, re.n_cub, 4 * re.n_face_quad)
     ex_rhs, ex_tr = kernel_flops_executed(npb, re.n_cub, 4 * re.n_face_quad)
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     roof = None
-    if world == 1 and prof_rhs > 0:
+    peak = None
+    if world == 1:
         fp64_dmma, fp64_dfma, fp64_k8, fp64_k16 = gpu.measure_fp64_peak(local_rank)
-        launches_rhs = 5 * args.steps
+        peak = max(fp64_dmma, fp64_dfma, fp64_k8, fp64_k16)
+        prof_steps = min(args.steps, 4)
+        prof_tr, prof_rhs = profile_steps(lv, cfg, dt, prof_steps)
+        launches_rhs = 5 * prof_steps
         t_rhs = prof_rhs / launches_rhs * 1e-3
         t_tr = prof_tr / launches_rhs * 1e-3
         fused = lv.fused_traces()
@@ -437,12 +479,12 @@ def main():
         ncu_file = ROOT / "profiles" / f"ncu_rhs_p{p}.json"
         if ncu_file.exists():
             traffic = json.loads(ncu_file.read_text()).get("dram_bytes_per_launch")
-        peak = max(fp64_dmma, fp64_dfma, fp64_k8, fp64_k16)
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "kernel": (f"k_rhs_row<P={p}> (fused volume+surface+lift+LSRK update"
                            + (" + next-stage traces" if fused else "") + ", FP64 DMMA, one m-tile row per warp)"
-                           if p in (4, 5) else f"RHS+update kernel <P={p}> (fused volume+surface+lift+LSRK update, FP64 DMMA)"),
+                           if p in (2, 3, 4, 5) else f"RHS+update kernel <P={p}> (fused volume+surface+lift+LSRK "
+                                                     f"update, FP64 DMMA)"),
                 "fused_traces": fused,
                 "algorithmic_flops_per_launch": F_k * K,
                 "peak_source": "max of the FP64 DMMA (m16n8k4/k8/k16) and DFMA peaks measured live on this "
@@ -452,7 +494,8 @@ def main():
                 "fp64_dfma_peak_tflops": fp64_dfma, "fp64_dmma_k8_tflops": fp64_k8,
                 "fp64_dmma_k16_tflops": fp64_k16,
                 "kernel_ms_avg": t_rhs * 1e3, "trace_kernel_ms_avg": t_tr * 1e3,
-                "rhs_share_of_stage": prof_rhs / (prof_rhs + prof_tr),
+                "profiled_steps": prof_steps,
+                "kernel_share_of_step": prof_rhs / prof_steps / ms_per_step,
                 "executed_dmma_tflops": ex_k * K / t_rhs / 1e12,
                 "hbm_achieved_gbs": B * K / t_rhs / 1e9, "hbm_peak_gbs": hbm_peak,
                 "hbm_frac": B * K / t_rhs / 1e9 / hbm_peak,
@@ -463,16 +506,22 @@ def main():
             "value": value, "unit": "DOF-updates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {**workload_config(args, world),
-                       **({"dist_backend": backend + " (host-staged halos; functional check, not a measurement)"}
-                          if world > 1 and backend != "nccl" else {})},
+            "config": workload_config(args, world),
             "setup_s": round(setup_s, 1), "gpu_launches": launches, "clocks": clocks}
+    if comm is not None:
+        line["config"]["multi_rank"] = ("cdg_gpu_comm (NCCL inside the library): per stage pack -> "
+                                        "ncclSend/Recv || interior tiles -> halo tiles")
     if e2e:
         line["e2e"] = e2e
     if roof:
         line["roofline"] = roof
+    if comm is not None:
+        comm.close()
+    lv.close()
+    if rank == 0 and world == 1 and args.curved_n > 0:
+        line["curved"] = curved_block(args, peak, hbm_peak)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(p, args.riemann)
+        line["cpu_baseline"] = cpu_baseline(p, args.riemann, n_cpu=args.cpu_n)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:

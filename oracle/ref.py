@@ -16,6 +16,36 @@ import numpy as np
 
 HERE = Path(__file__).resolve().parent
 LIB_PATH = HERE / "_ref" / "libcdg_ref.so"
+# the same sources built with BASELINE.md §3's flags (-O3 -march=native): the
+# CPU baseline / reference arm of bench.py; the bitwise-pinned build above is
+# the checker everywhere else
+PERF_LIB_PATH = HERE / "_ref" / "perf" / "libcdg_ref_perf.so"
+
+
+def use_perf_build() -> bool:
+    """Bind to the -O3 -march=native build (before the first call). True when
+    it exists and this CPU has the AVX-512 it was compiled for."""
+    global LIB_PATH
+    if _lib is not None or not PERF_LIB_PATH.exists():
+        return False
+    try:
+        flags = Path("/proc/cpuinfo").read_text()
+    except OSError:
+        return False
+    if "avx512f" not in flags or "amx_tile" not in flags:
+        return False
+    LIB_PATH = PERF_LIB_PATH
+    return True
+
+
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int)
@@ -74,6 +104,8 @@ def lib():
         L.ref_interpolate_to_faces.argtypes = [C.c_void_p, _dp, _dp]
         L.ref_rk_steps.argtypes = [C.c_void_p, C.POINTER(RunCfg), _dp, C.c_double, C.c_int, _dp, _dp,
                                    C.c_char_p, C.c_size_t]
+        L.ref_rk_steps_timed.argtypes = [C.c_void_p, C.POINTER(RunCfg), _dp, C.c_double, C.c_int, _dp, _dp, _dp,
+                                         C.c_char_p, C.c_size_t]
         L.ref_last_viscosity.argtypes = [C.c_void_p, _dp, _dp]
         L.ref_compute_timestep.argtypes = [C.c_void_p, C.POINTER(RunCfg), _dp, _dp, _dp, C.c_char_p,
                                            C.c_size_t]
@@ -259,6 +291,19 @@ class Level:
         if st:
             raise RefError(st, err.value.decode())
         return u, res
+
+    def rk_steps_timed(self, u, res, cfg: RunCfg, freestream, dt, nsteps=1):
+        """nsteps x rk_step with only the step loop timed (store copies outside);
+        returns (u, res, seconds per step)."""
+        u = np.array(u, np.float64, copy=True)
+        res = np.array(res, np.float64, copy=True)
+        fs = np.ascontiguousarray(freestream, np.float64)
+        secs = np.zeros(nsteps)
+        err = C.create_string_buffer(512)
+        st = lib().ref_rk_steps_timed(self.h, C.byref(cfg), _p(fs), dt, nsteps, _p(u), _p(res), _p(secs), err, 512)
+        if st:
+            raise RefError(st, err.value.decode())
+        return u, res, secs
 
     def last_viscosity(self, with_q=True):
         eps = np.zeros(self.K)

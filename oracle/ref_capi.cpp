@@ -17,6 +17,7 @@
 //   current_viscosity / aux_gradient         src/solver.cpp:87-91
 //   random_admissible_store recipe           src/bench.cpp:22-40 (restated: it
 //                                            is file-static in the reference)
+#include <chrono>
 #include <omp.h>
 
 #include <cstring>
@@ -414,6 +415,35 @@ int ref_rk_steps(void* h, const ref_run_cfg* c, const double* freestream, double
     const ConservedState fs = to_state(freestream);
     const RKScheme scheme = RKScheme::low_storage_rk4();
     for (int s = 0; s < nsteps; ++s) rk_step(*lv->level, u, res, cfg, fs, dt, scheme, *lv->ws);
+    save_store(u, u_io);
+    save_store(res, res_io);
+    return 0;
+  } catch (const std::exception& e) {
+    copy_err(e, err, errn);
+    return status_of(e);
+  }
+}
+
+// The CPU baseline's timing entry: the stores are built once from u_io /
+// res_io, then nsteps x rk_step run back to back and ONLY that loop is timed
+// (seconds[s] = wall time of step s, steady_clock); the stores are copied
+// back afterwards, outside the timed region.
+int ref_rk_steps_timed(void* h, const ref_run_cfg* c, const double* freestream, double dt, int nsteps,
+                       double* u_io, double* res_io, double* seconds, char* err, size_t errn) {
+  auto* lv = static_cast<RefLevel*>(h);
+  try {
+    SolutionStore u = lv->level->make_store();
+    SolutionStore res = lv->level->make_store();
+    load_store(u, u_io);
+    load_store(res, res_io);
+    const RunConfig cfg = to_cfg(c);
+    const ConservedState fs = to_state(freestream);
+    const RKScheme scheme = RKScheme::low_storage_rk4();
+    for (int s = 0; s < nsteps; ++s) {
+      const auto t0 = std::chrono::steady_clock::now();
+      rk_step(*lv->level, u, res, cfg, fs, dt, scheme, *lv->ws);
+      seconds[s] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
     save_store(u, u_io);
     save_store(res, res_io);
     return 0;

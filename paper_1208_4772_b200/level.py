@@ -59,35 +59,52 @@ def curved_geometry(nodes: np.ndarray, re: ReferenceElement):
     (n, sjac*w) [Kc, 4N_g, 4], M_e^-1 [Kc, N_p, N_p] and h = 6V/A [Kc]."""
     X = np.asarray(nodes, float)
     ng = re.n_face_quad
+    K = X.shape[0]
+    Xt = [np.ascontiguousarray(X[..., i]) for i in range(3)]  # x_i at the collocation nodes [Kc, N_p]
 
-    def fwd_at(dr, ds, dt):
-        return np.stack([np.einsum("qj,kjd->kqd", dr, X), np.einsum("qj,kjd->kqd", ds, X),
-                         np.einsum("qj,kjd->kqd", dt, X)], axis=3)  # [Kc, n, i, m]
+    def fwd_at(dr, ds, dt):  # F[i][m] = dx_i/dr_m at the n points, [Kc, n] each (one GEMM per entry)
+        return [[Xt[i] @ d.T for d in (dr, ds, dt)] for i in range(3)]
 
-    f = fwd_at(re.deriv_r, re.deriv_s, re.deriv_t)
-    jac = np.linalg.det(f)
+    F = fwd_at(re.deriv_r, re.deriv_s, re.deriv_t)
+    # 3x3 determinant and inverse by cofactors, inv[m][i] = dr_m/dx_i
+    inv = [[None] * 3 for _ in range(3)]
+    inv[0][0] = F[1][1] * F[2][2] - F[1][2] * F[2][1]
+    inv[1][0] = F[1][2] * F[2][0] - F[1][0] * F[2][2]
+    inv[2][0] = F[1][0] * F[2][1] - F[1][1] * F[2][0]
+    jac = F[0][0] * inv[0][0] + F[0][1] * inv[1][0] + F[0][2] * inv[2][0]
     if np.any(jac <= 1e-14):
         k, q = np.argwhere(jac <= 1e-14)[0]
         raise ArithmeticError(f"inverted curved element (list index {k}): mapping Jacobian {jac[k, q]} "
                               f"at quadrature node {q}")
-    inv = np.linalg.inv(f)                                   # [Kc, q, m, i]
+    inv[0][1] = F[0][2] * F[2][1] - F[0][1] * F[2][2]
+    inv[1][1] = F[0][0] * F[2][2] - F[0][2] * F[2][0]
+    inv[2][1] = F[0][1] * F[2][0] - F[0][0] * F[2][1]
+    inv[0][2] = F[0][1] * F[1][2] - F[0][2] * F[1][1]
+    inv[1][2] = F[0][2] * F[1][0] - F[0][0] * F[1][2]
+    inv[2][2] = F[0][0] * F[1][1] - F[0][1] * F[1][0]
     jw = jac * re.cub_weights[None, :]
-    jwr = (jw[:, :, None, None] * inv).reshape(X.shape[0], re.n_cub, 9)
-    ff = fwd_at(re.face_deriv_r, re.face_deriv_s, re.face_deriv_t)  # [Kc, nf, i, m]
-    face = np.empty((X.shape[0], 4 * ng, 4))
-    area = np.zeros(X.shape[0])
+    # J W dr_m/dx_i = W x cofactor (the 1/J of the inverse cancels)
+    jwr = np.stack([inv[m][i] * re.cub_weights[None, :] for m in range(3) for i in range(3)], axis=2)
+    FF = fwd_at(re.face_deriv_r, re.face_deriv_s, re.face_deriv_t)  # [i][m] -> [Kc, 4 N_g]
+    face = np.empty((K, 4 * ng, 4))
+    area = np.zeros(K)
     for fi, (a, b, c) in enumerate(FACE_VERTS):
         ra = 0.5 * (TET_VERTS[b] - TET_VERTS[a])
         rb = 0.5 * (TET_VERTS[c] - TET_VERTS[a])
         sl = slice(fi * ng, (fi + 1) * ng)
-        xa = ff[:, sl] @ ra
-        xb = ff[:, sl] @ rb
-        nraw = np.cross(xa, xb)
-        s = np.linalg.norm(nraw, axis=2)
-        face[:, sl, :3] = nraw / s[..., None]
+        xa = [sum(FF[i][m][:, sl] * ra[m] for m in range(3)) for i in range(3)]
+        xb = [sum(FF[i][m][:, sl] * rb[m] for m in range(3)) for i in range(3)]
+        n0 = xa[1] * xb[2] - xa[2] * xb[1]
+        n1 = xa[2] * xb[0] - xa[0] * xb[2]
+        n2 = xa[0] * xb[1] - xa[1] * xb[0]
+        s = np.sqrt(n0 * n0 + n1 * n1 + n2 * n2)
+        face[:, sl, 0], face[:, sl, 1], face[:, sl, 2] = n0 / s, n1 / s, n2 / s
         face[:, sl, 3] = s * re.face_weights[None, :]
         area += (s * re.face_weights[None, :]).sum(axis=1)
-    mass = np.einsum("qi,kq,qj->kij", re.interp_cub, jw, re.interp_cub)
+    # M_e = I_cub^T diag(J W) I_cub for every element as ONE GEMM: [Kc, N_cub] x [N_cub, N_p^2]
+    npb = re.n_basis
+    outer = (re.interp_cub[:, :, None] * re.interp_cub[:, None, :]).reshape(re.n_cub, npb * npb)
+    mass = (jw @ outer).reshape(K, npb, npb)
     minv = np.linalg.inv(mass)
     h = 6.0 * jw.sum(axis=1) / area
     return np.ascontiguousarray(jwr), np.ascontiguousarray(face), np.ascontiguousarray(minv), h, \

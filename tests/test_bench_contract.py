@@ -23,7 +23,7 @@ def _run(*args, timeout=600):
 
 
 def test_reference_arm_line(refmod):
-    d = _run("--impl", "reference", "--steps", "1", "--warmup", "1")
+    d = _run("--impl", "reference", "--steps", "1", "--warmup", "1", "--cpu-n", "8")
     assert BASE <= d.keys() and d["impl"] == "reference"
     baseline = json.loads((ROOT / "BASELINE.json").read_text())
     assert d["metric"] == baseline["metric"] and d["unit"] == "DOF-updates/s"
@@ -36,7 +36,7 @@ def test_reference_arm_line(refmod):
 
 @pytest.mark.gpu
 def test_our_arm_line_matches_the_reference_arm(gpu_lib):
-    d = _run("--cube-n", "16", "--steps", "3", "--warmup", "3", "--no-cpu-baseline")
+    d = _run("--cube-n", "16", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--curved-n", "8")
     assert BASE <= d.keys() and "impl" not in d
     assert d["metric"] == json.loads((ROOT / "BASELINE.json").read_text())["metric"]
     assert d["value"] > 0 and d["ms_per_step"] > 0 and d["warmup"] >= 3
@@ -47,5 +47,9 @@ def test_our_arm_line_matches_the_reference_arm(gpu_lib):
     assert r["bound"] == "tensor" and r["unit"] == "TFLOP/s" and 0 < r["frac"] < 1
     assert abs(r["achieved"] / r["peak"] - r["frac"]) < 1e-9
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= d["clocks"].keys()
-    ref_cfg = _run("--impl", "reference", "--cube-n", "16", "--steps", "1", "--warmup", "1")["config"]
+    c = d["curved"]  # the curved (isoparametric) path: its own value and roofline
+    assert c["curved_elements"] == c["elements"] == 6 * 8 ** 3 and c["value"] == c["llf"]["value"] > 0
+    for rm in ("llf", "hllc"):
+        assert 0 < c[rm]["roofline"]["frac"] < 1 and c[rm]["rhs_kernel_ms"] > 0
+    ref_cfg = _run("--impl", "reference", "--cube-n", "16", "--steps", "1", "--warmup", "1", "--cpu-n", "8")["config"]
     assert ref_cfg == d["config"]
