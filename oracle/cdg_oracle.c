@@ -398,7 +398,12 @@ int cdgo_level_create(const cdgo_desc *d, cdgo_level **out, char *err, size_t er
         double best = 1e300;
         for (int h = 0; h < ng; ++h) {
           const double *th = face_phys + ((size_t)nb * nf + nface * ng + h) * 3;
-          const double dx = mine[0] - th[0], dy = mine[1] - th[1], dz = mine[2] - th[2];
+          double dx = mine[0] - th[0], dy = mine[1] - th[1], dz = mine[2] - th[2];
+          /* periodic boxes (BASELINE config 1, not a reference feature): the
+             neighbour face is a translate, pair by minimum image */
+          if (d->period[0] > 0.0) dx -= d->period[0] * nearbyint(dx / d->period[0]);
+          if (d->period[1] > 0.0) dy -= d->period[1] * nearbyint(dy / d->period[1]);
+          if (d->period[2] > 0.0) dz -= d->period[2] * nearbyint(dz / d->period[2]);
           const double dist = sqrt(dx * dx + dy * dy + dz * dz);
           if (dist < best) {
             best = dist;

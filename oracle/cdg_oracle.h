@@ -35,6 +35,7 @@ typedef struct cdgo_desc {
   const int *neighbor, *neighbor_face; /* [K][4] */
   const int *bc;                       /* [K][4] 0 wall 1 farfield 2 symmetry */
   double freestream[5];
+  double period[3];                    /* > 0: periodic box length per axis (minimum-image pairing) */
 } cdgo_desc;
 
 typedef struct cdgo_cfg {

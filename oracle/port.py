@@ -25,7 +25,8 @@ class Desc(C.Structure):
                 ("padded", C.c_int)] + [(k, _dp) for k in (
                     "icub", "ig", "dr", "ds", "dt", "fdr", "fds", "fdt", "cub_w", "face_w", "vinv",
                     "elem_nodes", "pair_scale")] + [
-                ("neighbor", _ip), ("neighbor_face", _ip), ("bc", _ip), ("freestream", C.c_double * 5)]
+                ("neighbor", _ip), ("neighbor_face", _ip), ("bc", _ip), ("freestream", C.c_double * 5),
+                ("period", C.c_double * 3)]
 
 
 _lib = None
@@ -112,6 +113,8 @@ class OracleLevel:
         fs = np.zeros(5) if freestream is None else np.asarray(freestream, float)
         for c in range(5):
             d.freestream[c] = fs[c]
+        for a, L in enumerate(getattr(mesh, "period", None) or (0.0, 0.0, 0.0)):
+            d.period[a] = L
         self._desc = d
         h = C.c_void_p()
         err = C.create_string_buffer(512)

@@ -96,6 +96,8 @@ def lib():
         L.ref_level_create.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                        C.c_char_p, C.c_size_t]
         L.ref_level_free.argtypes = [C.c_void_p]
+        L.ref_level_make_periodic.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_char_p,
+                                              C.c_size_t]
         L.ref_level_sizes.argtypes = [C.c_void_p, _ip]
         L.ref_level_geometry.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, _dp, _dp, _ip, _ip, _ip, _ip]
         L.ref_level_operators.argtypes = [C.c_void_p, C.c_int, _dp, _dp, _dp, _dp]
@@ -291,6 +293,12 @@ class Level:
         if st:
             raise RefError(st, err.value.decode())
         return u, res
+
+    def make_periodic(self, period):
+        """Link the cube level's boundary faces to their translates (ref_periodic.cpp)."""
+        err = C.create_string_buffer(512)
+        if lib().ref_level_make_periodic(self.h, *[float(x) for x in period], err, 512):
+            raise RefError(1, err.value.decode())
 
     def rk_steps_timed(self, u, res, cfg: RunCfg, freestream, dt, nsteps=1):
         """nsteps x rk_step with only the step loop timed (store copies outside);

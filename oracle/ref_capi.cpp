@@ -64,6 +64,10 @@ int status_of(const std::exception& e) {
 
 }  // namespace
 
+namespace cdg_oracle {
+void make_periodic(cdg::DgLevel& level, const double period[3]);  // ref_periodic.cpp
+}
+
 extern "C" {
 
 // Mirrors cdg_gpu_run_config in include/cdg_gpu.h (same field order).
@@ -261,6 +265,18 @@ void* ref_level_create(void* mesh_h, int p, int bc_wall, int bc_far, int padded,
   }
 }
 void ref_level_free(void* h) { delete static_cast<RefLevel*>(h); }
+// Periodic box (BASELINE config 1): link every boundary face of the level to
+// its translate across the box (ref_periodic.cpp). Returns 0 / 1 (+ message).
+int ref_level_make_periodic(void* h, double lx, double ly, double lz, char* err, size_t errn) {
+  try {
+    const double period[3] = {lx, ly, lz};
+    cdg_oracle::make_periodic(*static_cast<RefLevel*>(h)->level, period);
+    return 0;
+  } catch (const std::exception& e) {
+    copy_err(e, err, errn);
+    return 1;
+  }
+}
 
 // sizes: [0]=K [1]=n_basis [2]=n_cub [3]=n_face_quad [4]=block [5]=trace_block [6]=degree
 void ref_level_sizes(void* h, int* sizes) {

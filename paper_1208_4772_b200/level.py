@@ -60,10 +60,14 @@ def curved_geometry(nodes: np.ndarray, re: ReferenceElement):
     X = np.asarray(nodes, float)
     ng = re.n_face_quad
     K = X.shape[0]
-    Xt = [np.ascontiguousarray(X[..., i]) for i in range(3)]  # x_i at the collocation nodes [Kc, N_p]
+    # Every per-element quantity is computed by the same batched (stacked)
+    # routine whatever the batch: an element's geometry does not depend on
+    # which or how many elements are built with it (a shard's curved elements
+    # get bit-identical tables to the whole mesh's; tests/test_gpu_comm.py).
 
-    def fwd_at(dr, ds, dt):  # F[i][m] = dx_i/dr_m at the n points, [Kc, n] each (one GEMM per entry)
-        return [[Xt[i] @ d.T for d in (dr, ds, dt)] for i in range(3)]
+    def fwd_at(dr, ds, dt):  # F[i][m] = dx_i/dr_m at the n points, [Kc, n] each
+        dx = [np.matmul(d, X) for d in (dr, ds, dt)]  # stacked [Kc, n, 3] per m
+        return [[np.ascontiguousarray(dx[m][..., i]) for m in range(3)] for i in range(3)]
 
     F = fwd_at(re.deriv_r, re.deriv_s, re.deriv_t)
     # 3x3 determinant and inverse by cofactors, inv[m][i] = dr_m/dx_i
@@ -101,11 +105,13 @@ def curved_geometry(nodes: np.ndarray, re: ReferenceElement):
         face[:, sl, 0], face[:, sl, 1], face[:, sl, 2] = n0 / s, n1 / s, n2 / s
         face[:, sl, 3] = s * re.face_weights[None, :]
         area += (s * re.face_weights[None, :]).sum(axis=1)
-    # M_e = I_cub^T diag(J W) I_cub for every element as ONE GEMM: [Kc, N_cub] x [N_cub, N_p^2]
+    # M_e = I_cub^T diag(J W) I_cub, stacked per element (chunks bound the temporary)
     npb = re.n_basis
-    outer = (re.interp_cub[:, :, None] * re.interp_cub[:, None, :]).reshape(re.n_cub, npb * npb)
-    mass = (jw @ outer).reshape(K, npb, npb)
-    minv = np.linalg.inv(mass)
+    minv = np.empty((K, npb, npb))
+    it = re.interp_cub.T[None]
+    for c0 in range(0, K, 8192):
+        sl = slice(c0, min(K, c0 + 8192))
+        minv[sl] = np.linalg.inv(np.matmul(it * jw[sl, None, :], re.interp_cub))
     h = 6.0 * jw.sum(axis=1) / area
     return np.ascontiguousarray(jwr), np.ascontiguousarray(face), np.ascontiguousarray(minv), h, \
         np.ascontiguousarray(jac)

@@ -43,6 +43,7 @@ class Mesh:
     n_halo: int = 0                 # ghost elements appended after the owned ones
     global_ids: np.ndarray = None   # [K+halo] global element ids
     tags: list = field(default_factory=lambda: ["wall"])
+    period: tuple | None = None     # box lengths of a periodic mesh (faces wrap around)
 
     @property
     def n_elements(self) -> int:
@@ -112,8 +113,15 @@ def _perm_codes(p):
     return out
 
 
-def cube_mesh(n: int, scale: float = 1.0, k_range: tuple[int, int] | None = None) -> Mesh:
+def cube_mesh(n: int, scale: float = 1.0, k_range: tuple[int, int] | None = None,
+              periodic: bool = False) -> Mesh:
     """make_cube_mesh(n, "wall") (meshgen.cpp:41-88), optionally one z-slab.
+
+    ``periodic=True``: the same elements with every boundary face linked to its
+    translate on the opposite side of the box (no boundary faces; BASELINE
+    config 1's periodic domain). The Kuhn split is translation invariant, so
+    opposite boundary faces are congruent triangles and the face links (and
+    their vertex permutations) come from matching vertex ids modulo n.
 
     With ``k_range=(k0,k1)`` the mesh holds the owned elements of cells
     k0..k1-1 followed by the ghost elements of the neighbouring cell layers
@@ -137,6 +145,17 @@ def cube_mesh(n: int, scale: float = 1.0, k_range: tuple[int, int] | None = None
     k = vid // ((n + 1) ** 2)
     verts = np.stack([i / n, j / n, k / n], axis=1) * scale
     tets_all = _orient(verts, tets_all)
+    if periodic:
+        if k_range is not None or n < 3:
+            raise ValueError("periodic cube meshes: whole mesh, n >= 3")
+        vi = vid[tets_all]
+        canon = (vi % (n + 1)) % n + n * (((vi // (n + 1)) % (n + 1)) % n + n * ((vi // (n + 1) ** 2) % n))
+        nb, nf, pc = connectivity(canon)
+        assert np.all(nb >= 0)
+        K = tets_all.shape[0]
+        return Mesh(vertices=verts, tets=tets_all, neighbor=nb, neighbor_face=nf, perm_code=pc,
+                    boundary_tag=np.full((K, 4), -1, np.int8), n_owned=K, n_halo=0,
+                    global_ids=np.arange(K, dtype=np.int64), tags=[], period=(scale, scale, scale))
     per_layer = 6 * n * n
     first = (k0 - g0) * per_layer
     owned = slice(first, first + (k1 - k0) * per_layer)
