@@ -3,7 +3,7 @@ restatement ``oracle/cdg_oracle.c`` (built to oracle/_ref/libcdg_oracle.so).
 
 This is the checker the GPU parity tests compare against; it is validated
 against the real reference (oracle/_ref/libcdg_ref.so) in
-tests/test_oracle_vs_reference.py. The product never imports it.
+tests/test_oracle_port.py (golden vectors dumped from oracle/_ref). The product never imports it.
 """
 from __future__ import annotations
 

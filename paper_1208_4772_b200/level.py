@@ -14,7 +14,7 @@ operator matrices):
   symmetric face rules (quadrature.hpp:33-36) that pairing is the barycentric
   permutation induced by FaceLink.perm (mesh.hpp:23-27), so one table per
   vertex permutation replaces the per-face node_map (verified against the
-  reference's node_map in tests/test_level_vs_reference.py).
+  reference's node_map in tests/test_mesh_level.py and tests/test_gpu_curved.py).
 """
 from __future__ import annotations
 
