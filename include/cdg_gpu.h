@@ -130,6 +130,29 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc *desc, int device, cdg_gpu_lev
                          char *err, size_t errlen);
 void cdg_gpu_level_destroy(cdg_gpu_level *lv);
 
+/* Scalable setup for straight-sided meshes (replaces building the reference's
+ * DgLevel, solver.cpp:97-179, ~140 KB per element): the affine geometry and
+ * the perm-based face-node pairing are computed inside the library from the
+ * caller's Mesh (mesh.hpp:23-57) in O(K). `tables` supplies the reference-element
+ * tables, degree / sizes, padded, freestream (its geometry / coupling fields
+ * are ignored); `mesh` the connectivity. Equivalent to cdg_gpu_level_create
+ * with the reference's nearest-point node_map (conforming faces, symmetric
+ * face rules). */
+typedef struct cdg_gpu_mesh_desc {
+  int n_vertices;
+  const double *vertices;     /* [nv][3] Mesh::vertices */
+  int n_elements;             /* K owned elements */
+  int n_halo;                 /* ghost elements (multi-GPU shards), 0 otherwise */
+  const int *tets;            /* [K][4] Mesh::tets (reference vertex order) */
+  const int *neighbor;        /* [K][4] FaceLink.other.element, -1 on boundary faces */
+  const int *neighbor_face;   /* [K][4] FaceLink.other.local_face */
+  const int *face_perm;       /* [K][4][3] FaceLink.perm: other_face_vertex[perm[i]] == self_face_vertex[i] */
+  const int *bc;              /* [K][4] CDG_GPU_BC_* on boundary faces (BcMap of the face's tag) */
+  const double *face_nodes;   /* [N_g][3] ReferenceElement::face_nodes() of face 0 */
+} cdg_gpu_mesh_desc;
+int cdg_gpu_level_create_from_mesh(const cdg_gpu_level_desc *tables, const cdg_gpu_mesh_desc *mesh, int device,
+                                   cdg_gpu_level **out, char *err, size_t errlen);
+
 /* Sizes: [0]=K [1]=N_p [2]=N_cub [3]=N_g [4]=caller block [5]=caller trace
  * block [6]=device block [7]=n_halo. */
 void cdg_gpu_level_sizes(const cdg_gpu_level *lv, int *sizes);

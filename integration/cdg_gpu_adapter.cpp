@@ -187,6 +187,81 @@ cdg_gpu_level* create_level(const DgLevel& level, const ConservedState& fs, cons
   return lv;
 }
 
+// Straight-sided meshes: the level straight from the Mesh (no DgLevel) --
+// cdg_gpu_level_create_from_mesh computes the affine geometry and the
+// FaceLink.perm pairing in the library, O(K) and ~100 bytes per element, so
+// run_steady reaches the 4M-element configuration (DgLevel needs ~140 KB per
+// element at P=4, solver.cpp:97-179).
+cdg_gpu_level* create_level_from_mesh(const Mesh& mesh, const ReferenceElement& re, const BcMap& bc_map,
+                                      const ConservedState& fs, bool padded) {
+  const int K = mesh.n_elements(), ng = re.n_face_quad();
+  std::vector<double> icub = row_major(re.interp_cub()), ig = row_major(re.interp_face()),
+                      dr = row_major(re.deriv_r()), ds = row_major(re.deriv_s()),
+                      dt = row_major(re.deriv_t()), vinv = row_major(re.vandermonde_inv());
+  const std::vector<double> vcub = row_major(modal_basis_eval(re.degree(), re.cub_nodes()));
+  std::vector<double> verts(3 * mesh.vertices.size()), fnodes(3 * (size_t)ng);
+  for (size_t v = 0; v < mesh.vertices.size(); ++v)
+    verts[3 * v] = mesh.vertices[v].x, verts[3 * v + 1] = mesh.vertices[v].y, verts[3 * v + 2] = mesh.vertices[v].z;
+  for (int g = 0; g < ng; ++g)
+    fnodes[3 * g] = re.face_nodes()[g].x, fnodes[3 * g + 1] = re.face_nodes()[g].y, fnodes[3 * g + 2] = re.face_nodes()[g].z;
+  std::vector<int> tets(4 * (size_t)K), nb(4 * (size_t)K), nbf(4 * (size_t)K), perm(12 * (size_t)K), bc(4 * (size_t)K);
+  for (int e = 0; e < K; ++e)
+    for (int f = 0; f < 4; ++f) {
+      const size_t i4 = 4 * (size_t)e + f;
+      tets[i4] = mesh.tets[e][f];
+      if (mesh.links[e][f]) {
+        const FaceLink& l = *mesh.links[e][f];
+        nb[i4] = l.other.element;
+        nbf[i4] = l.other.local_face;
+        for (int k = 0; k < 3; ++k) perm[3 * i4 + k] = l.perm[k];
+        bc[i4] = 0;
+      } else {
+        nb[i4] = -1;
+        nbf[i4] = 0;
+        perm[3 * i4] = 0, perm[3 * i4 + 1] = 1, perm[3 * i4 + 2] = 2;
+        const std::string& tag = mesh.boundary_faces[mesh.boundary_index[e][f]].tag;
+        int kind = -1;  // kind_for_tag (solver.cpp:136-140)
+        for (const auto& [name, k] : bc_map)
+          if (name == tag) {
+            kind = static_cast<int>(k);
+            break;
+          }
+        if (kind < 0) throw ConfigError("no boundary condition configured for mesh tag '" + tag + "'");
+        bc[i4] = kind;
+      }
+    }
+  cdg_gpu_level_desc d{};
+  d.degree = re.degree();
+  d.n_basis = re.n_basis();
+  d.n_cub = re.n_cub();
+  d.n_face_quad = ng;
+  d.padded = padded ? 1 : 0;
+  d.interp_cub = icub.data();
+  d.interp_face = ig.data();
+  d.deriv_r = dr.data();
+  d.deriv_s = ds.data();
+  d.deriv_t = dt.data();
+  d.cub_weights = re.cub_weights().data();
+  d.face_weights = re.face_weights().data();
+  d.vandermonde_inv = vinv.data();
+  d.modal_cub = vcub.data();
+  for (int c = 0; c < 5; ++c) d.freestream[c] = fs[c];
+  cdg_gpu_mesh_desc md{};
+  md.n_vertices = static_cast<int>(mesh.vertices.size());
+  md.vertices = verts.data();
+  md.n_elements = K;
+  md.tets = tets.data();
+  md.neighbor = nb.data();
+  md.neighbor_face = nbf.data();
+  md.face_perm = perm.data();
+  md.bc = bc.data();
+  md.face_nodes = fnodes.data();
+  cdg_gpu_level* lv = nullptr;
+  char err[512] = {0};
+  throw_status(cdg_gpu_level_create_from_mesh(&d, &md, adapter_device(), &lv, err, sizeof err), err);
+  return lv;
+}
+
 cdg_gpu_run_config to_cfg(const RunConfig& cfg) {
   cdg_gpu_run_config c{};
   if (cfg.riemann == "llf")
@@ -265,8 +340,10 @@ void rk_step(const DgLevel& level, SolutionStore& u, SolutionStore& res, const R
 }
 
 // run_steady (solver.cpp:594-676) with every level device-resident. Host work
-// per level is the reference's: build the DgLevel (setup tables), then one
-// cdg_gpu_run_level_live call; rows reach on_row live, at each check iteration.
+// per level: the level setup (straight meshes: in the library from the Mesh,
+// O(K); curved meshes: the reference's DgLevel for the curved geometry), then
+// one cdg_gpu_run_level_live call; rows reach on_row live, at each check
+// iteration.
 SteadyResult run_steady(const CurvedMesh& cmesh, const BcMap& bc_map, const RunConfig& cfg,
                         const ConservedState& freestream, const std::function<void(const ConvergenceRow&)>& on_row) {
   if (cfg.p_schedule.empty()) throw ConfigError("run_steady: empty p-schedule");
@@ -281,11 +358,19 @@ SteadyResult run_steady(const CurvedMesh& cmesh, const BcMap& bc_map, const RunC
   for (size_t li = 0; li < cfg.p_schedule.size(); ++li) {
     const int p = cfg.p_schedule[li];
     auto re = level_reference_element(cmesh, p, cfg);
-    DgLevel level(cmesh, re, bc_map, cfg.padded);
-    std::vector<char> mask(level.n_elements());
-    for (int e = 0; e < level.n_elements(); ++e) mask[e] = cmesh.is_curved(e) ? 1 : 0;
-    std::unique_ptr<cdg_gpu_level, void (*)(cdg_gpu_level*)> lv(create_level(level, freestream, mask),
-                                                                cdg_gpu_level_destroy);
+    // straight-sided meshes: the level straight from the Mesh (scalable
+    // setup); curved meshes: the reference's DgLevel supplies the per-node
+    // geometry of the curved elements (compute_mapping, operators.cpp:32-121)
+    std::unique_ptr<DgLevel> level;
+    std::unique_ptr<cdg_gpu_level, void (*)(cdg_gpu_level*)> lv(nullptr, cdg_gpu_level_destroy);
+    if (cmesh.n_curved() == 0) {
+      lv.reset(create_level_from_mesh(cmesh.mesh(), *re, bc_map, freestream, cfg.padded));
+    } else {
+      level = std::make_unique<DgLevel>(cmesh, re, bc_map, cfg.padded);
+      std::vector<char> mask(level->n_elements());
+      for (int e = 0; e < level->n_elements(); ++e) mask[e] = cmesh.is_curved(e) ? 1 : 0;
+      lv.reset(create_level(*level, freestream, mask));
+    }
     if (li == 0) {
       throw_status(cdg_gpu_fill_freestream(lv.get()), "fill_freestream failed");
     } else {
@@ -330,7 +415,7 @@ SteadyResult run_steady(const CurvedMesh& cmesh, const BcMap& bc_map, const RunC
       result.converged = converged != 0;
       if (sp.fixed_iterations > 0 && !result.log.empty())
         result.converged = result.log.back().residual < cfg.final_tolerance;
-      result.solution = level.make_store();
+      result.solution = SolutionStore(cmesh.mesh().n_elements(), re->n_basis(), cfg.padded);
       throw_status(cdg_gpu_get_state(lv.get(), result.solution.raw().data(), nullptr), "get_state failed");
     }
     result.final_degree = p;

@@ -1163,6 +1163,142 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
   return CDG_GPU_OK;
 }
 
+// Scalable level setup from the mesh itself (the C++ caller's Mesh /
+// FaceLink, mesh.hpp:23-57): the compact affine geometry (compute_mapping,
+// operators.cpp:32-121, for a straight tet: one metric, Jacobian and normal
+// per element / face) and the face-node pairing from FaceLink.perm (one table
+// per vertex permutation; on conforming faces with the symmetric face rules it
+// equals the reference's nearest-point node_map, solver.cpp:144-172) -- O(K),
+// ~100 bytes per element, instead of DgLevel's ~140 KB per element and
+// O(K N_g^2) pairing.
+int cdg_gpu_level_create_from_mesh(const cdg_gpu_level_desc* tables, const cdg_gpu_mesh_desc* m, int device,
+                                   cdg_gpu_level** out, char* err, size_t errlen) {
+  *out = nullptr;
+  cdg_gpu_level_desc d = *tables;
+  std::vector<double> metric, jac, normal, sjac, h;
+  std::vector<int> nb, nbf, bc, code, cmap;
+  const int st = guarded(err, errlen, [&] {
+    static const double TV[4][3] = {{-1, -1, -1}, {1, -1, -1}, {-1, 1, -1}, {-1, -1, 1}};  // refelem.hpp
+    static const int FV[4][3] = {{0, 2, 1}, {0, 1, 3}, {1, 2, 3}, {0, 3, 2}};             // reference face order
+    static const int PERMS[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+    const int K = m->n_elements, ng = tables->n_face_quad;
+    if (K < 1 || !m->vertices || !m->tets || !m->neighbor || !m->neighbor_face || !m->face_perm || !m->bc ||
+        !m->face_nodes)
+      throw Status(CDG_GPU_ERR_CONFIG, "level_create_from_mesh: incomplete mesh descriptor");
+    double wc = 0.0, wf = 0.0;
+    for (int q = 0; q < tables->n_cub; ++q) wc += tables->cub_weights[q];
+    for (int g = 0; g < ng; ++g) wf += tables->face_weights[g];
+    metric.resize((size_t)K * 9), jac.resize(K), normal.resize((size_t)K * 12), sjac.resize((size_t)K * 4),
+        h.resize(K), nb.resize((size_t)K * 4), nbf.resize((size_t)K * 4), bc.resize((size_t)K * 4),
+        code.resize((size_t)K * 4);
+    for (int e = 0; e < K; ++e) {
+      const int* t = m->tets + (size_t)e * 4;
+      double f[3][3];  // f[i][m] = dx_i/dr_m
+      for (int v = 0; v < 4; ++v)
+        if (t[v] < 0 || t[v] >= m->n_vertices) throw Status(CDG_GPU_ERR_CONFIG, "tet vertex index out of range");
+      const double* x0 = m->vertices + (size_t)t[0] * 3;
+      for (int mm = 0; mm < 3; ++mm) {
+        const double* x1 = m->vertices + (size_t)t[mm + 1] * 3;
+        for (int i = 0; i < 3; ++i) f[i][mm] = 0.5 * (x1[i] - x0[i]);
+      }
+      const double c00 = f[1][1] * f[2][2] - f[1][2] * f[2][1], c01 = f[1][2] * f[2][0] - f[1][0] * f[2][2],
+                   c02 = f[1][0] * f[2][1] - f[1][1] * f[2][0];
+      const double J = f[0][0] * c00 + f[0][1] * c01 + f[0][2] * c02;
+      if (!(J > 1e-14))
+        throw Status(CDG_GPU_ERR_NUMERICS, "inverted element " + std::to_string(e) + ": mapping Jacobian " +
+                                               std::to_string(J) + " at quadrature node 0");
+      const double inv[3][3] = {{c00 / J, (f[0][2] * f[2][1] - f[0][1] * f[2][2]) / J, (f[0][1] * f[1][2] - f[0][2] * f[1][1]) / J},
+                                {c01 / J, (f[0][0] * f[2][2] - f[0][2] * f[2][0]) / J, (f[0][2] * f[1][0] - f[0][0] * f[1][2]) / J},
+                                {c02 / J, (f[0][1] * f[2][0] - f[0][0] * f[2][1]) / J, (f[0][0] * f[1][1] - f[0][1] * f[1][0]) / J}};
+      for (int mm = 0; mm < 3; ++mm)
+        for (int i = 0; i < 3; ++i) metric[(size_t)e * 9 + mm * 3 + i] = inv[mm][i];
+      jac[e] = J;
+      double area = 0.0;
+      for (int fc = 0; fc < 4; ++fc) {
+        double xa[3], xb[3];
+        for (int i = 0; i < 3; ++i) {
+          xa[i] = xb[i] = 0.0;
+          for (int mm = 0; mm < 3; ++mm) {
+            xa[i] += f[i][mm] * 0.5 * (TV[FV[fc][1]][mm] - TV[FV[fc][0]][mm]);
+            xb[i] += f[i][mm] * 0.5 * (TV[FV[fc][2]][mm] - TV[FV[fc][0]][mm]);
+          }
+        }
+        const double n[3] = {xa[1] * xb[2] - xa[2] * xb[1], xa[2] * xb[0] - xa[0] * xb[2], xa[0] * xb[1] - xa[1] * xb[0]};
+        const double s = std::sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]);
+        for (int i = 0; i < 3; ++i) normal[(size_t)e * 12 + fc * 3 + i] = n[i] / s;
+        sjac[(size_t)e * 4 + fc] = s;
+        area += s * wf;
+        const size_t i4 = (size_t)e * 4 + fc;
+        nb[i4] = m->neighbor[i4];
+        nbf[i4] = nb[i4] >= 0 ? m->neighbor_face[i4] : 0;
+        bc[i4] = nb[i4] >= 0 ? 0 : m->bc[i4];
+        code[i4] = 0;
+        if (nb[i4] >= 0) {
+          const int* pm = m->face_perm + i4 * 3;
+          int c = -1;
+          for (int k = 0; k < 6; ++k)
+            if (PERMS[k][0] == pm[0] && PERMS[k][1] == pm[1] && PERMS[k][2] == pm[2]) c = k;
+          if (c < 0) throw Status(CDG_GPU_ERR_CONFIG, "face_perm is not a permutation of (0, 1, 2)");
+          code[i4] = c;
+        }
+      }
+      h[e] = 6.0 * J * wc / area;  // ElementGeometry::h() = 6V/A (operators.hpp:37)
+    }
+    // node maps per permutation: barycentric coordinates of face 0's rule on its
+    // vertices (A, B, C) = TV[0], TV[2], TV[1]; x = A + u (B - A) + v (C - A)
+    std::vector<double> lam((size_t)ng * 3);
+    {
+      const double* A = TV[FV[0][0]];
+      const double* B = TV[FV[0][1]];
+      const double* Cc = TV[FV[0][2]];
+      double e1[3], e2[3];
+      for (int i = 0; i < 3; ++i) e1[i] = B[i] - A[i], e2[i] = Cc[i] - A[i];
+      const double a11 = e1[0] * e1[0] + e1[1] * e1[1] + e1[2] * e1[2], a12 = e1[0] * e2[0] + e1[1] * e2[1] + e1[2] * e2[2],
+                   a22 = e2[0] * e2[0] + e2[1] * e2[1] + e2[2] * e2[2], det = a11 * a22 - a12 * a12;
+      for (int g = 0; g < ng; ++g) {
+        double r[3];
+        for (int i = 0; i < 3; ++i) r[i] = m->face_nodes[g * 3 + i] - A[i];
+        const double b1 = r[0] * e1[0] + r[1] * e1[1] + r[2] * e1[2], b2 = r[0] * e2[0] + r[1] * e2[1] + r[2] * e2[2];
+        const double u = (a22 * b1 - a12 * b2) / det, v = (a11 * b2 - a12 * b1) / det;
+        lam[g * 3 + 0] = 1.0 - u - v, lam[g * 3 + 1] = u, lam[g * 3 + 2] = v;
+      }
+    }
+    cmap.resize((size_t)6 * ng);
+    for (int k = 0; k < 6; ++k)
+      for (int g = 0; g < ng; ++g) {
+        double theirs[3];
+        for (int i = 0; i < 3; ++i) theirs[PERMS[k][i]] = lam[g * 3 + i];
+        int best_h = -1;
+        double best = 1e300;
+        for (int hh = 0; hh < ng; ++hh) {
+          double dd = 0.0;
+          for (int i = 0; i < 3; ++i) dd += (theirs[i] - lam[hh * 3 + i]) * (theirs[i] - lam[hh * 3 + i]);
+          if (dd < best) best = dd, best_h = hh;
+        }
+        if (std::sqrt(best) > 1e-10)
+          throw Status(CDG_GPU_ERR_CONFIG, "face rule is not invariant under the vertex permutation");
+        cmap[(size_t)k * ng + g] = best_h;
+      }
+    d.n_elements = K;
+    d.n_halo = m->n_halo;
+    d.metric = metric.data();
+    d.jac = jac.data();
+    d.face_normal = normal.data();
+    d.face_sjac = sjac.data();
+    d.h = h.data();
+    d.neighbor = nb.data();
+    d.neighbor_face = nbf.data();
+    d.bc = bc.data();
+    d.node_map = nullptr;
+    d.face_code = code.data();
+    d.code_node_map = cmap.data();
+    d.n_codes = 6;
+    d.n_curved = 0;
+  });
+  if (st != CDG_GPU_OK) return st;
+  return cdg_gpu_level_create(&d, device, out, err, errlen);
+}
+
 void cdg_gpu_level_destroy(cdg_gpu_level* lv) {
   if (!lv) return;
   cudaSetDevice(lv->device);

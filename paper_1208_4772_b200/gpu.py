@@ -67,6 +67,13 @@ class SteadyParams(C.Structure):
                 ("degree", C.c_int)]
 
 
+class MeshDesc(C.Structure):
+    """cdg_gpu_mesh_desc: the caller's Mesh for cdg_gpu_level_create_from_mesh."""
+    _fields_ = [("n_vertices", C.c_int), ("vertices", _dp), ("n_elements", C.c_int), ("n_halo", C.c_int),
+                ("tets", _ip), ("neighbor", _ip), ("neighbor_face", _ip), ("face_perm", _ip), ("bc", _ip),
+                ("face_nodes", _dp)]
+
+
 class LevelDesc(C.Structure):
     _fields_ = [("degree", C.c_int), ("n_basis", C.c_int), ("n_cub", C.c_int), ("n_face_quad", C.c_int),
                 ("n_elements", C.c_int), ("n_halo", C.c_int), ("padded", C.c_int),
@@ -137,6 +144,8 @@ def lib():
         L.cdg_gpu_p_refine_embed.argtypes = [vp, vp, _dp]
         L.cdg_gpu_run_level.argtypes = [vp, C.POINTER(RunConfig), C.POINTER(SteadyParams), _dp, C.c_int, _ip, _ip,
                                         C.c_char_p, C.c_size_t]
+        L.cdg_gpu_level_create_from_mesh.argtypes = [C.POINTER(LevelDesc), C.POINTER(MeshDesc), C.c_int,
+                                                     C.POINTER(vp), C.c_char_p, C.c_size_t]
         L.cdg_gpu_halo_define.argtypes = [vp, C.c_int, _ip, _ip, _ip, _ip, _ip]
         L.cdg_gpu_comm_unique_id.argtypes = [C.c_char_p, C.c_char_p, C.c_size_t]
         L.cdg_gpu_comm_create_nccl.argtypes = [vp, C.c_char_p, C.c_int, C.c_int, C.POINTER(vp), C.c_char_p,
@@ -222,6 +231,55 @@ class GpuLevel:
         self.K, self.n_basis, self.n_cub, self.n_face_quad = (int(x) for x in sz[:4])
         self.block, self.trace_block, self.device_block, self.n_halo = (int(x) for x in sz[4:])
         self.degree = p
+
+    @classmethod
+    def from_mesh(cls, mesh: Mesh, p: int, bc: int = 0, freestream=None, padded: bool = True, device: int = 0):
+        """Straight-sided level built INSIDE the library from the mesh
+        (cdg_gpu_level_create_from_mesh: affine geometry + perm-based pairing in
+        C++, the scalable setup a C++ caller gets without a DgLevel)."""
+        from .mesh import PERMS
+        self = cls.__new__(cls)
+        self.re = re = R.level_reference_element(p, False)
+        K = mesh.n_owned
+        t = {k: np.ascontiguousarray(getattr(re, k)) for k in
+             ("interp_cub", "interp_face", "deriv_r", "deriv_s", "deriv_t", "cub_weights", "face_weights",
+              "vandermonde_inv")}
+        t["modal_cub"] = np.ascontiguousarray(R.modal_basis_eval(re.degree, re.cub_nodes))
+        d = LevelDesc()
+        d.degree, d.n_basis, d.n_cub, d.n_face_quad = re.degree, re.n_basis, re.n_cub, re.n_face_quad
+        d.padded = int(padded)
+        d.interp_cub, d.interp_face = _p(t["interp_cub"]), _p(t["interp_face"])
+        d.deriv_r, d.deriv_s, d.deriv_t = _p(t["deriv_r"]), _p(t["deriv_s"]), _p(t["deriv_t"])
+        d.cub_weights, d.face_weights, d.vandermonde_inv = (_p(t["cub_weights"]), _p(t["face_weights"]),
+                                                             _p(t["vandermonde_inv"]))
+        d.modal_cub = _p(t["modal_cub"])
+        fs = np.zeros(5) if freestream is None else np.asarray(freestream, float)
+        for c in range(5):
+            d.freestream[c] = fs[c]
+        nb = np.ascontiguousarray(mesh.neighbor[:K], np.int32)
+        perm = np.asarray(PERMS, np.int32)[np.maximum(mesh.perm_code[:K], 0)]
+        arrs = dict(vertices=np.ascontiguousarray(mesh.vertices, np.float64),
+                    tets=np.ascontiguousarray(mesh.tets, np.int32), neighbor=nb,
+                    neighbor_face=np.ascontiguousarray(np.maximum(mesh.neighbor_face[:K], 0), np.int32),
+                    face_perm=np.ascontiguousarray(perm, np.int32),
+                    bc=np.ascontiguousarray(np.where(nb < 0, int(bc), 0), np.int32),
+                    face_nodes=np.ascontiguousarray(re.face_nodes[: re.n_face_quad], np.float64))
+        md = MeshDesc()
+        md.n_vertices, md.n_elements, md.n_halo = mesh.vertices.shape[0], K, mesh.n_halo
+        for k, a in arrs.items():
+            setattr(md, k, _p(a))
+        h = C.c_void_p()
+        err = C.create_string_buffer(1024)
+        _raise(lib().cdg_gpu_level_create_from_mesh(C.byref(d), C.byref(md), device, C.byref(h), err, 1024),
+               err.value.decode())
+        self.h, self._keep = h, (t, arrs, d, md)
+        self.arrays = None
+        sz = np.zeros(8, np.int32)
+        lib().cdg_gpu_level_sizes(self.h, _p(sz))
+        self.K, self.n_basis, self.n_cub, self.n_face_quad = (int(x) for x in sz[:4])
+        self.block, self.trace_block, self.device_block, self.n_halo = (int(x) for x in sz[4:])
+        self.degree = p
+        return self
 
     # -- lifecycle --------------------------------------------------------------
     def close(self):

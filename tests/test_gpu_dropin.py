@@ -55,3 +55,19 @@ def test_reference_acceptance_criteria_through_the_gpu_adapter(tmp_path):
     failed = re.findall(r"^\[FAIL\] C(\d+)", out, re.M)
     assert not failed, out[-3000:]
     assert sorted(int(c) for c in passed) == sorted(int(c) for c in crit), out[-3000:]
+
+
+def test_run_steady_at_headline_scale_through_the_dropin():
+    """The reference's make_cube_mesh(88) (4,088,832 tets) + cdg::run_steady at
+    P=4, resolved to the GPU adapter: straight-mesh levels come from
+    cdg_gpu_level_create_from_mesh, so the host never builds the ~570 GB
+    DgLevel (integration/run_steady_scale.cpp)."""
+    import json
+    exe = REF / "run_steady_gpu"
+    if not exe.exists():
+        pytest.skip("oracle/_ref/run_steady_gpu not built")
+    out = subprocess.run([str(exe), "88", "4", "10"], capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    assert d["elements"] == 6 * 88 ** 3 and d["rows"] == 2 and d["last_residual"] > 0
+    assert d["solution_values"] == d["elements"] * 5 * 48

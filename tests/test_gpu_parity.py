@@ -280,3 +280,26 @@ def test_viscous_rk_steps_inactive_is_bitwise_inviscid(gpu_lib):
         lv.rk_steps(cfg, 0.01, 3)
         outs.append(lv.get_state()[0])
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("p,riemann,bc", [(1, "llf", 1), (3, "hllc", 0), (4, "llf", 2), (5, "hllc", 1)])
+def test_level_from_mesh_matches_host_builder(gpu_lib, p, riemann, bc):
+    """cdg_gpu_level_create_from_mesh (geometry + pairing computed in C++ from
+    the Mesh / FaceLink.perm) == the host-built level, and == the oracle."""
+    from paper_1208_4772_b200 import mesh as M_
+    gpu = gpu_lib
+    m = M_.cube_mesh(4)
+    fs = gpu.make_state(1.0, [0.3, 0.1, -0.05], 1.0)
+    a = gpu.GpuLevel(m, p, bc=bc, freestream=fs)
+    b = gpu.GpuLevel.from_mesh(m, p, bc=bc, freestream=fs)
+    u0 = gpu.random_admissible_store(a, seed=11)
+    cfg = gpu.run_config(riemann)
+    ra, rb = a.compute_rhs(cfg, u0), b.compute_rhs(cfg, u0)
+    assert np.max(np.abs(ra - rb)) / np.max(np.abs(ra)) < 1e-13
+    dt = 0.3 * a.compute_timestep(cfg)
+    assert b.compute_timestep(cfg) == pytest.approx(a.compute_timestep(cfg), rel=1e-14)
+    for lv in (a, b):
+        lv.set_state(u0)
+        lv.rk_steps(cfg, dt, 3)
+    ua, ub = a.get_state()[0], b.get_state()[0]
+    assert np.max(np.abs(ua - ub)) / np.max(np.abs(ua)) < 1e-13
