@@ -824,8 +824,8 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
     lv->caller_padded = d->padded != 0;
     lv->caller_block = lv->caller_padded ? pad16(lv->np) : lv->np;
     lv->caller_tblock = lv->caller_padded ? pad16(lv->nf) : lv->nf;
-    lv->bp = pad16(lv->np);
-    lv->tb = pad16(lv->nf);
+    lv->bp = dev_block(lv->np);  // device layout (cdg_kernels.cuh); the caller's is pad16 or unpadded
+    lv->tb = dev_block(lv->nf);
     const int np = lv->np, ncub = lv->ncub, nf = lv->nf, ng = lv->ng, K = lv->K;
 
     // ---- shared operators (operators.cpp:135-165, factored) ---------------

@@ -31,6 +31,15 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 
 __host__ __device__ constexpr int round_up(int x, int m) { return (x + m - 1) / m * m; }
+// Device row length of the state (u, res, rhs: N_p values) and of the face
+// traces (4 N_g values): the values rounded up to the 8-wide k-step of the
+// DMMA contractions (the padding columns hold exact zeros, so every A-fragment
+// load and every epilogue store of a k-step stays inside its own row). The
+// reference's SolutionStore pads to 16 (padded.hpp:12); that is the CALLER's
+// layout -- set/get_state convert (cudaMemcpy2D) -- while HBM holds the
+// tighter rows: P=4 40 instead of 48 doubles (-17% state traffic), P=3 24
+// instead of 32, P=1 8 instead of 16.
+__host__ __device__ constexpr int dev_block(int values) { return round_up(values, 8); }
 __host__ __device__ constexpr int ceil_div(int x, int m) { return (x + m - 1) / m; }
 // leading dimension >= n with ld % 16 in {4, 12}: conflict-free A-fragment
 // loads (8 rows x 4 consecutive doubles per warp)
@@ -50,8 +59,8 @@ struct Cfg {
   static constexpr int MINB = MINB_;              // resident CTAs per SM (launch bounds)
   static constexpr int R = 5 * E;                 // rows per tile
   static constexpr int MT = R / 16;               // m16 tiles per tile
-  static constexpr int BP = round_up(NP, 16);     // device SolutionStore block (pad16)
-  static constexpr int TB = round_up(NF, 16);     // device trace block (pad16)
+  static constexpr int BP = dev_block(NP);        // device SolutionStore block (see dev_block)
+  static constexpr int TB = dev_block(NF);        // device trace block
   static constexpr int KP = round_up(NP, 8);      // K of the node->point GEMMs (k8 steps)
   static constexpr int KS1 = KP / 8;
   static constexpr int NCUB8 = round_up(NCUB, 8);

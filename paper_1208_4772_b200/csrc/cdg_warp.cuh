@@ -38,8 +38,8 @@ struct WCfg {
   static constexpr int NP = NP_, NCUB = NCUB_, NG = NG_, NF = 4 * NG_;
   static constexpr int EW = 16;                    // elements per warp tile
   static constexpr int WARPS = WARPS_, MINB = MINB_;
-  static constexpr int BP = round_up(NP, 16);      // device SolutionStore block
-  static constexpr int TB = round_up(NF, 16);      // device trace block
+  static constexpr int BP = dev_block(NP);         // device SolutionStore block
+  static constexpr int TB = dev_block(NF);         // device trace block
   static constexpr int KP = round_up(NP, 8);       // K of the nodal->cubature GEMM
   static constexpr int KS1 = KP / 8;
   static constexpr int NT = round_up(NP, 8) / 8;   // n-tiles of the RHS

@@ -21,6 +21,17 @@
 #define CDG_P4_E 16
 #endif
 
+// <CH, FCH, CTAs/SM> of the P=4 curved-mesh row kernel (k_rhs_rowc)
+#ifndef CDG_P4C_CH
+#define CDG_P4C_CH 8
+#endif
+#ifndef CDG_P4C_FCH
+#define CDG_P4C_FCH 32
+#endif
+#ifndef CDG_P4C_MINB
+#define CDG_P4C_MINB 4
+#endif
+
 namespace cdg_gpu {
 
 std::vector<KernelSet> kernel_sets_p4() {
@@ -28,7 +39,7 @@ std::vector<KernelSet> kernel_sets_p4() {
       // default: row kernel with fused traces (the next stage's traces from its
       // epilogue), unrolled GEMM k-steps and fused-trace n-tile groups
       with_row<35, 70, 16, CDG_P4_CH, CDG_P4_FCH, CDG_P4_MINB, CDG_P4_MODE, CDG_P4_E>(make_set<35, 70, 16, 16, 24, 2, 64>()),
-      with_rowc<35, 70, 56, 8, 32, 4>(with_row<35, 70, 56, 8, 32, 4, 192>(make_set<35, 70, 56, 16, 24, 2>()))};
+      with_rowc<35, 70, 56, CDG_P4C_CH, CDG_P4C_FCH, CDG_P4C_MINB>(with_row<35, 70, 56, 8, 32, 4, 192>(make_set<35, 70, 56, 16, 24, 2>()))};
 }
 
 }  // namespace cdg_gpu

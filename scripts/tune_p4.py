@@ -17,7 +17,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent.parent
 
 
-def child(lib, n, steps, riemann, p):
+def child(lib, n, steps, riemann, p, curved=False):
     sys.path.insert(0, str(ROOT))
     import numpy as np
     import torch
@@ -27,7 +27,13 @@ def child(lib, n, steps, riemann, p):
     import bench
     re = R.get_reference_element(p)
     part = partition.rank_part(n, 1, 0)
-    lv = gpu.GpuLevel(part.mesh, p, bc=0, freestream=bench.freestream_state(), re=re)
+    if curved:  # every element curved by the smooth map (bench.py's curved block)
+        from paper_1208_4772_b200 import mesh as M
+        re = R.level_reference_element(p, True)
+        lv = gpu.GpuLevel(part.mesh, p, bc=0, freestream=bench.freestream_state(), re=re,
+                          curved=(np.arange(part.mesh.n_owned), M.warped_nodes(part.mesh, re)))
+    else:
+        lv = gpu.GpuLevel(part.mesh, p, bc=0, freestream=bench.freestream_state(), re=re)
     K, npb = lv.K, lv.n_basis
     g = np.random.default_rng(42)
     u = np.zeros((K, 5, lv.block))
@@ -51,14 +57,16 @@ def child(lib, n, steps, riemann, p):
     lv.rk_steps(cfg, dt, steps)
     lv.set_profiling(False)
     t_tr, t_rhs, nl = lv.last_profile()
-    F, _, _ = bench.model_flops_bytes(npb, re.n_cub, 4 * re.n_face_quad)
+    F, F_rhs, _ = bench.model_flops_bytes(npb, re.n_cub, 4 * re.n_face_quad)
+    if not lv.fused_traces():
+        F = F_rhs
     peak = max(gpu.measure_fp64_peak(0))
     rhs_ms = t_rhs / (5 * steps)
     uu = lv.get_state()[0]
     print(json.dumps({"lib": str(lib), "K": K, "ms_per_step": ms_step, "rhs_ms": rhs_ms,
                       "frac_graph": F * K / (ms_step / 5 * 1e-3) / 1e12 / peak,
                       "frac_rhs": F * K / (rhs_ms * 1e-3) / 1e12 / peak, "peak": peak,
-                      "checksum": float(np.sum(uu)), "fused": lv.fused_traces()}), flush=True)
+                      "checksum": float(np.sum(uu)), "fused": lv.fused_traces(), "trace_ms": t_tr / (5 * steps)}), flush=True)
 
 
 def main():
@@ -68,14 +76,15 @@ def main():
     ap.add_argument("--steps", type=int, default=6)
     ap.add_argument("--riemann", default="llf")
     ap.add_argument("--child", action="store_true")
+    ap.add_argument("--curved", action="store_true")
     ap.add_argument("libs", nargs="+")
     a = ap.parse_args()
     if a.child:
-        child(a.libs[0], a.n, a.steps, a.riemann, a.p)
+        child(a.libs[0], a.n, a.steps, a.riemann, a.p, a.curved)
         return
     for lib in a.libs:
         r = subprocess.run([sys.executable, __file__, "--child", "--n", str(a.n), "--p", str(a.p), "--steps",
-                            str(a.steps), "--riemann", a.riemann, lib], capture_output=True, text=True, timeout=900)
+                            str(a.steps), "--riemann", a.riemann, lib] + (["--curved"] if a.curved else []), capture_output=True, text=True, timeout=900)
         out = r.stdout.strip().splitlines()
         print(out[-1] if out else json.dumps({"lib": lib, "error": r.stderr[-800:]}), flush=True)
 
