@@ -12,7 +12,6 @@
 #include "cdg_row.cuh"
 #include "cdg_rowc.cuh"
 #include "cdg_warp.cuh"
-#include "cdg_ws.cuh"
 
 namespace cdg_gpu {
 
@@ -86,24 +85,6 @@ KernelSet with_row(KernelSet k) {
   k.row_e = RC::E;
   k.row_nth = RC::NTH;
   k.row_ft = RC::FT;
-  return k;
-}
-
-// warp-specialized affine kernel (cdg_ws.cuh) in the row kernel's slots: same
-// operator fragments (natural pairing, CH-node chunks), fused traces
-template <int NP, int NCUB, int NG, int CH = 8, int FCH = 32, int NFW = 4, int MINB = 2>
-KernelSet with_ws(KernelSet k) {
-  using WC = WsCfg<NP, NCUB, NG, CH, FCH, NFW, MINB>;
-  k.row_update[0] = &k_rhs_ws<WC, true, 0>;
-  k.row_update[1] = &k_rhs_ws<WC, true, 1>;
-  k.row_only[0] = &k_rhs_ws<WC, false, 0>;
-  k.row_only[1] = &k_rhs_ws<WC, false, 1>;
-  k.smem_row = WC::SMEM_BYTES;
-  k.row_minb = MINB;
-  k.row_ch = CH;
-  k.row_e = WC::E;
-  k.row_nth = WC::NTH;
-  k.row_ft = true;
   return k;
 }
 

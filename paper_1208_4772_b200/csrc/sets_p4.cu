@@ -21,21 +21,6 @@
 #define CDG_P4_E 16
 #endif
 
-// 1: the warp-specialized kernel (cdg_ws.cuh) in the row slots of the P=4
-// straight set, <FCH, flux warps, CTAs/SM>
-#ifndef CDG_P4_WS
-#define CDG_P4_WS 0
-#endif
-#ifndef CDG_P4_WS_FCH
-#define CDG_P4_WS_FCH 32
-#endif
-#ifndef CDG_P4_WS_NFW
-#define CDG_P4_WS_NFW 4
-#endif
-#ifndef CDG_P4_WS_MINB
-#define CDG_P4_WS_MINB 2
-#endif
-
 // <CH, FCH, CTAs/SM> of the P=4 curved-mesh row kernel (k_rhs_rowc)
 #ifndef CDG_P4C_CH
 #define CDG_P4C_CH 8
@@ -53,11 +38,7 @@ std::vector<KernelSet> kernel_sets_p4() {
   return {
       // default: row kernel with fused traces (the next stage's traces from its
       // epilogue), unrolled GEMM k-steps and fused-trace n-tile groups
-#if CDG_P4_WS
-      with_ws<35, 70, 16, 8, CDG_P4_WS_FCH, CDG_P4_WS_NFW, CDG_P4_WS_MINB>(make_set<35, 70, 16, 16, 24, 2, 64>()),
-#else
       with_row<35, 70, 16, CDG_P4_CH, CDG_P4_FCH, CDG_P4_MINB, CDG_P4_MODE, CDG_P4_E>(make_set<35, 70, 16, 16, 24, 2, 64>()),
-#endif
       with_rowc<35, 70, 56, CDG_P4C_CH, CDG_P4C_FCH, CDG_P4C_MINB>(with_row<35, 70, 56, 8, 32, 4, 192>(make_set<35, 70, 56, 16, 24, 2>()))};
 }
 
