@@ -87,6 +87,10 @@ def lib():
         L.ref_mesh_sphere_shell.restype = C.c_void_p
         L.ref_mesh_sphere_shell.argtypes = [C.c_double, C.c_double, C.c_int, C.c_int]
         L.ref_mesh_free.argtypes = [C.c_void_p]
+        L.ref_mesh_from_arrays.restype = C.c_void_p
+        L.ref_mesh_from_arrays.argtypes = [C.c_int, _dp, C.c_int, _ip, C.c_int, _ip, _ip, _ip, C.c_char_p, C.c_char_p,
+                                           C.c_size_t]
+        L.ref_mesh_set_curved.argtypes = [C.c_void_p, C.c_int, C.c_int, _ip, _dp, C.c_char_p, C.c_size_t]
         L.ref_mesh_sphere_curved.restype = C.c_void_p
         L.ref_mesh_sphere_curved.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_size_t]
         L.ref_level_nodes.argtypes = [C.c_void_p, _dp, _ip]
@@ -154,9 +158,21 @@ def refelem_tables(p, cub_override=0, face_override=0) -> dict:
 
 
 class Mesh:
-    def __init__(self, kind="cube", n=2, scale=1.0, sphere=(1.0, 8.0, 2, 5)):
+    def __init__(self, kind="cube", n=2, scale=1.0, sphere=(1.0, 8.0, 2, 5), arrays=None):
+        """arrays (kind "arrays"): dict(vertices, tets, bf_elem, bf_face, bf_tag, tags) -- any
+        mesh through the reference's build_connectivity (cases.py generators)."""
         L = lib()
-        if kind == "cube":
+        if kind == "arrays":
+            a = arrays
+            v = np.ascontiguousarray(a["vertices"], np.float64)
+            t = np.ascontiguousarray(a["tets"], np.int32)
+            be, bfc, bt = (np.ascontiguousarray(a[k], np.int32) for k in ("bf_elem", "bf_face", "bf_tag"))
+            err = C.create_string_buffer(512)
+            self.h = L.ref_mesh_from_arrays(len(v), _p(v), len(t), _p(t), len(be), _p(be), _p(bfc), _p(bt),
+                                            ",".join(a["tags"]).encode(), err, 512)
+            if not self.h:
+                raise RefError(3, err.value.decode())
+        elif kind == "cube":
             self.h = L.ref_mesh_cube(n, scale)
         elif kind == "single_tet":
             self.h = L.ref_mesh_single_tet()
@@ -175,6 +191,14 @@ class Mesh:
         sz = np.zeros(3, np.int32)
         L.ref_mesh_sizes(self.h, _p(sz))
         self.n_vertices, self.n_elements = int(sz[0]), int(sz[1])
+
+    def set_curved(self, degree: int, ids, nodes):
+        """CurvedMesh of `degree` with elements ids curved to nodes [n][N_p][3]."""
+        ids = np.ascontiguousarray(ids, np.int32)
+        x = np.ascontiguousarray(nodes, np.float64)
+        err = C.create_string_buffer(512)
+        if lib().ref_mesh_set_curved(self.h, degree, len(ids), _p(ids), _p(x), err, 512):
+            raise RefError(1, err.value.decode())
 
     def export(self) -> dict:
         nv, ne = self.n_vertices, self.n_elements

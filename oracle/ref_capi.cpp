@@ -171,6 +171,56 @@ void* ref_mesh_two_tets() {
   m->mesh = make_two_tets("wall");
   return m;
 }
+// Any tet mesh from arrays (the generators of paper_1208_4772_b200/cases.py:
+// cylinder, NACA0012): vertices [nv][3], tets [K][4] (positively oriented),
+// boundary faces [nb] (element, local face, tag index into the comma-separated
+// tag_names); connectivity by the reference's own build_connectivity
+// (mesh.cpp:26-84) after validate_mesh.
+void* ref_mesh_from_arrays(int nv, const double* verts, int K, const int* tets, int nb, const int* bf_elem,
+                           const int* bf_face, const int* bf_tag, const char* tag_names, char* err, size_t errn) {
+  try {
+    auto* m = new RefMesh;
+    std::vector<std::string> names;
+    {
+      std::string cur;
+      for (const char* c = tag_names; *c; ++c) {
+        if (*c == ',') names.push_back(cur), cur.clear();
+        else cur += *c;
+      }
+      names.push_back(cur);
+    }
+    for (int v = 0; v < nv; ++v) m->mesh.vertices.push_back({verts[3 * v], verts[3 * v + 1], verts[3 * v + 2]});
+    for (int e = 0; e < K; ++e) m->mesh.tets.push_back({tets[4 * e], tets[4 * e + 1], tets[4 * e + 2], tets[4 * e + 3]});
+    for (int i = 0; i < nb; ++i) m->mesh.boundary_faces.push_back({bf_elem[i], bf_face[i], names.at(bf_tag[i])});
+    validate_mesh(m->mesh);
+    build_connectivity(m->mesh);
+    return m;
+  } catch (const std::exception& e) {
+    copy_err(e, err, errn);
+    return nullptr;
+  }
+}
+// Curve elements of a mesh: nodes [n][N_p(degree)][3] are the physical
+// collocation nodes of element ids[i] at `degree` (CurvedMesh::set_curved,
+// curved_mesh.hpp:24); levels of other degrees re-evaluate the map
+// (element_nodes_for_degree).
+int ref_mesh_set_curved(void* h, int degree, int n, const int* ids, const double* nodes, char* err, size_t errn) {
+  try {
+    auto* m = static_cast<RefMesh*>(h);
+    m->curved = std::make_unique<CurvedMesh>(m->mesh, degree);
+    const int np = (degree + 1) * (degree + 2) * (degree + 3) / 6;
+    for (int i = 0; i < n; ++i) {
+      std::vector<Vec3> x(np);
+      for (int j = 0; j < np; ++j)
+        x[j] = {nodes[((size_t)i * np + j) * 3], nodes[((size_t)i * np + j) * 3 + 1], nodes[((size_t)i * np + j) * 3 + 2]};
+      m->curved->set_curved(ids[i], std::move(x));
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    copy_err(e, err, errn);
+    return 1;
+  }
+}
 // All boundary faces of the sphere shell get tag "wall" or "farfield" via the
 // reference tags "sphere"/"farfield".
 void* ref_mesh_sphere_shell(double r_in, double r_out, int subdiv, int layers) {
@@ -255,7 +305,8 @@ void* ref_level_create(void* mesh_h, int p, int bc_wall, int bc_far, int padded,
     auto re = level_reference_element(*lv->cmesh, p, cfg);
     const BcMap bcs = {{"wall", static_cast<BcKind>(bc_wall)},
                        {"sphere", static_cast<BcKind>(bc_wall)},
-                       {"farfield", static_cast<BcKind>(bc_far)}};
+                       {"farfield", static_cast<BcKind>(bc_far)},
+                       {"symmetry", BcKind::Symmetry}};
     lv->level = std::make_unique<DgLevel>(*lv->cmesh, re, bcs, padded != 0);
     lv->ws = make_workspace(*lv->level);
     return lv;
@@ -524,7 +575,8 @@ int ref_run_steady(void* mesh_h, int bc_wall, int bc_far, const ref_run_cfg* c, 
     const CurvedMesh cmesh = m->curved ? *m->curved : CurvedMesh(m->mesh, cfg.p_schedule.back());
     const BcMap bcs = {{"wall", static_cast<BcKind>(bc_wall)},
                        {"sphere", static_cast<BcKind>(bc_wall)},
-                       {"farfield", static_cast<BcKind>(bc_far)}};
+                       {"farfield", static_cast<BcKind>(bc_far)},
+                       {"symmetry", BcKind::Symmetry}};
     const SteadyResult r = run_steady(cmesh, bcs, cfg, to_state(freestream), nullptr);
     *n_rows = static_cast<int>(r.log.size());
     for (int i = 0; i < *n_rows && i < max_rows; ++i) {

@@ -70,3 +70,110 @@ def vortex_store(mesh: Mesh, re, block: int, t: float = 0.0, **kw) -> np.ndarray
     u = np.zeros((mesh.n_owned, 5, block))
     u[:, :, : re.n_basis] = np.transpose(s, (0, 2, 1))
     return u.reshape(-1)
+
+
+# ---------------------------------------------------------------------------
+# Configs 2 and 3: O-grids around a cylinder and a NACA0012 section, every
+# element curved (isoparametric) by the exact smooth map of the grid
+# ---------------------------------------------------------------------------
+def ogrid_mesh(n_xi: int, n_eta: int, n_z: int, mapping, tags=("wall", "farfield", "symmetry")):
+    """Structured O-grid in parameter space (xi periodic in [0, 1), eta in
+    [0, 1] from the body to the far field, zeta in [0, 1] across the span),
+    each cell split into the 6 Kuhn tets of make_cube_mesh (meshgen.cpp:41-88),
+    physical vertices X = mapping(xi, eta, zeta) (arrays). Returns (Mesh,
+    params [K, 4, 3]): the (unwrapped) parameters of each tet's vertices, from
+    which ``ogrid_nodes`` places the curved collocation nodes.
+    Boundary faces: eta = 0 -> tags[0] (body), eta = 1 -> tags[1] (far field),
+    zeta = 0 / 1 -> tags[2] (symmetry planes: a 2D flow in a 3D slab)."""
+    from .mesh import KUHN_TETS, Mesh, _orient, connectivity
+    ni, nj, nk = n_xi, n_eta + 1, n_z + 1
+    vid = lambda i, j, k: ((k * nj + j) * ni + (i % ni))  # noqa: E731  (xi wraps)
+    kk, jj, ii = np.meshgrid(np.arange(n_z), np.arange(n_eta), np.arange(n_xi), indexing="ij")
+    kk, jj, ii = kk.ravel(), jj.ravel(), ii.ravel()
+    corners = np.empty((kk.size, 8), np.int64)
+    cpar = np.empty((kk.size, 8, 3))
+    for b in range(8):
+        di, dj, dk = b & 1, (b >> 1) & 1, (b >> 2) & 1
+        corners[:, b] = vid(ii + di, jj + dj, kk + dk)
+        cpar[:, b] = np.stack([(ii + di) / n_xi, (jj + dj) / n_eta, (kk + dk) / n_z], axis=1)
+    tets = corners[:, KUHN_TETS].reshape(-1, 4)
+    par = cpar[:, KUHN_TETS].reshape(-1, 4, 3)
+    gi, gj, gk = np.meshgrid(np.arange(ni), np.arange(nj), np.arange(nk), indexing="ij")
+    order = np.argsort(((gk * nj + gj) * ni + gi).ravel())
+    P = np.stack([gi.ravel() / n_xi, gj.ravel() / n_eta, gk.ravel() / n_z], axis=1)[order]
+    verts = np.stack(mapping(P[:, 0], P[:, 1], P[:, 2]), axis=1)
+    t0 = tets.copy()
+    tets = _orient(verts, tets)
+    swapped = tets[:, 0] != t0[:, 0]
+    par[swapped, 0], par[swapped, 1] = par[swapped, 1].copy(), par[swapped, 0].copy()
+    nb, nf, pc = connectivity(tets)
+    K = tets.shape[0]
+    # boundary tag of each unmatched face from its vertices' parameters
+    from .mesh import FACE_VERTS_ARR
+    fpar = par[:, FACE_VERTS_ARR]  # [K, 4, 3 verts, 3]
+    bt = np.full((K, 4), -1, np.int8)
+    bnd = nb < 0
+    eta, zeta = fpar[..., 1], fpar[..., 2]
+    bt[bnd & np.all(eta < 1e-12, axis=2)] = 0
+    bt[bnd & np.all(eta > 1 - 1e-12, axis=2)] = 1
+    bt[bnd & (np.all(zeta < 1e-12, axis=2) | np.all(zeta > 1 - 1e-12, axis=2))] = 2
+    if np.any(bnd & (bt < 0)):
+        raise ValueError("ogrid_mesh: unclassified boundary face")
+    m = Mesh(vertices=verts, tets=tets, neighbor=nb, neighbor_face=nf, perm_code=pc, boundary_tag=bt, n_owned=K,
+             n_halo=0, global_ids=np.arange(K, dtype=np.int64), tags=list(tags))
+    return m, par
+
+
+def ogrid_nodes(params: np.ndarray, re, mapping) -> np.ndarray:
+    """Curved collocation nodes [K, N_p, 3]: the grid map applied to the
+    barycentric interpolation of each tet's vertex parameters (an exact
+    isoparametric description of the body, continuous across faces)."""
+    r = re.colloc_nodes
+    lam = np.stack([1.0 - (3.0 + r.sum(axis=1)) / 2.0, (1.0 + r[:, 0]) / 2.0, (1.0 + r[:, 1]) / 2.0,
+                    (1.0 + r[:, 2]) / 2.0], axis=1)  # [N_p, 4]
+    q = np.einsum("jv,kvd->kjd", lam, params)
+    return np.stack(mapping(q[..., 0], q[..., 1], q[..., 2]), axis=-1)
+
+
+def cylinder_map(r0=0.5, r1=10.0, height=1.0):
+    """BASELINE config 3: circular cylinder of radius r0, far field at r1
+    (geometric radial spacing), span `height`."""
+    def f(xi, eta, zeta):
+        r = r0 * (r1 / r0) ** eta
+        th = 2.0 * np.pi * xi
+        return r * np.cos(th), r * np.sin(th), height * zeta
+    return f
+
+
+def naca0012_map(r_far=8.0, height=0.25, beta=3.0, t=0.12):
+    """BASELINE config 2: NACA0012 section (closed trailing edge,
+    y_t = 5t(0.2969 sqrt(x) - 0.1260x - 0.3516x^2 + 0.2843x^3 - 0.1036x^4)),
+    xi = 0 at the trailing edge over the upper surface to the leading edge
+    (xi = 1/2) and back along the lower surface (cosine clustering at both
+    edges); linear blend to a far-field circle of radius r_far about the
+    mid-chord, exponential clustering of eta at the wall."""
+    def f(xi, eta, zeta):
+        x = 0.5 * (1.0 + np.cos(2.0 * np.pi * xi))
+        yt = 5.0 * t * (0.2969 * np.sqrt(np.maximum(x, 0.0)) - 0.1260 * x - 0.3516 * x ** 2 + 0.2843 * x ** 3
+                        - 0.1036 * x ** 4)
+        y = np.where(np.mod(xi, 1.0) <= 0.5, yt, -yt)
+        th = 2.0 * np.pi * xi
+        cx, cy = 0.5 + r_far * np.cos(th), r_far * np.sin(th)
+        s = np.expm1(beta * eta) / np.expm1(beta)
+        return x + s * (cx - x), y + s * (cy - y), height * zeta
+    return f
+
+
+def freestream(mach: float, alpha_deg: float = 0.0, rho: float = 1.0, p: float = 1.0, gamma: float = 1.4):
+    """FreestreamConfig::state (config.cpp:12-24): flow in the x-y plane."""
+    c = np.sqrt(gamma * p / rho)
+    a = np.radians(alpha_deg)
+    v = mach * c * np.array([np.cos(a), np.sin(a), 0.0])
+    return np.array([rho, rho * v[0], rho * v[1], rho * v[2], p / (gamma - 1.0) + 0.5 * rho * v.dot(v)])
+
+
+def reference_arrays(mesh) -> dict:
+    """The mesh as the oracle façade's ref_mesh_from_arrays wants it."""
+    e, f = np.nonzero(mesh.neighbor < 0)
+    return dict(vertices=mesh.vertices, tets=mesh.tets, bf_elem=e, bf_face=f,
+                bf_tag=mesh.boundary_tag[e, f].astype(np.int32), tags=mesh.tags)

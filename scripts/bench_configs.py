@@ -3,12 +3,14 @@ bench.py): the GPU path (device-resident cdg_gpu_rk_steps) against the
 reference's own rk_step (oracle/_ref, all host threads) on the SAME level and
 state. Writes one JSON object per config to stdout.
 
-  C1  make_cube_mesh(11) = 7,986 affine tets, P=3, LLF, farfield, smooth state
-      (test_solver.cpp:44-59) -- the "isentropic vortex, ~8k affine, P=3" slot
-  C2  curved sphere shell (make_sphere_shell_mesh(1,8,2,5) curved at P=4 by the
-      reference's elasticity pipeline, 40% curved), HLLC, Persson-Peraire AV
-      forced on -- the NACA0012 "curved P=4 + AV" kernel proxy
-  C3  the same curved sphere at P=1..6, LLF -- the cylinder P=1..6 slot
+  C1  isentropic vortex on the periodic box periodic_cube(11) = 7,986 affine
+      tets, P=3, LLF (cases.py; the reference's kernels on the same periodic
+      coupling, oracle/ref_periodic.cpp)
+  C2  NACA0012 O-grid (cases.naca0012_map), every element curved, P=4,
+      M=0.8, alpha=1.25 deg, HLLC, Persson-Peraire AV (ramp)
+  C3  cylinder O-grid (cases.cylinder_map), every element curved, M=0.3,
+      P=1..6, LLF
+  plus GPU-only lines of C2 / C3 at a GPU-filling size.
 
 usage: python scripts/bench_configs.py [--quick]
 """
@@ -90,36 +92,84 @@ def run(name, rm, rl, lv, cfg_g, cfg_r, fs, u, p, gpu_steps, cpu_steps, note):
     print(json.dumps(out), flush=True)
 
 
+def body_level(mapping, dims, p, fs, with_ref=True):
+    from paper_1208_4772_b200 import cases, refelem as R
+    m, par = cases.ogrid_mesh(*dims, mapping)
+    re = R.level_reference_element(p, True)
+    nodes = cases.ogrid_nodes(par, re, mapping)
+    rm = rl = None
+    if with_ref:
+        rm = ref.Mesh("arrays", arrays=cases.reference_arrays(m))
+        rm.set_curved(p, np.arange(m.n_owned), nodes)
+        rl = ref.Level(rm, p, bc_wall=0, bc_far=1)
+        nodes = rl.nodes()[0]
+    lv = gpu.GpuLevel(m, p, bc={"wall": "slip_wall", "farfield": "farfield", "symmetry": "symmetry"},
+                      freestream=fs, curved=(np.arange(m.n_owned), nodes), re=re)
+    return m, rm, rl, lv
+
+
+def gpu_only(name, lv, cfg, u, steps, note):
+    import torch
+    dt = 0.25 * lv.compute_timestep(gpu.run_config("llf"))
+    lv.set_state(u)
+    lv.rk_steps(cfg, dt, 2)
+    torch.cuda.synchronize()
+    ext = torch.cuda.ExternalStream(lv.stream())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(ext)
+    lv.rk_steps(cfg, dt, steps)
+    e1.record(ext)
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) * 1e-3 / steps
+    print(json.dumps({"config": name, "elements": lv.K, "p": lv.degree,
+                      "gpu_dof_updates_per_s": lv.K * lv.n_basis * 25 / t, "gpu_ms_per_step": t * 1e3,
+                      "note": note}), flush=True)
+
+
 def main():
+    from paper_1208_4772_b200 import cases
     ref.num_threads(0)
     nthreads = ref.num_threads(__import__("os").cpu_count() or 1)
-    fs = gpu.make_state(1.0, [0.4, 0.05, -0.1], 1.0)
-    # C1
-    rm = ref.Mesh("cube", 11)
-    rl = ref.Level(rm, 3, bc_wall=1, bc_far=1)
-    lv = gpu.GpuLevel(gpu_mesh(rm, ["wall", "farfield"]), 3, bc={"wall": 1, "farfield": 1}, freestream=fs)
-    run("C1 cube(11) P=3 LLF farfield smooth", rm, rl, lv, gpu.run_config("llf"), ref.make_cfg("llf"), fs,
-        smooth_state(rl), 3, 200, 3 if QUICK else 10, f"reference rk_step on {nthreads} host threads")
-    # C2 / C3: the curved sphere at P (sphere_m038-like freestream)
-    c = np.sqrt(1.4)
-    fs2 = gpu.make_state(1.0, [0.38 * c, 0.0, 0.0], 1.0)
-    visc = dict(enabled=True, eps0=0.3, kappa=4.0, s0_offset=-100.0)
-    for p in ([4] if QUICK else [1, 2, 3, 4, 5]):
-        rmc = ref.Mesh("sphere_curved", sphere=(2, 5, p, p))
-        rlc = ref.Level(rmc, p, bc_wall=0, bc_far=1)
-        nodes, curved = rlc.nodes()
-        ids = np.nonzero(curved)[0]
-        mesh = gpu_mesh(rmc, ["sphere", "farfield"])
-        lvc = gpu.GpuLevel(mesh, p, bc={"sphere": 0, "farfield": 1}, freestream=fs2, curved=(ids, nodes[ids]))
-        u = rlc.random_admissible_store(5)
-        run(f"C3 curved sphere P={p} LLF", rmc, rlc, lvc, gpu.run_config("llf"), ref.make_cfg("llf"), fs2, u, p,
-            100, 2 if QUICK else 5, f"{len(ids)} of {rlc.K} elements curved")
-        if p == 4:
-            run("C2 curved sphere P=4 HLLC + AV (NACA proxy)", rmc, rlc, lvc,
-                gpu.run_config("hllc", viscosity=visc), ref.make_cfg("hllc", viscosity=visc), fs2, u, p,
-                50, 2 if QUICK else 3, "AV forced on every element (s0_offset=-100): sensor + aux gradient + "
-                                       "viscous flux each stage")
-        lvc.close()
+    # C1: periodic isentropic vortex
+    L = 10.0
+    mv = cases.periodic_cube(11, L)
+    rm = ref.Mesh("cube", 11, scale=L)
+    rl = ref.Level(rm, 3, bc_wall=0, bc_far=1)
+    rl.make_periodic((L, L, L))
+    fsv = cases.freestream(0.0)
+    lv = gpu.GpuLevel(mv, 3, freestream=fsv)
+    run("C1 isentropic vortex, periodic_cube(11), P=3, LLF", rm, rl, lv, gpu.run_config("llf"), ref.make_cfg("llf"),
+        fsv, cases.vortex_store(mv, lv.re, lv.block), 3, 200, 3 if QUICK else 10,
+        f"reference rk_step on {nthreads} host threads, periodic coupling (oracle/ref_periodic.cpp)")
+    lv.close()
+    # C2: NACA0012, M=0.8, alpha=1.25, P=4 curved, HLLC + AV (ramp)
+    fs2 = cases.freestream(0.8, 1.25)
+    visc = dict(enabled=True, eps0=0.02, kappa=4.0, s0_offset=2.0)
+    m, rm, rl, lv = body_level(cases.naca0012_map(), (64, 12, 1), 4, fs2)
+    run("C2 NACA0012 O-grid, all curved, P=4, M=0.8 a=1.25, HLLC + AV ramp", rm, rl, lv,
+        gpu.run_config("hllc", viscosity=visc), ref.make_cfg("hllc", viscosity=visc), fs2,
+        rl.random_admissible_store(5), 4, 50, 2 if QUICK else 3, "Persson-Peraire sensor + aux gradient + viscous "
+                                                                "flux each stage")
+    lv.close()
+    # C3: cylinder, P = 1..6
+    fs3 = cases.freestream(0.3)
+    for p in ([4] if QUICK else [1, 2, 3, 4, 5, 6]):
+        m, rm, rl, lv = body_level(cases.cylinder_map(), (32, 8, 2), p, fs3)
+        run(f"C3 cylinder O-grid, all curved, P={p}, LLF", rm, rl, lv, gpu.run_config("llf"), ref.make_cfg("llf"),
+            fs3, rl.random_admissible_store(5), p, 100, 2 if QUICK else 5, f"{rl.K} curved elements")
+        lv.close()
+    # GPU-filling sizes (GPU only)
+    m, _, _, lv = body_level(cases.naca0012_map(), (256, 48, 4), 4, fs2, with_ref=False)
+    u = gpu.random_admissible_store(lv, 5)
+    gpu_only("C2 NACA0012 O-grid 256x48x4, P=4, HLLC + AV ramp", lv, gpu.run_config("hllc", viscosity=visc), u,
+             5, "all elements curved")
+    gpu_only("C2 NACA0012 O-grid 256x48x4, P=4, HLLC inviscid", lv, gpu.run_config("hllc"), u, 5,
+             "all elements curved")
+    lv.close()
+    m, _, _, lv = body_level(cases.cylinder_map(), (256, 48, 4), 4, fs3, with_ref=False)
+    gpu_only("C3 cylinder O-grid 256x48x4, P=4, LLF", lv, gpu.run_config("llf"), gpu.random_admissible_store(lv, 5),
+             5, "all elements curved")
+    lv.close()
 
 
 if __name__ == "__main__":
