@@ -323,6 +323,11 @@ int cdg_gpu_set_max_ctas(cdg_gpu_level *lv, int max_ctas);
 #define CDG_GPU_PATH_GENERIC 1
 int cdg_gpu_set_kernel_path(cdg_gpu_level *lv, int path);
 
+/* HLLC -> LLF fallbacks counted since the level was created (degenerate wave
+ * speed estimates or a non-finite contact speed; RhsWorkspace::hllc_fallbacks,
+ * solver.cpp:52,436, euler.cpp:99-110). */
+int cdg_gpu_hllc_fallbacks(cdg_gpu_level *lv, long long *count);
+
 /* CUDA stream (cudaStream_t) the level launches on. */
 void *cdg_gpu_stream(cdg_gpu_level *lv);
 /* Kernel launches issued by this level since creation (evidence counter). */

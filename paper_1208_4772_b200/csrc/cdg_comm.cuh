@@ -118,6 +118,7 @@ const cdg_gpu_level& halo_of(const cdg_gpu_level* lv) {
 // Exchange the rows every shard just packed into send[parity] (width W =
 // halo_width(what)); what == 1 also reduces the shards' max eps into their gate.
 void comm_exchange(cdg_gpu_comm* c, int what) {
+  NvtxRange nvtx_(what == 2 ? "halo exchange (q traces)" : what == 1 ? "halo exchange (traces + sqrt eps)" : "halo exchange (traces)");
   const int n = (int)c->lv.size();
   for (int r = 0; r < n; ++r) {
     CUDA_OK(cudaSetDevice(c->lv[r]->device));
@@ -197,6 +198,7 @@ void comm_check_errors(cdg_gpu_comm* c) {
 void comm_rk_steps(cdg_gpu_comm* c, const cdg_gpu_run_config* cfg, int nsteps, double dt, const double* a,
                    const double* b) {
   if (cfg->riemann != 0 && cfg->riemann != 1) throw Status(CDG_GPU_ERR_CONFIG, "unknown Riemann solver (llf|hllc)");
+  NvtxRange nvtx_("cdg_gpu_comm_rk_steps");
   const int n = (int)c->lv.size();
   auto each = [&](auto&& fn) {
     for (int r = 0; r < n; ++r) {

@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rhs_curved(CurvedParams cp) {
           record_error(p.err, 2, p.elem_offset + eg, f, gq, um.r);
         double fs[5];
         if (p.gas.riemann == 1)
-          hllc_flux_fast(um, up, fn.x, fn.y, fn.z, gamma, fs);
+          hllc_flux_fast(um, up, fn.x, fn.y, fn.z, gamma, fs, p.gas.hllc_fallbacks);
         else
           llf_flux(um, up, fn.x, fn.y, fn.z, gamma, fs);
         if (VISC) {

@@ -5,6 +5,7 @@
 // preparation restates operators.cpp:123-167 (mass matrix, stiffness and face
 // mass) in the factored, element-independent form the GPU kernels consume.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -24,6 +25,13 @@
 using namespace cdg_gpu;
 
 namespace {
+
+// NVTX ranges around the host entry points (a profiler attached via
+// NVTX_INJECTION64_PATH sees them; otherwise the calls are no-ops)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 struct Status : std::runtime_error {
   int code;
@@ -189,6 +197,7 @@ struct cdg_gpu_level {
   double *d_vcub = nullptr, *d_wcub = nullptr, *d_jac = nullptr, *d_curved_jac = nullptr;
   int* d_curved_slot = nullptr;
   unsigned long long* d_maxeps = nullptr;
+  unsigned long long* d_fallbacks = nullptr;  // HLLC -> LLF fallbacks (RhsWorkspace::hllc_fallbacks)
   bool last_viscous = false;
   // geometry / coupling
   double* metric = nullptr;
@@ -693,6 +702,7 @@ struct SteadyOps {
 int run_level_loop(const SteadyOps& ops, const cdg_gpu_run_config* cfg, const cdg_gpu_steady_params* sp,
                    cdg_gpu_row_fn on_row, void* user, double* rows, int max_rows, int* n_rows, int* converged,
                    char* err, size_t errlen) {
+  NvtxRange nvtx_("run_steady level");
   // Carpenter-Kennedy LSRK4(5) coefficients (rk.hpp:15-24)
   static const double A[5] = {0.0, -567301805773.0 / 1357537059087.0, -2404267990393.0 / 2016746695238.0,
                               -3550918686646.0 / 2091501179385.0, -1275806237668.0 / 842570457699.0};
@@ -1124,6 +1134,9 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
     CUDA_OK(cudaMemset(lv->eps, 0, K * sizeof(double)));
     CUDA_OK(cudaMemset(lv->sqrt_eps, 0, (K + lv->n_halo) * sizeof(double)));
     CUDA_OK(cudaMalloc(&lv->d_maxeps, sizeof(unsigned long long)));
+    CUDA_OK(cudaMalloc(&lv->d_fallbacks, sizeof(unsigned long long)));
+    CUDA_OK(cudaMemset(lv->d_fallbacks, 0, sizeof(unsigned long long)));
+    lv->gas.hllc_fallbacks = lv->d_fallbacks;
     CUDA_OK(cudaMalloc(&lv->d_coef, sizeof(StageCoef)));
     CUDA_OK(cudaMallocHost(&lv->h_coef, sizeof(StageCoef)));
     CUDA_OK(cudaMalloc(&lv->d_err, sizeof(DevError)));
@@ -1309,7 +1322,7 @@ void cdg_gpu_level_destroy(cdg_gpu_level* lv) {
   for (void* p : {(void*)lv->u, (void*)lv->res, (void*)lv->rhs, (void*)(lv->tbuf[1] ? lv->tbuf[0] : lv->traces), (void*)lv->before,
                   (void*)lv->q, (void*)lv->qtr, (void*)lv->qcub, (void*)lv->eps, (void*)lv->sqrt_eps, (void*)lv->d_vinv, (void*)lv->d_vcub, (void*)lv->d_wcub, (void*)lv->d_jac,
                   (void*)lv->d_curved_jac, (void*)lv->d_curved_slot,
-                  (void*)lv->d_maxeps, (void*)lv->metric, (void*)lv->face, (void*)lv->conn,
+                  (void*)lv->d_maxeps, (void*)lv->d_fallbacks, (void*)lv->metric, (void*)lv->face, (void*)lv->conn,
                   (void*)lv->code_map, (void*)lv->h, (void*)lv->frag_icub, (void*)lv->frag_op2,
                   (void*)lv->frag_ig, (void*)lv->frag_aux, (void*)lv->frag_dtil, (void*)lv->wfrag1, (void*)lv->wfrag2v, (void*)lv->wfrag2f, (void*)lv->rfrag2, (void*)lv->tbuf[1],
                   (void*)lv->curved_ids, (void*)lv->curved_jwr, (void*)lv->curved_minv, (void*)lv->frag_opc,
@@ -1409,6 +1422,7 @@ int cdg_gpu_interpolate_to_faces(cdg_gpu_level* lv, double* traces_out) {
 
 int cdg_gpu_compute_rhs(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, double* rhs_out, char* err,
                         size_t errlen) {
+  NvtxRange nvtx_("cdg_gpu_compute_rhs");
   return guarded(err, errlen, [&] {
     CUDA_OK(cudaSetDevice(lv->device));
     if (cfg->riemann != 0 && cfg->riemann != 1)
@@ -1429,6 +1443,7 @@ int cdg_gpu_compute_rhs(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, double
 
 int cdg_gpu_rk_steps(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, int nsteps, double dt,
                      const double a[5], const double b[5], char* err, size_t errlen) {
+  NvtxRange nvtx_("cdg_gpu_rk_steps");
   return guarded(err, errlen, [&] {
     CUDA_OK(cudaSetDevice(lv->device));
     if (cfg->riemann != 0 && cfg->riemann != 1)
@@ -1643,6 +1658,16 @@ int cdg_gpu_set_kernel_path(cdg_gpu_level* lv, int path) {
   return CDG_GPU_OK;
 }
 
+int cdg_gpu_hllc_fallbacks(cdg_gpu_level* lv, long long* count) {
+  return guarded(nullptr, 0, [&] {
+    CUDA_OK(cudaSetDevice(lv->device));
+    unsigned long long v = 0;
+    CUDA_OK(cudaMemcpyAsync(&v, lv->d_fallbacks, sizeof v, cudaMemcpyDeviceToHost, lv->stream));
+    CUDA_OK(cudaStreamSynchronize(lv->stream));
+    *count = (long long)v;
+  });
+}
+
 int cdg_gpu_set_profiling(cdg_gpu_level* lv, int enabled) {
   lv->profiling = enabled != 0;
   return CDG_GPU_OK;
@@ -1675,6 +1700,7 @@ int cdg_gpu_aux_gradient(cdg_gpu_level* lv, int m, double* q_out) {
 
 int cdg_gpu_timestep(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, int use_viscosity, double* dt_out,
                      char* err, size_t errlen) {
+  NvtxRange nvtx_("cdg_gpu_timestep");
   return guarded(err, errlen, [&] {
     if (cfg->cfl <= 0.0) throw Status(CDG_GPU_ERR_CONFIG, "compute_timestep: CFL must be positive");
     if (!lv->h) throw Status(CDG_GPU_ERR_CONFIG, "compute_timestep: level created without h");
@@ -1713,6 +1739,7 @@ int cdg_gpu_snapshot(cdg_gpu_level* lv) {
 }
 
 int cdg_gpu_residual(cdg_gpu_level* lv, int kind, double dt, double* out) {
+  NvtxRange nvtx_("cdg_gpu_residual");
   return guarded(nullptr, 0, [&] {
     if (!lv->before) throw Status(CDG_GPU_ERR_CONFIG, "residual: no snapshot taken");
     CUDA_OK(cudaSetDevice(lv->device));

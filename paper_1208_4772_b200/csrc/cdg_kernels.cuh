@@ -142,6 +142,7 @@ struct GasParams {
   double gamma;
   double fs[5];  // freestream
   int riemann;   // 0 llf, 1 hllc
+  unsigned long long* hllc_fallbacks;  // RhsWorkspace::hllc_fallbacks (solver.cpp:52,436), may be null
 };
 
 // ---------------------------------------------------------------------------
@@ -327,7 +328,8 @@ __device__ __forceinline__ void hllc_flux(const State5& um, const State5& up, do
 // reference divides at every use, euler.cpp:70-138; rounding differs at the
 // 1e-16 level, the branch structure and the LLF fallback are the same)
 __device__ __forceinline__ void hllc_flux_fast(const State5& um, const State5& up, double nx, double ny,
-                                               double nz, double g, double (&out)[5]) {
+                                               double nz, double g, double (&out)[5],
+                                               unsigned long long* fallbacks = nullptr) {
   const double il = 1.0 / um.r, ir = 1.0 / up.r;
   const double pl = (g - 1.0) * (um.E - 0.5 * il * (um.mx * um.mx + um.my * um.my + um.mz * um.mz));
   const double pr = (g - 1.0) * (up.E - 0.5 * ir * (up.mx * up.mx + up.my * up.my + up.mz * up.mz));
@@ -353,13 +355,15 @@ __device__ __forceinline__ void hllc_flux_fast(const State5& um, const State5& u
     s_left = fmin(unl - cl, un_roe - c_roe);
     s_right = fmax(unr + cr, un_roe + c_roe);
   }
-  if (!(s_left < s_right)) {
+  if (!(s_left < s_right)) {  // LLF fallback, counted (euler.cpp:99-102)
+    if (fallbacks) atomicAdd(fallbacks, 1ULL);
     llf_flux_fast(um, up, nx, ny, nz, g, out);
     return;
   }
   const double s_star = (pr - pl + um.r * unl * (s_left - unl) - up.r * unr * (s_right - unr)) /
                         (um.r * (s_left - unl) - up.r * (s_right - unr));
-  if (!isfinite(s_star)) {
+  if (!isfinite(s_star)) {  // (euler.cpp:106-109)
+    if (fallbacks) atomicAdd(fallbacks, 1ULL);
     llf_flux_fast(um, up, nx, ny, nz, g, out);
     return;
   }
@@ -826,7 +830,7 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs(RhsParams p) {
           record_error(p.err, 2, p.elem_offset + eg, f, gq, um.r);
         double fs[5];
         if (RM == 1 || (RM == -1 && p.gas.riemann == 1))
-          hllc_flux_fast(um, up, fn.x, fn.y, fn.z, gamma, fs);
+          hllc_flux_fast(um, up, fn.x, fn.y, fn.z, gamma, fs, p.gas.hllc_fallbacks);
         else
           llf_flux_fast(um, up, fn.x, fn.y, fn.z, gamma, fs);
         if (VISC) {

@@ -408,7 +408,7 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_row(RhsParams p) {
         if (!admissible(um, gamma) || !admissible(up, gamma)) record_error(p.err, 2, p.elem_offset + eg, f, gq, um.r);
         double fs[5];
         if (RM == 1)
-          hllc_flux_fast(um, up, fn.x, fn.y, fn.z, gamma, fs);
+          hllc_flux_fast(um, up, fn.x, fn.y, fn.z, gamma, fs, p.gas.hllc_fallbacks);
         else
           llf_flux_fast(um, up, fn.x, fn.y, fn.z, gamma, fs);
 #pragma unroll

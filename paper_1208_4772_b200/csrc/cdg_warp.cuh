@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(32 * C::WARPS, C::MINB) k_rhs_warp(WarpParams 
         }
         double fs[5];
         if (RIEMANN == 1)
-          hllc_flux_fast(um, up, fn.x, fn.y, fn.z, gamma, fs);
+          hllc_flux_fast(um, up, fn.x, fn.y, fn.z, gamma, fs, p.gas.hllc_fallbacks);
         else
           llf_flux_fast(um, up, fn.x, fn.y, fn.z, gamma, fs);
 #pragma unroll
