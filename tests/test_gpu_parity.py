@@ -303,3 +303,18 @@ def test_level_from_mesh_matches_host_builder(gpu_lib, p, riemann, bc):
         lv.rk_steps(cfg, dt, 3)
     ua, ub = a.get_state()[0], b.get_state()[0]
     assert np.max(np.abs(ua - ub)) / np.max(np.abs(ua)) < 1e-13
+
+
+def test_hllc_fallback_counter(gpu_lib):
+    """RhsWorkspace::hllc_fallbacks (solver.cpp:52,436): admissible states give
+    proper wave-speed bounds (s_L < s_R, finite s*), so no HLLC evaluation of an
+    ordinary flow falls back to LLF; the counter is cumulative per level."""
+    from paper_1208_4772_b200 import mesh as M_
+    gpu = gpu_lib
+    lv = gpu.GpuLevel(M_.cube_mesh(3), 4, bc=0, freestream=gpu.make_state(1.0, [0.3, 0.0, 0.0], 1.0))
+    assert lv.hllc_fallbacks() == 0
+    lv.set_state(gpu.random_admissible_store(lv, seed=2))
+    cfg = gpu.run_config("hllc")
+    lv.rk_steps(cfg, 0.2 * lv.compute_timestep(cfg), 3)
+    lv.compute_rhs(cfg)
+    assert lv.hllc_fallbacks() == 0
