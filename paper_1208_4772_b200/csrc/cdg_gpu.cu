@@ -416,7 +416,8 @@ void launch_curved(cdg_gpu_level* lv, bool update, int stage, int mode = 0) {
               : mode == 1 ? (update ? lv->ks->rowc_visc_update[rm] : lv->ks->rowc_visc_only[rm])
                           : (update ? lv->ks->rowc_update[rm] : lv->ks->rowc_only[rm]);
     const int tiles = cp.ctiles ? cp.n_clist : (lv->n_curved + lv->ks->rowc_e - 1) / lv->ks->rowc_e;
-    fr<<<lv->cap(tiles, lv->ks->rowc_minb), lv->ks->rowc_nth, lv->ks->smem_rowc,
+    fr<<<lv->cap(tiles, mode == 2 ? lv->ks->rowc_aux_minb : lv->ks->rowc_minb), lv->ks->rowc_nth,
+         mode == 2 ? lv->ks->smem_rowc_aux : lv->ks->smem_rowc,
          lv->stream>>>(cp);
     ++lv->launches;
     return;
@@ -1160,6 +1161,9 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
     if (lv->ks->warp_update[0])
       for (auto fn : {lv->ks->warp_update[0], lv->ks->warp_update[1], lv->ks->warp_only[0], lv->ks->warp_only[1]})
         CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lv->ks->smem_warp));
+    if (lv->n_curved && lv->ks->rowc_aux)
+      CUDA_OK(cudaFuncSetAttribute(lv->ks->rowc_aux, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)lv->ks->smem_rowc_aux));
     if (lv->n_curved)
       for (auto fn : {lv->ks->curved_update, lv->ks->curved_only, lv->ks->curved_visc_update,
                       lv->ks->curved_visc_only, lv->ks->aux_curved})

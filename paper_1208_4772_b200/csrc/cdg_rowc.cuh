@@ -32,17 +32,25 @@
 
 namespace cdg_gpu {
 
-template <class C>
+// NA = 1: one accumulator set (RHS); NA = 3: the aux gradient's three
+// directions q_0..q_2 in ONE pass -- three G panels (volume) and three face
+// panels share the U_cub chunk, the face gathers and every B fragment.
+template <class C, int NA = 1>
 struct RowCurvedLayout {
   static constexpr int LDV = C::KP + 1;  // vol panel [R][LDV] (aliases the work area)
-  static constexpr int WORK = C::WORK > C::R * LDV ? C::WORK : C::R * LDV;
+  static constexpr int VOLA = C::R * C::LDC + NA * C::R * C::LDG;
+  static constexpr int FACEA = NA * C::R * C::LDF;
+  static constexpr int W1 = VOLA > FACEA ? VOLA : FACEA;
+  static constexpr int W2 = C::WORK > W1 ? C::WORK : W1;
+  static constexpr int WORK = W2 > NA * C::R * LDV ? W2 : NA * C::R * LDV;  // NA vol panels in the epilogue
   static constexpr size_t SMEM_BYTES = sizeof(double) * WORK + sizeof(int) * (C::E + C::E * 4 * 2);
 };
 
 template <class C, bool UPDATE, int RM, int KIND = 0>
 __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_rowc(CurvedParams cp) {
-  using L = RowCurvedLayout<C>;
   constexpr bool VISC = KIND == 1, AUX = KIND == 2;
+  constexpr int NA = AUX ? 3 : 1;  // accumulator sets (AUX: q_0, q_1, q_2 in one pass)
+  using L = RowCurvedLayout<C, NA>;
   constexpr bool UPD = UPDATE && !AUX;
   const RhsParams& p = cp.base;
   if (gated_off(p.gate, p.gate_when)) return;
@@ -80,11 +88,34 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_rowc(CurvedParams cp) {
     const double* u_lo = p.u + (ok_lo ? (size_t)el_lo * 5 + lr_lo % 5 : 0) * C::BP + 2 * tq;
     const double* u_hi = p.u + (ok_hi ? (size_t)el_hi * 5 + lr_hi % 5 : 0) * C::BP + 2 * tq;
 
-#pragma unroll 1
-    for (int ma = 0; ma < (AUX ? 3 : 1); ++ma) {  // AUX: gradient direction m
-      double acc[C::NT2][4];
+    {
+      double acc[NA][C::NT2][4];
 #pragma unroll
-      for (int i = 0; i < C::NT2; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.0;
+      for (int a = 0; a < NA; ++a)
+#pragma unroll
+        for (int i = 0; i < C::NT2; ++i) acc[a][i][0] = acc[a][i][1] = acc[a][i][2] = acc[a][i][3] = 0.0;
+      // acc[a] += P_a[rows, 8 nks] Op^T over the NA panels P_a = panel + a * pstride:
+      // one B fragment load feeds NA MMAs
+      auto contract = [&](const double* panel, int ld, size_t pstride, int nks, int nks_full, const double2* fb2) {
+        auto kstep = [&](int ks) {
+          AFrag a[NA];
+#pragma unroll
+          for (int k = 0; k < NA; ++k) a[k] = load_afrag(panel + k * pstride, ld, warp * 16, ks * 8, g, tq);
+#pragma unroll
+          for (int nt = 0; nt < C::NT2; ++nt) {
+            const double2 b = __ldg(fb2 + (ks * C::NT2 + nt) * 32 + lane);
+#pragma unroll
+            for (int k = 0; k < NA; ++k) mma_frag(acc[k][nt], a[k], b);
+          }
+        };
+        if (nks == nks_full) {
+#pragma unroll
+          for (int ks = 0; ks < nks_full; ++ks) kstep(ks);
+        } else {
+#pragma unroll 1
+          for (int ks = 0; ks < nks; ++ks) kstep(ks);
+        }
+      };
 
       // ---- volume: chunks of CH cubature nodes ------------------------------
 #pragma unroll 1
@@ -134,12 +165,15 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_rowc(CurvedParams cp) {
               const double* met = cp.jwr + ((size_t)ce * C::NCUB + q) * 9;
               if (AUX) {
                 const double se = p.sqrt_eps[sId[e]];
+                const double uv[5] = {uc[0], uc[C::LDC], uc[2 * C::LDC], uc[3 * C::LDC], uc[4 * C::LDC]};
 #pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                  const double jk = __ldg(met + k * 3 + ma);
+                for (int ma = 0; ma < 3; ++ma)
 #pragma unroll
-                  for (int c = 0; c < 5; ++c) gout[k * w + c * C::LDG] = -se * (jk * uc[c * C::LDC]);
-                }
+                  for (int k = 0; k < 3; ++k) {
+                    const double jk = __ldg(met + k * 3 + ma);
+#pragma unroll
+                    for (int c = 0; c < 5; ++c) gout[ma * C::R * C::LDG + k * w + c * C::LDG] = -se * (jk * uv[c]);
+                  }
               } else {
                 const State5 s{uc[0], uc[C::LDC], uc[2 * C::LDC], uc[3 * C::LDC], uc[4 * C::LDC]};
                 if (!admissible(s, gamma)) record_error(p.err, 1, p.elem_offset + sId[e], q, 0, s.r);
@@ -168,27 +202,17 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_rowc(CurvedParams cp) {
               }
             } else {
 #pragma unroll
-              for (int m = 0; m < 3; ++m)
+              for (int a = 0; a < NA; ++a)
 #pragma unroll
-                for (int c = 0; c < 5; ++c) gout[m * w + c * C::LDG] = 0.0;
+                for (int m = 0; m < 3; ++m)
+#pragma unroll
+                  for (int c = 0; c < 5; ++c) gout[a * C::R * C::LDG + m * w + c * C::LDG] = 0.0;
             }
           }
         }
         __syncthreads();
-        {  // GEMM2 (volume part): acc += G[rows, 3w] [D^T chunk]; full chunks unrolled
-          auto kstep = [&](int ks) {
-            const AFrag a = load_afrag(sG, C::LDG, warp * 16, ks * 8, g, tq);
-#pragma unroll
-            for (int nt = 0; nt < C::NT2; ++nt) mma_frag(acc[nt], a, __ldg(fb2 + (ks * C::NT2 + nt) * 32 + lane));
-          };
-          if (w == C::CH) {
-#pragma unroll
-            for (int ks = 0; ks < 3 * C::CH / 8; ++ks) kstep(ks);
-          } else {
-#pragma unroll 1
-            for (int ks = 0; ks < (3 * w) / 8; ++ks) kstep(ks);
-          }
-        }
+        // GEMM2 (volume part): acc += G[rows, 3w] [D^T chunk]; full chunks unrolled
+        contract(sG, C::LDG, (size_t)C::R * C::LDG, (3 * w) / 8, 3 * C::CH / 8, fb2);
       }
       __syncthreads();  // the face phase reuses the volume buffers
 
@@ -208,7 +232,9 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_rowc(CurvedParams cp) {
           const int ce = c0 + e, eg = sId[e];
           if (ce >= cp.Kc || fl >= wr) {
 #pragma unroll
-            for (int c = 0; c < 5; ++c) gout[c * C::LDF] = 0.0;
+            for (int a = 0; a < NA; ++a)
+#pragma unroll
+              for (int c = 0; c < 5; ++c) gout[a * C::R * C::LDF + c * C::LDF] = 0.0;
             continue;
           }
           const int f = fq / C::NG, gq = fq - f * C::NG;
@@ -227,14 +253,17 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_rowc(CurvedParams cp) {
           }
           if (AUX) {
             // central trace average with per-side sqrt(eps) (solver.cpp:291-309),
-            // fed negated to the [D^T | -I_g^T] operator
+            // fed negated to the [D^T | -I_g^T] operator, for the three directions
             const double se = p.sqrt_eps[eg];
             const double snb = cw.x >= 0 ? p.sqrt_eps[cw.x] : se;
-            const double nm = ma == 0 ? fn.x : (ma == 1 ? fn.y : fn.z);
             const double umv[5] = {um.r, um.mx, um.my, um.mz, um.E};
             const double upv[5] = {up.r, up.mx, up.my, up.mz, up.E};
+            const double nrm[3] = {fn.x, fn.y, fn.z};
 #pragma unroll
-            for (int c = 0; c < 5; ++c) gout[c * C::LDF] = -fn.w * (0.5 * (se * umv[c] + snb * upv[c]) * nm);
+            for (int ma = 0; ma < 3; ++ma)
+#pragma unroll
+              for (int c = 0; c < 5; ++c)
+                gout[ma * C::R * C::LDF + c * C::LDF] = -fn.w * (0.5 * (se * umv[c] + snb * upv[c]) * nrm[ma]);
             continue;
           }
           if (!admissible(um, gamma) || !admissible(up, gamma)) record_error(p.err, 2, p.elem_offset + eg, f, gq, um.r);
@@ -266,34 +295,24 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_rowc(CurvedParams cp) {
           for (int c = 0; c < 5; ++c) gout[c * C::LDF] = fn.w * fs[c];
         }
         __syncthreads();
-        {
-          const double2* fb2 = fb2all + (size_t)((C::K2CUB + f0) / 8) * C::NT2 * 32;
-          auto kstep = [&](int ks) {
-            const AFrag a = load_afrag(sF, C::LDF, warp * 16, ks * 8, g, tq);
-#pragma unroll
-            for (int nt = 0; nt < C::NT2; ++nt) mma_frag(acc[nt], a, __ldg(fb2 + (ks * C::NT2 + nt) * 32 + lane));
-          };
-          if (wp == C::FCH) {
-#pragma unroll
-            for (int ks = 0; ks < C::FCH / 8; ++ks) kstep(ks);
-          } else {
-#pragma unroll 1
-            for (int ks = 0; ks < wp / 8; ++ks) kstep(ks);
-          }
-        }
+        contract(sF, C::LDF, (size_t)C::R * C::LDF, wp / 8, C::FCH / 8,
+                 fb2all + (size_t)((C::K2CUB + f0) / 8) * C::NT2 * 32);
         __syncthreads();  // sF is rewritten by the next chunk / the vol panel
       }
 
       // ---- epilogue: vol -> smem, M_e^-1 vol -> update / rhs / q_m ------------
-      double* sV = sWork;
+      double* sV = sWork;  // [NA][R][LDV]
 #pragma unroll
-      for (int nt = 0; nt < C::NT2; ++nt) {
-        const int col = nt * 8 + 2 * tq;
-        sV[lr_lo * L::LDV + col] = acc[nt][0];
-        sV[lr_lo * L::LDV + col + 1] = acc[nt][1];
-        sV[lr_hi * L::LDV + col] = acc[nt][2];
-        sV[lr_hi * L::LDV + col + 1] = acc[nt][3];
-      }
+      for (int a = 0; a < NA; ++a)
+#pragma unroll
+        for (int nt = 0; nt < C::NT2; ++nt) {
+          const int col = nt * 8 + 2 * tq;
+          double* va = sV + (size_t)a * C::R * L::LDV;
+          va[lr_lo * L::LDV + col] = acc[a][nt][0];
+          va[lr_lo * L::LDV + col + 1] = acc[a][nt][1];
+          va[lr_hi * L::LDV + col] = acc[a][nt][2];
+          va[lr_hi * L::LDV + col + 1] = acc[a][nt][3];
+        }
       __syncthreads();
       double a_c = 0.0, b_c = 0.0, dt = 0.0;
       if (UPD) {
@@ -302,9 +321,10 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_rowc(CurvedParams cp) {
         dt = p.coef->dt;
       }
       // one thread per (element, node i): out_f(i) = sum_j (M_e^-1)[i][j] vol_f(j)
-      // for the five fields. The column stream of M_e^-1 is software-pipelined
-      // in groups of MG (the next group's loads are in flight while the current
-      // one is consumed); res and u are loaded up front, before the sums.
+      // for the five fields (AUX: of the three directions, one column stream of
+      // M_e^-1). The column stream is software-pipelined in groups of MG (the
+      // next group's loads are in flight while the current one is consumed);
+      // res and u are loaded up front, before the sums.
       constexpr int MG = 7, NGR = ceil_div(C::NP, MG);
       for (int idx = tid; idx < C::E * C::NP; idx += C::NTH) {
         const int e = idx / C::NP, i = idx - e * C::NP;
@@ -324,7 +344,11 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_rowc(CurvedParams cp) {
             uo[f] = p.u[g0 + (size_t)f * C::BP];
           }
         }
-        double out[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+        double out[NA][5];
+#pragma unroll
+        for (int a = 0; a < NA; ++a)
+#pragma unroll
+          for (int f = 0; f < 5; ++f) out[a][f] = 0.0;
 #pragma unroll 1
         for (int gr = 0; gr < NGR; ++gr) {
           const int j0 = gr * MG;
@@ -338,7 +362,9 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_rowc(CurvedParams cp) {
           for (int k = 0; k < MG; ++k)
             if (j0 + k < C::NP)
 #pragma unroll
-              for (int f = 0; f < 5; ++f) out[f] += m[k] * v[f * L::LDV + j0 + k];
+              for (int a = 0; a < NA; ++a)
+#pragma unroll
+                for (int f = 0; f < 5; ++f) out[a][f] += m[k] * v[(size_t)a * C::R * L::LDV + f * L::LDV + j0 + k];
 #pragma unroll
           for (int k = 0; k < MG; ++k) m[k] = mn[k];
         }
@@ -346,17 +372,18 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_rowc(CurvedParams cp) {
         for (int f = 0; f < 5; ++f) {
           const size_t gi = g0 + (size_t)f * C::BP;
           if (AUX) {
-            cp.q_out[ma * qstride + gi] = out[f];
+#pragma unroll
+            for (int a = 0; a < NA; ++a) cp.q_out[a * qstride + gi] = out[a][f];
           } else if (UPD) {
-            const double rn = a_c * ro[f] + dt * out[f];
+            const double rn = a_c * ro[f] + dt * out[0][f];
             p.res[gi] = rn;
             p.u[gi] = uo[f] + b_c * rn;
           } else {
-            p.rhs_out[gi] = out[f];
+            p.rhs_out[gi] = out[0][f];
           }
         }
       }
-      __syncthreads();  // sWork is reused by the next pass / tile
+      __syncthreads();  // sWork is reused by the next tile
     }
   }
 }

@@ -48,7 +48,8 @@ struct KernelSet {
   void (*rowc_visc_update[2])(CurvedParams) = {nullptr, nullptr};
   void (*rowc_visc_only[2])(CurvedParams) = {nullptr, nullptr};
   void (*rowc_aux)(CurvedParams) = nullptr;
-  size_t smem_rowc = 0;
+  size_t smem_rowc = 0, smem_rowc_aux = 0;
+  int rowc_aux_minb = 0;
   int rowc_minb = 0, rowc_ch = 0, rowc_e = 16, rowc_nth = 160;
 };
 
@@ -63,7 +64,12 @@ KernelSet with_rowc(KernelSet k) {
   k.rowc_visc_update[1] = &k_rhs_rowc<RC, true, 1, 1>;
   k.rowc_visc_only[0] = &k_rhs_rowc<RC, false, 0, 1>;
   k.rowc_visc_only[1] = &k_rhs_rowc<RC, false, 1, 1>;
-  k.rowc_aux = &k_rhs_rowc<RC, false, 0, 2>;
+  // aux gradient: the three directions in one pass (3 accumulator sets, 3x the
+  // panels) at 2 CTAs/SM
+  using RCA = RCfg<NP, NCUB, NG, CH, FCH, 2, MODE, E>;
+  k.rowc_aux = &k_rhs_rowc<RCA, false, 0, 2>;
+  k.smem_rowc_aux = RowCurvedLayout<RCA, 3>::SMEM_BYTES;
+  k.rowc_aux_minb = 2;
   k.smem_rowc = RowCurvedLayout<RC>::SMEM_BYTES;
   k.rowc_minb = MINB;
   k.rowc_ch = CH;
