@@ -120,8 +120,8 @@ def near_freestream(K, block, npb, fs, seed, amp=0.02):
 
 def gpu_only(name, lv, cfg, u, steps, note):
     import torch
-    dt = 0.25 * lv.compute_timestep(gpu.run_config("llf"))
     lv.set_state(u)
+    dt = 0.25 * lv.compute_timestep(gpu.run_config("llf"))
     lv.rk_steps(cfg, dt, 2)
     torch.cuda.synchronize()
     ext = torch.cuda.ExternalStream(lv.stream())
@@ -138,6 +138,8 @@ def gpu_only(name, lv, cfg, u, steps, note):
 
 def main():
     from paper_1208_4772_b200 import cases
+    if "--large-only" in sys.argv:
+        return large()
     ref.num_threads(0)
     nthreads = ref.num_threads(__import__("os").cpu_count() or 1)
     # C1: periodic isentropic vortex
@@ -169,7 +171,14 @@ def main():
             fs3, near_freestream(rl.K, rl.block, rl.n_basis, fs3, 5), p, 100, 2 if QUICK else 5,
             f"{rl.K} curved elements")
         lv.close()
-    # GPU-filling sizes (GPU only)
+    large()
+
+
+def large():
+    """C2 / C3 at GPU-filling sizes (GPU only)."""
+    from paper_1208_4772_b200 import cases
+    fs2, fs3 = cases.freestream(0.8, 1.25), cases.freestream(0.3)
+    visc = dict(enabled=True, eps0=0.02, kappa=4.0, s0_offset=2.0)
     m, _, _, lv = body_level(cases.naca0012_map(), (256, 48, 4), 4, fs2, with_ref=False)
     u = near_freestream(lv.K, lv.block, lv.n_basis, fs2, 5)
     gpu_only("C2 NACA0012 O-grid 256x48x4, P=4, HLLC + AV ramp", lv, gpu.run_config("hllc", viscosity=visc), u,
