@@ -190,6 +190,9 @@ struct cdg_gpu_level {
   long long launches = 0;
   // state
   double *u = nullptr, *res = nullptr, *rhs = nullptr, *traces = nullptr, *before = nullptr;
+  double* stage = nullptr;  // host <-> device layout conversion (copy_rows), caller layout
+  size_t stage_n = 0;
+  int stage_d2h_block = 0;  // caller row length of the last device->host staging (0: re-zero first)
   // viscous workspace
   double *q = nullptr, *qtr = nullptr, *qcub = nullptr, *eps = nullptr, *sqrt_eps = nullptr;
   double* d_vinv = nullptr;
@@ -1161,9 +1164,14 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
     if (lv->ks->warp_update[0])
       for (auto fn : {lv->ks->warp_update[0], lv->ks->warp_update[1], lv->ks->warp_only[0], lv->ks->warp_only[1]})
         CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lv->ks->smem_warp));
-    if (lv->n_curved && lv->ks->rowc_aux)
+    if (lv->n_curved && lv->ks->rowc_aux) {
       CUDA_OK(cudaFuncSetAttribute(lv->ks->rowc_aux, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)lv->ks->smem_rowc_aux));
+      for (auto fn : {lv->ks->rowc_update[0], lv->ks->rowc_update[1], lv->ks->rowc_only[0], lv->ks->rowc_only[1],
+                      lv->ks->rowc_visc_update[0], lv->ks->rowc_visc_update[1], lv->ks->rowc_visc_only[0],
+                      lv->ks->rowc_visc_only[1]})
+        CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lv->ks->smem_rowc));
+    }
     if (lv->n_curved)
       for (auto fn : {lv->ks->curved_update, lv->ks->curved_only, lv->ks->curved_visc_update,
                       lv->ks->curved_visc_only, lv->ks->aux_curved})
@@ -1326,7 +1334,7 @@ void cdg_gpu_level_destroy(cdg_gpu_level* lv) {
   for (void* p : {(void*)lv->u, (void*)lv->res, (void*)lv->rhs, (void*)(lv->tbuf[1] ? lv->tbuf[0] : lv->traces), (void*)lv->before,
                   (void*)lv->q, (void*)lv->qtr, (void*)lv->qcub, (void*)lv->eps, (void*)lv->sqrt_eps, (void*)lv->d_vinv, (void*)lv->d_vcub, (void*)lv->d_wcub, (void*)lv->d_jac,
                   (void*)lv->d_curved_jac, (void*)lv->d_curved_slot,
-                  (void*)lv->d_maxeps, (void*)lv->d_fallbacks, (void*)lv->metric, (void*)lv->face, (void*)lv->conn,
+                  (void*)lv->d_maxeps, (void*)lv->d_fallbacks, (void*)lv->stage, (void*)lv->metric, (void*)lv->face, (void*)lv->conn,
                   (void*)lv->code_map, (void*)lv->h, (void*)lv->frag_icub, (void*)lv->frag_op2,
                   (void*)lv->frag_ig, (void*)lv->frag_aux, (void*)lv->frag_dtil, (void*)lv->wfrag1, (void*)lv->wfrag2v, (void*)lv->wfrag2f, (void*)lv->rfrag2, (void*)lv->tbuf[1],
                   (void*)lv->curved_ids, (void*)lv->curved_jwr, (void*)lv->curved_minv, (void*)lv->frag_opc,
@@ -1359,14 +1367,49 @@ void cdg_gpu_level_sizes(const cdg_gpu_level* lv, int* s) {
 void* cdg_gpu_stream(cdg_gpu_level* lv) { return lv->stream; }
 long long cdg_gpu_launch_count(const cdg_gpu_level* lv) { return lv->launches; }
 
+// Row copy between the caller's layout and the device rows. Host <-> device
+// with different row lengths goes through a device staging buffer in the
+// CALLER's layout (one contiguous PCIe transfer + a pitched device-to-device
+// copy) -- a pitched copy straight from pageable host memory moves row by row.
+// The staging buffer is zeroed once and only its value columns are ever
+// written, so the caller's padding stays exactly zero.
 static void copy_rows(cdg_gpu_level* lv, double* dst, int dst_block, const double* src, int src_block,
                       int values, int rows, cudaMemcpyKind kind) {
   if (dst_block == src_block) {
     CUDA_OK(cudaMemcpyAsync(dst, src, (size_t)rows * src_block * sizeof(double), kind, lv->stream));
-  } else {
-    CUDA_OK(cudaMemcpy2DAsync(dst, dst_block * sizeof(double), src, src_block * sizeof(double),
-                              values * sizeof(double), rows, kind, lv->stream));
+    return;
   }
+  if (kind == cudaMemcpyHostToDevice || kind == cudaMemcpyDeviceToHost) {
+    const int cb = kind == cudaMemcpyHostToDevice ? src_block : dst_block;  // caller's row length
+    const size_t need = (size_t)rows * cb;
+    if (lv->stage_n < need) {
+      if (lv->stage) cudaFree(lv->stage);
+      lv->stage = nullptr;
+      lv->stage_n = 0;
+      CUDA_OK(cudaMalloc(&lv->stage, need * sizeof(double)));
+      lv->stage_n = need;
+      lv->stage_d2h_block = 0;
+    }
+    if (kind == cudaMemcpyHostToDevice) {
+      lv->stage_d2h_block = 0;
+      CUDA_OK(cudaMemcpyAsync(lv->stage, src, need * sizeof(double), kind, lv->stream));
+      CUDA_OK(cudaMemcpy2DAsync(dst, dst_block * sizeof(double), lv->stage, cb * sizeof(double),
+                                values * sizeof(double), rows, cudaMemcpyDeviceToDevice, lv->stream));
+    } else {
+      // the caller's padding columns must read back as zeros: re-zero when the
+      // staging buffer last held another layout or a host upload
+      if (lv->stage_d2h_block != cb) {
+        CUDA_OK(cudaMemsetAsync(lv->stage, 0, need * sizeof(double), lv->stream));
+        lv->stage_d2h_block = cb;
+      }
+      CUDA_OK(cudaMemcpy2DAsync(lv->stage, cb * sizeof(double), src, src_block * sizeof(double),
+                                values * sizeof(double), rows, cudaMemcpyDeviceToDevice, lv->stream));
+      CUDA_OK(cudaMemcpyAsync(dst, lv->stage, need * sizeof(double), kind, lv->stream));
+    }
+    return;
+  }
+  CUDA_OK(cudaMemcpy2DAsync(dst, dst_block * sizeof(double), src, src_block * sizeof(double),
+                            values * sizeof(double), rows, kind, lv->stream));
 }
 
 int cdg_gpu_set_state(cdg_gpu_level* lv, const double* u, const double* res) {
