@@ -1167,10 +1167,6 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
     if (lv->n_curved && lv->ks->rowc_aux) {
       CUDA_OK(cudaFuncSetAttribute(lv->ks->rowc_aux, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)lv->ks->smem_rowc_aux));
-      for (auto fn : {lv->ks->rowc_update[0], lv->ks->rowc_update[1], lv->ks->rowc_only[0], lv->ks->rowc_only[1],
-                      lv->ks->rowc_visc_update[0], lv->ks->rowc_visc_update[1], lv->ks->rowc_visc_only[0],
-                      lv->ks->rowc_visc_only[1]})
-        CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lv->ks->smem_rowc));
     }
     if (lv->n_curved)
       for (auto fn : {lv->ks->curved_update, lv->ks->curved_only, lv->ks->curved_visc_update,

@@ -79,13 +79,8 @@ struct RCfg {
   static constexpr int OPF = (FCH / 8) * NT2 * 64;
   static constexpr int OPB = !OPRING ? 0 : (OPV > OPF ? OPV : OPF);
   static constexpr int NCHT = NCH + NFCH;  // operator chunks per tile
-  // 2048: accumulator stash during the face fluxes ([NT2*4][NTH] doubles,
-  // thread-private): the Riemann solves run without the 4*NT2 accumulators live
-  static constexpr bool STASH = MODE_ & 2048;
-  static constexpr int STASH_N = STASH ? NT2 * 4 * NTH : 0;
-  static constexpr size_t SMEM_BYTES =
-      sizeof(double) * ((size_t)WORK + UPANEL + 2 * OPB + E * 9 + E * 4 * 4 + STASH_N) + sizeof(int) * (E * 4 * 2) +
-      2 * sizeof(unsigned long long);
+  static constexpr size_t SMEM_BYTES = sizeof(double) * ((size_t)WORK + UPANEL + 2 * OPB + E * 9 + E * 4 * 4) +
+                                       sizeof(int) * (E * 4 * 2) + 2 * sizeof(unsigned long long);
 };
 
 // ---- bulk-copy (TMA engine) + mbarrier helpers -----------------------------
@@ -157,7 +152,6 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_row(RhsParams p) {
   double4* sFace = reinterpret_cast<double4*>(sMet + C::E * 9);    // [E][4]
   int2* sConn = reinterpret_cast<int2*>(sFace + C::E * 4);         // [E][4]
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(sConn + C::E * 4);  // [2]
-  double* sStash = reinterpret_cast<double*>(bars + 2);           // [NT2*4][NTH] (C::STASH)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, tq = lane & 3;
@@ -370,21 +364,6 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_row(RhsParams p) {
 
     // ---- surface: chunks of FCH face nodes -------------------------------------
     double* sF = sWork;
-    auto stash = [&](bool store) {
-      if constexpr (C::STASH) {
-#pragma unroll
-        for (int nt = 0; nt < C::NT2; ++nt)
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            double& s_ = sStash[(nt * 4 + k) * C::NTH + tid];
-            if (store)
-              s_ = acc[nt][k];
-            else
-              acc[nt][k] = s_;
-          }
-      }
-    };
-    stash(true);
     // this thread's epilogue res values -> smem while the face phase runs
     double* sRes = sWork + C::R * C::LDF + tid * (2 * C::NT2 * 2);
     if (UPDATE && C::RESS) {
@@ -442,7 +421,6 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_row(RhsParams p) {
         fence_proxy_async();
         issue_op_chunk<C>(n + 1, sOp, bars, p.frag_icub, p.frag_op2);
       }
-      stash(false);
       {
         const double2* fb2;
         if (C::OPRING) {
@@ -472,10 +450,7 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_row(RhsParams p) {
         }
       }
       ++n;
-      if (fc + 1 < C::NFCH) {
-        stash(true);
-        __syncthreads();
-      }
+      if (fc + 1 < C::NFCH) __syncthreads();
     }
     if (UPDATE && C::RESS) cp_async_wait0();
     if (UPDATE && !C::UREG && !C::USMEM) load_u();  // old u for the update

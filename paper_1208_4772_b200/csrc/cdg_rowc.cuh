@@ -30,10 +30,6 @@
 #include "cdg_curved.cuh"
 #include "cdg_row.cuh"
 
-#ifndef CDG_ROWC_STASH
-#define CDG_ROWC_STASH 0
-#endif
-
 namespace cdg_gpu {
 
 // NA = 1: one accumulator set (RHS); NA = 3: the aux gradient's three
@@ -47,11 +43,7 @@ struct RowCurvedLayout {
   static constexpr int W1 = VOLA > FACEA ? VOLA : FACEA;
   static constexpr int W2 = C::WORK > W1 ? C::WORK : W1;
   static constexpr int WORK = W2 > NA * C::R * LDV ? W2 : NA * C::R * LDV;  // NA vol panels in the epilogue
-  // accumulator stash of the face phase ([NT2*4][NTH], thread-private): the
-  // accumulators leave the registers while the Riemann solves run
-  static constexpr bool STASH = CDG_ROWC_STASH && NA == 1;
-  static constexpr int STASH_N = STASH ? C::NT2 * 4 * C::NTH : 0;
-  static constexpr size_t SMEM_BYTES = sizeof(double) * (WORK + STASH_N) + sizeof(int) * (C::E + C::E * 4 * 2);
+  static constexpr size_t SMEM_BYTES = sizeof(double) * WORK + sizeof(int) * (C::E + C::E * 4 * 2);
 };
 
 template <class C, bool UPDATE, int RM, int KIND = 0>
@@ -64,8 +56,7 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_rowc(CurvedParams cp) {
   if (gated_off(p.gate, p.gate_when)) return;
   extern __shared__ __align__(16) double smem[];
   double* sWork = smem;
-  double* sStash = sWork + L::WORK;                          // [NT2*4][NTH] (L::STASH)
-  int2* sConn = reinterpret_cast<int2*>(sStash + L::STASH_N);  // [E][4]
+  int2* sConn = reinterpret_cast<int2*>(sWork + L::WORK);  // [E][4]
   int* sId = reinterpret_cast<int*>(sConn + C::E * 4);     // [E] element ids of the tile
   __shared__ int s_stop;
 
@@ -227,21 +218,6 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_rowc(CurvedParams cp) {
 
       // ---- surface: chunks of FCH face nodes ---------------------------------
       double* sF = sWork;
-      auto stash = [&](bool store) {
-        if constexpr (L::STASH) {
-#pragma unroll
-          for (int nt = 0; nt < C::NT2; ++nt)
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              double& s_ = sStash[(nt * 4 + k) * C::NTH + tid];
-              if (store)
-                s_ = acc[0][nt][k];
-              else
-                acc[0][nt][k] = s_;
-            }
-        }
-      };
-      stash(true);
 #pragma unroll 1
       for (int fc = 0; fc < C::NFCH; ++fc) {
         const int f0 = fc * C::FCH;
@@ -319,10 +295,8 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_rowc(CurvedParams cp) {
           for (int c = 0; c < 5; ++c) gout[c * C::LDF] = fn.w * fs[c];
         }
         __syncthreads();
-        stash(false);
         contract(sF, C::LDF, (size_t)C::R * C::LDF, wp / 8, C::FCH / 8,
                  fb2all + (size_t)((C::K2CUB + f0) / 8) * C::NT2 * 32);
-        if (fc + 1 < C::NFCH) stash(true);
         __syncthreads();  // sF is rewritten by the next chunk / the vol panel
       }
 
