@@ -134,3 +134,33 @@ def test_comm_numerics_error_reaches_caller(gpu_lib):
     with pytest.raises(gpu.NumericsError, match="inadmissible"):
         comm.rk_steps(gpu.run_config("llf"), 1e-3, 1)
     comm.close()
+
+
+def test_comm_nccl_single_rank_matches_level(gpu_lib):
+    """The NCCL transport's plumbing on a one-GPU box: libnccl.so.2 resolved
+    at run time, unique id, a 1-rank communicator over a whole-mesh shard
+    (no peers), the all-reduces of the viscous gate, dt, residual and the
+    error flag. Bitwise equal to the level's own rk_steps / run_level."""
+    gpu = gpu_lib
+    fs = gpu.make_state(1.0, [0.3, 0.1, 0.0], 1.0)
+    g = M.cube_mesh(4)
+    a = gpu.GpuLevel(g, 3, bc=1, freestream=fs)
+    b = gpu.GpuLevel(g, 3, bc=1, freestream=fs)
+    u0 = gpu.random_admissible_store(a, seed=9)
+    b.halo_define([])
+    comm = gpu.GpuComm.nccl(b, gpu.GpuComm.unique_id(), 0, 1)
+    for visc in (None, FORCED):
+        cfg = gpu.run_config("hllc", viscosity=visc)
+        for lv in (a, b):
+            lv.set_state(u0)
+        dt = 0.1 * a.compute_timestep(gpu.run_config("hllc"))
+        assert comm.compute_timestep(gpu.run_config("hllc")) == a.compute_timestep(gpu.run_config("hllc"))
+        a.rk_steps(cfg, dt, 2)
+        comm.rk_steps(cfg, dt, 2)
+        assert np.array_equal(a.get_state()[0], b.get_state()[0])
+    sp = gpu.SteadyParams(20, -1, 10, 1, 1e-30, 0.0, 3)
+    cfg = gpu.run_config("llf", cfl=0.3)
+    rows_a, _ = a.run_level(cfg, sp)
+    rows_b, _ = comm.run_level(cfg, sp)
+    assert np.allclose(rows_a, rows_b, rtol=1e-13, atol=0)  # l2 residual: the same partial sums
+    comm.close()
