@@ -333,7 +333,11 @@ void launch_traces(cdg_gpu_level* lv, const double* u, double* traces) {
   ++lv->launches;
 }
 
-bool fused_traces(const cdg_gpu_level* lv) { return lv->use_row && lv->ks->row_ft && lv->n_curved == 0; }
+// the RHS kernel of the level writes the next stage's traces (row kernel with
+// MODE 32, or the warp-tile kernel); curved levels use the trace kernel
+bool fused_traces(const cdg_gpu_level* lv) {
+  return lv->n_curved == 0 && ((lv->use_row && lv->ks->row_ft) || (!lv->use_row && lv->use_warp));
+}
 
 void ensure_tbuf(cdg_gpu_level* lv) {
   if (lv->tbuf[1]) return;
@@ -455,6 +459,8 @@ void launch_rhs_warp(cdg_gpu_level* lv, bool update, int stage) {
   w.tiles = affine_tiles(lv, &w.n_list);
   w.gate = lv->cur_gate;
   w.gate_when = lv->cur_gate_when;
+  w.traces_out = lv->cur_traces_out;
+  w.frag_ig_nat = reinterpret_cast<const double2*>(lv->frag_ig);
   const int tiles = w.tiles ? w.n_list : (lv->K + 15) / 16;
   if (tiles == 0) {
     launch_curved(lv, update, stage);
@@ -760,7 +766,7 @@ int run_level_loop(const SteadyOps& ops, const cdg_gpu_run_config* cfg, const cd
 extern "C" {
 
 int cdg_gpu_fused_traces(const cdg_gpu_level* lv) {
-  return (lv->use_row && lv->ks->row_ft && lv->n_curved == 0) ? 1 : 0;
+  return fused_traces(lv) ? 1 : 0;
 }
 
 const char* cdg_gpu_version(void) { return "cdg_gpu 0.1 (sm_100a, fp64 DMMA)"; }
@@ -839,7 +845,7 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
     lv->caller_block = lv->caller_padded ? pad16(lv->np) : lv->np;
     lv->caller_tblock = lv->caller_padded ? pad16(lv->nf) : lv->nf;
     lv->bp = dev_block(lv->np);  // device layout (cdg_kernels.cuh); the caller's is pad16 or unpadded
-    lv->tb = dev_block(lv->nf);
+    lv->tb = dev_tblock(lv->nf);
     const int np = lv->np, ncub = lv->ncub, nf = lv->nf, ng = lv->ng, K = lv->K;
 
     // ---- shared operators (operators.cpp:135-165, factored) ---------------

@@ -40,6 +40,10 @@ __host__ __device__ constexpr int round_up(int x, int m) { return (x + m - 1) / 
 // tighter rows: P=4 40 instead of 48 doubles (-17% state traffic), P=3 24
 // instead of 32, P=1 8 instead of 16.
 __host__ __device__ constexpr int dev_block(int values) { return round_up(values, 8); }
+// Face-trace rows (4 N_g values, always a multiple of 4): only pairs of
+// values are ever loaded or stored together, so the rows stay unpadded (P=1:
+// 12 instead of 16 doubles).
+__host__ __device__ constexpr int dev_tblock(int nf) { return round_up(nf, 4); }
 __host__ __device__ constexpr int ceil_div(int x, int m) { return (x + m - 1) / m; }
 // leading dimension >= n with ld % 16 in {4, 12}: conflict-free A-fragment
 // loads (8 rows x 4 consecutive doubles per warp)
@@ -60,7 +64,7 @@ struct Cfg {
   static constexpr int R = 5 * E;                 // rows per tile
   static constexpr int MT = R / 16;               // m16 tiles per tile
   static constexpr int BP = dev_block(NP);        // device SolutionStore block (see dev_block)
-  static constexpr int TB = dev_block(NF);        // device trace block
+  static constexpr int TB = dev_tblock(NF);       // device trace block
   static constexpr int KP = round_up(NP, 8);      // K of the node->point GEMMs (k8 steps)
   static constexpr int KS1 = KP / 8;
   static constexpr int NCUB8 = round_up(NCUB, 8);

@@ -48,7 +48,7 @@ struct RCfg {
   // 32: fused traces -- the epilogue also writes I_g u_new (the next stage's
   // face traces) to p.traces_out, which replaces the separate trace kernel
   static constexpr bool FT = MODE_ & 32;
-  static constexpr int BP = dev_block(NP), TB = dev_block(NF);
+  static constexpr int BP = dev_block(NP), TB = dev_tblock(NF);
   static constexpr int KP = round_up(NP, 8), KS1 = KP / 8, NT2 = KS1;
   static constexpr int NCUB8 = round_up(NCUB, 8), NF8 = round_up(NF, 8);
   static constexpr int CH = CH_, NCH = ceil_div(NCUB8, CH);

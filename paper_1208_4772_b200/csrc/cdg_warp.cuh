@@ -39,7 +39,7 @@ struct WCfg {
   static constexpr int EW = 16;                    // elements per warp tile
   static constexpr int WARPS = WARPS_, MINB = MINB_;
   static constexpr int BP = dev_block(NP);         // device SolutionStore block
-  static constexpr int TB = dev_block(NF);         // device trace block
+  static constexpr int TB = dev_tblock(NF);        // device trace block
   static constexpr int KP = round_up(NP, 8);       // K of the nodal->cubature GEMM
   static constexpr int KS1 = KP / 8;
   static constexpr int NT = round_up(NP, 8) / 8;   // n-tiles of the RHS
@@ -86,6 +86,8 @@ struct WarpParams {
   int n_list;
   const unsigned long long* gate;  // optional launch gate (see gated_off)
   int gate_when;
+  double* traces_out;         // fused traces of u_new (next stage), or null
+  const double2* frag_ig_nat; // I_g B fragments, natural pairing [NF8/8][KS1][32]
 };
 
 template <class C, bool UPDATE, int RIEMANN>
@@ -291,9 +293,48 @@ __global__ void __launch_bounds__(32 * C::WARPS, C::MINB) k_rhs_warp(WarpParams 
             const double n0 = a_c * rs.x + dt * r0, n1 = a_c * rs.y + dt * r1;
             *reinterpret_cast<double2*>(p.res + rowoff + col) = make_double2(n0, n1);
             const double2 uo = *reinterpret_cast<const double2*>(sU + (c * C::EW + e) * C::LDU + col);
-            *reinterpret_cast<double2*>(p.u + rowoff + col) = make_double2(uo.x + b_c * n0, uo.y + b_c * n1);
+            const double w0 = uo.x + b_c * n0, w1 = uo.y + b_c * n1;
+            *reinterpret_cast<double2*>(p.u + rowoff + col) = make_double2(w0, w1);
+            acc[c][n][2 * hh] = w0;  // u_new in the accumulator (= natural-pairing A fragment) layout
+            acc[c][n][2 * hh + 1] = w1;
           } else {
             *reinterpret_cast<double2*>(p.rhs_out + rowoff + col) = make_double2(r0, r1);
+          }
+        }
+      }
+    }
+    if (UPDATE && p.traces_out) {
+      // next stage's traces T = u_new I_g^T (solver.cpp:200-208) from the
+      // registers, field by field; the trace kernel's pairing and fragments
+      // (k_interp<NAT>), so fused and separate traces agree bit for bit
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int eg = e0 + g + 8 * hh;
+        const bool skip = eg >= p.K || (__ldg(reinterpret_cast<const int*>(p.conn + (size_t)min(eg, p.K - 1) * 4) + 1) &
+                                        kCurvedBit);
+        if (skip)
+#pragma unroll
+          for (int c = 0; c < 5; ++c)
+#pragma unroll
+            for (int n = 0; n < C::NT; ++n) acc[c][n][2 * hh] = acc[c][n][2 * hh + 1] = 0.0;
+      }
+      constexpr int NFT = round_up(C::NF, 8) / 8;
+#pragma unroll
+      for (int c = 0; c < 5; ++c) {
+#pragma unroll
+        for (int nt = 0; nt < NFT; ++nt) {
+          double tacc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+          for (int ks = 0; ks < C::NT; ++ks)
+            mma_frag(tacc, AFrag{acc[c][ks][0], acc[c][ks][2], acc[c][ks][1], acc[c][ks][3]},
+                     __ldg(p.frag_ig_nat + ((size_t)nt * C::NT + ks) * 32 + lane));
+          const int col = nt * 8 + 2 * t;
+          if (col < C::NF) {
+            const int e_lo = e0 + g, e_hi = e_lo + 8;
+            if (e_lo < p.K)
+              *reinterpret_cast<double2*>(p.traces_out + ((size_t)e_lo * 5 + c) * C::TB + col) = make_double2(tacc[0], tacc[1]);
+            if (e_hi < p.K)
+              *reinterpret_cast<double2*>(p.traces_out + ((size_t)e_hi * 5 + c) * C::TB + col) = make_double2(tacc[2], tacc[3]);
           }
         }
       }
