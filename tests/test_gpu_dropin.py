@@ -71,3 +71,21 @@ def test_run_steady_at_headline_scale_through_the_dropin():
     d = json.loads(out.stdout.strip().splitlines()[-1])
     assert d["elements"] == 6 * 88 ** 3 and d["rows"] == 2 and d["last_residual"] > 0
     assert d["solution_values"] == d["elements"] * 5 * 48
+
+
+def test_output_path_from_a_gpu_run(tmp_path):
+    """§8 f4: cdg::run_steady through the drop-in, the SteadyResult written with
+    the reference's CDS1 writer, read back bit for bit, exported with its VTK
+    writer (the CLI's solve + export sequence, cli_ops.cpp:119-171), and the
+    log / state against the reference CPU run_steady on the same case
+    (integration/dropin_output.cpp)."""
+    import json
+    exe = REF / "dropin_output"
+    if not exe.exists():
+        pytest.skip("oracle/_ref/dropin_output not built")
+    out = subprocess.run([str(exe), str(tmp_path)], capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stdout + out.stderr[-2000:]
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    assert d["cds1_roundtrip_bitwise"] and d["rows_match"] and d["rows"] == 8 and d["final_degree"] == 2
+    assert d["log_rel_diff"] < 1e-10 and d["state_rel_diff"] < 1e-11
+    assert d["vtk_bytes"] > 0 and (tmp_path / "gpu_state.vtk").read_text().startswith("# vtk DataFile")
