@@ -470,6 +470,7 @@ def main():
         t_rhs = prof_rhs / launches_rhs * 1e-3
         t_tr = prof_tr / launches_rhs * 1e-3
         fused = lv.fused_traces()
+        kname = lv.rhs_kernel()
         # the fused kernel also produces the next stage's traces: its work is the
         # whole stage model F (trace GEMM included); else F_rhs
         F_k = F if fused else F_rhs
@@ -481,10 +482,10 @@ def main():
             traffic = json.loads(ncu_file.read_text()).get("dram_bytes_per_launch")
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": traffic,
-                "kernel": (f"k_rhs_row<P={p}> (fused volume+surface+lift+LSRK update"
-                           + (" + next-stage traces" if fused else "") + ", FP64 DMMA, one m-tile row per warp)"
-                           if p in (2, 3, 4, 5) else f"RHS+update kernel <P={p}> (fused volume+surface+lift+LSRK "
-                                                     f"update, FP64 DMMA)"),
+                "kernel": f"{kname}<P={p}> (fused volume+surface+lift+LSRK update"
+                          + (" + next-stage traces" if fused else "") + ", FP64 DMMA"
+                          + (", warp-autonomous: 3 elements per warp, no CTA barrier" if kname == "k_rhs_wa" else "")
+                          + ")",
                 "fused_traces": fused,
                 "algorithmic_flops_per_launch": F_k * K,
                 "peak_source": "max of the FP64 DMMA (m16n8k4/k8/k16) and DFMA peaks measured live on this "

@@ -338,6 +338,8 @@ long long cdg_gpu_launch_count(const cdg_gpu_level *lv);
 int cdg_gpu_set_profiling(cdg_gpu_level *lv, int enabled);
 int cdg_gpu_last_profile(cdg_gpu_level *lv, double *out3);
 
+/* Name of the affine RHS + update kernel the level runs (evidence labels). */
+const char *cdg_gpu_rhs_kernel(const cdg_gpu_level *lv);
 const char *cdg_gpu_version(void);
 /* FP64 roofline denominators measured on `device` (TFLOP/s): out[0] DMMA
  * m16n8k4, out[1] DFMA, out[2] DMMA m16n8k8, out[3] DMMA m16n8k16. */

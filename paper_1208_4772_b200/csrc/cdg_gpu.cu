@@ -769,6 +769,12 @@ int cdg_gpu_fused_traces(const cdg_gpu_level* lv) {
   return fused_traces(lv) ? 1 : 0;
 }
 
+const char* cdg_gpu_rhs_kernel(const cdg_gpu_level* lv) {
+  if (lv->use_row) return lv->ks->row_name;
+  if (lv->use_warp) return "k_rhs_warp";
+  return "k_rhs";
+}
+
 const char* cdg_gpu_version(void) { return "cdg_gpu 0.1 (sm_100a, fp64 DMMA)"; }
 
 // out[0] = DMMA m16n8k4, out[1] = DFMA, out[2] = DMMA m16n8k8, out[3] = DMMA m16n8k16 TFLOP/s

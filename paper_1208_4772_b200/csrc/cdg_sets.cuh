@@ -11,6 +11,7 @@
 #include "cdg_kernels.cuh"
 #include "cdg_row.cuh"
 #include "cdg_rowc.cuh"
+#include "cdg_wa.cuh"
 #include "cdg_warp.cuh"
 
 namespace cdg_gpu {
@@ -42,6 +43,7 @@ struct KernelSet {
   size_t smem_row = 0;
   int row_minb = 0, row_ch = 0, row_e = 16, row_nth = 160;
   bool row_ft = false;  // row kernel writes the next stage's traces (MODE 32)
+  const char* row_name = "k_rhs_row";  // the kernel in the row slots
   // row-per-warp inviscid kernel for curved elements (cdg_rowc.cuh)
   void (*rowc_update[2])(CurvedParams) = {nullptr, nullptr};  // [riemann]
   void (*rowc_only[2])(CurvedParams) = {nullptr, nullptr};
@@ -91,6 +93,26 @@ KernelSet with_row(KernelSet k) {
   k.row_e = RC::E;
   k.row_nth = RC::NTH;
   k.row_ft = RC::FT;
+  return k;
+}
+
+// warp-autonomous affine kernel (cdg_wa.cuh) in the row kernel's slots: same
+// operator fragments (natural pairing, CH-node chunks), fused traces; a CTA
+// "tile" is 3 elements per warp
+template <int NP, int NCUB, int NG, int CH = 8, int FCH = 32, int WARPS = 5, int MINB = 4, bool UREG = false>
+KernelSet with_wa(KernelSet k) {
+  using WC = WaCfg<NP, NCUB, NG, CH, FCH, WARPS, MINB, UREG>;
+  k.row_update[0] = &k_rhs_wa<WC, true, 0>;
+  k.row_update[1] = &k_rhs_wa<WC, true, 1>;
+  k.row_only[0] = &k_rhs_wa<WC, false, 0>;
+  k.row_only[1] = &k_rhs_wa<WC, false, 1>;
+  k.smem_row = WC::SMEM_BYTES;
+  k.row_minb = MINB;
+  k.row_ch = CH;
+  k.row_e = WC::E;
+  k.row_nth = WC::NTH;
+  k.row_ft = true;
+  k.row_name = "k_rhs_wa";
   return k;
 }
 

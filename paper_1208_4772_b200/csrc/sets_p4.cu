@@ -20,6 +20,21 @@
 #ifndef CDG_P4_E
 #define CDG_P4_E 16
 #endif
+// 1 (default): the warp-autonomous kernel (cdg_wa.cuh) for the straight P=4
+// set -- 16 warps x 1 CTA per SM, 128 registers (0.62 of the FP64 peak vs
+// 0.58 for the row kernel, scripts/tune_p4.py)
+#ifndef CDG_P4_WA
+#define CDG_P4_WA 1
+#endif
+#ifndef CDG_P4_WA_WARPS
+#define CDG_P4_WA_WARPS 16
+#endif
+#ifndef CDG_P4_WA_MINB
+#define CDG_P4_WA_MINB 1
+#endif
+#ifndef CDG_P4_WA_UREG
+#define CDG_P4_WA_UREG 0
+#endif
 
 // <CH, FCH, CTAs/SM> of the P=4 curved-mesh row kernel (k_rhs_rowc)
 #ifndef CDG_P4C_CH
@@ -38,7 +53,11 @@ std::vector<KernelSet> kernel_sets_p4() {
   return {
       // default: row kernel with fused traces (the next stage's traces from its
       // epilogue), unrolled GEMM k-steps and fused-trace n-tile groups
+#if CDG_P4_WA
+      with_wa<35, 70, 16, 8, CDG_P4_FCH, CDG_P4_WA_WARPS, CDG_P4_WA_MINB, CDG_P4_WA_UREG>(make_set<35, 70, 16, 16, 24, 2, 64>()),
+#else
       with_row<35, 70, 16, CDG_P4_CH, CDG_P4_FCH, CDG_P4_MINB, CDG_P4_MODE, CDG_P4_E>(make_set<35, 70, 16, 16, 24, 2, 64>()),
+#endif
       with_rowc<35, 70, 56, CDG_P4C_CH, CDG_P4C_FCH, CDG_P4C_MINB>(with_row<35, 70, 56, 8, 32, 4, 192>(make_set<35, 70, 56, 16, 24, 2>()))};
 }
 

@@ -146,6 +146,8 @@ def lib():
                                         C.c_char_p, C.c_size_t]
         L.cdg_gpu_level_create_from_mesh.argtypes = [C.POINTER(LevelDesc), C.POINTER(MeshDesc), C.c_int,
                                                      C.POINTER(vp), C.c_char_p, C.c_size_t]
+        L.cdg_gpu_rhs_kernel.argtypes = [vp]
+        L.cdg_gpu_rhs_kernel.restype = C.c_char_p
         L.cdg_gpu_hllc_fallbacks.argtypes = [vp, C.POINTER(C.c_longlong)]
         L.cdg_gpu_halo_define.argtypes = [vp, C.c_int, _ip, _ip, _ip, _ip, _ip]
         L.cdg_gpu_comm_unique_id.argtypes = [C.c_char_p, C.c_char_p, C.c_size_t]
@@ -374,6 +376,10 @@ class GpuLevel:
         out = np.zeros(1)
         _raise(lib().cdg_gpu_residual(self.h, 1 if kind == "l2" else 0, dt, _p(out)), "residual failed")
         return float(out[0])
+
+    def rhs_kernel(self) -> str:
+        """The affine RHS + update kernel this level runs (k_rhs_wa / k_rhs_row / ...)."""
+        return lib().cdg_gpu_rhs_kernel(self.h).decode()
 
     def hllc_fallbacks(self) -> int:
         """HLLC -> LLF fallbacks since creation (RhsWorkspace::hllc_fallbacks, solver.cpp:52,436)."""
