@@ -309,7 +309,7 @@ def curved_block(args, peak, hbm_peak):
         ach = F_rhs * K / t_rhs_s / 1e12
         r = {"value": K * npb * 25 * steps / (ms * 1e-3), "unit": "DOF-updates/s", "ms_per_step": ms / steps,
              "steps": steps, "rhs_kernel_ms": t_rhs_s * 1e3, "trace_kernel_ms": t_tr_s * 1e3,
-             "roofline": {"bound": "tensor", "kernel": "k_rhs_rowc<P=4> (curved: per-node metrics, fused "
+             "roofline": {"bound": "tensor", "kernel": f"{lv.curved_kernel()}<P={p}> (curved: per-node metrics, fused "
                           "volume+surface+lift, M_e^-1 epilogue + LSRK update)", "achieved": ach, "peak": peak,
                           "unit": "TFLOP/s", "frac": ach / peak, "algorithmic_flops_per_elem": F_rhs,
                           "model_bytes_per_elem": B + geo,

@@ -340,6 +340,8 @@ int cdg_gpu_last_profile(cdg_gpu_level *lv, double *out3);
 
 /* Name of the affine RHS + update kernel the level runs (evidence labels). */
 const char *cdg_gpu_rhs_kernel(const cdg_gpu_level *lv);
+/* Name of the curved-element RHS + update kernel ("" without curved elements). */
+const char *cdg_gpu_curved_kernel(const cdg_gpu_level *lv);
 const char *cdg_gpu_version(void);
 /* FP64 roofline denominators measured on `device` (TFLOP/s): out[0] DMMA
  * m16n8k4, out[1] DFMA, out[2] DMMA m16n8k8, out[3] DMMA m16n8k16. */

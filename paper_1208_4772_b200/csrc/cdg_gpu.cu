@@ -422,9 +422,10 @@ void launch_curved(cdg_gpu_level* lv, bool update, int stage, int mode = 0) {
     auto fr = mode == 2   ? lv->ks->rowc_aux
               : mode == 1 ? (update ? lv->ks->rowc_visc_update[rm] : lv->ks->rowc_visc_only[rm])
                           : (update ? lv->ks->rowc_update[rm] : lv->ks->rowc_only[rm]);
-    const int tiles = cp.ctiles ? cp.n_clist : (lv->n_curved + lv->ks->rowc_e - 1) / lv->ks->rowc_e;
-    fr<<<lv->cap(tiles, mode == 2 ? lv->ks->rowc_aux_minb : lv->ks->rowc_minb), lv->ks->rowc_nth,
-         mode == 2 ? lv->ks->smem_rowc_aux : lv->ks->smem_rowc,
+    const int Ec = mode == 2 ? lv->ks->rowc_aux_e : lv->ks->rowc_e;  // curved entries per CTA tile
+    const int tiles = cp.ctiles ? cp.n_clist : (lv->n_curved + Ec - 1) / Ec;
+    fr<<<lv->cap(tiles, mode == 2 ? lv->ks->rowc_aux_minb : lv->ks->rowc_minb),
+         mode == 2 ? lv->ks->rowc_aux_nth : lv->ks->rowc_nth, mode == 2 ? lv->ks->smem_rowc_aux : lv->ks->smem_rowc,
          lv->stream>>>(cp);
     ++lv->launches;
     return;
@@ -773,6 +774,11 @@ const char* cdg_gpu_rhs_kernel(const cdg_gpu_level* lv) {
   if (lv->use_row) return lv->ks->row_name;
   if (lv->use_warp) return "k_rhs_warp";
   return "k_rhs";
+}
+
+const char* cdg_gpu_curved_kernel(const cdg_gpu_level* lv) {
+  if (!lv->n_curved) return "";
+  return lv->use_rowc ? lv->ks->rowc_name : "k_rhs_curved";
 }
 
 const char* cdg_gpu_version(void) { return "cdg_gpu 0.1 (sm_100a, fp64 DMMA)"; }
@@ -1179,6 +1185,10 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
     if (lv->n_curved && lv->ks->rowc_aux) {
       CUDA_OK(cudaFuncSetAttribute(lv->ks->rowc_aux, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)lv->ks->smem_rowc_aux));
+      for (auto fn : {lv->ks->rowc_update[0], lv->ks->rowc_update[1], lv->ks->rowc_only[0], lv->ks->rowc_only[1],
+                      lv->ks->rowc_visc_update[0], lv->ks->rowc_visc_update[1], lv->ks->rowc_visc_only[0],
+                      lv->ks->rowc_visc_only[1]})
+        CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lv->ks->smem_rowc));
     }
     if (lv->n_curved)
       for (auto fn : {lv->ks->curved_update, lv->ks->curved_only, lv->ks->curved_visc_update,

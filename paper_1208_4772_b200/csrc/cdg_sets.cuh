@@ -12,6 +12,7 @@
 #include "cdg_row.cuh"
 #include "cdg_rowc.cuh"
 #include "cdg_wa.cuh"
+#include "cdg_wac.cuh"
 #include "cdg_warp.cuh"
 
 namespace cdg_gpu {
@@ -51,7 +52,8 @@ struct KernelSet {
   void (*rowc_visc_only[2])(CurvedParams) = {nullptr, nullptr};
   void (*rowc_aux)(CurvedParams) = nullptr;
   size_t smem_rowc = 0, smem_rowc_aux = 0;
-  int rowc_aux_minb = 0;
+  int rowc_aux_minb = 0, rowc_aux_e = 16, rowc_aux_nth = 160;
+  const char* rowc_name = "k_rhs_rowc";
   int rowc_minb = 0, rowc_ch = 0, rowc_e = 16, rowc_nth = 160;
 };
 
@@ -72,6 +74,8 @@ KernelSet with_rowc(KernelSet k) {
   k.rowc_aux = &k_rhs_rowc<RCA, false, 0, 2>;
   k.smem_rowc_aux = RowCurvedLayout<RCA, 3>::SMEM_BYTES;
   k.rowc_aux_minb = 2;
+  k.rowc_aux_e = RCA::E;
+  k.rowc_aux_nth = RCA::NTH;
   k.smem_rowc = RowCurvedLayout<RC>::SMEM_BYTES;
   k.rowc_minb = MINB;
   k.rowc_ch = CH;
@@ -93,6 +97,27 @@ KernelSet with_row(KernelSet k) {
   k.row_e = RC::E;
   k.row_nth = RC::NTH;
   k.row_ft = RC::FT;
+  return k;
+}
+
+// warp-autonomous curved kernel (cdg_wac.cuh) in the curved RHS slots (apply
+// after with_rowc: the aux gradient stays on k_rhs_rowc)
+template <int NP, int NCUB, int NG, int CH = 8, int FCH = 32, int WARPS = 16, int MINB = 1>
+KernelSet with_wac(KernelSet k) {
+  using WC = WacCfg<NP, NCUB, NG, CH, FCH, WARPS, MINB>;
+  k.rowc_update[0] = &k_rhs_wac<WC, true, 0>;
+  k.rowc_update[1] = &k_rhs_wac<WC, true, 1>;
+  k.rowc_only[0] = &k_rhs_wac<WC, false, 0>;
+  k.rowc_only[1] = &k_rhs_wac<WC, false, 1>;
+  k.rowc_visc_update[0] = &k_rhs_wac<WC, true, 0, 1>;
+  k.rowc_visc_update[1] = &k_rhs_wac<WC, true, 1, 1>;
+  k.rowc_visc_only[0] = &k_rhs_wac<WC, false, 0, 1>;
+  k.rowc_visc_only[1] = &k_rhs_wac<WC, false, 1, 1>;
+  k.smem_rowc = WC::SMEM_BYTES;
+  k.rowc_minb = MINB;
+  k.rowc_e = WC::E;
+  k.rowc_nth = WC::NTH;
+  k.rowc_name = "k_rhs_wac";
   return k;
 }
 

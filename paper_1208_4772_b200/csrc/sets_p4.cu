@@ -47,6 +47,19 @@
 #define CDG_P4C_MINB 4
 #endif
 
+// 1 (default): the warp-autonomous curved kernel (cdg_wac.cuh) for the curved
+// P=4 set, 16 warps x 1 CTA per SM (0.434 / 0.367 of the FP64 peak LLF / HLLC
+// vs 0.422 / 0.355 for k_rhs_rowc); the aux gradient stays on k_rhs_rowc
+#ifndef CDG_P4C_WAC
+#define CDG_P4C_WAC 1
+#endif
+#ifndef CDG_P4C_WAC_WARPS
+#define CDG_P4C_WAC_WARPS 16
+#endif
+#ifndef CDG_P4C_WAC_MINB
+#define CDG_P4C_WAC_MINB 1
+#endif
+
 namespace cdg_gpu {
 
 std::vector<KernelSet> kernel_sets_p4() {
@@ -58,7 +71,12 @@ std::vector<KernelSet> kernel_sets_p4() {
 #else
       with_row<35, 70, 16, CDG_P4_CH, CDG_P4_FCH, CDG_P4_MINB, CDG_P4_MODE, CDG_P4_E>(make_set<35, 70, 16, 16, 24, 2, 64>()),
 #endif
+#if CDG_P4C_WAC
+      with_wac<35, 70, 56, 8, CDG_P4C_FCH, CDG_P4C_WAC_WARPS, CDG_P4C_WAC_MINB>(
+          with_rowc<35, 70, 56, CDG_P4C_CH, CDG_P4C_FCH, CDG_P4C_MINB>(with_row<35, 70, 56, 8, 32, 4, 192>(make_set<35, 70, 56, 16, 24, 2>())))};
+#else
       with_rowc<35, 70, 56, CDG_P4C_CH, CDG_P4C_FCH, CDG_P4C_MINB>(with_row<35, 70, 56, 8, 32, 4, 192>(make_set<35, 70, 56, 16, 24, 2>()))};
+#endif
 }
 
 }  // namespace cdg_gpu

@@ -148,6 +148,8 @@ def lib():
                                                      C.POINTER(vp), C.c_char_p, C.c_size_t]
         L.cdg_gpu_rhs_kernel.argtypes = [vp]
         L.cdg_gpu_rhs_kernel.restype = C.c_char_p
+        L.cdg_gpu_curved_kernel.argtypes = [vp]
+        L.cdg_gpu_curved_kernel.restype = C.c_char_p
         L.cdg_gpu_hllc_fallbacks.argtypes = [vp, C.POINTER(C.c_longlong)]
         L.cdg_gpu_halo_define.argtypes = [vp, C.c_int, _ip, _ip, _ip, _ip, _ip]
         L.cdg_gpu_comm_unique_id.argtypes = [C.c_char_p, C.c_char_p, C.c_size_t]
@@ -380,6 +382,10 @@ class GpuLevel:
     def rhs_kernel(self) -> str:
         """The affine RHS + update kernel this level runs (k_rhs_wa / k_rhs_row / ...)."""
         return lib().cdg_gpu_rhs_kernel(self.h).decode()
+
+    def curved_kernel(self) -> str:
+        """The curved-element RHS + update kernel ('' without curved elements)."""
+        return lib().cdg_gpu_curved_kernel(self.h).decode()
 
     def hllc_fallbacks(self) -> int:
         """HLLC -> LLF fallbacks since creation (RhsWorkspace::hllc_fallbacks, solver.cpp:52,436)."""
