@@ -124,9 +124,10 @@ KernelSet with_wac(KernelSet k) {
 // warp-autonomous affine kernel (cdg_wa.cuh) in the row kernel's slots: same
 // operator fragments (natural pairing, CH-node chunks), fused traces; a CTA
 // "tile" is 3 elements per warp
-template <int NP, int NCUB, int NG, int CH = 8, int FCH = 32, int WARPS = 5, int MINB = 4, bool UREG = false>
+template <int NP, int NCUB, int NG, int CH = 8, int FCH = 32, int WARPS = 5, int MINB = 4, bool UREG = false,
+          bool FT = true>
 KernelSet with_wa(KernelSet k) {
-  using WC = WaCfg<NP, NCUB, NG, CH, FCH, WARPS, MINB, UREG>;
+  using WC = WaCfg<NP, NCUB, NG, CH, FCH, WARPS, MINB, UREG, FT>;
   k.row_update[0] = &k_rhs_wa<WC, true, 0>;
   k.row_update[1] = &k_rhs_wa<WC, true, 1>;
   k.row_only[0] = &k_rhs_wa<WC, false, 0>;
@@ -136,7 +137,7 @@ KernelSet with_wa(KernelSet k) {
   k.row_ch = CH;
   k.row_e = WC::E;
   k.row_nth = WC::NTH;
-  k.row_ft = true;
+  k.row_ft = FT;
   k.row_name = "k_rhs_wa";
   return k;
 }

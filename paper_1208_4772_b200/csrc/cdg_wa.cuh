@@ -20,8 +20,10 @@
 
 namespace cdg_gpu {
 
-template <int NP_, int NCUB_, int NG_, int CH_ = 8, int FCH_ = 32, int WARPS_ = 5, int MINB_ = 4, bool UREG_ = false>
+template <int NP_, int NCUB_, int NG_, int CH_ = 8, int FCH_ = 32, int WARPS_ = 5, int MINB_ = 4, bool UREG_ = false,
+          bool FT_ = true>
 struct WaCfg {
+  static constexpr bool FT = FT_;  // the epilogue writes the next stage's traces (else the trace kernel does)
   static constexpr bool UREG = UREG_;  // U fragments kept in registers for the whole tile (else reloaded per chunk)
   static constexpr int NP = NP_, NCUB = NCUB_, NG = NG_, NF = 4 * NG_;
   static constexpr int EPW = 3, WARPS = WARPS_, E = EPW * WARPS_, NTH = 32 * WARPS_, MINB = MINB_;
@@ -264,7 +266,7 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_wa(RhsParams p) {
         }
       }
     }
-    if (UPDATE && p.traces_out) {
+    if (C::FT && UPDATE && p.traces_out) {
       // next stage's traces T = u_new I_g^T (solver.cpp:200-208) from the
       // registers; the trace kernel's pairing and fragments (bit-identical)
 #pragma unroll

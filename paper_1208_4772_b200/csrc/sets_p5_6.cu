@@ -3,13 +3,16 @@
 #define CDG_SET_TU
 #include "cdg_sets.cuh"
 
+
 namespace cdg_gpu {
 
 std::vector<KernelSet> kernel_sets_p5_6() {
   return {
-      // p=5: row-per-warp kernel (11.2 ms vs 11.9 for the CTA kernel at 511k
-      // tets); p=6: CTA kernel with 8-node chunks (27.8 vs 34.8 ms)
-      with_row<56, 126, 56, 8, 32, 3, 192>(make_set<56, 126, 56, 16, 16, 2>()),
+      // p=5: the warp-autonomous kernel with fused traces, 16 warps x 1 CTA/SM
+      // (56.2 ms per step at 511k tets vs 64.7 for the row kernel + trace kernel)
+      with_wa<56, 126, 56, 8, 32, 16, 1, false, true>(make_set<56, 126, 56, 16, 16, 2>()),
+      // p=6: CTA kernel with 8-node chunks (27.8 vs 34.8 ms; the warp-autonomous
+      // kernel 3% slower here)
       make_set<84, 210, 84, 16, 8, 2, 16>(),
       with_rowc<56, 210, 84, 8, 32, 3>(with_row<56, 210, 84, 8, 32, 3, 192>(make_set<56, 210, 84, 16, 16, 2>())), make_set<84, 330, 165, 16>()};
 }
