@@ -121,6 +121,19 @@ KernelSet with_wac(KernelSet k) {
   return k;
 }
 
+// the aux gradient (three directions, one pass) on the warp-autonomous curved
+// mapping: AWARPS warps x 1 CTA per SM
+template <int NP, int NCUB, int NG, int CH = 8, int FCH = 32, int AWARPS = 8>
+KernelSet with_wac_aux(KernelSet k) {
+  using WA = WacCfg<NP, NCUB, NG, CH, FCH, AWARPS, 1, 3>;
+  k.rowc_aux = &k_rhs_wac<WA, false, 0, 2>;
+  k.smem_rowc_aux = WA::SMEM_BYTES;
+  k.rowc_aux_minb = 1;
+  k.rowc_aux_e = WA::E;
+  k.rowc_aux_nth = WA::NTH;
+  return k;
+}
+
 // warp-autonomous affine kernel (cdg_wa.cuh) in the row kernel's slots: same
 // operator fragments (natural pairing, CH-node chunks), fused traces; a CTA
 // "tile" is 3 elements per warp

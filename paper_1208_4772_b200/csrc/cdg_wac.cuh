@@ -5,16 +5,17 @@
 // curved elements (15 gathered (element, field) rows + 1 padding row), so the
 // GEMMs, the pointwise and face fluxes and the M_e^-1 GEMV only exchange data
 // through warp-private shared panels (__syncwarp); no CTA barrier.
-// KIND 0: inviscid RHS (+ update); 1: viscous RHS (+ update). (The aux
-// gradient, KIND 2, stays on k_rhs_rowc.)
+// KIND 0: inviscid RHS (+ update); 1: viscous RHS (+ update); 2: the aux
+// gradient q_0..q_2 in one pass (NA = 3 accumulator sets and panels).
 #pragma once
 
 #include "cdg_rowc.cuh"
 
 namespace cdg_gpu {
 
-template <int NP_, int NCUB_, int NG_, int CH_ = 8, int FCH_ = 32, int WARPS_ = 16, int MINB_ = 1>
+template <int NP_, int NCUB_, int NG_, int CH_ = 8, int FCH_ = 32, int WARPS_ = 16, int MINB_ = 1, int NA_ = 1>
 struct WacCfg {
+  static constexpr int NA = NA_;  // accumulator sets: 1 (RHS) or 3 (aux gradient)
   static constexpr int NP = NP_, NCUB = NCUB_, NG = NG_, NF = 4 * NG_;
   static constexpr int EPW = 3, WARPS = WARPS_, E = EPW * WARPS_, NTH = 32 * WARPS_, MINB = MINB_;
   static constexpr int BP = dev_block(NP), TB = dev_tblock(NF);
@@ -25,7 +26,7 @@ struct WacCfg {
   static constexpr int K2CUB = 3 * NCUB8, K2 = K2CUB + NF8;
   static constexpr int LDC = frag_ld8(CH), LDG = frag_ld8(3 * CH), LDF = frag_ld8(FCH);
   static constexpr int LDV = KP + 1;  // vol panel of the epilogue
-  static constexpr int VOLW = 16 * LDC + 16 * LDG, FACEW = 16 * LDF, EPIW = 16 * LDV;
+  static constexpr int VOLW = 16 * LDC + NA_ * 16 * LDG, FACEW = NA_ * 16 * LDF, EPIW = NA_ * 16 * LDV;
   static constexpr int W1 = VOLW > FACEW ? VOLW : FACEW;
   static constexpr int WORKW = W1 > EPIW ? W1 : EPIW;  // doubles per warp (phases alias)
   // per warp: [work panels | conn (int2) | ids (int)], a multiple of 2 doubles
@@ -36,8 +37,10 @@ struct WacCfg {
 
 template <class C, bool UPDATE, int RM, int KIND = 0>
 __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_wac(CurvedParams cp) {
-  constexpr bool VISC = KIND == 1;
-  static_assert(KIND == 0 || KIND == 1, "the aux gradient stays on k_rhs_rowc");
+  constexpr bool VISC = KIND == 1, AUX = KIND == 2;
+  constexpr int NA = C::NA;
+  static_assert(NA == (AUX ? 3 : 1), "the aux gradient needs the 3-panel layout");
+  constexpr bool UPD = UPDATE && !AUX;
   const RhsParams& p = cp.base;
   if (gated_off(p.gate, p.gate_when)) return;
   extern __shared__ __align__(16) double smem[];
@@ -54,15 +57,16 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_wac(CurvedParams cp) {
   const int n_tiles = (cp.Kc + C::E - 1) / C::E;
   const double2* fb1all = reinterpret_cast<const double2*>(p.frag_icub);
   const double2* fb2all = reinterpret_cast<const double2*>(cp.frag_opc);
-  constexpr int LDQ = round_up(C::NCUB, 8);  // qcub row stride
-  const size_t qcs = (size_t)p.K * 5 * LDQ;  // qcub direction stride
+  constexpr int LDQ = round_up(C::NCUB, 8);       // qcub row stride
+  const size_t qcs = (size_t)p.K * 5 * LDQ;       // qcub direction stride
+  const size_t qstride = (size_t)p.K * 5 * C::BP;  // q_out direction stride
 
   const int n_iter = cp.ctiles ? cp.n_clist : n_tiles;  // optional curved-tile list (multi-GPU split)
   for (int it_t = blockIdx.x; it_t < n_iter; it_t += gridDim.x) {
     const int tile = cp.ctiles ? __ldg(cp.ctiles + it_t) : it_t;
     const int c0 = tile * C::E + warp * C::EPW;  // this warp's three curved-list entries
     if (c0 >= cp.Kc) continue;                    // warp-uniform
-    if (__shfl_sync(0xffffffffu, lane == 0 ? *(volatile int*)&p.err->flag : 0, 0)) return;
+    if (!AUX && __shfl_sync(0xffffffffu, lane == 0 ? *(volatile int*)&p.err->flag : 0, 0)) return;
     if (lane < C::EPW) sId[lane] = c0 + lane < cp.Kc ? __ldg(cp.ids + c0 + lane) : -1;
     __syncwarp();
     if (lane < C::EPW * 4) {
@@ -76,14 +80,24 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_wac(CurvedParams cp) {
     const double* u_hi = p.u + (ok_hi ? (size_t)el_hi * 5 + (g + 8) % 5 : 0) * C::BP + 2 * tq;
     __syncwarp();
 
-    double acc[C::NT2][4];
+    double acc[NA][C::NT2][4];
 #pragma unroll
-    for (int i = 0; i < C::NT2; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.0;
+    for (int a = 0; a < NA; ++a)
+#pragma unroll
+      for (int i = 0; i < C::NT2; ++i) acc[a][i][0] = acc[a][i][1] = acc[a][i][2] = acc[a][i][3] = 0.0;
+    // acc[a] += P_a Op^T over the NA panels P_a = panel + a * pstride (one B load feeds NA MMAs)
     auto contract = [&](const double* panel, int ld, int nks, int nks_full, const double2* fb2) {
+      const int pstride = 16 * ld;
       auto kstep = [&](int ks) {
-        const AFrag a = load_afrag(panel, ld, 0, ks * 8, g, tq);
+        AFrag a[NA];
 #pragma unroll
-        for (int nt = 0; nt < C::NT2; ++nt) mma_frag(acc[nt], a, __ldg(fb2 + (ks * C::NT2 + nt) * 32 + lane));
+        for (int k = 0; k < NA; ++k) a[k] = load_afrag(panel + k * pstride, ld, 0, ks * 8, g, tq);
+#pragma unroll
+        for (int nt = 0; nt < C::NT2; ++nt) {
+          const double2 b = __ldg(fb2 + (ks * C::NT2 + nt) * 32 + lane);
+#pragma unroll
+          for (int k = 0; k < NA; ++k) mma_frag(acc[k][nt], a[k], b);
+        }
       };
       if (nks == nks_full) {
 #pragma unroll
@@ -134,7 +148,20 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_wac(CurvedParams cp) {
           const double* uc = sC + (e * 5) * C::LDC + ql;
           double* gout = sG + (e * 5) * C::LDG + ql;
           const int ce = c0 + e;
-          if (q < C::NCUB && ce < cp.Kc) {
+          if (q < C::NCUB && ce < cp.Kc && AUX) {
+            // G_k = -se (J W dr_k/dx_m) U_cub for the three directions m
+            const double* met = cp.jwr + ((size_t)ce * C::NCUB + q) * 9;
+            const double se = p.sqrt_eps[sId[e]];
+            const double uv[5] = {uc[0], uc[C::LDC], uc[2 * C::LDC], uc[3 * C::LDC], uc[4 * C::LDC]};
+#pragma unroll
+            for (int ma = 0; ma < 3; ++ma)
+#pragma unroll
+              for (int k = 0; k < 3; ++k) {
+                const double jk = __ldg(met + k * 3 + ma);
+#pragma unroll
+                for (int c = 0; c < 5; ++c) gout[ma * 16 * C::LDG + k * w + c * C::LDG] = -se * (jk * uv[c]);
+              }
+          } else if (q < C::NCUB && ce < cp.Kc) {
             const double* met = cp.jwr + ((size_t)ce * C::NCUB + q) * 9;
             const State5 s{uc[0], uc[C::LDC], uc[2 * C::LDC], uc[3 * C::LDC], uc[4 * C::LDC]};
             if (!admissible(s, gamma)) record_error(p.err, 1, p.elem_offset + sId[e], q, 0, s.r);
@@ -162,13 +189,17 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_wac(CurvedParams cp) {
             }
           } else {
 #pragma unroll
-            for (int m = 0; m < 3; ++m)
+            for (int a = 0; a < NA; ++a)
 #pragma unroll
-              for (int c = 0; c < 5; ++c) gout[m * w + c * C::LDG] = 0.0;
+              for (int m = 0; m < 3; ++m)
+#pragma unroll
+                for (int c = 0; c < 5; ++c) gout[a * 16 * C::LDG + m * w + c * C::LDG] = 0.0;
           }
         }
       }
-      if (lane < 3 * w) sG[15 * C::LDG + lane] = 0.0;  // the padding row
+      if (lane < 3 * w)
+#pragma unroll
+        for (int a = 0; a < NA; ++a) sG[a * 16 * C::LDG + 15 * C::LDG + lane] = 0.0;  // the padding row
       __syncwarp();
       contract(sG, C::LDG, (3 * w) / 8, 3 * C::CH / 8, fb2all + (size_t)(3 * q0 / 8) * C::NT2 * 32);
       __syncwarp();
@@ -188,7 +219,9 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_wac(CurvedParams cp) {
         const int ce = c0 + e, eg = sId[e];
         if (ce >= cp.Kc || fl >= wr) {
 #pragma unroll
-          for (int c = 0; c < 5; ++c) gout[c * C::LDF] = 0.0;
+          for (int a = 0; a < NA; ++a)
+#pragma unroll
+            for (int c = 0; c < 5; ++c) gout[a * 16 * C::LDF + c * C::LDF] = 0.0;
           continue;
         }
         const int f = fq / C::NG, gq = fq - f * C::NG;
@@ -204,6 +237,21 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_wac(CurvedParams cp) {
           up = State5{tp[0], tp[C::TB], tp[2 * C::TB], tp[3 * C::TB], tp[4 * C::TB]};
         } else {
           up = boundary_state(um, fn.x, fn.y, fn.z, (cw.y >> 2) & 3, p.gas);
+        }
+        if (AUX) {
+          // central trace average with per-side sqrt(eps) (solver.cpp:291-309),
+          // fed negated to the [D^T | -I_g^T] operator, for the three directions
+          const double se = p.sqrt_eps[eg];
+          const double snb = cw.x >= 0 ? p.sqrt_eps[cw.x] : se;
+          const double umv[5] = {um.r, um.mx, um.my, um.mz, um.E};
+          const double upv[5] = {up.r, up.mx, up.my, up.mz, up.E};
+          const double nrm[3] = {fn.x, fn.y, fn.z};
+#pragma unroll
+          for (int ma = 0; ma < 3; ++ma)
+#pragma unroll
+            for (int c = 0; c < 5; ++c)
+              gout[ma * 16 * C::LDF + c * C::LDF] = -fn.w * (0.5 * (se * umv[c] + snb * upv[c]) * nrm[ma]);
+          continue;
         }
         if (!admissible(um, gamma) || !admissible(up, gamma)) record_error(p.err, 2, p.elem_offset + eg, f, gq, um.r);
         double fs[5];
@@ -233,7 +281,9 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_wac(CurvedParams cp) {
 #pragma unroll
         for (int c = 0; c < 5; ++c) gout[c * C::LDF] = fn.w * fs[c];
       }
-      if (lane < wp) sF[15 * C::LDF + lane] = 0.0;  // the padding row
+      if (lane < wp)
+#pragma unroll
+        for (int a = 0; a < NA; ++a) sF[a * 16 * C::LDF + 15 * C::LDF + lane] = 0.0;  // the padding row
       __syncwarp();
       contract(sF, C::LDF, wp / 8, C::FCH / 8, fb2all + (size_t)((C::K2CUB + f0) / 8) * C::NT2 * 32);
       __syncwarp();
@@ -241,16 +291,19 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_wac(CurvedParams cp) {
 
     // ---- epilogue: vol -> warp panel, M_e^-1 vol -> update / rhs ----------------
 #pragma unroll
-    for (int nt = 0; nt < C::NT2; ++nt) {
-      const int col = nt * 8 + 2 * tq;
-      sV[g * C::LDV + col] = acc[nt][0];
-      sV[g * C::LDV + col + 1] = acc[nt][1];
-      sV[(g + 8) * C::LDV + col] = acc[nt][2];
-      sV[(g + 8) * C::LDV + col + 1] = acc[nt][3];
-    }
+    for (int a = 0; a < NA; ++a)
+#pragma unroll
+      for (int nt = 0; nt < C::NT2; ++nt) {
+        const int col = nt * 8 + 2 * tq;
+        double* va = sV + a * 16 * C::LDV;
+        va[g * C::LDV + col] = acc[a][nt][0];
+        va[g * C::LDV + col + 1] = acc[a][nt][1];
+        va[(g + 8) * C::LDV + col] = acc[a][nt][2];
+        va[(g + 8) * C::LDV + col + 1] = acc[a][nt][3];
+      }
     __syncwarp();
     double a_c = 0.0, b_c = 0.0, dt = 0.0;
-    if (UPDATE) {
+    if (UPD) {
       a_c = p.coef->a[p.stage];
       b_c = p.coef->b[p.stage];
       dt = p.coef->dt;
@@ -269,14 +322,18 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_wac(CurvedParams cp) {
 #pragma unroll
       for (int k = 0; k < MG; ++k) m[k] = k < C::NP ? __ldg(mcol + (size_t)k * C::NP) : 0.0;
       double ro[5], uo[5];
-      if (UPDATE) {
+      if (UPD) {
 #pragma unroll
         for (int f = 0; f < 5; ++f) {
           ro[f] = p.res[g0 + (size_t)f * C::BP];
           uo[f] = p.u[g0 + (size_t)f * C::BP];
         }
       }
-      double out[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+      double out[NA][5];
+#pragma unroll
+      for (int a = 0; a < NA; ++a)
+#pragma unroll
+        for (int f = 0; f < 5; ++f) out[a][f] = 0.0;
 #pragma unroll 1
       for (int gr = 0; gr < NGR; ++gr) {
         const int j0 = gr * MG;
@@ -290,19 +347,24 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_wac(CurvedParams cp) {
         for (int k = 0; k < MG; ++k)
           if (j0 + k < C::NP)
 #pragma unroll
-            for (int f = 0; f < 5; ++f) out[f] += m[k] * v[f * C::LDV + j0 + k];
+            for (int a = 0; a < NA; ++a)
+#pragma unroll
+              for (int f = 0; f < 5; ++f) out[a][f] += m[k] * v[a * 16 * C::LDV + f * C::LDV + j0 + k];
 #pragma unroll
         for (int k = 0; k < MG; ++k) m[k] = mn[k];
       }
 #pragma unroll
       for (int f = 0; f < 5; ++f) {
         const size_t gi = g0 + (size_t)f * C::BP;
-        if (UPDATE) {
-          const double rn = a_c * ro[f] + dt * out[f];
+        if (AUX) {
+#pragma unroll
+          for (int a = 0; a < NA; ++a) cp.q_out[a * qstride + gi] = out[a][f];
+        } else if (UPD) {
+          const double rn = a_c * ro[f] + dt * out[0][f];
           p.res[gi] = rn;
           p.u[gi] = uo[f] + b_c * rn;
         } else {
-          p.rhs_out[gi] = out[f];
+          p.rhs_out[gi] = out[0][f];
         }
       }
     }

@@ -59,6 +59,10 @@
 #ifndef CDG_P4C_WAC_MINB
 #define CDG_P4C_WAC_MINB 1
 #endif
+// warps of the warp-autonomous aux-gradient kernel (0: k_rhs_rowc KIND 2)
+#ifndef CDG_P4C_AUXW
+#define CDG_P4C_AUXW 0
+#endif
 
 namespace cdg_gpu {
 
@@ -71,7 +75,10 @@ std::vector<KernelSet> kernel_sets_p4() {
 #else
       with_row<35, 70, 16, CDG_P4_CH, CDG_P4_FCH, CDG_P4_MINB, CDG_P4_MODE, CDG_P4_E>(make_set<35, 70, 16, 16, 24, 2, 64>()),
 #endif
-#if CDG_P4C_WAC
+#if CDG_P4C_WAC && CDG_P4C_AUXW
+      with_wac_aux<35, 70, 56, 8, 32, CDG_P4C_AUXW>(with_wac<35, 70, 56, 8, CDG_P4C_FCH, CDG_P4C_WAC_WARPS, CDG_P4C_WAC_MINB>(
+          with_rowc<35, 70, 56, CDG_P4C_CH, CDG_P4C_FCH, CDG_P4C_MINB>(with_row<35, 70, 56, 8, 32, 4, 192>(make_set<35, 70, 56, 16, 24, 2>()))))};
+#elif CDG_P4C_WAC
       with_wac<35, 70, 56, 8, CDG_P4C_FCH, CDG_P4C_WAC_WARPS, CDG_P4C_WAC_MINB>(
           with_rowc<35, 70, 56, CDG_P4C_CH, CDG_P4C_FCH, CDG_P4C_MINB>(with_row<35, 70, 56, 8, 32, 4, 192>(make_set<35, 70, 56, 16, 24, 2>())))};
 #else

@@ -17,7 +17,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent.parent
 
 
-def child(lib, n, steps, riemann, p, curved=False):
+def child(lib, n, steps, riemann, p, curved=False, visc=False):
     sys.path.insert(0, str(ROOT))
     import numpy as np
     import torch
@@ -44,6 +44,9 @@ def child(lib, n, steps, riemann, p, curved=False):
     lv.set_state(u.reshape(-1))
     cfg = gpu.run_config(riemann)
     dt = 0.5 * lv.compute_timestep(cfg)
+    if visc:  # Persson-Peraire AV forced on every element (bench_curved.py --visc)
+        cfg = gpu.run_config(riemann, viscosity=dict(enabled=True, eps0=0.01, kappa=4.0, s0_offset=-100.0))
+        dt *= 0.4
     lv.rk_steps(cfg, dt, 2)
     torch.cuda.synchronize()
     ext = torch.cuda.ExternalStream(lv.stream())
@@ -65,7 +68,7 @@ def child(lib, n, steps, riemann, p, curved=False):
     uu = lv.get_state()[0]
     print(json.dumps({"lib": str(lib), "K": K, "ms_per_step": ms_step, "rhs_ms": rhs_ms,
                       "frac_graph": F * K / (ms_step / 5 * 1e-3) / 1e12 / peak,
-                      "frac_rhs": F * K / (rhs_ms * 1e-3) / 1e12 / peak, "peak": peak,
+                      "frac_rhs": F * K / (rhs_ms * 1e-3) / 1e12 / peak if rhs_ms > 0 else None, "peak": peak,
                       "checksum": float(np.sum(uu)), "fused": lv.fused_traces(), "trace_ms": t_tr / (5 * steps)}), flush=True)
 
 
@@ -77,14 +80,15 @@ def main():
     ap.add_argument("--riemann", default="llf")
     ap.add_argument("--child", action="store_true")
     ap.add_argument("--curved", action="store_true")
+    ap.add_argument("--visc", action="store_true")
     ap.add_argument("libs", nargs="+")
     a = ap.parse_args()
     if a.child:
-        child(a.libs[0], a.n, a.steps, a.riemann, a.p, a.curved)
+        child(a.libs[0], a.n, a.steps, a.riemann, a.p, a.curved, a.visc)
         return
     for lib in a.libs:
         r = subprocess.run([sys.executable, __file__, "--child", "--n", str(a.n), "--p", str(a.p), "--steps",
-                            str(a.steps), "--riemann", a.riemann, lib] + (["--curved"] if a.curved else []), capture_output=True, text=True, timeout=900)
+                            str(a.steps), "--riemann", a.riemann, lib] + (["--curved"] if a.curved else []) + (["--visc"] if a.visc else []), capture_output=True, text=True, timeout=900)
         out = r.stdout.strip().splitlines()
         print(out[-1] if out else json.dumps({"lib": lib, "error": r.stderr[-800:]}), flush=True)
 
