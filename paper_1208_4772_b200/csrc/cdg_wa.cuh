@@ -18,6 +18,10 @@
 
 #include "cdg_row.cuh"
 
+#ifndef CDG_WA_FUNROLL
+#define CDG_WA_FUNROLL 1
+#endif
+
 namespace cdg_gpu {
 
 template <int NP_, int NCUB_, int NG_, int CH_ = 8, int FCH_ = 32, int WARPS_ = 5, int MINB_ = 4, bool UREG_ = false,
@@ -41,6 +45,7 @@ struct WaCfg {
   static constexpr int PERW = round_up(EPW * 4 * 4 + WORKW + EPW * 9 + EPW * 4, 4);
   static constexpr size_t SMEM_BYTES = sizeof(double) * (size_t)PERW * WARPS_;
   static constexpr int IT_P = ceil_div(EPW * CH, 32), IT_F = ceil_div(EPW * FCH, 32);
+  static constexpr int FUNROLL = CDG_WA_FUNROLL;  // face-item loop unroll (tuning)
 };
 
 template <class C, bool UPDATE, int RM>
@@ -190,7 +195,7 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_wa(RhsParams p) {
     for (int fc = 0; fc < C::NFCH; ++fc) {
       const int f0 = fc * C::FCH;
       const int wr = min(C::FCH, C::NF - f0), wp = round_up(wr, 8);
-#pragma unroll 1
+#pragma unroll C::FUNROLL
       for (int it = 0; it < C::IT_F; ++it) {
         const int idx = lane + it * 32;
         if (idx >= C::EPW * wp) break;

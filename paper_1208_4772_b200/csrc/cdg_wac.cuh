@@ -11,6 +11,10 @@
 
 #include "cdg_rowc.cuh"
 
+#ifndef CDG_WAC_FUNROLL
+#define CDG_WAC_FUNROLL 1
+#endif
+
 namespace cdg_gpu {
 
 template <int NP_, int NCUB_, int NG_, int CH_ = 8, int FCH_ = 32, int WARPS_ = 16, int MINB_ = 1, int NA_ = 1>
@@ -33,6 +37,7 @@ struct WacCfg {
   static constexpr int PERW = round_up(WORKW + EPW * 4 + ceil_div(EPW, 2), 2);
   static constexpr size_t SMEM_BYTES = sizeof(double) * (size_t)PERW * WARPS_;
   static constexpr int IT_P = ceil_div(EPW * CH, 32), IT_F = ceil_div(EPW * FCH, 32);
+  static constexpr int FUNROLL = CDG_WAC_FUNROLL;  // face-item loop unroll (tuning)
 };
 
 template <class C, bool UPDATE, int RM, int KIND = 0>
@@ -210,7 +215,7 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_wac(CurvedParams cp) {
     for (int fc = 0; fc < C::NFCH; ++fc) {
       const int f0 = fc * C::FCH;
       const int wr = min(C::FCH, C::NF - f0), wp = round_up(wr, 8);
-#pragma unroll 1
+#pragma unroll C::FUNROLL
       for (int it = 0; it < C::IT_F; ++it) {
         const int idx = lane + it * 32;
         if (idx >= C::EPW * wp) break;
