@@ -16,6 +16,7 @@
 #include <map>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "cdg_gpu.h"
@@ -190,9 +191,10 @@ struct cdg_gpu_level {
   long long launches = 0;
   // state
   double *u = nullptr, *res = nullptr, *rhs = nullptr, *traces = nullptr, *before = nullptr;
-  double* stage = nullptr;  // host <-> device layout conversion (copy_rows), caller layout
-  size_t stage_n = 0;
-  int stage_d2h_block = 0;  // caller row length of the last device->host staging (0: re-zero first)
+  // pinned two-slot ring of the host <-> device state copies (copy_rows)
+  double* ring[2] = {nullptr, nullptr};
+  size_t ring_doubles = 0;
+  cudaEvent_t ring_ev[2] = {nullptr, nullptr};
   // viscous workspace
   double *q = nullptr, *qtr = nullptr, *qcub = nullptr, *eps = nullptr, *sqrt_eps = nullptr;
   double* d_vinv = nullptr;
@@ -1352,7 +1354,7 @@ void cdg_gpu_level_destroy(cdg_gpu_level* lv) {
   for (void* p : {(void*)lv->u, (void*)lv->res, (void*)lv->rhs, (void*)(lv->tbuf[1] ? lv->tbuf[0] : lv->traces), (void*)lv->before,
                   (void*)lv->q, (void*)lv->qtr, (void*)lv->qcub, (void*)lv->eps, (void*)lv->sqrt_eps, (void*)lv->d_vinv, (void*)lv->d_vcub, (void*)lv->d_wcub, (void*)lv->d_jac,
                   (void*)lv->d_curved_jac, (void*)lv->d_curved_slot,
-                  (void*)lv->d_maxeps, (void*)lv->d_fallbacks, (void*)lv->stage, (void*)lv->metric, (void*)lv->face, (void*)lv->conn,
+                  (void*)lv->d_maxeps, (void*)lv->d_fallbacks, (void*)lv->metric, (void*)lv->face, (void*)lv->conn,
                   (void*)lv->code_map, (void*)lv->h, (void*)lv->frag_icub, (void*)lv->frag_op2,
                   (void*)lv->frag_ig, (void*)lv->frag_aux, (void*)lv->frag_dtil, (void*)lv->wfrag1, (void*)lv->wfrag2v, (void*)lv->wfrag2f, (void*)lv->rfrag2, (void*)lv->tbuf[1],
                   (void*)lv->curved_ids, (void*)lv->curved_jwr, (void*)lv->curved_minv, (void*)lv->frag_opc,
@@ -1363,6 +1365,10 @@ void cdg_gpu_level_destroy(cdg_gpu_level* lv) {
     if (p) cudaFree(p);
   for (double* p : {lv->hsend[0], lv->hsend[1], lv->hrecv})
     if (p) cudaFree(p);
+  for (int s = 0; s < 2; ++s) {
+    if (lv->ring[s]) cudaFreeHost(lv->ring[s]);
+    if (lv->ring_ev[s]) cudaEventDestroy(lv->ring_ev[s]);
+  }
   if (lv->h_coef) cudaFreeHost(lv->h_coef);
   if (lv->h_err) cudaFreeHost(lv->h_err);
   for (auto& e : lv->ev)
@@ -1391,39 +1397,92 @@ long long cdg_gpu_launch_count(const cdg_gpu_level* lv) { return lv->launches; }
 // copy) -- a pitched copy straight from pageable host memory moves row by row.
 // The staging buffer is zeroed once and only its value columns are ever
 // written, so the caller's padding stays exactly zero.
-static void copy_rows(cdg_gpu_level* lv, double* dst, int dst_block, const double* src, int src_block,
-                      int values, int rows, cudaMemcpyKind kind) {
-  if (dst_block == src_block) {
-    CUDA_OK(cudaMemcpyAsync(dst, src, (size_t)rows * src_block * sizeof(double), kind, lv->stream));
+// rows [0, rows) split over up to 16 host threads (the pinned-ring packing)
+static void parallel_rows(int rows, const std::function<void(int, int)>& f) {
+  const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+  const int nt = std::min({hw, 16, std::max(1, rows / 4096)});
+  if (nt <= 1) {
+    f(0, rows);
     return;
   }
+  std::vector<std::thread> th;
+  const int per = (rows + nt - 1) / nt;
+  for (int i = 0; i < nt; ++i) {
+    const int r0 = i * per, r1 = std::min(rows, r0 + per);
+    if (r0 < r1) th.emplace_back([&f, r0, r1] { f(r0, r1); });
+  }
+  for (auto& t : th) t.join();
+}
+
+// Rows of `values` doubles between a row length of src_block and dst_block.
+// Host <-> device: the caller's (pageable) rows are packed by host threads into
+// a pinned two-slot ring in the device layout and moved by DMA, one slot
+// packing while the other transfers (the reference's SolutionStore round trip
+// of rk_step through the adapter); device <-> device: one 2D copy.
+static void copy_rows(cdg_gpu_level* lv, double* dst, int dst_block, const double* src, int src_block,
+                      int values, int rows, cudaMemcpyKind kind) {
   if (kind == cudaMemcpyHostToDevice || kind == cudaMemcpyDeviceToHost) {
-    const int cb = kind == cudaMemcpyHostToDevice ? src_block : dst_block;  // caller's row length
-    const size_t need = (size_t)rows * cb;
-    if (lv->stage_n < need) {
-      if (lv->stage) cudaFree(lv->stage);
-      lv->stage = nullptr;
-      lv->stage_n = 0;
-      CUDA_OK(cudaMalloc(&lv->stage, need * sizeof(double)));
-      lv->stage_n = need;
-      lv->stage_d2h_block = 0;
-    }
-    if (kind == cudaMemcpyHostToDevice) {
-      lv->stage_d2h_block = 0;
-      CUDA_OK(cudaMemcpyAsync(lv->stage, src, need * sizeof(double), kind, lv->stream));
-      CUDA_OK(cudaMemcpy2DAsync(dst, dst_block * sizeof(double), lv->stage, cb * sizeof(double),
-                                values * sizeof(double), rows, cudaMemcpyDeviceToDevice, lv->stream));
-    } else {
-      // the caller's padding columns must read back as zeros: re-zero when the
-      // staging buffer last held another layout or a host upload
-      if (lv->stage_d2h_block != cb) {
-        CUDA_OK(cudaMemsetAsync(lv->stage, 0, need * sizeof(double), lv->stream));
-        lv->stage_d2h_block = cb;
+    const bool h2d = kind == cudaMemcpyHostToDevice;
+    const int db = h2d ? dst_block : src_block, hb = h2d ? src_block : dst_block;  // device / host rows
+    if (!lv->ring[0]) {
+      lv->ring_doubles = (size_t)8 << 20;  // 64 MB per slot
+      for (int s = 0; s < 2; ++s) {
+        CUDA_OK(cudaHostAlloc(&lv->ring[s], lv->ring_doubles * sizeof(double), cudaHostAllocDefault));
+        CUDA_OK(cudaEventCreateWithFlags(&lv->ring_ev[s], cudaEventDisableTiming));
       }
-      CUDA_OK(cudaMemcpy2DAsync(lv->stage, cb * sizeof(double), src, src_block * sizeof(double),
-                                values * sizeof(double), rows, cudaMemcpyDeviceToDevice, lv->stream));
-      CUDA_OK(cudaMemcpyAsync(dst, lv->stage, need * sizeof(double), kind, lv->stream));
     }
+    const int rc = (int)std::max<size_t>(1, lv->ring_doubles / db);  // rows per slot
+    const int nchunks = (rows + rc - 1) / rc;
+    auto chunk = [&](int c, int* r0, int* n) {
+      *r0 = c * rc;
+      *n = std::min(rc, rows - *r0);
+    };
+    if (h2d) {
+      for (int c = 0; c < nchunks; ++c) {
+        int r0, n;
+        chunk(c, &r0, &n);
+        const int s = c & 1;
+        CUDA_OK(cudaEventSynchronize(lv->ring_ev[s]));  // the slot's previous transfer is done
+        double* pin = lv->ring[s];
+        parallel_rows(n, [&](int a, int b) {
+          for (int r = a; r < b; ++r) {
+            double* pr = pin + (size_t)r * db;
+            std::memcpy(pr, src + (size_t)(r0 + r) * hb, (size_t)values * sizeof(double));
+            if (db > values) std::memset(pr + values, 0, (size_t)(db - values) * sizeof(double));
+          }
+        });
+        CUDA_OK(cudaMemcpyAsync(dst + (size_t)r0 * db, pin, (size_t)n * db * sizeof(double), kind, lv->stream));
+        CUDA_OK(cudaEventRecord(lv->ring_ev[s], lv->stream));
+      }
+    } else {
+      auto unpack = [&](int c) {
+        int r0, n;
+        chunk(c, &r0, &n);
+        const int s = c & 1;
+        CUDA_OK(cudaEventSynchronize(lv->ring_ev[s]));
+        const double* pin = lv->ring[s];
+        parallel_rows(n, [&](int a, int b) {
+          for (int r = a; r < b; ++r) {
+            double* hr = dst + (size_t)(r0 + r) * hb;
+            std::memcpy(hr, pin + (size_t)r * db, (size_t)values * sizeof(double));
+            if (hb > values) std::memset(hr + values, 0, (size_t)(hb - values) * sizeof(double));  // caller padding
+          }
+        });
+      };
+      for (int c = 0; c < nchunks; ++c) {
+        int r0, n;
+        chunk(c, &r0, &n);
+        const int s = c & 1;  // its previous chunk (c - 2) was unpacked in iteration c - 1
+        CUDA_OK(cudaMemcpyAsync(lv->ring[s], src + (size_t)r0 * db, (size_t)n * db * sizeof(double), kind, lv->stream));
+        CUDA_OK(cudaEventRecord(lv->ring_ev[s], lv->stream));
+        if (c > 0) unpack(c - 1);
+      }
+      if (nchunks > 0) unpack(nchunks - 1);
+    }
+    return;
+  }
+  if (dst_block == src_block) {
+    CUDA_OK(cudaMemcpyAsync(dst, src, (size_t)rows * src_block * sizeof(double), kind, lv->stream));
     return;
   }
   CUDA_OK(cudaMemcpy2DAsync(dst, dst_block * sizeof(double), src, src_block * sizeof(double),
