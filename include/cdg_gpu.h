@@ -316,11 +316,17 @@ int cdg_gpu_set_max_ctas(cdg_gpu_level *lv, int max_ctas);
 
 /* Kernel family of a level. DEFAULT: the per-order choice compiled into the
  * kernel-set table (row-per-warp / warp-tile kernels with fused traces where
- * measured fastest). GENERIC: the CTA kernels (k_rhs,
- * k_rhs_curved) for every element, the p >= 6 path; tests cross-check the two
- * families against each other and against the reference at every order. */
+ * measured fastest; at p <= 2 on single-shard straight meshes
+ * the neighbour-state kernel, which reads the neighbours' nodal states
+ * instead of stored traces and so agrees with the other paths to rounding
+ * only). GENERIC: the CTA kernels (k_rhs, k_rhs_curved) for every element,
+ * the p >= 6 path. TRACED: DEFAULT without the neighbour-state kernel (every
+ * stage through stored traces, the paths that agree bit for bit). Tests
+ * cross-check the families against each other and against the reference at
+ * every order. */
 #define CDG_GPU_PATH_DEFAULT 0
 #define CDG_GPU_PATH_GENERIC 1
+#define CDG_GPU_PATH_TRACED 2
 int cdg_gpu_set_kernel_path(cdg_gpu_level *lv, int path);
 
 /* HLLC -> LLF fallbacks counted since the level was created (degenerate wave

@@ -224,6 +224,15 @@ struct cdg_gpu_level {
   double gft_gamma[2] = {0.0, 0.0};
   int gft_launches = 0;
   bool use_row = false;
+  // neighbour-state path (cdg_ns.cuh): state ping-pong u = ubuf[ucur], no stored traces
+  bool use_ns = false;
+  double* ubuf[2] = {nullptr, nullptr};
+  int ucur = 0;
+  double* d_ig = nullptr;  // I_g row-major [NF][NP]
+  cudaGraphExec_t gns[2] = {nullptr, nullptr};
+  int gns_riemann[2] = {-1, -1};
+  double gns_gamma[2] = {0.0, 0.0};
+  int gns_launches = 0;
   const int* cur_tiles = nullptr;  // tile list of the next RHS launch (null: all)
   const unsigned long long* cur_gate = nullptr;  // launch gate of the next launches (null: none)
   int cur_gate_when = 0;
@@ -339,6 +348,27 @@ void launch_traces(cdg_gpu_level* lv, const double* u, double* traces) {
 // MODE 32, or the warp-tile kernel); curved levels use the trace kernel
 bool fused_traces(const cdg_gpu_level* lv) {
   return lv->n_curved == 0 && ((lv->use_row && lv->ks->row_ft) || (!lv->use_row && lv->use_warp));
+}
+
+// the captured graphs that bake the state pointer u and the trace buffers
+void drop_graphs_except_ns(cdg_gpu_level* lv) {
+  if (lv->graph) cudaGraphExecDestroy(lv->graph), lv->graph = nullptr;
+  if (lv->graph_visc) cudaGraphExecDestroy(lv->graph_visc), lv->graph_visc = nullptr;
+  for (auto& ge : lv->gft)
+    if (ge) cudaGraphExecDestroy(ge), ge = nullptr;
+}
+
+// the neighbour-state kernel runs inviscid stages of an all-affine level
+// without halo rows or phase lists (single-shard runs)
+bool ns_path(const cdg_gpu_level* lv) {
+  return lv->use_ns && lv->n_curved == 0 && lv->n_halo == 0 && !lv->cur_tiles && !lv->cur_gate;
+}
+
+void ensure_ubuf(cdg_gpu_level* lv) {
+  if (lv->ubuf[1]) return;
+  const size_t n = (size_t)lv->K * 5 * lv->bp;
+  CUDA_OK(cudaMalloc(&lv->ubuf[1], n * sizeof(double)));
+  CUDA_OK(cudaMemset(lv->ubuf[1], 0, n * sizeof(double)));  // padding columns: zero, never written
 }
 
 void ensure_tbuf(cdg_gpu_level* lv) {
@@ -475,6 +505,34 @@ void launch_rhs_warp(cdg_gpu_level* lv, bool update, int stage) {
   fn<<<ctas, 32 * lv->ks->warp_warps, lv->ks->smem_warp, lv->stream>>>(w);
   ++lv->launches;
   launch_curved(lv, update, stage);
+}
+
+// one stage of the neighbour-state kernel: reads u_in (own + neighbour rows)
+// and res, writes res and u_out (cdg_ns.cuh)
+void launch_rhs_ns(cdg_gpu_level* lv, int stage, const double* u_in, double* u_out) {
+  WarpParams w{};
+  w.u = const_cast<double*>(u_in);
+  w.u_out = u_out;
+  w.res = lv->res;
+  w.metric = lv->metric;
+  w.face = lv->face;
+  w.conn = lv->conn;
+  w.code_map = lv->code_map;
+  w.frag1 = reinterpret_cast<const double2*>(lv->wfrag1);
+  w.frag2v = reinterpret_cast<const double2*>(lv->wfrag2v);
+  w.frag2f = reinterpret_cast<const double2*>(lv->wfrag2f);
+  w.ig = lv->d_ig;
+  w.coef = lv->d_coef;
+  w.stage = stage;
+  w.K = lv->K;
+  w.elem_offset = 0;
+  w.gas = lv->gas;
+  w.err = lv->d_err;
+  const int tiles = (lv->K + 15) / 16;
+  const int ctas = lv->cap((tiles + lv->ks->ns_warps - 1) / lv->ks->ns_warps, lv->ks->ns_minb);
+  const int rm = lv->gas.riemann == 1 ? 1 : 0;
+  lv->ks->ns_update[rm]<<<ctas, 32 * lv->ks->ns_warps, lv->ks->smem_ns, lv->stream>>>(w);
+  ++lv->launches;
 }
 
 void launch_rhs_row(cdg_gpu_level* lv, bool update, int stage) {
@@ -960,10 +1018,14 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
       for (int fc = 0; fc < nfch; ++fc)
         for (int n = 0; n < nt; ++n) frag_nat(f2f, neg_lift, np, nf, n, fc);
       lv->wfrag1 = dev_upload(f1);
-      if (!lv->ks->warp_update[0]) f2v.clear(), f2f.clear();
+      if (!lv->ks->warp_update[0] && !lv->ks->ns_update[0]) f2v.clear(), f2f.clear();
       lv->wfrag2v = dev_upload(f2v);
       lv->wfrag2f = dev_upload(f2f);
       lv->use_warp = lv->ks->warp_update[0] != nullptr;
+    }
+    if (lv->ks->ns_update[0] && lv->wfrag2v) {
+      lv->d_ig = dev_upload(ig);
+      lv->use_ns = true;
     }
     if (d->vandermonde_inv) {
       lv->d_vinv = dev_upload(std::vector<double>(d->vandermonde_inv, d->vandermonde_inv + (size_t)np * np));
@@ -1146,6 +1208,7 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
     const size_t n = (size_t)K * 5 * lv->bp;
     const size_t ntr = (size_t)(K + lv->n_halo) * 5 * lv->tb;
     CUDA_OK(cudaMalloc(&lv->u, n * sizeof(double)));
+    lv->ubuf[0] = lv->u;
     CUDA_OK(cudaMalloc(&lv->res, n * sizeof(double)));
     CUDA_OK(cudaMalloc(&lv->rhs, n * sizeof(double)));
     CUDA_OK(cudaMalloc(&lv->traces, ntr * sizeof(double)));
@@ -1184,6 +1247,9 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
     if (lv->ks->warp_update[0])
       for (auto fn : {lv->ks->warp_update[0], lv->ks->warp_update[1], lv->ks->warp_only[0], lv->ks->warp_only[1]})
         CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lv->ks->smem_warp));
+    if (lv->ks->ns_update[0])
+      for (auto fn : {lv->ks->ns_update[0], lv->ks->ns_update[1]})
+        CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lv->ks->smem_ns));
     if (lv->n_curved && lv->ks->rowc_aux) {
       CUDA_OK(cudaFuncSetAttribute(lv->ks->rowc_aux, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)lv->ks->smem_rowc_aux));
@@ -1351,7 +1417,9 @@ void cdg_gpu_level_destroy(cdg_gpu_level* lv) {
   if (lv->graph_visc) cudaGraphExecDestroy(lv->graph_visc);
   for (auto ge : lv->gft)
     if (ge) cudaGraphExecDestroy(ge);
-  for (void* p : {(void*)lv->u, (void*)lv->res, (void*)lv->rhs, (void*)(lv->tbuf[1] ? lv->tbuf[0] : lv->traces), (void*)lv->before,
+  for (auto ge : lv->gns)
+    if (ge) cudaGraphExecDestroy(ge);
+  for (void* p : {(void*)lv->ubuf[0], (void*)lv->ubuf[1], (void*)lv->d_ig, (void*)lv->res, (void*)lv->rhs, (void*)(lv->tbuf[1] ? lv->tbuf[0] : lv->traces), (void*)lv->before,
                   (void*)lv->q, (void*)lv->qtr, (void*)lv->qcub, (void*)lv->eps, (void*)lv->sqrt_eps, (void*)lv->d_vinv, (void*)lv->d_vcub, (void*)lv->d_wcub, (void*)lv->d_jac,
                   (void*)lv->d_curved_jac, (void*)lv->d_curved_slot,
                   (void*)lv->d_maxeps, (void*)lv->d_fallbacks, (void*)lv->metric, (void*)lv->face, (void*)lv->conn,
@@ -1618,6 +1686,62 @@ int cdg_gpu_rk_steps(cdg_gpu_level* lv, const cdg_gpu_run_config* cfg, int nstep
       lv->last_viscous = bits != 0;
       return;
     }
+    if (ns_path(lv)) {
+      // neighbour-state kernel: stage s reads ubuf[(b+s)%2] and writes the
+      // other; five stages per step, so the state changes buffer every step
+      ensure_ubuf(lv);
+      double* const u_entry = lv->u;
+      auto stage_launch = [&](int b, int stage) {
+        launch_rhs_ns(lv, stage, lv->ubuf[(b + stage) & 1], lv->ubuf[(b + stage + 1) & 1]);
+      };
+      if (lv->profiling) {
+        float t_rhs = 0.f;
+        for (int s = 0; s < nsteps; ++s) {
+          for (int stage = 0; stage < 5; ++stage) {
+            CUDA_OK(cudaEventRecord(lv->ev[1], lv->stream));
+            stage_launch(lv->ucur, stage);
+            CUDA_OK(cudaEventRecord(lv->ev[2], lv->stream));
+            CUDA_OK(cudaEventSynchronize(lv->ev[2]));
+            float y;
+            CUDA_OK(cudaEventElapsedTime(&y, lv->ev[1], lv->ev[2]));
+            t_rhs += y;
+          }
+          lv->ucur ^= 1;
+          lv->u = lv->ubuf[lv->ucur];
+        }
+        lv->prof[0] = 0.0;
+        lv->prof[1] = t_rhs;
+        lv->prof[2] = 5.0 * nsteps;
+      } else {
+        for (int s = 0; s < nsteps; ++s) {
+          const int b = lv->ucur;
+          if (!lv->gns[b] || lv->gns_riemann[b] != cfg->riemann || lv->gns_gamma[b] != cfg->gamma) {
+            if (lv->gns[b]) cudaGraphExecDestroy(lv->gns[b]);
+            lv->gns[b] = nullptr;
+            cudaGraph_t g;
+            const long long l0 = lv->launches;
+            CUDA_OK(cudaStreamBeginCapture(lv->stream, cudaStreamCaptureModeThreadLocal));
+            for (int stage = 0; stage < 5; ++stage) stage_launch(b, stage);
+            lv->gns_launches = (int)(lv->launches - l0);
+            lv->launches = l0;
+            CUDA_OK(cudaStreamEndCapture(lv->stream, &g));
+            CUDA_OK(cudaGraphInstantiate(&lv->gns[b], g, 0));
+            CUDA_OK(cudaGraphDestroy(g));
+            lv->gns_riemann[b] = cfg->riemann;
+            lv->gns_gamma[b] = cfg->gamma;
+          }
+          CUDA_OK(cudaGraphLaunch(lv->gns[b], lv->stream));
+          lv->launches += lv->gns_launches;
+          lv->ucur ^= 1;
+          lv->u = lv->ubuf[lv->ucur];
+        }
+      }
+      lv->traces_valid = false;                       // no traces on this path
+      if (lv->u != u_entry) drop_graphs_except_ns(lv);  // they baked the other state buffer
+      CUDA_OK(cudaGetLastError());
+      check_device_error(lv);
+      return;
+    }
     if (fused_traces(lv)) {
       // fused traces: each RHS launch writes the next stage's traces into the
       // other half of a double buffer; a trace kernel seeds it only when the
@@ -1747,11 +1871,12 @@ int cdg_gpu_set_freestream(cdg_gpu_level* lv, const double* fs) {
     cudaGraphExecDestroy(lv->graph_visc);
     lv->graph_visc = nullptr;
   }
-  for (auto& ge : lv->gft)
-    if (!same && ge) {
-      cudaGraphExecDestroy(ge);
-      ge = nullptr;
-    }
+  for (auto* gs : {lv->gft, lv->gns})
+    for (int i = 0; i < 2; ++i)
+      if (!same && gs[i]) {
+        cudaGraphExecDestroy(gs[i]);
+        gs[i] = nullptr;
+      }
   for (int c = 0; c < 5; ++c) {
     lv->freestream[c] = fs[c];
     lv->gas.fs[c] = fs[c];
@@ -1763,16 +1888,17 @@ int cdg_gpu_set_max_ctas(cdg_gpu_level* lv, int max_ctas) {
   if (max_ctas < 0) return CDG_GPU_ERR_CONFIG;
   lv->max_ctas = max_ctas;
   // grids are baked into the captured graphs
-  if (lv->graph) cudaGraphExecDestroy(lv->graph), lv->graph = nullptr;
-  if (lv->graph_visc) cudaGraphExecDestroy(lv->graph_visc), lv->graph_visc = nullptr;
-  for (auto& ge : lv->gft)
+  drop_graphs_except_ns(lv);
+  for (auto& ge : lv->gns)
     if (ge) cudaGraphExecDestroy(ge), ge = nullptr;
   return CDG_GPU_OK;
 }
 
 int cdg_gpu_set_kernel_path(cdg_gpu_level* lv, int path) {
-  if (path != CDG_GPU_PATH_DEFAULT && path != CDG_GPU_PATH_GENERIC) return CDG_GPU_ERR_CONFIG;
+  if (path != CDG_GPU_PATH_DEFAULT && path != CDG_GPU_PATH_GENERIC && path != CDG_GPU_PATH_TRACED)
+    return CDG_GPU_ERR_CONFIG;
   const bool generic = path == CDG_GPU_PATH_GENERIC;
+  lv->use_ns = path == CDG_GPU_PATH_DEFAULT && lv->d_ig != nullptr;
   lv->use_row = !generic && lv->ks->row_update[0] != nullptr;
   lv->use_warp = !generic && lv->ks->warp_update[0] != nullptr;
   lv->use_rowc = !generic && lv->rfrag_opc != nullptr;

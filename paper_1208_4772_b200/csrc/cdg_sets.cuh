@@ -9,6 +9,7 @@
 #include "cdg_aux.cuh"
 #include "cdg_curved.cuh"
 #include "cdg_kernels.cuh"
+#include "cdg_ns.cuh"
 #include "cdg_row.cuh"
 #include "cdg_rowc.cuh"
 #include "cdg_wa.cuh"
@@ -38,6 +39,10 @@ struct KernelSet {
   void (*warp_only[2])(WarpParams) = {nullptr, nullptr};
   size_t smem_warp = 0;
   int warp_warps = 0, warp_minb = 0;
+  // neighbour-state kernel (cdg_ns.cuh): affine levels, no stored traces, p <= 2
+  void (*ns_update[2])(WarpParams) = {nullptr, nullptr};  // [riemann]
+  size_t smem_ns = 0;
+  int ns_warps = 0, ns_minb = 0;
   // row-per-warp inviscid kernel (cdg_row.cuh), p = 4
   void (*row_update[2])(RhsParams) = {nullptr, nullptr};  // [riemann]
   void (*row_only[2])(RhsParams) = {nullptr, nullptr};
@@ -165,6 +170,17 @@ KernelSet with_warp(KernelSet k) {
   k.smem_warp = W::SMEM_BYTES;
   k.warp_warps = WARPS;
   k.warp_minb = MINB;
+  return k;
+}
+
+template <int NP, int NCUB, int NG, int WARPS = 4, int MINB = 4>
+KernelSet with_ns(KernelSet k) {
+  using N = NsCfg<NP, NCUB, NG, WARPS, MINB>;
+  k.ns_update[0] = &k_rhs_ns<N, 0>;
+  k.ns_update[1] = &k_rhs_ns<N, 1>;
+  k.smem_ns = N::SMEM_BYTES;
+  k.ns_warps = WARPS;
+  k.ns_minb = MINB;
   return k;
 }
 

@@ -88,6 +88,8 @@ struct WarpParams {
   int gate_when;
   double* traces_out;         // fused traces of u_new (next stage), or null
   const double2* frag_ig_nat; // I_g B fragments, natural pairing [NF8/8][KS1][32]
+  double* u_out;              // k_rhs_ns: the new state (u is the stage-start state)
+  const double* ig;           // k_rhs_ns: I_g row-major [NF][NP]
 };
 
 template <class C, bool UPDATE, int RIEMANN>

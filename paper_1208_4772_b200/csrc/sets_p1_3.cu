@@ -3,6 +3,13 @@
 #define CDG_SET_TU
 #include "cdg_sets.cuh"
 
+#ifndef CDG_P1NS_MINB
+#define CDG_P1NS_MINB 4
+#endif
+#ifndef CDG_P1NS_WARPS
+#define CDG_P1NS_WARPS 4
+#endif
+
 namespace cdg_gpu {
 
 std::vector<KernelSet> kernel_sets_p1_3() {
@@ -10,7 +17,7 @@ std::vector<KernelSet> kernel_sets_p1_3() {
       // straight-sided strengths (2p+1 / 2p): refelem.cpp:311-317
       // p=1: warp-tile kernel, 4 CTAs (16 warps) per SM at 128 registers (0.40 ms
       // vs 0.52 at 2 CTAs/SM and 0.50 for the row kernel, make_cube_mesh(44))
-      with_rowc<4, 5, 3, 8, 32, 4>(with_warp<4, 5, 3, 4, 4>(make_set<4, 5, 3, 16, 8, 2>())),
+      with_ns<4, 5, 3, CDG_P1NS_WARPS, CDG_P1NS_MINB>(with_rowc<4, 5, 3, 8, 32, 4>(with_warp<4, 5, 3, 4, 4>(make_set<4, 5, 3, 16, 8, 2>()))),
       // p=2: row-per-warp kernel with fused traces and unrolled k-steps (3.14e10
       // DOF-updates/s vs 2.41e10 for the warp-tile kernel + trace kernel; the
       // warp-autonomous kernel 8% slower here); the set serves curved-mesh p=2

@@ -404,8 +404,10 @@ class GpuLevel:
         _raise(lib().cdg_gpu_set_max_ctas(self.h, int(n)), "set_max_ctas failed")
 
     def set_kernel_path(self, path: str):
-        """'default' (per-order compiled choice) or 'generic' (CTA kernels everywhere)."""
-        code = {"default": 0, "generic": 1}[path]
+        """'default' (per-order compiled choice), 'generic' (CTA kernels
+        everywhere) or 'traced' (default without the neighbour-state kernel:
+        every stage through stored traces, bitwise equal to the split paths)."""
+        code = {"default": 0, "generic": 1, "traced": 2}[path]
         _raise(lib().cdg_gpu_set_kernel_path(self.h, code), "set_kernel_path failed")
 
     def set_profiling(self, on: bool):

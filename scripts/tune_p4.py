@@ -3,8 +3,9 @@ builds of the C ABI side by side on the same synthetic workload.
 
     python scripts/tune_p4.py [--n 64] [--steps 6] [--riemann llf] LIB [LIB ...]
 
-Each LIB (paper_1208_4772_b200/libcdg_gpu.so or a build.build_variant library)
-runs in its own process. Per library: graph-replayed ms per RK step (CUDA
+Each LIB (paper_1208_4772_b200/libcdg_gpu.so or a build.build_variant library,
+optionally suffixed @traced / @generic for that kernel path) runs in its own
+process. Per library: graph-replayed ms per RK step (CUDA
 events on the level's stream), the profiled per-launch RHS-kernel time, the
 FP64 fraction of the stage model, and a checksum of the state after the steps
 (equal checksums: identical arithmetic)."""
@@ -23,6 +24,7 @@ def child(lib, n, steps, riemann, p, curved=False, visc=False):
     import torch
 
     from paper_1208_4772_b200 import gpu, partition, refelem as R
+    lib, _, path = str(lib).partition("@")  # LIB@traced|generic: that kernel path
     gpu.use_library(lib)
     import bench
     re = R.get_reference_element(p)
@@ -34,6 +36,8 @@ def child(lib, n, steps, riemann, p, curved=False, visc=False):
                           curved=(np.arange(part.mesh.n_owned), M.warped_nodes(part.mesh, re)))
     else:
         lv = gpu.GpuLevel(part.mesh, p, bc=0, freestream=bench.freestream_state(), re=re)
+    if path:
+        lv.set_kernel_path(path)
     K, npb = lv.K, lv.n_basis
     g = np.random.default_rng(42)
     u = np.zeros((K, 5, lv.block))
@@ -66,7 +70,7 @@ def child(lib, n, steps, riemann, p, curved=False, visc=False):
     peak = max(gpu.measure_fp64_peak(0))
     rhs_ms = t_rhs / (5 * steps)
     uu = lv.get_state()[0]
-    print(json.dumps({"lib": str(lib), "K": K, "ms_per_step": ms_step, "rhs_ms": rhs_ms,
+    print(json.dumps({"lib": str(lib) + ("@" + path if path else ""), "K": K, "ms_per_step": ms_step, "rhs_ms": rhs_ms,
                       "frac_graph": F * K / (ms_step / 5 * 1e-3) / 1e12 / peak,
                       "frac_rhs": F * K / (rhs_ms * 1e-3) / 1e12 / peak if rhs_ms > 0 else None, "peak": peak,
                       "checksum": float(np.sum(uu)), "fused": lv.fused_traces(), "trace_ms": t_tr / (5 * steps)}), flush=True)

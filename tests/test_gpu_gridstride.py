@@ -97,10 +97,11 @@ def test_p4_cube14_rk_steps_match_reference_default_and_capped_grid(gpu_lib, ref
 
 @pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7, 8])
 @pytest.mark.parametrize("riemann", ["llf", "hllc"])
-@pytest.mark.parametrize("path", ["default", "generic"])
+@pytest.mark.parametrize("path", ["default", "generic", "traced"])
 def test_capped_grid_is_bitwise_default_grid_and_matches_oracle(gpu_lib, p, riemann, path):
-    """Every kernel family (warp-tile p=1, row-per-warp p=2..5 with fused traces
-    at p<=4, CTA kernel p>=6 and the generic path everywhere) with 2 CTAs in
+    """Every kernel family (neighbour-state p=1, warp-tile p=1 on the traced
+    path, row-per-warp / warp-autonomous p=2..5 with fused traces at p<=4, CTA
+    kernel p>=6 and the generic path everywhere) with 2 CTAs in
     the grid: RHS and 3 RK steps bitwise equal to the default grid, and the
     RK steps within the north_star tolerance of the oracle."""
     gpu = gpu_lib
