@@ -469,12 +469,18 @@ def main():
         launches_rhs = 5 * prof_steps
         t_rhs = prof_rhs / launches_rhs * 1e-3
         t_tr = prof_tr / launches_rhs * 1e-3
-        fused = lv.fused_traces()
         kname = lv.rhs_kernel()
+        ns = kname == "k_rhs_ns"
+        fused = lv.fused_traces() or ns
         # the fused kernel also produces the next stage's traces: its work is the
-        # whole stage model F (trace GEMM included); else F_rhs
+        # whole stage model F (trace GEMM included); else F_rhs.
+        # k_rhs_ns interpolates the face states itself (no stored traces): F, and
+        # its bytes are the state (u, res read + write), one read of each
+        # element's state as a neighbour, and the geometry -- no trace rows
         F_k = F if fused else F_rhs
         ex_k = ex_rhs + ex_tr if fused else ex_rhs
+        if ns:
+            B = 200 * npb + 208 + 32
         achieved = F_k * K / t_rhs / 1e12
         traffic = None
         ncu_file = ROOT / "profiles" / f"ncu_rhs_p{p}.json"
@@ -483,7 +489,8 @@ def main():
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "kernel": f"{kname}<P={p}> (fused volume+surface+lift+LSRK update"
-                          + (" + next-stage traces" if fused else "") + ", FP64 DMMA"
+                          + (" + face states interpolated from the nodal states (no stored traces)" if ns
+                             else " + next-stage traces" if fused else "") + ", FP64 DMMA"
                           + (", warp-autonomous: 3 elements per warp, no CTA barrier" if kname == "k_rhs_wa" else "")
                           + ")",
                 "fused_traces": fused,
@@ -498,6 +505,7 @@ def main():
                 "profiled_steps": prof_steps,
                 "kernel_share_of_step": prof_rhs / prof_steps / ms_per_step,
                 "executed_dmma_tflops": ex_k * K / t_rhs / 1e12,
+                "model_bytes_per_element": B,
                 "hbm_achieved_gbs": B * K / t_rhs / 1e9, "hbm_peak_gbs": hbm_peak,
                 "hbm_frac": B * K / t_rhs / 1e9 / hbm_peak,
                 "stage_model_tflops": F * K / ((t_rhs + t_tr)) / 1e12}

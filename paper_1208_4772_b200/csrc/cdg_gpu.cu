@@ -831,6 +831,7 @@ int cdg_gpu_fused_traces(const cdg_gpu_level* lv) {
 }
 
 const char* cdg_gpu_rhs_kernel(const cdg_gpu_level* lv) {
+  if (ns_path(lv)) return "k_rhs_ns";  // inviscid rk_steps
   if (lv->use_row) return lv->ks->row_name;
   if (lv->use_warp) return "k_rhs_warp";
   return "k_rhs";
