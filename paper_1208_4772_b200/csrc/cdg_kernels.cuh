@@ -635,11 +635,9 @@ __device__ __forceinline__ void tile_coords(int t_begin, int i, int& mt, int& nt
   }
 }
 
-// DBG (timing experiments only): 1 = skip the SIMT pointwise/face work,
-// 2 = skip the tensor-core GEMMs. Never used for results.
 // RM: Riemann solver baked in at compile time (0 LLF, 1 HLLC, -1 runtime
 // p.gas.riemann): the LLF-only instantiation needs far fewer registers.
-template <class C, bool UPDATE, bool VISC, int DBG = 0, int RM = -1>
+template <class C, bool UPDATE, bool VISC, int RM = -1>
 __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs(RhsParams p) {
   if (gated_off(p.gate, p.gate_when)) return;
   extern __shared__ __align__(16) double smem[];
@@ -718,20 +716,20 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs(RhsParams p) {
     for (int ch = 0; ch < C::NCH; ++ch) {
       const int q0 = ch * C::CH;
       const int w = (C::NCUB8 - q0) < C::CH ? (C::NCUB8 - q0) : C::CH;  // 16 or 8
-      if (DBG != 2) gemm1_chunk<C>(sU, sC, fb1, q0, w, warp, lane);
+      gemm1_chunk<C>(sU, sC, fb1, q0, w, warp, lane);
       __syncthreads();
       // pointwise Euler flux -> contravariant flux G_m = sum_d (dr_m/dx_d) F_d
 #pragma unroll
       for (int it = 0; it < C::IT_P; ++it) {
         const int idx = tid + it * C::NTH;
-        if (DBG != 1 && idx < C::E * w) {
+        if (idx < C::E * w) {
           const int e = idx / w, ql = idx - e * w, q = q0 + ql;
           const double* uc = sC + (e * 5) * C::LDC + ql;
           double* gout = sG + (e * 5) * C::LDG;
           double G[3][5];
           if (q < C::NCUB && e0 + e < p.K) {
             const State5 s{uc[0], uc[C::LDC], uc[2 * C::LDC], uc[3 * C::LDC], uc[4 * C::LDC]};
-            if (DBG == 0 && !admissible(s, gamma)) record_error(p.err, 1, p.elem_offset + e0 + e, q, 0, s.r);
+            if (!admissible(s, gamma)) record_error(p.err, 1, p.elem_offset + e0 + e, q, 0, s.r);
             const double ir = 1.0 / s.r;
             const double pr = (gamma - 1.0) * (s.E - 0.5 * ir * (s.mx * s.mx + s.my * s.my + s.mz * s.mz));
             const double vx = s.mx * ir, vy = s.my * ir, vz = s.mz * ir;
@@ -789,12 +787,10 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs(RhsParams p) {
         }
       }
       __syncthreads();
-      if (DBG != 2) {
-        if (w == C::CH)
-          gemm2_fixed<C, 3 * C::CH / 8>(acc, sG, fb2, (3 * q0) / 8, t_begin, t_end, lane);
-        else
-          gemm2_partial<C>(acc, sG, fb2, (3 * q0) / 8, (3 * w) / 8, t_begin, t_end, lane);
-      }
+      if (w == C::CH)
+        gemm2_fixed<C, 3 * C::CH / 8>(acc, sG, fb2, (3 * q0) / 8, t_begin, t_end, lane);
+      else
+        gemm2_partial<C>(acc, sG, fb2, (3 * q0) / 8, (3 * w) / 8, t_begin, t_end, lane);
       __syncthreads();
     }
 
@@ -806,7 +802,7 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs(RhsParams p) {
 #pragma unroll 1
       for (int it = 0; it < C::IT_F; ++it) {
         const int idx = tid + it * C::NTH;
-        if (DBG == 1 || idx >= C::E * wp) continue;
+        if (idx >= C::E * wp) continue;
         const int e = idx / wp, fl = idx - e * wp, fq = f0 + fl;
         double* gout = sG + (e * 5) * C::LDG + pcol(fl);
         const int eg = e0 + e;
@@ -830,7 +826,7 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs(RhsParams p) {
         } else {
           up = boundary_state(um, fn.x, fn.y, fn.z, (cw.y >> 2) & 3, p.gas);
         }
-        if (DBG == 0 && (!admissible(um, gamma) || !admissible(up, gamma)))
+        if (!admissible(um, gamma) || !admissible(up, gamma))
           record_error(p.err, 2, p.elem_offset + eg, f, gq, um.r);
         double fs[5];
         if (RM == 1 || (RM == -1 && p.gas.riemann == 1))
@@ -861,12 +857,10 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs(RhsParams p) {
         for (int c = 0; c < 5; ++c) gout[c * C::LDG] = fn.w * fs[c];
       }
       __syncthreads();
-      if (DBG != 2) {
-        if (wp == C::FCH)
-          gemm2_fixed<C, C::FCH / 8>(acc, sG, fb2, (C::K2CUB + f0) / 8, t_begin, t_end, lane);
-        else
-          gemm2_partial<C>(acc, sG, fb2, (C::K2CUB + f0) / 8, wp / 8, t_begin, t_end, lane);
-      }
+      if (wp == C::FCH)
+        gemm2_fixed<C, C::FCH / 8>(acc, sG, fb2, (C::K2CUB + f0) / 8, t_begin, t_end, lane);
+      else
+        gemm2_partial<C>(acc, sG, fb2, (C::K2CUB + f0) / 8, wp / 8, t_begin, t_end, lane);
       __syncthreads();
     }
 

@@ -140,7 +140,6 @@ __global__ void __launch_bounds__(32 * C::WARPS, C::MINB) k_rhs_warp(WarpParams 
       for (int n = 0; n < C::NT; ++n) acc[c][n][0] = acc[c][n][1] = acc[c][n][2] = acc[c][n][3] = 0.0;
 
     // ---- volume ------------------------------------------------------------
-#ifndef CDG_W_NOVOL
 #pragma unroll 1
     for (int ch = 0; ch < C::NCH; ++ch) {
       double uc[5][4];
@@ -209,10 +208,8 @@ __global__ void __launch_bounds__(32 * C::WARPS, C::MINB) k_rhs_warp(WarpParams 
         }
       }
     }
-#endif
 
     // ---- surface: chunks of 8 face nodes -------------------------------------
-#ifndef CDG_W_NOFACE
 #pragma unroll 1
     for (int fc = 0; fc < C::NFCH; ++fc) {
       double2 b[C::NT];
@@ -260,7 +257,6 @@ __global__ void __launch_bounds__(32 * C::WARPS, C::MINB) k_rhs_warp(WarpParams 
 #pragma unroll
         for (int n = 0; n < C::NT; ++n) dmma_k8(acc[c][n], fl[0][c], fl[2][c], fl[1][c], fl[3][c], b[n].x, b[n].y);
     }
-#endif
 
     // ---- epilogue: rhs -> (res, u) update or rhs store -----------------------
     double a_c = 0.0, b_c = 0.0, dt = 0.0;
