@@ -1,6 +1,6 @@
 """Small cases for compute-sanitizer (racecheck / synccheck / memcheck /
-initcheck) over the hot kernels: the fused P=4 row kernel (k_rhs_row, fused
-traces, HLLC and LLF) and the curved row kernel (k_rhs_rowc) with the grid
+initcheck) over the hot kernels: the fused P=4 kernel (fused traces, HLLC
+and LLF), the p=1 neighbour-state kernel and the curved kernel with the grid
 capped at 2 CTAs, so every CTA runs several tiles through the grid-stride
 loop (the cross-tile shared-memory restaging and the fused-trace double
 buffer are exercised), plus the curved viscous path and a 2-shard multi-rank
@@ -23,6 +23,15 @@ for riemann in ("llf", "hllc"):
     lv.rk_steps(cfg, dt, 1)
     lv.compute_rhs(cfg)
     print("affine p=4", riemann, "fused", lv.fused_traces(), flush=True)
+    lv.close()
+for riemann in ("llf", "hllc"):  # p=1: the neighbour-state kernel (ping-pong state, no traces)
+    lv = gpu.GpuLevel(m, 1, bc=1, freestream=fs)
+    lv.set_max_ctas(2)
+    lv.set_state(gpu.random_admissible_store(lv, seed=6))
+    cfg = gpu.run_config(riemann)
+    dt = 0.2 * lv.compute_timestep(cfg)
+    lv.rk_steps(cfg, dt, 3)
+    print("affine p=1", riemann, lv.rhs_kernel(), flush=True)
     lv.close()
 re = R.level_reference_element(4, True)
 ids = np.arange(m.n_owned)
