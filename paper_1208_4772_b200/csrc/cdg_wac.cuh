@@ -14,6 +14,9 @@
 #ifndef CDG_WAC_FUNROLL
 #define CDG_WAC_FUNROLL 1
 #endif
+#ifndef CDG_WAC_METPRE
+#define CDG_WAC_METPRE 1  // a lane's per-node metrics loaded before the chunk's GEMM1 (latency hidden)
+#endif
 
 namespace cdg_gpu {
 
@@ -38,6 +41,7 @@ struct WacCfg {
   static constexpr size_t SMEM_BYTES = sizeof(double) * (size_t)PERW * WARPS_;
   static constexpr int IT_P = ceil_div(EPW * CH, 32), IT_F = ceil_div(EPW * FCH, 32);
   static constexpr int FUNROLL = CDG_WAC_FUNROLL;  // face-item loop unroll (tuning)
+  static constexpr bool METPRE = CDG_WAC_METPRE && IT_P == 1;
 };
 
 template <class C, bool UPDATE, int RM, int KIND = 0>
@@ -119,6 +123,14 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_wac(CurvedParams cp) {
       const int q0 = ch * C::CH;
       const int w = min(C::CH, C::NCUB8 - q0);
       const double2* fb1 = fb1all + (size_t)(q0 / 8) * C::KS1 * 32;
+      double mpre[9];  // METPRE: this lane's pointwise item's metrics, in flight during GEMM1
+      if (C::METPRE) {
+        const int e = lane / w, q = q0 + lane - e * w;
+        const bool ok = lane < C::EPW * w && q < C::NCUB && c0 + e < cp.Kc;
+        const double* met = cp.jwr + (ok ? ((size_t)(c0 + e) * C::NCUB + q) * 9 : 0);
+#pragma unroll
+        for (int k = 0; k < 9; ++k) mpre[k] = ok ? __ldg(met + k) : 0.0;
+      }
       {  // GEMM1: U_cub[rows, q0:q0+w], the gathered U rows as A fragments
         double c1[C::CH / 8][4];
 #pragma unroll
@@ -162,7 +174,7 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_wac(CurvedParams cp) {
             for (int ma = 0; ma < 3; ++ma)
 #pragma unroll
               for (int k = 0; k < 3; ++k) {
-                const double jk = __ldg(met + k * 3 + ma);
+                const double jk = C::METPRE ? mpre[k * 3 + ma] : __ldg(met + k * 3 + ma);
 #pragma unroll
                 for (int c = 0; c < 5; ++c) gout[ma * 16 * C::LDG + k * w + c * C::LDG] = -se * (jk * uv[c]);
               }
@@ -178,7 +190,9 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_wac(CurvedParams cp) {
             if (VISC) se = p.sqrt_eps[sId[e]];
 #pragma unroll
             for (int m = 0; m < 3; ++m) {
-              const double r0 = __ldg(met + m * 3), r1 = __ldg(met + m * 3 + 1), r2 = __ldg(met + m * 3 + 2);
+              const double r0 = C::METPRE ? mpre[m * 3] : __ldg(met + m * 3),
+                           r1 = C::METPRE ? mpre[m * 3 + 1] : __ldg(met + m * 3 + 1),
+                           r2 = C::METPRE ? mpre[m * 3 + 2] : __ldg(met + m * 3 + 2);
               const double um = r0 * vx + r1 * vy + r2 * vz;
               double gm[5] = {s.r * um, s.mx * um + pr * r0, s.my * um + pr * r1, s.mz * um + pr * r2, ep * um};
               if (VISC && se > 0.0) {
