@@ -21,6 +21,12 @@
 #ifndef CDG_WA_FUNROLL
 #define CDG_WA_FUNROLL 1
 #endif
+#ifndef CDG_WA_ASTAGE
+#define CDG_WA_ASTAGE 1  // HLLC: the tile's metrics / face geometry / connectivity by cp.async, waited after the first GEMM1
+#endif
+#ifndef CDG_WA_RES2
+#define CDG_WA_RES2 1  // LLF, p <= 4: both rows' old res values loaded before the first store (+0.5% at P=4)
+#endif
 
 namespace cdg_gpu {
 
@@ -79,14 +85,36 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_wa(RhsParams p) {
     // row r of the m-tile: element e0 + r/5, field r%5 (r = 15: padding)
     const int r_lo = row0 + g, r_hi = r_lo + 8;
     const bool ok_lo = r_lo < n_rows, ok_hi = (g + 8 < 15) && r_hi < n_rows;
-    for (int idx = lane; idx < C::EPW * 9; idx += 32)
-      sMet[idx] = e0 + idx / 9 < p.K ? __ldg(p.metric + (size_t)e0 * 9 + idx) : 0.0;
-    for (int idx = lane; idx < C::EPW * 4; idx += 32) {
-      const bool ok = e0 + idx / 4 < p.K;
-      sFace[idx] = ok ? p.face[(size_t)e0 * 4 + idx] : make_double4(0, 0, 1, 0);
-      sConn[idx] = ok ? p.conn[(size_t)e0 * 4 + idx] : make_int2(-1, pack_face(0, 0, 1, 0));
+    constexpr bool AST = CDG_WA_ASTAGE && RM == 1;  // measured: HLLC +1.4%, LLF -0.5%
+    if (AST) {  // in flight during the first chunk's GEMM1
+      for (int idx = lane; idx < C::EPW * 9; idx += 32) {
+        if (e0 + idx / 9 < p.K)
+          cp_async8_sh(sMet + idx, p.metric + (size_t)e0 * 9 + idx);
+        else
+          sMet[idx] = 0.0;
+      }
+      for (int idx = lane; idx < C::EPW * 8; idx += 32) {  // 16-byte halves of the double4s
+        if (e0 + idx / 8 < p.K)
+          cp_async16_sh(reinterpret_cast<double*>(sFace) + 2 * idx, reinterpret_cast<const double*>(p.face + (size_t)e0 * 4) + 2 * idx);
+        else
+          reinterpret_cast<double2*>(sFace)[idx] = (idx & 1) ? make_double2(1.0, 0.0) : make_double2(0.0, 0.0);
+      }
+      for (int idx = lane; idx < C::EPW * 4; idx += 32) {
+        if (e0 + idx / 4 < p.K)
+          cp_async8_sh(sConn + idx, p.conn + (size_t)e0 * 4 + idx);
+        else
+          sConn[idx] = make_int2(-1, pack_face(0, 0, 1, 0));
+      }
+    } else {
+      for (int idx = lane; idx < C::EPW * 9; idx += 32)
+        sMet[idx] = e0 + idx / 9 < p.K ? __ldg(p.metric + (size_t)e0 * 9 + idx) : 0.0;
+      for (int idx = lane; idx < C::EPW * 4; idx += 32) {
+        const bool ok = e0 + idx / 4 < p.K;
+        sFace[idx] = ok ? p.face[(size_t)e0 * 4 + idx] : make_double4(0, 0, 1, 0);
+        sConn[idx] = ok ? p.conn[(size_t)e0 * 4 + idx] : make_int2(-1, pack_face(0, 0, 1, 0));
+      }
+      __syncwarp();
     }
-    __syncwarp();
 
     const double* u_lo = p.u + (size_t)min(r_lo, n_rows - 1) * C::BP + 2 * tq;
     const double* u_hi = p.u + (size_t)min(r_hi, n_rows - 1) * C::BP + 2 * tq;
@@ -146,6 +174,7 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_wa(RhsParams p) {
             *reinterpret_cast<double2*>(o + 8 * C::LDC) = make_double2(c1[j][2], c1[j][3]);
           }
       }
+      if (AST && ch == 0) cp_async_wait0();  // the tile's staged metrics / faces / connectivity
       __syncwarp();
       // pointwise Euler flux -> contravariant flux G_m = sum_d (dr_m/dx_d) F_d
 #pragma unroll
@@ -245,13 +274,25 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_wa(RhsParams p) {
     }
     const bool cur_lo = (sConn[(g / 5) * 4].y & kCurvedBit) != 0;
     const bool cur_hi = g + 8 < 15 && (sConn[((g + 8) / 5) * 4].y & kCurvedBit) != 0;
+    constexpr bool R2 = CDG_WA_RES2 && RM == 0 && C::NT2 <= 5;  // HLLC and p=5 spill with both rows live
+    double2 rsv2[R2 ? 2 : 1][C::NT2];
+    if (R2 && UPDATE)
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const bool ok = (hh ? ok_hi : ok_lo) && !(hh ? cur_hi : cur_lo);
+        const size_t rowoff = (size_t)(hh ? r_hi : r_lo) * C::BP;
+#pragma unroll
+        for (int j = 0; j < C::NT2; ++j)
+          rsv2[R2 ? hh : 0][j] =
+              ok ? *reinterpret_cast<const double2*>(p.res + rowoff + j * 8 + 2 * tq) : make_double2(0.0, 0.0);
+      }
 #pragma unroll
     for (int hh = 0; hh < 2; ++hh) {
       const bool ok = hh ? ok_hi : ok_lo;
       if (!ok || (hh ? cur_hi : cur_lo)) continue;  // curved rows: the curved kernel
       const size_t rowoff = (size_t)(hh ? r_hi : r_lo) * C::BP;
-      double2 rsv[C::NT2];
-      if (UPDATE)  // every old res value of the row before any store
+      double2* rsv = rsv2[R2 ? hh : 0];
+      if (UPDATE && !R2)  // every old res value of the row before any store
 #pragma unroll
         for (int j = 0; j < C::NT2; ++j) rsv[j] = *reinterpret_cast<const double2*>(p.res + rowoff + j * 8 + 2 * tq);
 #pragma unroll

@@ -467,6 +467,13 @@ class GpuLevel:
         return rows[: min(int(n[0]), max_rows)], bool(conv[0])
 
 
+def _torch_nccl_first():
+    """The library resolves libnccl.so.2 at run time (dlopen): load torch (and
+    the NCCL it is built against) first, so that one NCCL serves both -- the
+    soname would otherwise bind torch to whichever NCCL was loaded first."""
+    import torch  # noqa: F401
+
+
 class GpuComm:
     """Multi-rank driver over shards (GpuLevel with ghost elements + halo_define):
     rk_steps / timestep / residual / run_level over every rank (cdg_gpu_comm_*).
@@ -482,6 +489,7 @@ class GpuComm:
 
     @staticmethod
     def unique_id() -> bytes:
+        _torch_nccl_first()
         buf = C.create_string_buffer(128)
         err = C.create_string_buffer(1024)
         _raise(lib().cdg_gpu_comm_unique_id(buf, err, 1024), err.value.decode())
@@ -497,6 +505,7 @@ class GpuComm:
 
     @classmethod
     def nccl(cls, level, uid: bytes, rank: int, nranks: int):
+        _torch_nccl_first()
         h = C.c_void_p()
         err = C.create_string_buffer(1024)
         _raise(lib().cdg_gpu_comm_create_nccl(level.h, uid, rank, nranks, C.byref(h), err, 1024),
