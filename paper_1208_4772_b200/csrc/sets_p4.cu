@@ -49,7 +49,8 @@
 
 // 1 (default): the warp-autonomous curved kernel (cdg_wac.cuh) for the curved
 // P=4 set, 16 warps x 1 CTA per SM (0.434 / 0.367 of the FP64 peak LLF / HLLC
-// vs 0.422 / 0.355 for k_rhs_rowc); the aux gradient stays on k_rhs_rowc
+// vs 0.422 / 0.355 for k_rhs_rowc; 12 / 10 / 8 warps with 168+ registers:
+// 0.403 / 0.342 / 0.324); the aux gradient: CDG_P4C_AUXW below
 #ifndef CDG_P4C_WAC
 #define CDG_P4C_WAC 1
 #endif
