@@ -344,10 +344,15 @@ void launch_traces(cdg_gpu_level* lv, const double* u, double* traces) {
   ++lv->launches;
 }
 
-// the RHS kernel of the level writes the next stage's traces (row kernel with
-// MODE 32, or the warp-tile kernel); curved levels use the trace kernel
+// the RHS kernels of the level write the next stage's traces: the affine
+// kernel (row kernel with MODE 32, warp-autonomous with FT, or the warp-tile
+// kernel) for the affine elements and, on curved levels, k_rhs_wac for the
+// curved ones (all-curved levels need only the latter)
 bool fused_traces(const cdg_gpu_level* lv) {
-  return lv->n_curved == 0 && ((lv->use_row && lv->ks->row_ft) || (!lv->use_row && lv->use_warp));
+  const bool affine_ft = (lv->use_row && lv->ks->row_ft) || (!lv->use_row && lv->use_warp);
+  if (lv->n_curved == 0) return affine_ft;
+  const bool curved_ft = lv->use_rowc && lv->ks->rowc_ft;
+  return curved_ft && (affine_ft || lv->n_curved == lv->K);
 }
 
 // the captured graphs that bake the state pointer u and the trace buffers

@@ -59,6 +59,7 @@ struct KernelSet {
   size_t smem_rowc = 0, smem_rowc_aux = 0;
   int rowc_aux_minb = 0, rowc_aux_e = 16, rowc_aux_nth = 160;
   const char* rowc_name = "k_rhs_rowc";
+  bool rowc_ft = false;  // the curved update kernel writes the next stage's traces (k_rhs_wac)
   int rowc_minb = 0, rowc_ch = 0, rowc_e = 16, rowc_nth = 160;
 };
 
@@ -123,6 +124,7 @@ KernelSet with_wac(KernelSet k) {
   k.rowc_e = WC::E;
   k.rowc_nth = WC::NTH;
   k.rowc_name = "k_rhs_wac";
+  k.rowc_ft = WC::FT;
   return k;
 }
 

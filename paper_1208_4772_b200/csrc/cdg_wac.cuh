@@ -14,6 +14,9 @@
 #ifndef CDG_WAC_FUNROLL
 #define CDG_WAC_FUNROLL 1
 #endif
+#ifndef CDG_WAC_FT
+#define CDG_WAC_FT 1  // fused next-stage traces from the update kernel (fused-trace path)
+#endif
 #ifndef CDG_WAC_METPRE
 #define CDG_WAC_METPRE 1  // a lane's per-node metrics loaded before the chunk's GEMM1 (latency hidden)
 #endif
@@ -42,6 +45,8 @@ struct WacCfg {
   static constexpr int IT_P = ceil_div(EPW * CH, 32), IT_F = ceil_div(EPW * FCH, 32);
   static constexpr int FUNROLL = CDG_WAC_FUNROLL;  // face-item loop unroll (tuning)
   static constexpr bool METPRE = CDG_WAC_METPRE && IT_P == 1;
+  static constexpr bool FT = CDG_WAC_FT;
+  static constexpr int NFT = NF8 / 8;  // n-tiles of the fused traces
 };
 
 template <class C, bool UPDATE, int RM, int KIND = 0>
@@ -384,6 +389,35 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_wac(CurvedParams cp) {
           p.u[gi] = uo[f] + b_c * rn;
         } else {
           p.rhs_out[gi] = out[0][f];
+        }
+      }
+    }
+    if (C::FT && UPD && !VISC && p.traces_out) {
+      // next stage's traces T = u_new I_g^T (solver.cpp:200-208): the warp's
+      // rows of u_new (just stored; visible to the warp after __syncwarp) as
+      // natural-pairing A fragments times the trace kernel's B fragments --
+      // k_interp<NAT>'s arithmetic, so fused and separate traces agree bit for bit
+      __syncwarp();
+      AFrag ua[C::KS1];
+#pragma unroll
+      for (int ks = 0; ks < C::KS1; ++ks) {
+        double2 x = make_double2(0.0, 0.0), y = make_double2(0.0, 0.0);
+        if (ok_lo) x = *reinterpret_cast<const double2*>(u_lo + ks * 8);
+        if (ok_hi) y = *reinterpret_cast<const double2*>(u_hi + ks * 8);
+        ua[ks] = AFrag{x.x, y.x, x.y, y.y};
+      }
+      const double2* fig = reinterpret_cast<const double2*>(p.frag_ig_nat);
+      double* t_lo = p.traces_out + ((size_t)(ok_lo ? el_lo : 0) * 5 + g % 5) * C::TB;
+      double* t_hi = p.traces_out + ((size_t)(ok_hi ? el_hi : 0) * 5 + (g + 8) % 5) * C::TB;
+#pragma unroll 2
+      for (int nt = 0; nt < C::NFT; ++nt) {
+        double tacc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int ks = 0; ks < C::KS1; ++ks) mma_frag(tacc, ua[ks], __ldg(fig + ((size_t)nt * C::KS1 + ks) * 32 + lane));
+        const int col = nt * 8 + 2 * tq;
+        if (col < C::NF) {
+          if (ok_lo) *reinterpret_cast<double2*>(t_lo + col) = make_double2(tacc[0], tacc[1]);
+          if (ok_hi) *reinterpret_cast<double2*>(t_hi + col) = make_double2(tacc[2], tacc[3]);
         }
       }
     }
