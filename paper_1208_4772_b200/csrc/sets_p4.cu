@@ -54,6 +54,12 @@
 #ifndef CDG_P4C_WAC
 #define CDG_P4C_WAC 1
 #endif
+// MODE of the row kernel that serves the affine elements of curved P=4 levels
+// (192: no fused traces -- mixed levels keep the trace kernel; 224: fused,
+// measured 2-3% slower per step at 40% / 10% curved)
+#ifndef CDG_P4C_ROWMODE
+#define CDG_P4C_ROWMODE 192
+#endif
 #ifndef CDG_P4C_WAC_WARPS
 #define CDG_P4C_WAC_WARPS 16
 #endif
@@ -79,12 +85,12 @@ std::vector<KernelSet> kernel_sets_p4() {
 #endif
 #if CDG_P4C_WAC && CDG_P4C_AUXW
       with_wac_aux<35, 70, 56, 8, 32, CDG_P4C_AUXW>(with_wac<35, 70, 56, 8, CDG_P4C_FCH, CDG_P4C_WAC_WARPS, CDG_P4C_WAC_MINB>(
-          with_rowc<35, 70, 56, CDG_P4C_CH, CDG_P4C_FCH, CDG_P4C_MINB>(with_row<35, 70, 56, 8, 32, 4, 192>(make_set<35, 70, 56, 16, 24, 2>()))))};
+          with_rowc<35, 70, 56, CDG_P4C_CH, CDG_P4C_FCH, CDG_P4C_MINB>(with_row<35, 70, 56, 8, 32, 4, CDG_P4C_ROWMODE>(make_set<35, 70, 56, 16, 24, 2>()))))};
 #elif CDG_P4C_WAC
       with_wac<35, 70, 56, 8, CDG_P4C_FCH, CDG_P4C_WAC_WARPS, CDG_P4C_WAC_MINB>(
-          with_rowc<35, 70, 56, CDG_P4C_CH, CDG_P4C_FCH, CDG_P4C_MINB>(with_row<35, 70, 56, 8, 32, 4, 192>(make_set<35, 70, 56, 16, 24, 2>())))};
+          with_rowc<35, 70, 56, CDG_P4C_CH, CDG_P4C_FCH, CDG_P4C_MINB>(with_row<35, 70, 56, 8, 32, 4, CDG_P4C_ROWMODE>(make_set<35, 70, 56, 16, 24, 2>())))};
 #else
-      with_rowc<35, 70, 56, CDG_P4C_CH, CDG_P4C_FCH, CDG_P4C_MINB>(with_row<35, 70, 56, 8, 32, 4, 192>(make_set<35, 70, 56, 16, 24, 2>()))};
+      with_rowc<35, 70, 56, CDG_P4C_CH, CDG_P4C_FCH, CDG_P4C_MINB>(with_row<35, 70, 56, 8, 32, 4, CDG_P4C_ROWMODE>(make_set<35, 70, 56, 16, 24, 2>()))};
 #endif
 }
 

@@ -45,8 +45,11 @@ def main():
     ap.add_argument("--riemann", default="llf")
     ap.add_argument("--amp", type=float, default=0.02)
     ap.add_argument("--visc", action="store_true", help="Persson-Peraire AV forced on every element")
+    ap.add_argument("--lib", default=None, help="a build.build_variant library (tuning)")
     args = ap.parse_args()
     import torch
+    if args.lib:
+        gpu.use_library(args.lib)
 
     mesh = M.cube_mesh(args.n)
     K = mesh.n_owned
@@ -92,13 +95,14 @@ def main():
     Kc = len(ids)
     # the rhs time covers both kernels when --frac < 1; F_rhs is the same model
     # for both (curved-mesh quadrature on every element)
-    ach = F_rhs * K / t_rhs_s / 1e12
+    F_k = F if lv.fused_traces() else F_rhs  # fused: the RHS kernels also write the next stage's traces
+    ach = F_k * K / t_rhs_s / 1e12
     geo = 8 * (9 * re.n_cub + 4 * 4 * re.n_face_quad + npb * npb)
     out = {"config": f"make_cube_mesh({args.n}) = {K} tets, {Kc} curved (smooth map, amp {args.amp}), "
                      f"P={args.p} (N_cub={re.n_cub}, N_f={4 * re.n_face_quad}), {args.riemann.upper()}",
            "dof_updates_per_s": K * npb * 25 / (ms_step * 1e-3), "ms_per_step": ms_step,
            "rhs_kernel_ms": t_rhs_s * 1e3, "trace_kernel_ms": t_tr_s * 1e3,
-           "rhs_model_flop_per_elem": F_rhs, "rhs_tflops": ach, "fp64_peak_tflops": peak, "frac": ach / peak,
+           "rhs_model_flop_per_elem": F_k, "fused_traces": lv.fused_traces(), "rhs_tflops": ach, "fp64_peak_tflops": peak, "frac": ach / peak,
            "model_bytes_per_elem": B + geo * Kc / K,
            "hbm_gbs": (B + geo * Kc / K) * K / (t_rhs_s + t_tr_s) / 1e9}
     if t_rhs == 0:  # viscous steps run as one CUDA graph: no per-kernel split
