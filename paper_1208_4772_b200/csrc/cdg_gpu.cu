@@ -1498,12 +1498,20 @@ static void copy_rows(cdg_gpu_level* lv, double* dst, int dst_block, const doubl
   if (kind == cudaMemcpyHostToDevice || kind == cudaMemcpyDeviceToHost) {
     const bool h2d = kind == cudaMemcpyHostToDevice;
     const int db = h2d ? dst_block : src_block, hb = h2d ? src_block : dst_block;  // device / host rows
-    if (!lv->ring[0]) {
-      lv->ring_doubles = (size_t)8 << 20;  // 64 MB per slot
+    // slots of up to 64 MB, no larger than the copy (small levels pin little)
+    const size_t want = std::min<size_t>((size_t)8 << 20, std::max<size_t>((size_t)rows * db, 1));
+    if (lv->ring_doubles < want) {
       for (int s = 0; s < 2; ++s) {
-        CUDA_OK(cudaHostAlloc(&lv->ring[s], lv->ring_doubles * sizeof(double), cudaHostAllocDefault));
-        CUDA_OK(cudaEventCreateWithFlags(&lv->ring_ev[s], cudaEventDisableTiming));
+        if (lv->ring_ev[s]) CUDA_OK(cudaEventSynchronize(lv->ring_ev[s]));
+        if (lv->ring[s]) cudaFreeHost(lv->ring[s]);
+        lv->ring[s] = nullptr;
       }
+      lv->ring_doubles = 0;
+      for (int s = 0; s < 2; ++s) {
+        CUDA_OK(cudaHostAlloc(&lv->ring[s], want * sizeof(double), cudaHostAllocDefault));
+        if (!lv->ring_ev[s]) CUDA_OK(cudaEventCreateWithFlags(&lv->ring_ev[s], cudaEventDisableTiming));
+      }
+      lv->ring_doubles = want;
     }
     const int rc = (int)std::max<size_t>(1, lv->ring_doubles / db);  // rows per slot
     const int nchunks = (rows + rc - 1) / rc;
