@@ -355,6 +355,19 @@ bool fused_traces(const cdg_gpu_level* lv) {
   return curved_ft && (affine_ft || lv->n_curved == lv->K);
 }
 
+// Grid sizing of the warp-autonomous kernel on a single-shard level: one warp
+// per 3-element group, 16 warps per SM. A level whose groups fill the resident
+// warps once and then less than 60% of them a second time (e.g. 7,986 tets:
+// 2,662 groups on 2,368 warps) takes the CTA kernel (16-element tiles), 12-17%
+// faster there; from ~16k tets up the warp-autonomous kernel wins.
+bool wa_poorly_quantized(const cdg_gpu_level* lv) {
+  if (std::strcmp(lv->ks->row_name, "k_rhs_wa") != 0 || lv->n_halo > 0 || lv->n_curved > 0) return false;
+  const long groups = (lv->K + 2) / 3;
+  const long slots = (long)lv->n_sms * (lv->ks->row_nth / 32) * lv->ks->row_minb;
+  const long waves = (groups + slots - 1) / slots;
+  return waves == 2 && (double)groups / (double)(slots * waves) < 0.6;
+}
+
 // the captured graphs that bake the state pointer u and the trace buffers
 void drop_graphs_except_ns(cdg_gpu_level* lv) {
   if (lv->graph) cudaGraphExecDestroy(lv->graph), lv->graph = nullptr;
@@ -1210,6 +1223,8 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
     lv->code_map = dev_upload(codes);
     if (d->h) lv->h = dev_upload(std::vector<double>(d->h, d->h + K));
 
+    if (lv->use_row && wa_poorly_quantized(lv)) lv->use_row = false;  // (n_curved known here)
+
     // ---- state + workspace -------------------------------------------------
     const size_t n = (size_t)K * 5 * lv->bp;
     const size_t ntr = (size_t)(K + lv->n_halo) * 5 * lv->tb;
@@ -1913,7 +1928,7 @@ int cdg_gpu_set_kernel_path(cdg_gpu_level* lv, int path) {
     return CDG_GPU_ERR_CONFIG;
   const bool generic = path == CDG_GPU_PATH_GENERIC;
   lv->use_ns = path == CDG_GPU_PATH_DEFAULT && lv->d_ig != nullptr;
-  lv->use_row = !generic && lv->ks->row_update[0] != nullptr;
+  lv->use_row = !generic && lv->ks->row_update[0] != nullptr && !wa_poorly_quantized(lv);
   lv->use_warp = !generic && lv->ks->warp_update[0] != nullptr;
   lv->use_rowc = !generic && lv->rfrag_opc != nullptr;
   lv->traces_valid = false;
