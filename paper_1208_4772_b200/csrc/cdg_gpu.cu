@@ -678,8 +678,15 @@ void launch_aux(cdg_gpu_level* lv) {
   const size_t n = (size_t)lv->K * 5 * lv->bp;
   const size_t nt = (size_t)(lv->K + lv->n_halo) * 5 * lv->tb;
   const size_t nc = (size_t)lv->K * 5 * ((lv->ncub + 7) / 8 * 8);
+  {  // the normal component of q's traces (the BR1 face term's only use of them)
+    const int blocks = (lv->n_rows() + lv->ks->qn_rows - 1) / lv->ks->qn_rows;  // row blocks, one per CTA
+    lv->ks->qn_traces<<<blocks, kThreads, lv->ks->smem_qn, lv->stream>>>(
+        lv->q, n, lv->qtr, lv->frag_ig, lv->face, lv->curved_face, lv->n_curved ? lv->d_curved_slot : nullptr,
+        lv->n_rows(), blocks, lv->cur_gate, lv->cur_gate_when);
+    ++lv->launches;
+  }
+  (void)nt;
   for (int m = 0; m < 3; ++m) {
-    launch_traces(lv, lv->q + m * n, lv->qtr + m * nt);
     // I_cub q_m once per element (the RHS kernels' viscous volume term)
     const int tiles = lv->n_tiles();
     lv->ks->cubinterp<<<tiles, kThreads, lv->ks->smem_traces, lv->stream>>>(
@@ -1285,6 +1292,7 @@ int cdg_gpu_level_create(const cdg_gpu_level_desc* d, int device, cdg_gpu_level*
         CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lv->ks->smem_curved));
     for (auto fn : {lv->ks->traces, lv->ks->cubinterp})
       CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lv->ks->smem_traces));
+    CUDA_OK(cudaFuncSetAttribute(lv->ks->qn_traces, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lv->ks->smem_qn));
     CUDA_OK(cudaDeviceSynchronize());
   });
   if (st != CDG_GPU_OK) {
@@ -2133,17 +2141,16 @@ void set_halo_lists(cdg_gpu_level* lv, int n_send, const int* send_ef, int n_rec
 }
 
 // what: 0 U traces, 1 U traces + sqrt(eps) of the element, 2 the three q_m traces
-int halo_width(const cdg_gpu_level* lv, int what) { return what == 2 ? 15 * lv->ng : 5 * lv->ng + (what == 1); }
+int halo_width(const cdg_gpu_level* lv, int what) { return what == 2 ? 5 * lv->ng : 5 * lv->ng + (what == 1); }
 
 // pack (dir 0: owned faces -> buf) / unpack (dir 1: buf -> ghost faces)
 void halo_move(cdg_gpu_level* lv, int dir, int what, double* buf) {
   const int n = dir == 0 ? lv->n_send : lv->n_recv;
   if (!n) return;
   HaloXfer x{};
-  if (what == 2) {
-    const size_t qs = (size_t)(lv->K + lv->n_halo) * 5 * lv->tb;
-    x.nplanes = 3;
-    for (int m = 0; m < 3; ++m) x.plane[m] = lv->qtr + m * qs;
+  if (what == 2) {  // the normal component of q's traces (one plane)
+    x.nplanes = 1;
+    x.plane[0] = lv->qtr;
   } else {
     x.nplanes = 1;
     x.plane[0] = lv->traces;

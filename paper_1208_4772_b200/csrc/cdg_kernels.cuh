@@ -468,6 +468,76 @@ k_interp(const double* __restrict__ u, double* __restrict__ out, const double* _
   }
 }
 
+// Normal component of the aux-gradient traces, the only combination the BR1
+// viscous face term uses (solver.cpp:438-453: sum_m 0.5 (se q_m + snb q_m^+) n_m):
+//   qn[e][c][fq] = sum_m n_m(e, fq) (I_g q_m)[e][c][fq]
+// the three q_m tiles staged like k_interp<NAT> (same fragments and pairing,
+// so each I_g q_m equals the trace kernel's bit for bit), projected on the
+// element's own outward normal at the face node (per face on straight
+// elements, per face node on curved ones). The consumer flips the sign of a
+// neighbour's value (its outward normal is -n at the paired node). One row
+// of 5 N_g values per face instead of 15.
+// rows per CTA pass of k_qn_traces: the trace kernel's tile when its three
+// panels fit 160 KB of shared memory, else one m16 block (p >= 7)
+template <class C>
+__host__ __device__ constexpr int qn_block_rows() { return 3 * C::R * C::LDU * 8 <= 160 * 1024 ? C::R : 16; }
+
+template <class C>
+__global__ void __launch_bounds__(kThreads)
+k_qn_traces(const double* __restrict__ q, size_t qstride, double* __restrict__ out, const double* __restrict__ frag_op,
+            const double4* __restrict__ face, const double4* __restrict__ curved_face,
+            const int* __restrict__ curved_slot, int n_rows, int n_blocks, const unsigned long long* gate,
+            int gate_when) {
+  if (gated_off(gate, gate_when)) return;
+  constexpr int BR = qn_block_rows<C>();
+  extern __shared__ __align__(16) double smem[];  // [3][BR][LDU]: a row block of the three q_m
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  constexpr int NT = round_up(C::NF, 8) / 8;
+  constexpr int T = (BR / 16) * NT;
+  constexpr int V = C::KP / 2;
+  const double2* fb = reinterpret_cast<const double2*>(frag_op);
+  for (int blk = blockIdx.x; blk < n_blocks; blk += gridDim.x) {
+    const int row0 = blk * BR;
+    for (int idx = tid; idx < 3 * BR * V; idx += kThreads) {
+      const int m = idx / (BR * V), rj = idx - m * (BR * V), r = rj / V, j = rj - r * V;
+      double2 x = make_double2(0.0, 0.0);
+      if (row0 + r < n_rows) x = *reinterpret_cast<const double2*>(q + m * qstride + (size_t)(row0 + r) * C::BP + 2 * j);
+      *reinterpret_cast<double2*>(smem + (m * BR + r) * C::LDU + 2 * j) = x;
+    }
+    __syncthreads();
+    for (int t = warp; t < T; t += kWarps) {
+      const int mt = t / NT, nt = t % NT;
+      double acc[3][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+#pragma unroll 4
+      for (int ks = 0; ks < C::KS1; ++ks) {
+        const double2 b = __ldg(fb + ((size_t)nt * C::KS1 + ks) * 32 + lane);
+#pragma unroll
+        for (int m = 0; m < 3; ++m) mma_frag(acc[m], load_afrag(smem + m * BR * C::LDU, C::LDU, mt * 16, ks * 8, g, tq), b);
+      }
+      const int col = nt * 8 + 2 * tq;
+      if (col < C::NF) {
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int r = row0 + mt * 16 + g + 8 * hh;
+          if (r >= n_rows) continue;
+          const int e = r / 5;
+          const int slot = curved_slot ? __ldg(curved_slot + e) : -1;
+          double v[2];
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int fq = col + i;
+            const double4 n = slot >= 0 ? curved_face[(size_t)slot * C::NF + fq] : face[(size_t)e * 4 + fq / C::NG];
+            v[i] = n.x * acc[0][2 * hh + i] + n.y * acc[1][2 * hh + i] + n.z * acc[2][2 * hh + i];
+          }
+          *reinterpret_cast<double2*>(out + (size_t)r * C::TB + col) = make_double2(v[0], v[1]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Kernel 2: fused volume + surface + lift (+ low-storage RK update)
 // ---------------------------------------------------------------------------
@@ -838,19 +908,13 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs(RhsParams p) {
           const double se = sSe[e];
           const bool has_nb = cw.x >= 0;
           const double snb = has_nb ? p.sqrt_eps[cw.x] : se;
-          const double nrm[3] = {fn.x, fn.y, fn.z};
 #pragma unroll
           for (int c = 0; c < 5; ++c) {
-            double visc = 0.0;
-#pragma unroll
-            for (int m = 0; m < 3; ++m) {
-              const double* qt = p.qtr + m * p.qtr_stride;
-              const double qs = qt[((size_t)eg * 5 + c) * C::TB + fq];
-              const double qn =
-                  has_nb ? qt[((size_t)cw.x * 5 + c) * C::TB + (cw.y & 3) * C::NG + h] : qs;
-              visc += 0.5 * (se * qs + snb * qn) * nrm[m];
-            }
-            fs[c] -= visc;
+            // q.n on both sides from the normal-projected traces (k_qn_traces); the
+            // neighbour's value is on its own outward normal, -n here
+            const double qs = p.qtr[((size_t)eg * 5 + c) * C::TB + fq];
+            const double qn = has_nb ? -p.qtr[((size_t)cw.x * 5 + c) * C::TB + (cw.y & 3) * C::NG + h] : qs;
+            fs[c] -= 0.5 * (se * qs + snb * qn);
           }
         }
 #pragma unroll

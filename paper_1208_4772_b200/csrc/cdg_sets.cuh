@@ -23,6 +23,10 @@ struct KernelSet {
   size_t smem_traces, smem_rhs, smem_aux;
   void (*traces)(const double*, double*, const double*, int, int, const unsigned long long*, int);
   void (*cubinterp)(const double*, double*, const double*, int, int, const unsigned long long*, int);
+  void (*qn_traces)(const double*, size_t, double*, const double*, const double4*, const double4*, const int*, int, int,
+                    const unsigned long long*, int);
+  size_t smem_qn = 0;
+  int qn_rows = 16;  // rows per CTA pass of qn_traces
   void (*rhs_update)(RhsParams);
   void (*rhs_only)(RhsParams);
   void (*aux_q)(AuxParams);
@@ -206,6 +210,9 @@ KernelSet make_set() {
   k.smem_aux = C8::SMEM_BYTES;
   k.traces = &k_interp<C8, C8::NF, C8::TB, true>;
   k.cubinterp = &k_interp<C8, C8::NCUB, round_up(NCUB, 8)>;
+  k.qn_traces = &k_qn_traces<C8>;
+  k.smem_qn = sizeof(double) * 3 * qn_block_rows<C8>() * C8::LDU;
+  k.qn_rows = qn_block_rows<C8>();
   k.rhs_update = &k_rhs<C, true, false>;
   k.rhs_only = &k_rhs<C, false, false>;
   k.aux_q = &k_aux_q<C8>;

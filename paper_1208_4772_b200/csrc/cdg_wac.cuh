@@ -288,18 +288,13 @@ __global__ void __launch_bounds__(C::NTH, C::MINB) k_rhs_wac(CurvedParams cp) {
           const double se = p.sqrt_eps[eg];
           const bool has_nb = cw.x >= 0;
           const double snb = has_nb ? p.sqrt_eps[cw.x] : se;
-          const double nrm[3] = {fn.x, fn.y, fn.z};
 #pragma unroll
           for (int c = 0; c < 5; ++c) {
-            double visc = 0.0;
-#pragma unroll
-            for (int m = 0; m < 3; ++m) {
-              const double* qt = p.qtr + m * p.qtr_stride;
-              const double qs = qt[((size_t)eg * 5 + c) * C::TB + fq];
-              const double qn = has_nb ? qt[((size_t)cw.x * 5 + c) * C::TB + (cw.y & 3) * C::NG + h] : qs;
-              visc += 0.5 * (se * qs + snb * qn) * nrm[m];
-            }
-            fs[c] -= visc;
+            // q.n on both sides from the normal-projected traces (k_qn_traces); the
+            // neighbour's value is on its own outward normal, -n here
+            const double qs = p.qtr[((size_t)eg * 5 + c) * C::TB + fq];
+            const double qn = has_nb ? -p.qtr[((size_t)cw.x * 5 + c) * C::TB + (cw.y & 3) * C::NG + h] : qs;
+            fs[c] -= 0.5 * (se * qs + snb * qn);
           }
         }
 #pragma unroll
