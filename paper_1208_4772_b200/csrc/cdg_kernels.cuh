@@ -477,10 +477,11 @@ k_interp(const double* __restrict__ u, double* __restrict__ out, const double* _
 // elements, per face node on curved ones). The consumer flips the sign of a
 // neighbour's value (its outward normal is -n at the paired node). One row
 // of 5 N_g values per face instead of 15.
-// rows per CTA pass of k_qn_traces: the trace kernel's tile when its three
-// panels fit 160 KB of shared memory, else one m16 block (p >= 7)
+// rows per CTA pass of k_qn_traces: two m16 blocks (AV step at 82,944 curved
+// P=4 tets: 16 / 32 / 48 / 80 rows -> 27.9 / 27.4 / 27.5 / 27.5 ms); the
+// three panels fit shared memory at every order (p=8: 129 KB)
 template <class C>
-__host__ __device__ constexpr int qn_block_rows() { return 3 * C::R * C::LDU * 8 <= 160 * 1024 ? C::R : 16; }
+__host__ __device__ constexpr int qn_block_rows() { return 32; }
 
 template <class C>
 __global__ void __launch_bounds__(kThreads)
